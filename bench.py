@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""bench.py — smoother-application throughput of the Neumann-series smoothers
+(arXiv 2112.14681) on B200, in the driver's JSON-line contract.
+
+A "step" is one smoother application nsm_smooth(nu = 1): residual r = b - A x,
+the Jacobi-iterated triangular solves and the fused x update (SURVEY.md §8(a)
+rows a2-a6; a7 halo exchange when N > 1).  value = algorithmic bytes of all
+steps of all ranks / max-over-ranks device time, in GB/s (BASELINE.json
+metric "smoother sweep GB/s (frac of HBM peak) and ms per pGS/ILU apply").
+
+Workload (default): BASELINE.json configs[1] = C2, 3-D 7-point Laplacian
+128^3, ILU(0) with k_l = k_u = 2 Jacobi sweeps; with N GPUs the grid is
+128 x 128 x 128N split into z-slabs (weak scaling, HYBRID halo exchange).
+--config C3/C4/C5 select the other BASELINE workloads.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl nsm|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "smoother sweep GB/s (frac of HBM peak) and ms per pGS/ILU apply at 1/2/4/8"
+WORKLOADS = {
+    # name: (generator edge N, kind, k_l, k_u, description)
+    "C2": (128, "ilu", 2, 2, "C2: 3D 7-point Laplacian 128^3 per GPU, ILU(0) factors, Jacobi-iterated L/U solves k_l=k_u=2, nu=1"),
+    "C3": (256, "pgs", 2, 0, "C3: 3D 27-point variable-coefficient pressure matrix 256^3 (Nalu-Wind shaped), pGS k=2, nu=1"),
+    "C4": (256, "ilu", 2, 2, "C4: convection-diffusion 256^3 + RCM (PeleLM shaped), ILU(0) k_l=k_u=2, nu=1"),
+    "C5": (256, "pgs", 2, 0, "C5: 7-point Laplacian 256^3 rows per GPU, z-slab partition, pGS k=2, nu=1"),
+}
+
+
+# ------------------------------------------------------------------ helpers --
+def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k_l: int, k_u: int,
+                      n_ghost: int = 0) -> dict:
+    """Bytes each kernel of one application must move (DESIGN.md §6 byte
+    model): every stored matrix entry once (8 B value + 4 B int32 column),
+    every n-vector the kernel reads or writes once; gathered neighbour values
+    are counted once (they hit L1/L2 after first touch)."""
+    res = 12 * nnz_off + 32 * n + 8 * n_ghost           # A streams, d, x, b, write r
+    out = {"residual": res}
+    if kind == "pgs":
+        sw = []
+        for j in range(1, k_l + 1):
+            b = 12 * nnz_l + 16 * n                       # L streams, rhs, d
+            b += 0 if j == 1 else 8 * n                   # previous iterate (first sweep recomputes r/d)
+            b += 16 * n if j == k_l else 8 * n            # last: x read+write; else write g
+            sw.append(b)
+        if k_l == 0:
+            sw.append(32 * n)                             # x += r/d
+        out["sweeps"] = sw
+    else:
+        sl, su = [], []
+        for j in range(1, k_l + 1):
+            b = 12 * nnz_l + 8 * n + (0 if j == 1 else 8 * n) + 8 * n   # Ls, rhs, prev iterate, write y
+            if j == k_l and k_u == 0:
+                b += 16 * n                               # dU, x read+write instead of the y write
+            sl.append(b)
+        for j in range(1, k_u + 1):
+            b = 12 * nnz_u + 16 * n + (0 if j == 1 else 8 * n)  # Us, y, dU, prev iterate
+            b += 16 * n if j == k_u else 8 * n
+            su.append(b)
+        if k_l == 0 and k_u == 0:
+            sl.append(32 * n)
+        out["l_sweeps"], out["u_sweeps"] = sl, su
+    out["total"] = res + sum(sum(v) for k, v in out.items() if isinstance(v, list))
+    return out
+
+
+def hbm_peak() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz, self.ok = [], set(), None, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"] if not self.ok else []}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def build_workload(cfg: str, rank: int, nranks: int):
+    """Matrix rows of this rank (global column ids), partition offsets, kind."""
+    import inputs
+    N, kind, k_l, k_u, desc = WORKLOADS[cfg]
+    if cfg in ("C2", "C5"):
+        n_loc = N ** 3
+        A = inputs.laplace(N, N, N * nranks, rank * n_loc, (rank + 1) * n_loc)
+        offsets = np.arange(nranks + 1, dtype=np.int64) * n_loc
+    else:
+        if nranks > 1:
+            raise SystemExit(f"--config {cfg} is a single-GPU workload; use C2 or C5 for N > 1")
+        A = inputs.config_matrix(cfg)
+        offsets = np.array([0, A.nrows], dtype=np.int64)
+    return A, offsets, kind, k_l, k_u, desc
+
+
+def split_counts(A):
+    """nnz of the strict lower / upper parts and off-diagonal of this row block."""
+    rows = np.repeat(np.arange(A.nrows, dtype=np.int64) + A.row_begin, np.diff(A.rowptr))
+    lower = int(np.count_nonzero(A.col < rows))
+    upper = int(np.count_nonzero(A.col > rows))
+    return lower, upper, lower + upper
+
+
+def flush_l2(buf):
+    buf.add_(1.0)  # writes 256 MB (> 126 MB L2) between timed steps
+
+
+# ---------------------------------------------------------------- reference --
+def run_reference(args, rank, nranks):
+    """The oracle (oracle/) timed as it stands on the host cores: the base
+    contract's reference arm for this tier (no runnable reference code)."""
+    if rank != 0:
+        return
+    import inputs
+    import oracle
+    A, offsets, kind, k_l, k_u, desc = build_workload(args.config, 0, 1)
+    nl, nu_, noff = split_counts(A)
+    ab = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u)["total"]
+    b, x0 = inputs.uniform(inputs.SEED_B, A.nrows), inputs.uniform(inputs.SEED_X0, A.nrows)
+    F = oracle.ilu0(A) if kind == "ilu" else None
+
+    def step(x):
+        if kind == "ilu":
+            return oracle.ilu_apply(A, F, b, x, k_l, k_u)
+        return oracle.pgs_apply(A, b, x, k_l)
+
+    x = x0
+    for _ in range(args.warmup):
+        x = step(x)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x = step(x)
+    dt = time.perf_counter() - t0
+    v = ab * args.steps / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "n": A.nrows, "nnz": A.nnz},
+            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} full applications of the workload (single-threaded C oracle)"},
+            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- nsm --
+def run_nsm(args, rank, nranks, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    import paper_2112_14681_b200 as nsm
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    A, offsets, kind, k_l, k_u, desc = build_workload(args.config, rank, nranks)
+    F = nsm.ilu0(A, row_begin=A.row_begin) if kind == "ilu" else None
+    S = nsm.Smoother(A, F, device=local_rank, rank=rank, nranks=nranks, row_offsets=offsets)
+    if nranks > 1:
+        S.connect(dist)
+    nl, nu_, noff = split_counts(A)
+    model = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost)
+    ab = model["total"]
+    b = torch.from_numpy(inputs.uniform(inputs.SEED_B, A.nrows, idx0=A.row_begin)).to(dev)
+    x0 = torch.from_numpy(inputs.uniform(inputs.SEED_X0, A.nrows, idx0=A.row_begin)).to(dev)
+    x = x0.clone()
+    flush = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        S.smooth(b, x, kind, nu=1, k_l=k_l, k_u=k_u)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if nranks > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    args.warmup = max(args.warmup, 3)       # contract: W >= 3
+    for _ in range(args.warmup):
+        step()
+    S.check()
+    launches0, _ = S.stats()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        for e0, e1 in evs:
+            flush_l2(flush)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+        barrier()
+    launches = S.stats()[0] - launches0
+    S.check()
+    t_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if nranks > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    ms_step = t_ms / args.steps
+    value = ab * nranks * args.steps / (t_ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+
+    # ---- dominant kernel: the residual pass, timed alone through nsm_residual
+    r = torch.empty_like(b)
+    for _ in range(3):
+        S.residual(b, x, r)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+    for e0, e1 in kev:
+        flush_l2(flush)
+        e0.record(stream)
+        S.residual(b, x, r)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in kev]))
+    k_bytes = model["residual"]
+    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(args.config, {}).get("residual")
+            traffic = tr
+    except Exception:
+        pass
+
+    # ---- end to end through the public API with host buffers
+    bh = b.cpu().pin_memory()
+    xh = x0.cpu().pin_memory()
+    xo = torch.empty_like(xh).pin_memory()
+    eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    bd, xd = torch.empty_like(b), torch.empty_like(x)
+    barrier()
+    for e0, e1 in eev:
+        flush_l2(flush)
+        e0.record(stream)
+        bd.copy_(bh, non_blocking=True)
+        xd.copy_(xh, non_blocking=True)
+        S.smooth(bd, xd, kind, nu=1, k_l=k_l, k_u=k_u)
+        xo.copy_(xd, non_blocking=True)
+        e1.record(stream)
+    barrier()
+    te = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in eev)], dtype=torch.float64, device=dev)
+    if nranks > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = ab * nranks * args.steps / (float(te.item()) * 1e-3) / 1e9
+
+    # ---- CPU oracle baseline (rank 0, N = 1, bounded sample)
+    cpu = None
+    if rank == 0 and nranks == 1 and not args.no_cpu:
+        import oracle
+        An = A
+        Fo = oracle.ilu0(An) if kind == "ilu" else None
+        bn, xn = b.cpu().numpy(), x0.cpu().numpy()
+        cnt, t0 = 0, time.perf_counter()
+        while cnt < 200 and (time.perf_counter() - t0 < args.cpu_seconds or cnt == 0):
+            xn = oracle.ilu_apply(An, Fo, bn, xn, k_l, k_u) if kind == "ilu" else oracle.pgs_apply(An, bn, xn, k_l)
+            cnt += 1
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(ab * cnt / dt / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"{cnt} full applications of the same workload, single-threaded C oracle ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": nranks, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "n_per_gpu": A.nrows, "nnz_per_gpu": A.nnz, "kind": kind, "k_l": k_l,
+                       "k_u": k_u, "nu": 1, "partition": "z-slab rows" if nranks > 1 else "none",
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "bytes_per_step_per_gpu": ab, "frac_of_hbm_peak": round(value / nranks / peak, 4)},
+            "ms_per_apply": round(ms_step, 4),
+            "roofline": {"bound": "hbm", "kernel": "k_residual (r = b - A x)", "achieved": round(k_gbs, 1),
+                         "peak": peak, "unit": "GB/s", "frac": round(k_gbs / peak, 4), "traffic": traffic,
+                         "peak_source": peak_src, "bytes_per_launch": k_bytes, "ms_per_launch": round(k_ms, 4)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": 16 * A.nrows,
+                    "d2h_bytes_per_step": 8 * A.nrows},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    S.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=list(WORKLOADS))
+    ap.add_argument("--impl", default="nsm", choices=["nsm", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    nranks = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, nranks)
+        return
+    if nranks > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_nsm(args, rank, nranks, local_rank)
+    if nranks > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,190 @@
+/*
+ * nsm.h — Neumann-series smoothers for B200 (sm_100a): the C-ABI boundary.
+ *
+ * The library implements the data-parallel hot path of arXiv 2112.14681
+ * ("Neumann series in GMRES and algebraic multigrid smoothers", PAPER.md):
+ * the sparse triangular solves inside the C-AMG smoothers are replaced by
+ * SpMV-only Jacobi inner sweeps, i.e. truncated Neumann series.
+ *
+ *   polynomial Gauss-Seidel (§5.2):
+ *       r = b - A x ;  g0 = D^{-1} r ;  g_{j+1} = D^{-1}(r - L g_j) (k times) ;
+ *       x = x + g_k  =  x + sum_{j=0..k} (-D^{-1}L)^j D^{-1} r
+ *   ILU(0) with Jacobi-iterated factor solves (§5.3, Alg. 2 P:L1020-1045 with
+ *   the LDU row scaling of P:L858-874 / P:L1012-1013 in place of Ruiz):
+ *       r = b - A x ;  y = sum_{j<=kL} (-L_s)^j r ;
+ *       z = sum_{j<=kU} (-D_U^{-1} U_s)^j D_U^{-1} y ;  x = x + z
+ *
+ * Sweep-count convention (reading R1): k counts products with the
+ * strict triangle AFTER the diagonally scaled start, so k sweeps give k+1
+ * Neumann terms and k = 0 is pure diagonal scaling (Jacobi).
+ *
+ * Conventions for every call:
+ *   - Matrices enter as HOST CSR (nsm_csr), 0-based, int64 row pointers and
+ *     GLOBAL int64 column ids, columns strictly ascending within a row.  The
+ *     library copies what it needs at setup and never retains the pointers.
+ *   - Vectors (b, x, r) are DEVICE pointers to fp64 arrays of length n_local
+ *     (the handle's row count), caller-owned, on the handle's device.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Hot calls are asynchronous on that stream, never allocate and
+ *     never synchronise; their return value only reports argument and launch
+ *     errors.  Divergence (a non-finite value produced by a sweep) is recorded
+ *     in a sticky device flag and reported by nsm_check().
+ *   - A handle owns device workspace: it must not be used concurrently from
+ *     two streams.  Distinct handles are independent.
+ *   - All arithmetic is fp64.  Each row sum is accumulated sequentially in
+ *     ascending column order without FMA contraction and D^{-1} is an IEEE
+ *     division, the same rounding sequence the oracle uses (R10).
+ */
+#ifndef NSM_H
+#define NSM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nsm_handle nsm_handle;
+
+typedef enum {
+    NSM_OK = 0,
+    NSM_ERR_ARG = 1,        /* bad argument: NULL pointer, negative count, aliasing */
+    NSM_ERR_PATTERN = 2,    /* CSR invariant violated: rowptr not monotone, columns
+                               unsorted/duplicated/out of range, factor not triangular */
+    NSM_ERR_ZERO_DIAG = 3,  /* missing or zero diagonal / pivot (row in nsm_last_error) */
+    NSM_ERR_NONFINITE = 4,  /* a sweep produced Inf/NaN (divergence) */
+    NSM_ERR_CUDA = 5,       /* CUDA runtime error (message in nsm_last_error) */
+    NSM_ERR_OOM = 6,        /* device or host allocation failed */
+    NSM_ERR_STATE = 7,      /* call not valid for this handle (e.g. ILU call on a pGS handle) */
+    NSM_ERR_DIST = 8        /* halo plan / peer connection error */
+} nsm_status;
+
+typedef enum {
+    NSM_PGS = 0,   /* polynomial Gauss-Seidel, §5.2 */
+    NSM_ILU0 = 1   /* ILU(0) with Jacobi-iterated L and U solves, §5.3 / Alg. 2 */
+} nsm_kind;
+
+typedef enum {
+    NSM_DIST_HYBRID = 0, /* hypre's hybrid smoother: the x halo is exchanged
+                            once per outer iteration for the residual; the inner sweeps
+                            drop couplings to other ranks (block-Jacobi across ranks) */
+    NSM_DIST_GLOBAL = 1  /* exact global Neumann sweeps: the lower (L sweeps) or upper
+                            (U sweeps) ghost values of the inner iterate are exchanged
+                            before every sweep; the result does not depend on the
+                            partition */
+} nsm_dist_mode;
+
+/* HOST CSR block: rows [row_begin, row_begin + nrows) of an ncols-column
+ * matrix (row_begin comes from nsm_dist; 0 on a single GPU).  rowptr has
+ * nrows + 1 entries starting at 0; colind holds GLOBAL column ids. */
+typedef struct {
+    int64_t nrows;
+    int64_t ncols;
+    const int64_t *rowptr;
+    const int64_t *colind;
+    const double *val;
+} nsm_csr;
+
+/* Row-block partition.  HOST array
+ * row_offsets[nranks + 1], ascending, row_offsets[0] = 0: rank q owns global
+ * rows [row_offsets[q], row_offsets[q+1]).  The CSR passed to nsm_setup must
+ * hold exactly this rank's rows. */
+typedef struct {
+    int rank;
+    int nranks;
+    const int64_t *row_offsets;
+    nsm_dist_mode mode;
+} nsm_dist;
+
+/*
+ * nsm_setup — build the split-triangular device storage (§8(a) row a1).
+ *   A:    the system matrix (P:L717-721 splitting A = L + D + U).  Required.
+ *   F:    NULL for pGS.  For ILU(0): the incomplete factors stored on ONE
+ *         pattern (nsm_ilu0 output layout): strictly-lower entries = L_s of
+ *         the unit-lower L = I + L_s, upper entries incl. the
+ *         diagonal = U = D_U (I + D_U^{-1} U_s).  Rows/columns as A.
+ *   dist: NULL on one GPU; else this rank's place in the row partition.
+ *   device: CUDA device ordinal the handle lives on.
+ * Validates both matrices synchronously (NSM_ERR_PATTERN / NSM_ERR_ZERO_DIAG
+ * with the offending global row in nsm_last_error(NULL)), copies them to the
+ * device as SELL-32 slices and allocates all workspace.  On
+ * failure *out is NULL.  Synchronous w.r.t. the host.
+ */
+nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const nsm_dist *dist,
+                     int device);
+
+/*
+ * nsm_ilu0 — ILU(0) factorisation on the host (setup input for nsm_setup;
+ * not on the timed path).  IKJ variant restricted to the
+ * pattern of A, no pivoting.  `fval` (length nnz(A), caller-allocated HOST
+ * memory) receives the factor values on A's pattern in the layout nsm_setup
+ * expects for F.  With a dist partition of nranks > 1 pass the rank's own
+ * rows and row_begin: the factorisation is of the diagonal block A_pp
+ * (block-Jacobi ILU, HYBRID reading R5) and off-block entries get 0.
+ * Zero pivot -> NSM_ERR_ZERO_DIAG.
+ */
+nsm_status nsm_ilu0(const nsm_csr *A, int64_t row_begin, double *fval);
+
+/* r = b - A x.  With nranks > 1 the x halo is exchanged first.
+ * b, x, r: device, length n_local; r must not alias b or x. */
+nsm_status nsm_residual(nsm_handle *h, const double *b, const double *x, double *r, void *stream);
+
+/*
+ * nsm_lsolve — approximate the lower-triangular solve by k Jacobi sweeps
+ * (eq:jr-initial-guess / eq:jacobi P:L753-764; eq:LUiterMat P:L826-828):
+ *   pGS handle: x = sum_{j=0..k} (-D^{-1} L)^j D^{-1} r    ((D + L) of A)
+ *   ILU handle: x = sum_{j=0..k} (-L_s)^j r                (unit-lower factor)
+ * k = 0 is legal (diagonal scaling).  r and x must not alias.  In HYBRID
+ * mode couplings to other ranks are dropped; in GLOBAL mode lower ghosts of
+ * every iterate are exchanged.
+ */
+nsm_status nsm_lsolve(nsm_handle *h, const double *r, double *x, int k_sweeps, void *stream);
+
+/*
+ * nsm_usolve — same for the upper triangle (eq:Neu P:L1064-1066):
+ *   pGS handle: x = sum_{j=0..k} (-D^{-1} U)^j D^{-1} r    ((D + U) of A)
+ *   ILU handle: x = sum_{j=0..k} (-D_U^{-1} U_s)^j D_U^{-1} r   (U factor)
+ */
+nsm_status nsm_usolve(nsm_handle *h, const double *r, double *x, int k_sweeps, void *stream);
+
+/*
+ * nsm_smooth — nu outer smoothing iterations in place on x (eq:one-stage
+ * P:L723-725; §8(a) rows a2-a6):
+ *   NSM_PGS : x <- x + sum_{j<=k_l} (-D^{-1}L)^j D^{-1} (b - A x)     (k_u ignored)
+ *   NSM_ILU0: x <- x + U~^{-1}_{k_u} L~^{-1}_{k_l} (b - A x)  (Jacobi-iterated factors)
+ * x_is_zero != 0 asserts x == 0 on entry, so the first residual is b and is
+ * not computed (V-cycle pre-smoothing; exact).  b and x must not alias.
+ * Requesting NSM_ILU0 on a handle set up without factors -> NSM_ERR_STATE.
+ */
+nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, int nu, int k_l,
+                      int k_u, int x_is_zero, void *stream);
+
+/* y = A x  (plain SpMV with the stored split; used by the GMRES/V-cycle
+ * driver).  With nranks > 1 the x halo is exchanged first. */
+nsm_status nsm_spmv(nsm_handle *h, const double *x, double *y, void *stream);
+
+/* Synchronises the stream, then reports NSM_ERR_NONFINITE if any sweep since
+ * setup (or the last nsm_check) produced Inf/NaN; *first_bad_sweep receives
+ * the smallest global sweep counter that did (-1 if none).  Clears the flag. */
+nsm_status nsm_check(nsm_handle *h, int64_t *first_bad_sweep, void *stream);
+
+/* Handle facts: local rows, ghost columns, stored (unpadded) entries and the
+ * device bytes of the split storage. */
+nsm_status nsm_info(const nsm_handle *h, int64_t *n_local, int64_t *n_ghost, int64_t *nnz_offdiag,
+                    int64_t *device_bytes);
+
+/* Counters since setup: kernels this handle launched (every launch of every
+ * call) and halo exchanges it performed.  Host-side, no synchronisation. */
+nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *halo_exchanges);
+
+/* Last error message: of `h`, or of the last failed setup when h == NULL.
+ * The pointer stays valid until the next call on the same handle. */
+const char *nsm_last_error(const nsm_handle *h);
+
+/* Frees all device memory of the handle (synchronises its device).  NULL ok. */
+void nsm_destroy(nsm_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSM_H */

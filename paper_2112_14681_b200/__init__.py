@@ -1,0 +1,15 @@
+"""paper_2112_14681_b200 — Neumann-series smoothers (arXiv 2112.14681) for B200.
+
+Thin Python binding over the C-ABI library libnsm.so (include/nsm.h).  Every
+step of the smoother runs in the library's sm_100a kernels; this module only
+marshals arguments (host CSR arrays at setup, device pointers and the
+current CUDA stream at call time).  There is no CPU fallback: if libnsm.so
+is missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+from ._lib import (NSM_DIST_GLOBAL, NSM_DIST_HYBRID, NSM_ILU0, NSM_PGS, NsmError, Smoother, exported_symbols,
+                   ilu0, lib_path, load)
+
+__all__ = ["Smoother", "NsmError", "ilu0", "load", "lib_path", "exported_symbols", "NSM_PGS", "NSM_ILU0",
+           "NSM_DIST_HYBRID", "NSM_DIST_GLOBAL"]

@@ -1,0 +1,222 @@
+"""ctypes binding of libnsm.so — argument marshalling only (include/nsm.h)."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "libnsm.so")
+_lib = None
+
+NSM_PGS, NSM_ILU0 = 0, 1
+NSM_DIST_HYBRID, NSM_DIST_GLOBAL = 0, 1
+_STATUS = {0: "NSM_OK", 1: "NSM_ERR_ARG", 2: "NSM_ERR_PATTERN", 3: "NSM_ERR_ZERO_DIAG", 4: "NSM_ERR_NONFINITE",
+           5: "NSM_ERR_CUDA", 6: "NSM_ERR_OOM", 7: "NSM_ERR_STATE", 8: "NSM_ERR_DIST"}
+
+# every symbol include/nsm.h declares (tests check the .so exports them)
+SYMBOLS = ["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_spmv",
+           "nsm_check", "nsm_info", "nsm_stats", "nsm_last_error", "nsm_destroy"]
+
+
+class NsmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = _STATUS.get(status, str(status))
+        super().__init__(f"{self.name}: {msg}")
+
+
+class _Csr(ctypes.Structure):
+    _fields_ = [("nrows", ctypes.c_int64), ("ncols", ctypes.c_int64), ("rowptr", ctypes.c_void_p),
+                ("colind", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
+class _Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("row_offsets", ctypes.c_void_p),
+                ("mode", ctypes.c_int)]
+
+
+def lib_path() -> str:
+    return _LIBPATH
+
+
+def load():
+    """Load libnsm.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIBPATH):
+        raise ImportError(f"{_LIBPATH} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+    L = ctypes.CDLL(_LIBPATH)
+    vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    P = ctypes.POINTER
+    L.nsm_setup.argtypes = [P(vp), P(_Csr), P(_Csr), P(_Dist), ci]
+    L.nsm_ilu0.argtypes = [P(_Csr), i64, vp]
+    L.nsm_residual.argtypes = [vp, vp, vp, vp, vp]
+    L.nsm_spmv.argtypes = [vp, vp, vp, vp]
+    L.nsm_lsolve.argtypes = [vp, vp, vp, ci, vp]
+    L.nsm_usolve.argtypes = [vp, vp, vp, ci, vp]
+    L.nsm_smooth.argtypes = [vp, ci, vp, vp, ci, ci, ci, ci, vp]
+    L.nsm_check.argtypes = [vp, P(i64), vp]
+    L.nsm_info.argtypes = [vp, P(i64), P(i64), P(i64), P(i64)]
+    L.nsm_stats.argtypes = [vp, P(i64), P(i64)]
+    L.nsm_last_error.argtypes = [vp]
+    L.nsm_last_error.restype = ctypes.c_char_p
+    L.nsm_destroy.argtypes = [vp]
+    L.nsm_destroy.restype = None
+    for name in ["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
+                 "nsm_check", "nsm_info", "nsm_stats"]:
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def exported_symbols() -> list[str]:
+    L = load()
+    return [s for s in SYMBOLS if hasattr(L, s)]
+
+
+def _err(handle) -> str:
+    m = load().nsm_last_error(handle)
+    return m.decode() if m else ""
+
+
+def _csr_struct(A, keep: list):
+    """A: object with nrows, ncols, rowptr, col, val (numpy)."""
+    rp = np.ascontiguousarray(A.rowptr, dtype=np.int64)
+    ci = np.ascontiguousarray(A.col, dtype=np.int64)
+    va = np.ascontiguousarray(A.val, dtype=np.float64)
+    keep += [rp, ci, va]
+    return _Csr(int(A.nrows), int(A.ncols), rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
+
+
+class _FactorView:
+    def __init__(self, A, fval):
+        self.nrows, self.ncols, self.rowptr, self.col = A.nrows, A.ncols, A.rowptr, A.col
+        self.val = np.ascontiguousarray(fval, dtype=np.float64)
+
+
+def ilu0(A, row_begin: int = 0) -> np.ndarray:
+    """Host ILU(0) values on A's pattern (nsm_ilu0; strict lower = L_s,
+    upper incl. diagonal = U)."""
+    L = load()
+    keep: list = []
+    cs = _csr_struct(A, keep)
+    out = np.empty(int(A.rowptr[-1]), dtype=np.float64)
+    st = L.nsm_ilu0(ctypes.byref(cs), int(row_begin), out.ctypes.data)
+    if st != 0:
+        raise NsmError(st, _err(None))
+    return out
+
+
+class Smoother:
+    """One nsm handle: the split storage of A (and optionally its ILU(0)
+    factors) resident on a CUDA device.  Vectors are float64 CUDA tensors of
+    length n_local; calls run on the current torch stream (or `stream`)."""
+
+    def __init__(self, A, F=None, *, device: int | None = None, rank: int = 0, nranks: int = 1,
+                 row_offsets=None, mode: int = NSM_DIST_HYBRID):
+        import torch  # plumbing: device selection and streams only
+        self._torch = torch
+        L = load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        keep: list = []
+        ca = _csr_struct(A, keep)
+        cf = None
+        if F is not None:
+            Fv = F if hasattr(F, "rowptr") else _FactorView(A, F)
+            cf = _csr_struct(Fv, keep)
+        dist = None
+        if nranks > 1:
+            ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+            keep.append(ro)
+            dist = _Dist(int(rank), int(nranks), ro.ctypes.data, int(mode))
+        h = ctypes.c_void_p()
+        st = L.nsm_setup(ctypes.byref(h), ctypes.byref(ca), ctypes.byref(cf) if cf is not None else None,
+                         ctypes.byref(dist) if dist is not None else None, self.device)
+        if st != 0:
+            raise NsmError(st, _err(None))
+        self._h = h
+        self.has_ilu = F is not None
+        n, ng, nnz, db = (ctypes.c_int64() for _ in range(4))
+        L.nsm_info(h, ctypes.byref(n), ctypes.byref(ng), ctypes.byref(nnz), ctypes.byref(db))
+        self.n, self.n_ghost, self.nnz_offdiag, self.device_bytes = n.value, ng.value, nnz.value, db.value
+
+    # -- marshalling helpers ------------------------------------------------
+    def _stream(self, stream):
+        if stream is None:
+            return self._torch.cuda.current_stream(self.device).cuda_stream
+        return getattr(stream, "cuda_stream", stream)
+
+    def _vec(self, t, name):
+        torch = self._torch
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+                and t.numel() == self.n and t.device.index == self.device):
+            raise TypeError(f"{name}: expected a contiguous float64 CUDA tensor of length {self.n} on cuda:{self.device}")
+        return t.data_ptr()
+
+    def _new(self):
+        return self._torch.empty(self.n, dtype=self._torch.float64, device=f"cuda:{self.device}")
+
+    def _call(self, st):
+        if st != 0:
+            raise NsmError(st, _err(self._h))
+
+    # -- the C-ABI entry points ----------------------------------------------
+    def residual(self, b, x, r=None, stream=None):
+        r = self._new() if r is None else r
+        self._call(load().nsm_residual(self._h, self._vec(b, "b"), self._vec(x, "x"), self._vec(r, "r"),
+                                       self._stream(stream)))
+        return r
+
+    def spmv(self, x, y=None, stream=None):
+        y = self._new() if y is None else y
+        self._call(load().nsm_spmv(self._h, self._vec(x, "x"), self._vec(y, "y"), self._stream(stream)))
+        return y
+
+    def lsolve(self, r, k, x=None, stream=None):
+        x = self._new() if x is None else x
+        self._call(load().nsm_lsolve(self._h, self._vec(r, "r"), self._vec(x, "x"), int(k), self._stream(stream)))
+        return x
+
+    def usolve(self, r, k, x=None, stream=None):
+        x = self._new() if x is None else x
+        self._call(load().nsm_usolve(self._h, self._vec(r, "r"), self._vec(x, "x"), int(k), self._stream(stream)))
+        return x
+
+    def smooth(self, b, x, kind="pgs", nu=1, k_l=2, k_u=None, x_is_zero=False, stream=None):
+        kd = {"pgs": NSM_PGS, "ilu": NSM_ILU0, "ilu0": NSM_ILU0}[kind] if isinstance(kind, str) else int(kind)
+        k_u = k_l if k_u is None else k_u
+        self._call(load().nsm_smooth(self._h, kd, self._vec(b, "b"), self._vec(x, "x"), int(nu), int(k_l), int(k_u),
+                                     int(bool(x_is_zero)), self._stream(stream)))
+        return x
+
+    def check(self, stream=None):
+        """Synchronises; returns None, or raises NsmError(NSM_ERR_NONFINITE)."""
+        bad = ctypes.c_int64()
+        self._call(load().nsm_check(self._h, ctypes.byref(bad), self._stream(stream)))
+        return None
+
+    def stats(self):
+        """(kernel launches, halo exchanges) since setup."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._call(load().nsm_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().nsm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,243 @@
+// builder.cpp — split-triangular storage builder.
+//
+// Splits a host CSR row block into the paper's A = L + D + U (P:L181-186,
+// P:L717-721) and packs each strict part as SELL-32 slices (nsm_internal.h).
+// Couplings to columns owned by other ranks go to separate ghost parts LG
+// (columns below the block) and UG (above), so that visiting LG, L, D, U, UG
+// in this order is still the ascending column order of the full row.
+// Also: nsm_ilu0's host ILU(0) factorisation (setup input).
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "nsm_internal.h"
+
+namespace nsm {
+
+namespace {
+
+enum Part { P_LG = 0, P_L = 1, P_D = 2, P_U = 3, P_UG = 4 };
+
+inline int classify(int64_t i_glob, int64_t c, int64_t rb, int64_t re) {
+    if (c < rb) return P_LG;
+    if (c >= re) return P_UG;
+    if (c < i_glob) return P_L;
+    if (c == i_glob) return P_D;
+    return P_U;
+}
+
+// Pack per-row entry lists into SELL-32.  cnt[i] = entries of row i in this
+// part; first[i] = index into the CSR arrays of the row's first such entry
+// (entries of one part are contiguous in a sorted row); colmap maps a CSR
+// column to the stored int32 index.
+template <class ColMap>
+void pack(int64_t n, const std::vector<int32_t> &cnt, const std::vector<int64_t> &first,
+          const int64_t *ci, const double *va, ColMap colmap, SellHost *out) {
+    int64_t ns = (n + kSlice - 1) / kSlice;
+    out->ptr.assign(ns + 1, 0);
+    std::vector<int32_t> w(ns, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < ns; ++s) {
+        int32_t m = 0;
+        for (int64_t i = s * kSlice; i < std::min(n, (s + 1) * kSlice); ++i) m = std::max(m, cnt[i]);
+        w[s] = m;
+    }
+    int32_t maxw = 0;
+    int64_t nnz = 0;
+    for (int64_t s = 0; s < ns; ++s) {
+        out->ptr[s + 1] = out->ptr[s] + (int64_t)w[s] * kSlice;
+        maxw = std::max(maxw, w[s]);
+    }
+    for (int64_t i = 0; i < n; ++i) nnz += cnt[i];
+    out->maxw = maxw;
+    out->nnz = nnz;
+    int64_t tot = out->ptr[ns];
+    out->col.assign(tot, 0);
+    out->val.assign(tot, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < ns; ++s) {
+        int64_t base = out->ptr[s];
+        for (int l = 0; l < kSlice; ++l) {
+            int64_t i = s * kSlice + l;
+            int32_t c = i < n ? cnt[i] : 0;
+            // padding column: the row itself (local) or 0 (ghost parts): any
+            // valid address, multiplied by 0.0
+            int32_t pad = colmap.pad(i < n ? i : 0);
+            for (int32_t j = 0; j < w[s]; ++j) {
+                int64_t e = base + (int64_t)j * kSlice + l;
+                if (j < c) {
+                    int64_t src = first[i] + j;
+                    out->col[e] = colmap(ci[src]);
+                    out->val[e] = va[src];
+                } else {
+                    out->col[e] = pad;
+                    out->val[e] = 0.0;
+                }
+            }
+        }
+    }
+}
+
+struct LocalMap {
+    int64_t rb;
+    int32_t operator()(int64_t c) const { return (int32_t)(c - rb); }
+    int32_t pad(int64_t i) const { return (int32_t)i; }
+};
+struct GhostMap {
+    const std::vector<int64_t> *gid;
+    int32_t operator()(int64_t c) const {
+        return (int32_t)(std::lower_bound(gid->begin(), gid->end(), c) - gid->begin());
+    }
+    int32_t pad(int64_t) const { return 0; }
+};
+
+}  // namespace
+
+nsm_status build_split(const nsm_csr *A, int64_t rb, int64_t re, Split *out, std::string *err) {
+    const int64_t n = A->nrows;
+    const int64_t *rp = A->rowptr;
+    const int64_t *ci = A->colind;
+    const double *va = A->val;
+    if (n != re - rb || n < 0 || !rp || (rp[n] > 0 && (!ci || !va))) {
+        *err = "nsm_setup: inconsistent CSR arguments";
+        return NSM_ERR_ARG;
+    }
+    if (n >= (int64_t)1 << 31 || A->ncols >= (int64_t)1 << 31) {
+        *err = "nsm_setup: more than 2^31-1 rows/columns per rank is not supported (int32 device indices)";
+        return NSM_ERR_ARG;
+    }
+    if (rp[0] != 0) { *err = "nsm_setup: rowptr[0] != 0"; return NSM_ERR_PATTERN; }
+    // ---- validate (P:L717-721 needs a nonzero diagonal; S:L24-27 invariants)
+    int bad_kind = 0;  // 1 pattern, 2 diagonal
+#pragma omp parallel for schedule(static) reduction(max : bad_kind)
+    for (int64_t i = 0; i < n; ++i) {
+        int kind = 0;
+        if (rp[i + 1] < rp[i]) kind = 1;
+        else {
+            bool has_d = false;
+            for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+                int64_t c = ci[p];
+                if (c < 0 || c >= A->ncols || (p > rp[i] && ci[p - 1] >= c)) { kind = 1; break; }
+                if (c == rb + i) has_d = va[p] != 0.0 && std::isfinite(va[p]);
+            }
+            if (!kind && !has_d) kind = 2;
+        }
+        bad_kind = std::max(bad_kind, kind);
+    }
+    if (bad_kind) {
+        // report the first offending row deterministically
+        for (int64_t i = 0; i < n; ++i) {
+            bool pat = rp[i + 1] < rp[i], has_d = false;
+            for (int64_t p = rp[i]; !pat && p < rp[i + 1]; ++p) {
+                int64_t c = ci[p];
+                if (c < 0 || c >= A->ncols || (p > rp[i] && ci[p - 1] >= c)) pat = true;
+                else if (c == rb + i) has_d = va[p] != 0.0 && std::isfinite(va[p]);
+            }
+            if (pat) {
+                *err = "nsm_setup: CSR pattern invariant violated at global row " + std::to_string(rb + i);
+                return NSM_ERR_PATTERN;
+            }
+            if (!has_d) {
+                *err = "nsm_setup: missing or zero diagonal at global row " + std::to_string(rb + i);
+                return NSM_ERR_ZERO_DIAG;
+            }
+        }
+    }
+    // ---- per-row part counts
+    std::vector<int32_t> cnt[5];
+    std::vector<int64_t> first[5];
+    for (int k = 0; k < 5; ++k) { cnt[k].assign(n, 0); first[k].assign(n, 0); }
+    out->d.assign(n, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        for (int k = 0; k < 5; ++k) first[k][i] = rp[i];
+        int prev = -1;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            int k = classify(rb + i, ci[p], rb, re);
+            if (k != prev) { first[k][i] = p; prev = k; }
+            cnt[k][i]++;
+            if (k == P_D) out->d[i] = va[p];
+        }
+    }
+    // ---- ghost columns (ascending global ids)
+    std::vector<int64_t> &g = out->ghost_gid;
+    g.clear();
+    for (int64_t i = 0; i < n; ++i) {
+        for (int k : {P_LG, P_UG})
+            for (int32_t j = 0; j < cnt[k][i]; ++j) g.push_back(ci[first[k][i] + j]);
+    }
+    std::sort(g.begin(), g.end());
+    g.erase(std::unique(g.begin(), g.end()), g.end());
+    out->n = n;
+    out->row_begin = rb;
+    out->n_ghost = (int64_t)g.size();
+    LocalMap lm{rb};
+    GhostMap gm{&g};
+    pack(n, cnt[P_L], first[P_L], ci, va, lm, &out->L);
+    pack(n, cnt[P_U], first[P_U], ci, va, lm, &out->U);
+    pack(n, cnt[P_LG], first[P_LG], ci, va, gm, &out->LG);
+    pack(n, cnt[P_UG], first[P_UG], ci, va, gm, &out->UG);
+    out->nnz_off = out->L.nnz + out->U.nnz + out->LG.nnz + out->UG.nnz;
+    return NSM_OK;
+}
+
+// ILU(0) on the pattern of A (IKJ, no pivoting, the building
+// block of P:L945 / P:L1409-1421).  Row i is eliminated with the already
+// factored rows k < i in ascending k; the update of entry (i, j) by row k is
+// found by merging the sorted column lists of rows i and k (entries outside
+// the pattern are dropped: zero fill).  With row_begin the block is the
+// diagonal block of a row partition: columns outside [row_begin, row_begin+n)
+// are not eliminated and get the value 0.
+nsm_status ilu0_host(const nsm_csr *A, int64_t rb, double *fval, std::string *err) {
+    const int64_t n = A->nrows;
+    const int64_t *rp = A->rowptr;
+    const int64_t *ci = A->colind;
+    const double *va = A->val;
+    if (!rp || !fval || n < 0 || (rp[n] > 0 && (!ci || !va))) { *err = "nsm_ilu0: bad argument"; return NSM_ERR_ARG; }
+    const int64_t re = rb + n;
+    std::vector<int64_t> dpos(n, -1);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            if (ci[p] == rb + i) dpos[i] = p;
+            bool inblock = ci[p] >= rb && ci[p] < re;
+            fval[p] = inblock ? va[p] : 0.0;
+        }
+        if (dpos[i] < 0) {
+            *err = "nsm_ilu0: missing diagonal at global row " + std::to_string(rb + i);
+            return NSM_ERR_ZERO_DIAG;
+        }
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t gi = rb + i;
+        for (int64_t p = rp[i]; p < rp[i + 1] && ci[p] < gi; ++p) {
+            if (ci[p] < rb) continue;  // other rank's column: not part of A_pp
+            const int64_t k = ci[p] - rb;
+            const double ukk = fval[dpos[k]];
+            if (ukk == 0.0) {
+                *err = "nsm_ilu0: zero pivot at global row " + std::to_string(rb + k);
+                return NSM_ERR_ZERO_DIAG;
+            }
+            const double lik = fval[p] / ukk;
+            fval[p] = lik;
+            // merge row k (columns > k) with row i (columns > ci[p])
+            int64_t q = dpos[k] + 1, t = p + 1;
+            const int64_t qe = rp[k + 1], te = rp[i + 1];
+            while (q < qe && t < te) {
+                const int64_t cq = ci[q], ct = ci[t];
+                if (cq >= re) break;
+                if (cq < ct) ++q;
+                else if (ct < cq) ++t;
+                else { fval[t] = fval[t] - lik * fval[q]; ++q; ++t; }
+            }
+        }
+        if (fval[dpos[i]] == 0.0) {
+            *err = "nsm_ilu0: zero pivot at global row " + std::to_string(gi);
+            return NSM_ERR_ZERO_DIAG;
+        }
+    }
+    return NSM_OK;
+}
+
+}  // namespace nsm

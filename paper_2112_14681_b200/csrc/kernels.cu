@@ -1,0 +1,224 @@
+// kernels.cu — sm_100a kernels of the Neumann-series smoothers
+// (DESIGN.md §6 "Kernels").
+//
+// The hot path is a streaming sparse gather-reduce in fp64 (≈0.17 flop/B): it
+// is HBM-bound, so there is no tensor-core work (tcgen05/TMEM do not apply).
+// What matters is moving the SELL-32 value/index streams at full HBM
+// bandwidth (coalesced 256 B / 128 B warp loads, no L1 allocation, L2
+// evict-first), keeping the small gathered vectors (x, r, g, d) in L1/L2, and
+// enough independent loads in flight per thread.
+//
+// Numerics: one thread owns one row and accumulates its sum sequentially in
+// ascending column order with explicit round-to-nearest multiply and add
+// (no FMA contraction), and D^{-1} is an IEEE division — the exact rounding
+// sequence of the oracle (reading R10), so GPU and oracle agree
+// bit for bit on the same inputs.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nsm_internal.h"
+
+namespace nsm {
+
+namespace {
+
+constexpr int kThreads = 256;                 // 8 warps = 8 slices per CTA
+constexpr int kSlicesPerCta = kThreads / kSlice;
+
+// ---- memory access helpers -------------------------------------------------
+// Matrix streams are read exactly once per pass: no L1 allocation, and mark
+// them evict-first in L2 so they do not push out the gathered vectors.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_stream(const double *a, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t *a, uint64_t pol) {
+    int32_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
+// Gather source of a sweep: either a stored iterate g[c], or (for the first
+// sweep, eq:jr-initial-guess g^(0) = D^{-1} r) the scaled right-hand side
+// rhs[c] / d[c] recomputed on the fly, which saves writing and re-reading g^(0).
+struct GatherPlain {
+    const double *__restrict__ g;
+    __device__ __forceinline__ double operator()(int32_t c) const { return __ldg(g + c); }
+};
+struct GatherScaled {
+    const double *__restrict__ rhs;
+    const double *__restrict__ d;
+    __device__ __forceinline__ double operator()(int32_t c) const { return __ddiv_rn(__ldg(rhs + c), __ldg(d + c)); }
+};
+
+// acc += sum over the slice-s entries of this lane's row, in stored order
+// (= ascending columns).  Entries past the row's length are padding (val 0).
+template <class G>
+__device__ __forceinline__ double accum(const SellView P, int64_t s, int lane, const G &gather, double acc,
+                                        uint64_t pol) {
+    const int64_t b = __ldg(P.ptr + s) + lane, e = __ldg(P.ptr + s + 1);
+#pragma unroll 4
+    for (int64_t p = b; p < e; p += kSlice) {
+        const double v = ld_stream(P.val + p, pol);
+        const int32_t c = ld_stream(P.col + p, pol);
+        acc = __dadd_rn(acc, __dmul_rn(v, gather(c)));
+    }
+    return acc;
+}
+
+__device__ __forceinline__ void flag_nonfinite(double v, unsigned long long *flag, int64_t sweep_id) {
+    if (!isfinite(v)) atomicMin(flag, (unsigned long long)sweep_id);
+}
+
+__device__ __forceinline__ bool slice_of(int nslices, const int32_t *list, int64_t *s, int *lane) {
+    const int64_t w = (int64_t)blockIdx.x * kSlicesPerCta + (threadIdx.x >> 5);
+    if (w >= nslices) return false;
+    *s = list ? (int64_t)list[w] : w;
+    *lane = threadIdx.x & 31;
+    return true;
+}
+
+// ---- residual / SpMV (row a2) ------------------------------------------------
+// acc_i = sum_{j ascending} a_ij x_j over LG (ghosts below), L, D, U, UG
+// (ghosts above); then  OUT_R: r = b - acc;  OUT_AX: y = acc.
+enum { OUT_R = 0, OUT_AX = 1 };
+
+template <int OUT>
+__global__ void __launch_bounds__(kThreads) k_residual(int64_t n, int nslices, const int32_t *__restrict__ list,
+                                                       SellView LG, SellView L, SellView U, SellView UG, int has_ghost,
+                                                       const double *__restrict__ d, const double *__restrict__ b,
+                                                       const double *__restrict__ x, const double *__restrict__ ghost,
+                                                       double *__restrict__ out) {
+    int64_t s;
+    int lane;
+    if (!slice_of(nslices, list, &s, &lane)) return;
+    const uint64_t pol = policy_evict_first();
+    const int64_t i = s * kSlice + lane;
+    const GatherPlain gx{x};
+    double acc = 0.0;
+    if (has_ghost) acc = accum(LG, s, lane, GatherPlain{ghost}, acc, pol);
+    acc = accum(L, s, lane, gx, acc, pol);
+    if (i < n) acc = __dadd_rn(acc, __dmul_rn(__ldg(d + i), __ldg(x + i)));
+    acc = accum(U, s, lane, gx, acc, pol);
+    if (has_ghost) acc = accum(UG, s, lane, GatherPlain{ghost}, acc, pol);
+    if (i < n) out[i] = OUT == OUT_R ? __dsub_rn(__ldg(b + i), acc) : acc;
+}
+
+// ---- inner Jacobi sweep (rows a3, a4, a5) -----------------------------------
+//   v_i = (rhs_i - sum_{j in T(i)} t_ij gin_j) / dT_i      (UNIT: no division)
+// eq:jacobi for pGS (T = L, dT = D); the unit-lower ILU factor
+// (G_L = I - L) and the row-scaled U factor (G_U = I - D_U^{-1}U,
+// P:L829) with the same kernel.  Epilogues:
+//   EPI_STORE      gout_i = v
+//   EPI_XADD       x_i += v                     (last sweep)
+//   EPI_STORE2     gout_i = v ; gout2_i = v / dnext_i   (last L sweep of ILU:
+//                  y and the U-solve start z^(0) = D_U^{-1} y in one pass)
+//   EPI_XADD_SCALE x_i += v / dnext_i            (ILU with k_u = 0)
+
+template <bool UNIT, int EPI, class G>
+__global__ void __launch_bounds__(kThreads) k_sweep(int64_t n, int nslices, const int32_t *__restrict__ list,
+                                                    SellView T, SellView TG, int has_ghost,
+                                                    const double *__restrict__ dT, const double *__restrict__ rhs,
+                                                    G gin, const double *__restrict__ ghost,
+                                                    double *__restrict__ gout, double *__restrict__ x,
+                                                    const double *__restrict__ dnext, double *__restrict__ gout2,
+                                                    unsigned long long *flag, int64_t sweep_id) {
+    int64_t s;
+    int lane;
+    if (!slice_of(nslices, list, &s, &lane)) return;
+    const uint64_t pol = policy_evict_first();
+    const int64_t i = s * kSlice + lane;
+    double acc = 0.0;
+    if (has_ghost) acc = accum(TG, s, lane, GatherPlain{ghost}, acc, pol);
+    acc = accum(T, s, lane, gin, acc, pol);
+    if (i >= n) return;
+    double v = __dsub_rn(__ldg(rhs + i), acc);
+    if (!UNIT) v = __ddiv_rn(v, __ldg(dT + i));
+    flag_nonfinite(v, flag, sweep_id);
+    if (EPI == EPI_STORE) gout[i] = v;
+    if (EPI == EPI_XADD) x[i] = __dadd_rn(x[i], v);
+    if (EPI == EPI_STORE2) { gout[i] = v; gout2[i] = __ddiv_rn(v, __ldg(dnext + i)); }
+    if (EPI == EPI_XADD_SCALE) x[i] = __dadd_rn(x[i], __ddiv_rn(v, __ldg(dnext + i)));
+}
+
+// ---- diagonal scaling:  out = rhs / d  or  x += rhs / d  (k = 0 cases) -------
+template <bool XADD>
+__global__ void __launch_bounds__(kThreads) k_scale(int64_t n, const double *__restrict__ rhs,
+                                                    const double *__restrict__ d, double *__restrict__ out,
+                                                    unsigned long long *flag, int64_t sweep_id) {
+    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (i >= n) return;
+    const double v = d ? __ddiv_rn(__ldg(rhs + i), __ldg(d + i)) : __ldg(rhs + i);
+    flag_nonfinite(v, flag, sweep_id);
+    out[i] = XADD ? __dadd_rn(out[i], v) : v;
+}
+
+inline unsigned grid_for(int nslices) { return (unsigned)((nslices + kSlicesPerCta - 1) / kSlicesPerCta); }
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers --
+cudaError_t launch_residual(bool spmv, int64_t n, int nslices, const int32_t *list, const Sell &LG, const Sell &L,
+                            const Sell &U, const Sell &UG, bool has_ghost, const double *d, const double *b,
+                            const double *x, const double *ghost, double *out, cudaStream_t st) {
+    if (nslices <= 0) return cudaSuccess;
+    if (spmv)
+        k_residual<OUT_AX><<<grid_for(nslices), kThreads, 0, st>>>(n, nslices, list, view(LG), view(L), view(U),
+                                                                   view(UG), has_ghost, d, b, x, ghost, out);
+    else
+        k_residual<OUT_R><<<grid_for(nslices), kThreads, 0, st>>>(n, nslices, list, view(LG), view(L), view(U),
+                                                                  view(UG), has_ghost, d, b, x, ghost, out);
+    return cudaGetLastError();
+}
+
+template <bool UNIT, int EPI>
+static cudaError_t sweep_epi(const SweepArgs &a, cudaStream_t st) {
+    dim3 g(grid_for(a.nslices));
+    SellView TG = a.TG ? view(*a.TG) : SellView{nullptr, nullptr, nullptr};
+    if (a.gin_scaled && !UNIT)
+        k_sweep<UNIT, EPI, GatherScaled><<<g, kThreads, 0, st>>>(a.n, a.nslices, a.list, view(*a.T), TG,
+                                                                 a.has_ghost, a.dT, a.rhs, GatherScaled{a.rhs, a.dT},
+                                                                 a.ghost, a.gout, a.x, a.dnext, a.gout2, a.flag,
+                                                                 a.sweep_id);
+    else
+        k_sweep<UNIT, EPI, GatherPlain><<<g, kThreads, 0, st>>>(a.n, a.nslices, a.list, view(*a.T), TG,
+                                                                a.has_ghost, a.dT, a.rhs,
+                                                                GatherPlain{a.gin_scaled ? a.rhs : a.gin}, a.ghost,
+                                                                a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t st) {
+    if (a.nslices <= 0) return cudaSuccess;
+    if (a.unit) {
+        switch (a.epi) {
+            case EPI_STORE: return sweep_epi<true, EPI_STORE>(a, st);
+            case EPI_XADD: return sweep_epi<true, EPI_XADD>(a, st);
+            case EPI_STORE2: return sweep_epi<true, EPI_STORE2>(a, st);
+            default: return sweep_epi<true, EPI_XADD_SCALE>(a, st);
+        }
+    }
+    switch (a.epi) {
+        case EPI_STORE: return sweep_epi<false, EPI_STORE>(a, st);
+        case EPI_XADD: return sweep_epi<false, EPI_XADD>(a, st);
+        case EPI_STORE2: return sweep_epi<false, EPI_STORE2>(a, st);
+        default: return sweep_epi<false, EPI_XADD_SCALE>(a, st);
+    }
+}
+
+cudaError_t launch_scale(bool xadd, int64_t n, const double *rhs, const double *d, double *out,
+                         unsigned long long *flag, int64_t sweep_id, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    unsigned g = (unsigned)((n + kThreads - 1) / kThreads);
+    if (xadd) k_scale<true><<<g, kThreads, 0, st>>>(n, rhs, d, out, flag, sweep_id);
+    else k_scale<false><<<g, kThreads, 0, st>>>(n, rhs, d, out, flag, sweep_id);
+    return cudaGetLastError();
+}
+
+}  // namespace nsm

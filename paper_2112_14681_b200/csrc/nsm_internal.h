@@ -1,0 +1,97 @@
+// nsm_internal.h — device data layout shared by the builder, the kernels and
+// the C-ABI glue of libnsm.so (DESIGN.md §5 "Data layout in HBM").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nsm.h"
+
+namespace nsm {
+
+constexpr int kSlice = 32;  // SELL-C slice height = warp width: one thread per row
+
+// One strictly-triangular (or ghost) part in SELL-32 form (σ = 1: rows keep
+// their order).  Slice s holds rows [32 s, 32 s + 32); its entries occupy
+// [ptr[s], ptr[s+1]) laid out column-major: entry j of lane l at
+// ptr[s] + 32 j + l.  Width w_s = (ptr[s+1]-ptr[s]) / 32 = longest row of
+// the slice; shorter rows are padded with val = 0 and col = a valid index.
+// Within a row the entries are in ascending column order.
+struct Sell {
+    int64_t *ptr = nullptr;   // device, nslices + 1
+    int32_t *col = nullptr;   // device, padded entries
+    double *val = nullptr;    // device, padded entries
+    int64_t padded = 0;       // stored entries incl. padding
+    int64_t nnz = 0;          // real entries
+    int32_t maxw = 0;         // widest slice
+    bool empty() const { return padded == 0; }
+};
+
+// Host-side staging of a Sell before upload.
+struct SellHost {
+    std::vector<int64_t> ptr;
+    std::vector<int32_t> col;
+    std::vector<double> val;
+    int64_t nnz = 0;
+    int32_t maxw = 0;
+};
+
+// What the kernels need of one part: raw pointers (kernel argument).
+struct SellView {
+    const int64_t *ptr;
+    const int32_t *col;
+    const double *val;
+};
+
+inline SellView view(const Sell &s) { return SellView{s.ptr, s.col, s.val}; }
+
+// Result of splitting a CSR row block (builder.cpp).
+struct Split {
+    int64_t n = 0, row_begin = 0, n_ghost = 0;
+    std::vector<double> d;            // diagonal of A (or of U for factors)
+    SellHost L, U;                    // strict lower / upper, LOCAL columns
+    SellHost LG, UG;                  // couplings to ghost columns below / above the block
+    std::vector<int64_t> ghost_gid;   // global id of ghost k (ascending)
+    int64_t nnz_off = 0;
+};
+
+// Builds the SELL split of rows [row_begin, row_begin + n) of A.
+//   unit_lower: the strictly-lower part belongs to a unit-lower factor (the
+//               stored diagonal is the U factor's; used for ILU factors).
+// Returns NSM_OK or an error with a message.
+nsm_status build_split(const nsm_csr *A, int64_t row_begin, int64_t row_end, Split *out, std::string *err);
+
+// ---- kernel launchers (kernels.cu) ------------------------------------------
+// Sweep epilogues (see k_sweep in kernels.cu).
+enum { EPI_STORE = 0, EPI_XADD = 1, EPI_STORE2 = 2, EPI_XADD_SCALE = 3 };
+
+struct SweepArgs {
+    int64_t n;
+    int nslices;
+    const int32_t *list;     // slice list or nullptr (= all slices 0..nslices-1)
+    const Sell *T, *TG;      // local strict triangle, ghost part (or nullptr)
+    bool has_ghost;
+    bool unit;               // unit diagonal: no division
+    int epi;
+    bool gin_scaled;         // gather rhs[c]/dT[c] instead of gin[c] (first sweep)
+    const double *dT, *rhs, *gin, *ghost;
+    double *gout, *x;
+    const double *dnext;
+    double *gout2;
+    unsigned long long *flag;
+    int64_t sweep_id;
+};
+
+cudaError_t launch_residual(bool spmv, int64_t n, int nslices, const int32_t *list, const Sell &LG, const Sell &L,
+                            const Sell &U, const Sell &UG, bool has_ghost, const double *d, const double *b,
+                            const double *x, const double *ghost, double *out, cudaStream_t st);
+cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t st);
+cudaError_t launch_scale(bool xadd, int64_t n, const double *rhs, const double *d, double *out,
+                         unsigned long long *flag, int64_t sweep_id, cudaStream_t st);
+
+// Host ILU(0) (nsm_ilu0).
+nsm_status ilu0_host(const nsm_csr *A, int64_t row_begin, double *fval, std::string *err);
+
+}  // namespace nsm

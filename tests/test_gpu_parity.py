@@ -1,0 +1,211 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle on the same
+seeded inputs (-m gpu).
+
+Bar (BASELINE.json north_star): normwise relative error <= 1e-12 per smoother
+application.  Because the kernels reproduce the oracle's rounding sequence
+(per-row ascending sums, no FMA, IEEE division — DESIGN.md R10), the tests
+also assert bit-for-bit equality; the 1e-12 check is the contract, the
+bitwise check guards the design claim.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+import inputs
+import oracle
+import paper_2112_14681_b200 as nsm
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def relerr(got, want):
+    nw = np.linalg.norm(want)
+    return np.linalg.norm(got - want) / (nw if nw > 0 else 1.0)
+
+
+def agree(got, want, what=""):
+    e = relerr(got, want)
+    assert e <= TOL, f"{what}: relerr {e:.3e}"
+    nbad = int(np.sum(got != want))
+    assert nbad == 0, f"{what}: {nbad} of {len(want)} entries differ (relerr {e:.2e})"
+
+
+def random_sparse(n, seed, avg=9, maxrow=70):
+    """Irregular rows (lengths 1 .. maxrow): exercises SELL padding."""
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for i in range(n):
+        m = int(min(maxrow, rng.geometric(1.0 / avg)))
+        c = rng.choice(n, size=min(m, n), replace=False)
+        rows += [i] * len(c)
+        cols += list(c)
+    M = sp.csr_matrix((rng.uniform(-1, 1, len(rows)), (rows, cols)), shape=(n, n))
+    M = M + sp.diags(np.abs(M).sum(1).A1 + 1.0)
+    return inputs.CSR.from_scipy(M)
+
+
+SMALL = {
+    "C1": lambda: inputs.config_matrix("C1"),
+    "lap3d_ragged": lambda: inputs.laplace(13, 11, 7),           # n = 1001
+    "var27_9": lambda: inputs.var27(9),
+    "cd_rcm_10": lambda: inputs.convdiff(10),
+    "random_irregular": lambda: random_sparse(997, 5),
+}
+
+
+@pytest.fixture(scope="module", params=list(SMALL))
+def case(request):
+    A = SMALL[request.param]()
+    F = oracle.ilu0(A)[2]
+    S = nsm.Smoother(A, F)
+    yield request.param, A, F, S
+    S.close()
+
+
+def test_residual_spmv(case):
+    name, A, F, S = case
+    b, x = inputs.uniform(0, A.nrows), inputs.uniform(1, A.nrows)
+    agree(host(S.residual(dev(b), dev(x))), oracle.residual(A, b, x), name + " residual")
+    agree(host(S.spmv(dev(x))), oracle.spmv(A, x), name + " spmv")
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 7])
+def test_tri_solves(case, k):
+    name, A, F, S = case
+    r = inputs.uniform(3, A.nrows)
+    # handle with factors: lsolve/usolve act on the ILU factors
+    Ff = (A.rowptr, A.col, F)
+    Fs = sp.csr_matrix((F, A.col, A.rowptr), shape=(A.nrows, A.nrows))
+    agree(host(S.lsolve(dev(r), k)), oracle.tri_jacobi(Fs, r, k, lower=True, unit=True), f"{name} ilu lsolve k={k}")
+    agree(host(S.usolve(dev(r), k)), oracle.tri_jacobi(Fs, r, k, lower=False), f"{name} ilu usolve k={k}")
+    del Ff
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_pgs_tri_solves(k):
+    A = inputs.var27(7)
+    with nsm.Smoother(A) as S:
+        r = inputs.uniform(3, A.nrows)
+        agree(host(S.lsolve(dev(r), k)), oracle.tri_jacobi(A, r, k, lower=True), f"pgs lsolve k={k}")
+        agree(host(S.usolve(dev(r), k)), oracle.tri_jacobi(A, r, k, lower=False), f"pgs usolve k={k}")
+
+
+@pytest.mark.parametrize("k,nu,xz", [(0, 1, False), (1, 1, False), (2, 1, False), (3, 1, False), (2, 3, False),
+                                     (0, 2, True), (2, 1, True), (3, 2, True)])
+def test_pgs_smooth(case, k, nu, xz):
+    name, A, F, S = case
+    b = inputs.uniform(0, A.nrows)
+    x0 = np.zeros(A.nrows) if xz else inputs.uniform(1, A.nrows)
+    x = dev(x0)
+    S.smooth(dev(b), x, "pgs", nu=nu, k_l=k, x_is_zero=xz)
+    agree(host(x), oracle.pgs_apply(A, b, x0, k, nu=nu, x_is_zero=xz), f"{name} pgs k={k} nu={nu} xz={xz}")
+
+
+@pytest.mark.parametrize("kl,ku,nu,xz", [(2, 2, 1, False), (0, 0, 1, False), (0, 2, 1, False), (2, 0, 1, False),
+                                         (3, 1, 2, False), (1, 3, 1, True), (0, 0, 2, True), (10, 10, 1, False)])
+def test_ilu_smooth(case, kl, ku, nu, xz):
+    name, A, F, S = case
+    b = inputs.uniform(0, A.nrows)
+    x0 = np.zeros(A.nrows) if xz else inputs.uniform(1, A.nrows)
+    x = dev(x0)
+    S.smooth(dev(b), x, "ilu", nu=nu, k_l=kl, k_u=ku, x_is_zero=xz)
+    want = oracle.ilu_apply(A, (A.rowptr, A.col, F), b, x0, kl, ku, nu=nu, x_is_zero=xz)
+    agree(host(x), want, f"{name} ilu kl={kl} ku={ku} nu={nu} xz={xz}")
+
+
+def test_config1_integer_bitwise():
+    """C1 with integer b, x = 0: the oracle is exact (pinned against integer
+    arithmetic in test_oracle_pins); the GPU must be bit-identical."""
+    A = inputs.config_matrix("C1")
+    b = inputs.uniform_int(0, A.nrows, 20)
+    with nsm.Smoother(A) as S:
+        for k in (1, 2, 3):
+            x = torch.zeros(A.nrows, dtype=torch.float64, device="cuda")
+            S.smooth(dev(b), x, "pgs", k_l=k, x_is_zero=True)
+            assert np.array_equal(host(x), oracle.pgs_apply(A, b, np.zeros(A.nrows), k, x_is_zero=True))
+
+
+def test_edge_sizes():
+    # n = 1, diagonal matrix (empty triangles), a row longer than a warp
+    for A in [inputs.CSR.from_scipy(sp.csr_matrix(np.array([[4.0]]))),
+              inputs.CSR.from_scipy(sp.diags(np.arange(1.0, 40.0)).tocsr()),
+              inputs.random_dense(40, seed=2, diag_shift=30.0)]:
+        b, x0 = inputs.uniform(0, A.nrows), inputs.uniform(1, A.nrows)
+        with nsm.Smoother(A, oracle.ilu0(A)[2]) as S:
+            x = dev(x0)
+            S.smooth(dev(b), x, "pgs", k_l=3)
+            agree(host(x), oracle.pgs_apply(A, b, x0, 3), f"edge n={A.nrows}")
+            x = dev(x0)
+            S.smooth(dev(b), x, "ilu", k_l=2, k_u=2)
+            agree(host(x), oracle.ilu_apply(A, oracle.ilu0(A), b, x0, 2, 2), f"edge ilu n={A.nrows}")
+
+
+def test_empty_matrix():
+    A = inputs.CSR(0, 0, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    with nsm.Smoother(A) as S:
+        e = torch.zeros(0, dtype=torch.float64, device="cuda")
+        S.smooth(e, torch.zeros(0, dtype=torch.float64, device="cuda"), "pgs", k_l=2)
+        S.check()
+
+
+def test_divergence_flag():
+    """Jacobi on a highly non-normal triangle may diverge: a
+    non-finite sweep output is reported by nsm_check with its sweep index."""
+    n = 64
+    M = sp.diags([np.full(n - 1, -1e300), np.full(n, 1e-10)], [-1, 0]).tocsr()
+    A = inputs.CSR.from_scipy(M)
+    with nsm.Smoother(A) as S:
+        S.lsolve(dev(np.ones(n)), 3)
+        with pytest.raises(nsm.NsmError) as e:
+            S.check()
+        assert e.value.name == "NSM_ERR_NONFINITE"
+        S.check()  # flag is cleared
+
+
+def test_errors_and_determinism():
+    A = inputs.laplace(9, 9, 9)
+    b = dev(inputs.uniform(0, A.nrows))
+    with nsm.Smoother(A) as S:
+        with pytest.raises(nsm.NsmError) as e:
+            S.smooth(b, dev(np.zeros(A.nrows)), "ilu", k_l=1)
+        assert e.value.name == "NSM_ERR_STATE"
+        with pytest.raises(nsm.NsmError) as e:
+            S.smooth(b, b, "pgs", k_l=1)
+        assert e.value.name == "NSM_ERR_ARG"
+        x1, x2 = dev(np.zeros(A.nrows)), dev(np.zeros(A.nrows))
+        S.smooth(b, x1, "pgs", nu=2, k_l=3)
+        S.smooth(b, x2, "pgs", nu=2, k_l=3)
+        assert torch.equal(x1, x2)
+
+
+# ------------------------------------------------------- full BASELINE sizes --
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+def test_full_size_parity(cfg):
+    """BASELINE.json configs at full size, in the launch configuration bench.py
+    times (one nsm_smooth per application); the oracle computes the whole
+    vector (a few seconds of CPU)."""
+    A = inputs.config_matrix(cfg)
+    kind = {"C2": "ilu", "C3": "pgs", "C4": "ilu", "C5": "pgs"}[cfg]
+    F = oracle.ilu0(A)[2] if kind == "ilu" else None
+    b, x0 = inputs.uniform(0, A.nrows), inputs.uniform(1, A.nrows)
+    with nsm.Smoother(A, F) as S:
+        x = dev(x0)
+        S.smooth(dev(b), x, kind, nu=1, k_l=2, k_u=2)
+        got = host(x)
+    if kind == "ilu":
+        want = oracle.ilu_apply(A, (A.rowptr, A.col, F), b, x0, 2, 2)
+    else:
+        want = oracle.pgs_apply(A, b, x0, 2)
+    agree(got, want, cfg)
