@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "nsm_internal.h"
 
 namespace nsm {
@@ -72,6 +74,49 @@ __device__ __forceinline__ double accum(const SellView P, int64_t s, int lane, c
     return acc;
 }
 
+// Register-blocked form of accum for the hot loops: the first CH entries of
+// the row are loaded by CH independent, predicated loads issued back to back
+// (memory-level parallelism: all value/index requests of a row are in
+// flight together), multiplied by their gathered operands as they arrive,
+// then summed in stored order.  Entries beyond CH (rows wider than the
+// chunk) continue with the plain loop, so the summation order is unchanged.
+template <int CH>
+struct Chunk {
+    double v[CH];
+    int32_t c[CH];
+    int w;
+    int64_t base;
+    __device__ __forceinline__ void load(const SellView P, int64_t s, int lane, uint64_t pol) {
+        const int64_t b = __ldg(P.ptr + s), e = __ldg(P.ptr + s + 1);
+        w = (int)((e - b) / kSlice);
+        base = b + lane;
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+            if (j < w) {
+                v[j] = ld_stream(P.val + base + (int64_t)j * kSlice, pol);
+                c[j] = ld_stream(P.col + base + (int64_t)j * kSlice, pol);
+            }
+        }
+    }
+    template <class G>
+    __device__ __forceinline__ void gather_mul(const G &g) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) v[j] = __dmul_rn(v[j], g(c[j]));
+    }
+    template <class G>
+    __device__ __forceinline__ double add(double acc, const SellView P, const G &g, uint64_t pol) const {
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) acc = __dadd_rn(acc, v[j]);
+        for (int j = CH; j < w; ++j) {
+            const int64_t p = base + (int64_t)j * kSlice;
+            acc = __dadd_rn(acc, __dmul_rn(ld_stream(P.val + p, pol), g(ld_stream(P.col + p, pol))));
+        }
+        return acc;
+    }
+};
+
 __device__ __forceinline__ void flag_nonfinite(double v, unsigned long long *flag, int64_t sweep_id) {
     if (!isfinite(v)) atomicMin(flag, (unsigned long long)sweep_id);
 }
@@ -89,7 +134,7 @@ __device__ __forceinline__ bool slice_of(int nslices, const int32_t *list, int64
 // (ghosts above); then  OUT_R: r = b - acc;  OUT_AX: y = acc.
 enum { OUT_R = 0, OUT_AX = 1 };
 
-template <int OUT>
+template <int OUT, int CH>
 __global__ void __launch_bounds__(kThreads) k_residual(int64_t n, int nslices, const int32_t *__restrict__ list,
                                                        SellView LG, SellView L, SellView U, SellView UG, int has_ghost,
                                                        const double *__restrict__ d, const double *__restrict__ b,
@@ -100,14 +145,24 @@ __global__ void __launch_bounds__(kThreads) k_residual(int64_t n, int nslices, c
     if (!slice_of(nslices, list, &s, &lane)) return;
     const uint64_t pol = policy_evict_first();
     const int64_t i = s * kSlice + lane;
+    const bool row = i < n;
     const GatherPlain gx{x};
+    // issue every independent load of the row first
+    Chunk<CH> cl, cu;
+    cl.load(L, s, lane, pol);
+    cu.load(U, s, lane, pol);
+    const double di = row ? __ldg(d + i) : 0.0, xi = row ? __ldg(x + i) : 0.0;
+    const double bi = (OUT == OUT_R && row) ? __ldg(b + i) : 0.0;
+    cl.gather_mul(gx);
+    cu.gather_mul(gx);
+    // then sum in ascending column order: LG, L, D, U, UG
     double acc = 0.0;
     if (has_ghost) acc = accum(LG, s, lane, GatherPlain{ghost}, acc, pol);
-    acc = accum(L, s, lane, gx, acc, pol);
-    if (i < n) acc = __dadd_rn(acc, __dmul_rn(__ldg(d + i), __ldg(x + i)));
-    acc = accum(U, s, lane, gx, acc, pol);
+    acc = cl.add(acc, L, gx, pol);
+    acc = __dadd_rn(acc, __dmul_rn(di, xi));
+    acc = cu.add(acc, U, gx, pol);
     if (has_ghost) acc = accum(UG, s, lane, GatherPlain{ghost}, acc, pol);
-    if (i < n) out[i] = OUT == OUT_R ? __dsub_rn(__ldg(b + i), acc) : acc;
+    if (row) out[i] = OUT == OUT_R ? __dsub_rn(bi, acc) : acc;
 }
 
 // ---- inner Jacobi sweep (rows a3, a4, a5) -----------------------------------
@@ -121,7 +176,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(int64_t n, int nslices, c
 //                  y and the U-solve start z^(0) = D_U^{-1} y in one pass)
 //   EPI_XADD_SCALE x_i += v / dnext_i            (ILU with k_u = 0)
 
-template <bool UNIT, int EPI, class G>
+template <bool UNIT, int EPI, class G, int CH>
 __global__ void __launch_bounds__(kThreads) k_sweep(int64_t n, int nslices, const int32_t *__restrict__ list,
                                                     SellView T, SellView TG, int has_ghost,
                                                     const double *__restrict__ dT, const double *__restrict__ rhs,
@@ -134,17 +189,25 @@ __global__ void __launch_bounds__(kThreads) k_sweep(int64_t n, int nslices, cons
     if (!slice_of(nslices, list, &s, &lane)) return;
     const uint64_t pol = policy_evict_first();
     const int64_t i = s * kSlice + lane;
+    const bool row = i < n;
+    Chunk<CH> ct;
+    ct.load(T, s, lane, pol);
+    const double ri = row ? __ldg(rhs + i) : 0.0;
+    const double di = (!UNIT && row) ? __ldg(dT + i) : 1.0;
+    const double xi = ((EPI == EPI_XADD || EPI == EPI_XADD_SCALE) && row) ? x[i] : 0.0;
+    const double dn = ((EPI == EPI_STORE2 || EPI == EPI_XADD_SCALE) && row) ? __ldg(dnext + i) : 1.0;
+    ct.gather_mul(gin);
     double acc = 0.0;
     if (has_ghost) acc = accum(TG, s, lane, GatherPlain{ghost}, acc, pol);
-    acc = accum(T, s, lane, gin, acc, pol);
-    if (i >= n) return;
-    double v = __dsub_rn(__ldg(rhs + i), acc);
-    if (!UNIT) v = __ddiv_rn(v, __ldg(dT + i));
+    acc = ct.add(acc, T, gin, pol);
+    if (!row) return;
+    double v = __dsub_rn(ri, acc);
+    if (!UNIT) v = __ddiv_rn(v, di);
     flag_nonfinite(v, flag, sweep_id);
     if (EPI == EPI_STORE) gout[i] = v;
-    if (EPI == EPI_XADD) x[i] = __dadd_rn(x[i], v);
-    if (EPI == EPI_STORE2) { gout[i] = v; gout2[i] = __ddiv_rn(v, __ldg(dnext + i)); }
-    if (EPI == EPI_XADD_SCALE) x[i] = __dadd_rn(x[i], __ddiv_rn(v, __ldg(dnext + i)));
+    if (EPI == EPI_XADD) x[i] = __dadd_rn(xi, v);
+    if (EPI == EPI_STORE2) { gout[i] = v; gout2[i] = __ddiv_rn(v, dn); }
+    if (EPI == EPI_XADD_SCALE) x[i] = __dadd_rn(xi, __ddiv_rn(v, dn));
 }
 
 // ---- diagonal scaling:  out = rhs / d  or  x += rhs / d  (k = 0 cases) -------
@@ -164,52 +227,75 @@ inline unsigned grid_for(int nslices) { return (unsigned)((nslices + kSlicesPerC
 }  // namespace
 
 // ---------------------------------------------------------------- launchers --
+// Register chunk CH: the smallest of 4 / 8 / 16 covering the widest slice
+// (wider rows continue in the plain loop).
+static inline int chunk_for(int maxw) { return maxw <= 4 ? 4 : (maxw <= 8 ? 8 : 16); }
+
+template <int OUT, int CH>
+static void residual_ch(int64_t n, int nslices, const int32_t *list, const Sell &LG, const Sell &L, const Sell &U,
+                        const Sell &UG, bool has_ghost, const double *d, const double *b, const double *x,
+                        const double *ghost, double *out, cudaStream_t st) {
+    k_residual<OUT, CH><<<grid_for(nslices), kThreads, 0, st>>>(n, nslices, list, view(LG), view(L), view(U),
+                                                                view(UG), has_ghost, d, b, x, ghost, out);
+}
+
 cudaError_t launch_residual(bool spmv, int64_t n, int nslices, const int32_t *list, const Sell &LG, const Sell &L,
                             const Sell &U, const Sell &UG, bool has_ghost, const double *d, const double *b,
                             const double *x, const double *ghost, double *out, cudaStream_t st) {
     if (nslices <= 0) return cudaSuccess;
-    if (spmv)
-        k_residual<OUT_AX><<<grid_for(nslices), kThreads, 0, st>>>(n, nslices, list, view(LG), view(L), view(U),
-                                                                   view(UG), has_ghost, d, b, x, ghost, out);
-    else
-        k_residual<OUT_R><<<grid_for(nslices), kThreads, 0, st>>>(n, nslices, list, view(LG), view(L), view(U),
-                                                                  view(UG), has_ghost, d, b, x, ghost, out);
+    const int ch = chunk_for(std::max(L.maxw, U.maxw));
+#define NSM_RES(OUT)                                                                                        \
+    (ch == 4 ? residual_ch<OUT, 4>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, st)      \
+             : ch == 8 ? residual_ch<OUT, 8>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, st) \
+                       : residual_ch<OUT, 16>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, st))
+    if (spmv) NSM_RES(OUT_AX);
+    else NSM_RES(OUT_R);
+#undef NSM_RES
     return cudaGetLastError();
 }
 
-template <bool UNIT, int EPI>
-static cudaError_t sweep_epi(const SweepArgs &a, cudaStream_t st) {
+template <bool UNIT, int EPI, int CH>
+static void sweep_ch(const SweepArgs &a, cudaStream_t st) {
     dim3 g(grid_for(a.nslices));
     SellView TG = a.TG ? view(*a.TG) : SellView{nullptr, nullptr, nullptr};
-    if (a.gin_scaled && !UNIT)
-        k_sweep<UNIT, EPI, GatherScaled><<<g, kThreads, 0, st>>>(a.n, a.nslices, a.list, view(*a.T), TG,
-                                                                 a.has_ghost, a.dT, a.rhs, GatherScaled{a.rhs, a.dT},
-                                                                 a.ghost, a.gout, a.x, a.dnext, a.gout2, a.flag,
-                                                                 a.sweep_id);
-    else
-        k_sweep<UNIT, EPI, GatherPlain><<<g, kThreads, 0, st>>>(a.n, a.nslices, a.list, view(*a.T), TG,
-                                                                a.has_ghost, a.dT, a.rhs,
-                                                                GatherPlain{a.gin_scaled ? a.rhs : a.gin}, a.ghost,
-                                                                a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
-    return cudaGetLastError();
+    if constexpr (!UNIT) {
+        if (a.gin_scaled) {
+            k_sweep<UNIT, EPI, GatherScaled, CH><<<g, kThreads, 0, st>>>(
+                a.n, a.nslices, a.list, view(*a.T), TG, a.has_ghost, a.dT, a.rhs, GatherScaled{a.rhs, a.dT}, a.ghost,
+                a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
+            return;
+        }
+    }
+    // unit diagonal: g^(0) = rhs itself
+    k_sweep<UNIT, EPI, GatherPlain, CH><<<g, kThreads, 0, st>>>(
+        a.n, a.nslices, a.list, view(*a.T), TG, a.has_ghost, a.dT, a.rhs, GatherPlain{a.gin_scaled ? a.rhs : a.gin},
+        a.ghost, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
+}
+
+template <bool UNIT, int EPI>
+static void sweep_epi(const SweepArgs &a, cudaStream_t st) {
+    switch (chunk_for(a.T->maxw)) {
+        case 4: sweep_ch<UNIT, EPI, 4>(a, st); break;
+        case 8: sweep_ch<UNIT, EPI, 8>(a, st); break;
+        default: sweep_ch<UNIT, EPI, 16>(a, st); break;
+    }
+}
+
+template <bool UNIT>
+static void sweep_unit(const SweepArgs &a, cudaStream_t st) {
+    switch (a.epi) {
+        case EPI_STORE: sweep_epi<UNIT, EPI_STORE>(a, st); break;
+        case EPI_XADD: sweep_epi<UNIT, EPI_XADD>(a, st); break;
+        default: sweep_epi<UNIT, EPI_XADD_SCALE>(a, st); break;
+    }
 }
 
 cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t st) {
     if (a.nslices <= 0) return cudaSuccess;
-    if (a.unit) {
-        switch (a.epi) {
-            case EPI_STORE: return sweep_epi<true, EPI_STORE>(a, st);
-            case EPI_XADD: return sweep_epi<true, EPI_XADD>(a, st);
-            case EPI_STORE2: return sweep_epi<true, EPI_STORE2>(a, st);
-            default: return sweep_epi<true, EPI_XADD_SCALE>(a, st);
-        }
-    }
-    switch (a.epi) {
-        case EPI_STORE: return sweep_epi<false, EPI_STORE>(a, st);
-        case EPI_XADD: return sweep_epi<false, EPI_XADD>(a, st);
-        case EPI_STORE2: return sweep_epi<false, EPI_STORE2>(a, st);
-        default: return sweep_epi<false, EPI_XADD_SCALE>(a, st);
-    }
+    if (a.epi == EPI_STORE2) return cudaErrorInvalidValue;  // reserved, not used by api.cu
+    if (a.unit) sweep_unit<true>(a, st);
+    else sweep_unit<false>(a, st);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_scale(bool xadd, int64_t n, const double *rhs, const double *d, double *out,
