@@ -125,6 +125,54 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
  */
 nsm_status nsm_ilu0(const nsm_csr *A, int64_t row_begin, double *fval);
 
+/* ---- multi-GPU halo plan (setup time) ---------
+ * A handle set up with nranks > 1 owns a "mailbox" (device memory: one flag
+ * per source rank + two parity copies of its ghost array) that its
+ * neighbours write into directly over NVLink / NVSwitch.  Connecting a set of
+ * ranks takes four host steps, all synchronous, done once after nsm_setup
+ * (the Python binding does them with torch.distributed as plumbing):
+ *   1. nsm_halo_plan: the global rows this rank needs from each rank (its
+ *      ghost columns, ascending, grouped by owner).  Host-only: no device.
+ *   2. nsm_halo_set_send(h, q, rows, count): the global rows (owned here) rank
+ *      q needs — i.e. rank q's step-1 list for us.  Call for every q whose
+ *      list is non-empty.
+ *   3. nsm_halo_mailbox exports the mailbox (base pointer, a 64-byte
+ *      cudaIpcMemHandle_t, and recv_offsets[q] = first ghost index owned by
+ *      q); every neighbour q then calls nsm_halo_connect_ipc (other process)
+ *      or nsm_halo_connect (same process and device) with it.
+ *   4. nsm_halo_commit uploads the tables.  Hot calls that need an exchange
+ *      before commit return NSM_ERR_STATE.
+ * Exchanges are symmetric (every neighbour is signalled every time), so all
+ * ranks must issue the same sequence of hot calls.  A neighbour that does
+ * not answer within 20 s makes the waiting kernel give up; nsm_check then
+ * reports NSM_ERR_DIST (no GPU hang).
+ */
+
+/* recv_counts[nranks] receives, per owner rank, how many ghost columns this
+ * rank's rows reference; ghost_rows (NULL, or n_ghost entries) their global
+ * ids ascending; *n_ghost their total.  The CSR is this rank's row block. */
+nsm_status nsm_halo_plan(const nsm_csr *A, const nsm_dist *dist, int64_t *recv_counts, int64_t *ghost_rows,
+                         int64_t *n_ghost);
+
+/* The global rows owned by this rank that rank q needs (q's nsm_halo_plan
+ * list for this rank).  NSM_ERR_DIST if a row is not owned here. */
+nsm_status nsm_halo_set_send(nsm_handle *h, int q, const int64_t *rows, int64_t count);
+
+/* Exports this rank's mailbox: *base (device pointer, may be NULL), the IPC
+ * handle (64 bytes, may be NULL) and recv_offsets[nranks] (may be NULL). */
+nsm_status nsm_halo_mailbox(nsm_handle *h, void **base, void *ipc_handle, int64_t *recv_offsets);
+
+/* Connect to neighbour q's mailbox: peer_n_ghost = q's ghost count,
+ * peer_recv_off = q's recv_offsets[this rank].  _ipc opens the handle of
+ * another process (closed again by nsm_destroy); the plain form takes a
+ * pointer valid in this process (ranks sharing one device and process). */
+nsm_status nsm_halo_connect_ipc(nsm_handle *h, int q, const void *ipc_handle, int64_t peer_n_ghost,
+                                int64_t peer_recv_off);
+nsm_status nsm_halo_connect(nsm_handle *h, int q, void *peer_base, int64_t peer_n_ghost, int64_t peer_recv_off);
+
+/* Finalise the halo tables (after every nsm_halo_set_send / connect). */
+nsm_status nsm_halo_commit(nsm_handle *h);
+
 /* r = b - A x.  With nranks > 1 the x halo is exchanged first.
  * b, x, r: device, length n_local; r must not alias b or x. */
 nsm_status nsm_residual(nsm_handle *h, const double *b, const double *x, double *r, void *stream);

@@ -16,8 +16,10 @@ _STATUS = {0: "NSM_OK", 1: "NSM_ERR_ARG", 2: "NSM_ERR_PATTERN", 3: "NSM_ERR_ZERO
            5: "NSM_ERR_CUDA", 6: "NSM_ERR_OOM", 7: "NSM_ERR_STATE", 8: "NSM_ERR_DIST"}
 
 # every symbol include/nsm.h declares (tests check the .so exports them)
-SYMBOLS = ["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_spmv",
-           "nsm_check", "nsm_info", "nsm_stats", "nsm_last_error", "nsm_destroy"]
+SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_spmv",
+                  "nsm_check", "nsm_info", "nsm_stats", "nsm_last_error", "nsm_destroy", "nsm_halo_plan",
+                  "nsm_halo_set_send", "nsm_halo_mailbox", "nsm_halo_connect_ipc", "nsm_halo_connect",
+                  "nsm_halo_commit"])
 
 
 class NsmError(RuntimeError):
@@ -61,12 +63,19 @@ def load():
     L.nsm_check.argtypes = [vp, P(i64), vp]
     L.nsm_info.argtypes = [vp, P(i64), P(i64), P(i64), P(i64)]
     L.nsm_stats.argtypes = [vp, P(i64), P(i64)]
+    L.nsm_halo_plan.argtypes = [P(_Csr), P(_Dist), vp, vp, P(i64)]
+    L.nsm_halo_set_send.argtypes = [vp, ci, vp, i64]
+    L.nsm_halo_mailbox.argtypes = [vp, P(vp), vp, vp]
+    L.nsm_halo_connect_ipc.argtypes = [vp, ci, vp, i64, i64]
+    L.nsm_halo_connect.argtypes = [vp, ci, vp, i64, i64]
+    L.nsm_halo_commit.argtypes = [vp]
     L.nsm_last_error.argtypes = [vp]
     L.nsm_last_error.restype = ctypes.c_char_p
     L.nsm_destroy.argtypes = [vp]
     L.nsm_destroy.restype = None
     for name in ["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
-                 "nsm_check", "nsm_info", "nsm_stats"]:
+                 "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
+                 "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -110,6 +119,37 @@ def ilu0(A, row_begin: int = 0) -> np.ndarray:
     return out
 
 
+def halo_plan(A, row_offsets, rank: int):
+    """Host-only (no device): the ghost columns of this rank's row block,
+    grouped by owner.  Returns {q: int64 array of global rows needed from q}."""
+    L = load()
+    keep: list = []
+    cs = _csr_struct(A, keep)
+    ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    nranks = len(ro) - 1
+    dist = _Dist(int(rank), int(nranks), ro.ctypes.data, NSM_DIST_HYBRID)
+    counts = np.zeros(nranks, dtype=np.int64)
+    ng = ctypes.c_int64()
+    st = L.nsm_halo_plan(ctypes.byref(cs), ctypes.byref(dist), counts.ctypes.data, None, ctypes.byref(ng))
+    if st != 0:
+        raise NsmError(st, _err(None))
+    rows = np.zeros(ng.value, dtype=np.int64)
+    st = L.nsm_halo_plan(ctypes.byref(cs), ctypes.byref(dist), counts.ctypes.data, rows.ctypes.data, ctypes.byref(ng))
+    if st != 0:
+        raise NsmError(st, _err(None))
+    off = np.concatenate([[0], np.cumsum(counts)])
+    return {q: rows[off[q]:off[q + 1]] for q in range(nranks) if counts[q] > 0}
+
+
+def exchange_plan(requests: dict, rank: int, nranks: int, all_gather_object) -> dict:
+    """Given this rank's {q: rows needed from q}, return {q: rows q needs from
+    this rank}, using a collective `all_gather_object(list_out, obj)` (the
+    torch.distributed signature: plumbing only)."""
+    allreq = [None] * nranks
+    all_gather_object(allreq, {int(q): np.asarray(v, dtype=np.int64) for q, v in requests.items()})
+    return {q: allreq[q][rank] for q in range(nranks) if q != rank and rank in allreq[q]}
+
+
 class Smoother:
     """One nsm handle: the split storage of A (and optionally its ILU(0)
     factors) resident on a CUDA device.  Vectors are float64 CUDA tensors of
@@ -139,6 +179,8 @@ class Smoother:
             raise NsmError(st, _err(None))
         self._h = h
         self.has_ilu = F is not None
+        self.rank, self.nranks = int(rank), int(nranks)
+        self.requests = halo_plan(A, row_offsets, rank) if nranks > 1 else {}
         n, ng, nnz, db = (ctypes.c_int64() for _ in range(4))
         L.nsm_info(h, ctypes.byref(n), ctypes.byref(ng), ctypes.byref(nnz), ctypes.byref(db))
         self.n, self.n_ghost, self.nnz_offdiag, self.device_bytes = n.value, ng.value, nnz.value, db.value
@@ -197,6 +239,63 @@ class Smoother:
         bad = ctypes.c_int64()
         self._call(load().nsm_check(self._h, ctypes.byref(bad), self._stream(stream)))
         return None
+
+    # -- multi-GPU wiring (plumbing around the nsm_halo_* calls) ---------------
+    def _neighbours(self, sends):
+        return sorted(set(self.requests) | {q for q, v in sends.items() if len(v) > 0})
+
+    def _set_sends(self, sends):
+        L = load()
+        for q, rows in sends.items():
+            rows = np.ascontiguousarray(rows, dtype=np.int64)
+            self._call(L.nsm_halo_set_send(self._h, int(q), rows.ctypes.data if len(rows) else None, len(rows)))
+
+    def _mailbox(self):
+        base = ctypes.c_void_p()
+        ipc = ctypes.create_string_buffer(64)
+        offs = np.zeros(self.nranks, dtype=np.int64)
+        self._call(load().nsm_halo_mailbox(self._h, ctypes.byref(base), ipc, offs.ctypes.data))
+        return base.value, ipc.raw, offs
+
+    def connect(self, dist=None, group=None):
+        """Wire the halo exchange across processes (one rank per GPU): the plan
+        and the CUDA IPC mailbox handles travel over torch.distributed."""
+        if self.nranks == 1:
+            return
+        if dist is None:
+            import torch.distributed as dist
+        ago = lambda out, obj: dist.all_gather_object(out, obj, group=group)
+        sends = exchange_plan(self.requests, self.rank, self.nranks, ago)
+        self._set_sends(sends)
+        base, ipc, offs = self._mailbox()
+        info = [None] * self.nranks
+        ago(info, (ipc, offs, self.n_ghost))
+        L = load()
+        for q in self._neighbours(sends):
+            qipc, qoffs, qng = info[q]
+            buf = ctypes.create_string_buffer(qipc, 64)
+            self._call(L.nsm_halo_connect_ipc(self._h, int(q), buf, int(qng), int(qoffs[self.rank])))
+        self._call(L.nsm_halo_commit(self._h))
+
+    @staticmethod
+    def connect_local(ranks):
+        """Wire the halo exchange between handles of ONE process on ONE device
+        (virtual ranks: tests and single-GPU emulation of a partition)."""
+        nranks = len(ranks)
+        allreq = [S.requests for S in ranks]
+        L = load()
+        sends = []
+        for S in ranks:
+            sd = {q: allreq[q][S.rank] for q in range(nranks) if q != S.rank and S.rank in allreq[q]}
+            S._set_sends(sd)
+            sends.append(sd)
+        boxes = [S._mailbox() for S in ranks]
+        for S, sd in zip(ranks, sends):
+            for q in S._neighbours(sd):
+                qbase, _, qoffs = boxes[q]
+                S._call(L.nsm_halo_connect(S._h, int(q), qbase, int(ranks[q].n_ghost), int(qoffs[S.rank])))
+        for S in ranks:
+            S._call(L.nsm_halo_commit(S._h))
 
     def stats(self):
         """(kernel launches, halo exchanges) since setup."""

@@ -1,25 +1,41 @@
 // api.cu — the C-ABI of libnsm.so (include/nsm.h).
 //
-// Owns the handle (device copies of the split storage + workspace) and
-// turns each nsm_* call into a fixed sequence of kernel launches on the
-// caller's stream (no allocation, no host synchronisation on hot calls).
+// Owns the handle (device copies of the split storage, workspace, halo
+// mailbox) and turns each nsm_* call into a fixed sequence of kernel launches
+// on the caller's stream: no allocation and no host synchronisation on the
+// hot calls.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <climits>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "nsm_internal.h"
 
 using namespace nsm;
 
+namespace {
+
+struct Peer {
+    int q = -1;
+    std::vector<int32_t> send_rows;   // local rows rank q needs from us
+    bool send_set = false;
+    int32_t *d_send_rows = nullptr;
+    double *remote_data = nullptr;    // q's ghost data base + q's offset for our block
+    int64_t remote_stride = 0;        // q's n_ghost (parity stride)
+    unsigned long long *remote_flags = nullptr;
+    void *ipc_base = nullptr;         // opened IPC mapping to close at destroy
+    bool connected = false;
+};
+
+}  // namespace
+
 struct nsm_handle {
     int device = 0;
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
-    int rank = 0, nranks = 1;
-    nsm_dist_mode mode = NSM_DIST_HYBRID;
     // A = L + D + U (+ ghost couplings LG / UG)
     double *d = nullptr;
     Sell L, U, LG, UG;
@@ -27,12 +43,30 @@ struct nsm_handle {
     bool has_ilu = false;
     double *dU = nullptr;
     Sell Ls, Us, LsG, UsG;
-    // workspace: three n-vectors, ghost values, divergence flag
+    // workspace: three n-vectors, divergence flag
     double *w[3] = {nullptr, nullptr, nullptr};
-    double *ghost = nullptr;
     unsigned long long *flag = nullptr;
     int64_t sweep_counter = 0;
     int64_t launches = 0, exchanges = 0;
+    // ---- distribution (row-block partition)
+    int rank = 0, nranks = 1;
+    nsm_dist_mode mode = NSM_DIST_HYBRID;
+    std::vector<int64_t> row_offsets, ghost_gid, recv_off;  // recv_off[q]: first ghost owned by q
+    int32_t *interior = nullptr, *boundary = nullptr;       // slice lists
+    int n_interior = 0, n_boundary = 0;
+    void *mailbox = nullptr;           // [flags: nranks u64, padded][data: 2 x n_ghost f64]
+    size_t mailbox_bytes = 0, flags_bytes = 0;
+    unsigned long long *mb_flags = nullptr;
+    double *mb_data = nullptr;
+    std::vector<Peer> peers;           // symmetric neighbour set, ascending q
+    PutDesc *d_put = nullptr;
+    int *d_peer_ids = nullptr;
+    unsigned int *d_counters = nullptr, *d_dist_err = nullptr;
+    int put_grid = 0;
+    bool committed = false;
+    unsigned long long exch_seq = 0;
+    unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
+    double *ghost_null = nullptr;      // 1-element dummy ghost buffer (single rank)
     std::string err;
 };
 
@@ -84,8 +118,19 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->d);
     cudaFree(h->dU);
     for (double *&p : h->w) cudaFree(p);
-    cudaFree(h->ghost);
     cudaFree(h->flag);
+    cudaFree(h->interior);
+    cudaFree(h->boundary);
+    for (Peer &p : h->peers) {
+        cudaFree(p.d_send_rows);
+        if (p.ipc_base) cudaIpcCloseMemHandle(p.ipc_base);
+    }
+    cudaFree(h->mailbox);
+    cudaFree(h->d_put);
+    cudaFree(h->d_peer_ids);
+    cudaFree(h->d_counters);
+    cudaFree(h->d_dist_err);
+    cudaFree(h->ghost_null);
     delete h;
 }
 
@@ -96,61 +141,122 @@ nsm_status cuda_fail(nsm_handle *h, cudaError_t e, const char *where) {
 
 inline cudaStream_t S(void *s) { return (cudaStream_t)s; }
 
-bool overlap(const double *a, const double *b, int64_t n) {
-    return a && b && a < b + n && b < a + n;
+bool overlap(const double *a, const double *b, int64_t n) { return a && b && a < b + n && b < a + n; }
+
+bool distributed(const nsm_handle *h) { return h->nranks > 1; }
+
+Peer *find_peer(nsm_handle *h, int q) {
+    for (Peer &p : h->peers)
+        if (p.q == q) return &p;
+    return nullptr;
 }
 
-// One stage of the Jacobi-iterated solve: k sweeps on T from g^(0) = rhs / dT
-// (gin_scaled first sweep), writing the final iterate with epilogue `epi`.
-// bufs: two scratch vectors for the ping-pong, distinct from rhs.
+// ---- one pass over the slices, with or without a halo exchange --------------
+// launch(list, count, with_ghost, ghost): run the kernel on a slice list.
+// With an exchange of `src` (scaled by 1/scale if given): put -> interior
+// slices (overlap with the NVLink transfer) -> wait -> boundary slices.
+template <class F>
+nsm_status pass(nsm_handle *h, bool exchange, const double *src, const double *scale, cudaStream_t s, F launch) {
+    if (!exchange || !distributed(h)) {
+        cudaError_t e = launch((const int32_t *)nullptr, h->nslices, false, (const double *)h->ghost_null);
+        if (h->n > 0) ++h->launches;
+        return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "kernel launch");
+    }
+    if (!h->committed) {
+        h->err = "halo exchange requested before nsm_halo_commit";
+        return NSM_ERR_STATE;
+    }
+    const unsigned long long seq = ++h->exch_seq;
+    const int parity = (int)(seq & 1);
+    const double *ghost = h->mb_data + (int64_t)parity * h->n_ghost;
+    cudaError_t e = launch_halo_put(h->d_put, (int)h->peers.size(), h->put_grid, src, scale, parity, seq,
+                                    h->d_counters, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "halo put");
+    if (h->n_interior > 0) {
+        e = launch(h->interior, h->n_interior, false, ghost);
+        ++h->launches;
+        if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch (interior)");
+    }
+    e = launch_halo_wait(h->mb_flags, h->d_peer_ids, (int)h->peers.size(), seq, h->timeout_ns, h->d_dist_err, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "halo wait");
+    if (h->n_boundary > 0) {
+        e = launch(h->boundary, h->n_boundary, true, ghost);
+        ++h->launches;
+        if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch (boundary)");
+    }
+    h->launches += h->peers.empty() ? 0 : 2;
+    ++h->exchanges;
+    return NSM_OK;
+}
+
+// One stage of a Jacobi-iterated triangular solve: k >= 1 sweeps on T from
+// g^(0) = rhs / dT (recomputed in the first sweep's gather), the final
+// iterate written with epilogue last_epi.  bufA/bufB: ping-pong scratch.
+// TG: ghost couplings of T, used in GLOBAL mode (exchange before each sweep).
 struct Stage {
     const Sell *T;
+    const Sell *TG;
     const double *dT;    // nullptr = unit diagonal
     const double *rhs;
     int k;
 };
 
 nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB, int last_epi, double *last_out,
-                      double *x, const double *dnext, double *gout2, cudaStream_t s) {
-    // k >= 1 required here; k == 0 is handled by the caller (scale kernels).
+                      double *x, const double *dnext, cudaStream_t s) {
+    const bool global = distributed(h) && h->mode == NSM_DIST_GLOBAL;
     const double *gin = nullptr;
     for (int j = 1; j <= st.k; ++j) {
         const bool last = j == st.k;
-        SweepArgs a{};
-        a.n = h->n;
-        a.nslices = h->nslices;
-        a.list = nullptr;
-        a.T = st.T;
-        a.TG = nullptr;
-        a.has_ghost = false;
-        a.unit = st.dT == nullptr;
-        a.epi = last ? last_epi : EPI_STORE;
-        a.gin_scaled = j == 1;
-        a.dT = st.dT;
-        a.rhs = st.rhs;
-        a.gin = gin;
-        a.ghost = h->ghost;
         double *out = last ? last_out : ((j & 1) ? bufA : bufB);
-        a.gout = out;
-        a.x = x;
-        a.dnext = dnext;
-        a.gout2 = gout2;
-        a.flag = h->flag;
-        a.sweep_id = ++h->sweep_counter;
-        cudaError_t e = launch_sweep(a, s);
-        if (e != cudaSuccess) return cuda_fail(h, e, "sweep launch");
-        ++h->launches;
+        const int64_t sid = ++h->sweep_counter;
+        // the ghost values a GLOBAL sweep needs are those of its input iterate:
+        // g^(0) = rhs / dT for the first sweep, the previous output after that
+        const double *xsrc = j == 1 ? st.rhs : gin;
+        const double *xscale = j == 1 ? st.dT : nullptr;
+        nsm_status r = pass(h, global, xsrc, xscale, s,
+                            [&](const int32_t *list, int cnt, bool with_ghost, const double *ghost) {
+                                SweepArgs a{};
+                                a.n = h->n;
+                                a.nslices = cnt;
+                                a.list = list;
+                                a.T = st.T;
+                                a.TG = st.TG;
+                                a.has_ghost = with_ghost;
+                                a.unit = st.dT == nullptr;
+                                a.epi = last ? last_epi : EPI_STORE;
+                                a.gin_scaled = j == 1;
+                                a.dT = st.dT;
+                                a.rhs = st.rhs;
+                                a.gin = gin;
+                                a.ghost = ghost;
+                                a.gout = out;
+                                a.x = x;
+                                a.dnext = dnext;
+                                a.gout2 = nullptr;
+                                a.flag = h->flag;
+                                a.sweep_id = sid;
+                                return launch_sweep(a, s);
+                            });
+        if (r != NSM_OK) return r;
         gin = out;
     }
     return NSM_OK;
 }
 
 nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double *out, bool spmv, cudaStream_t s) {
-    cudaError_t e = launch_residual(spmv, h->n, h->nslices, nullptr, h->LG, h->L, h->U, h->UG, h->n_ghost > 0,
-                                    h->d, b, x, h->ghost, out, s);
-    if (h->n > 0) ++h->launches;
-    return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "residual launch");
+    return pass(h, true, x, nullptr, s, [&](const int32_t *list, int cnt, bool with_ghost, const double *ghost) {
+        return launch_residual(spmv, h->n, cnt, list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost, out,
+                               s);
+    });
 }
+
+nsm_status scale_into(nsm_handle *h, bool xadd, const double *rhs, const double *d, double *out, cudaStream_t s) {
+    cudaError_t e = launch_scale(xadd, h->n, rhs, d, out, h->flag, ++h->sweep_counter, s);
+    if (h->n > 0) ++h->launches;
+    return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "scale launch");
+}
+
+size_t flags_bytes_for(int nranks) { return (((size_t)nranks * 8 + 255) / 256) * 256; }
 
 }  // namespace
 
@@ -163,15 +269,61 @@ nsm_status nsm_ilu0(const nsm_csr *A, int64_t row_begin, double *fval) {
     return ilu0_host(A, row_begin, fval, &g_setup_err);
 }
 
+nsm_status nsm_halo_plan(const nsm_csr *A, const nsm_dist *dist, int64_t *recv_counts, int64_t *ghost_rows,
+                         int64_t *n_ghost) {
+    if (!A || !dist || dist->nranks < 1 || !dist->row_offsets || !recv_counts || !n_ghost) {
+        g_setup_err = "nsm_halo_plan: NULL argument";
+        return NSM_ERR_ARG;
+    }
+    const int64_t *ro = dist->row_offsets;
+    const int64_t rb = ro[dist->rank], re = ro[dist->rank + 1];
+    if (A->nrows != re - rb) { g_setup_err = "nsm_halo_plan: CSR rows do not match the partition"; return NSM_ERR_DIST; }
+    std::vector<int64_t> g;
+    for (int64_t i = 0; i < A->nrows; ++i)
+        for (int64_t p = A->rowptr[i]; p < A->rowptr[i + 1]; ++p)
+            if (A->colind[p] < rb || A->colind[p] >= re) g.push_back(A->colind[p]);
+    std::sort(g.begin(), g.end());
+    g.erase(std::unique(g.begin(), g.end()), g.end());
+    for (int q = 0; q < dist->nranks; ++q) recv_counts[q] = 0;
+    for (int64_t c : g) {
+        int q = (int)(std::upper_bound(ro, ro + dist->nranks + 1, c) - ro) - 1;
+        if (q < 0 || q >= dist->nranks) { g_setup_err = "nsm_halo_plan: column outside the partition"; return NSM_ERR_DIST; }
+        recv_counts[q]++;
+    }
+    if (ghost_rows) std::copy(g.begin(), g.end(), ghost_rows);
+    *n_ghost = (int64_t)g.size();
+    return NSM_OK;
+}
+
 nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const nsm_dist *dist, int device) {
     if (!out || !A) { g_setup_err = "nsm_setup: NULL argument"; return NSM_ERR_ARG; }
     *out = nullptr;
-    int64_t rb = 0, re = A->nrows;
+    int rank = 0, nranks = 1;
+    int64_t rb = 0, re = A->nrows, nglob = A->nrows;
     if (dist && dist->nranks > 1) {
-        g_setup_err = "nsm_setup: multi-rank handles are not built by this entry point yet";
-        return NSM_ERR_DIST;
+        if (!dist->row_offsets || dist->rank < 0 || dist->rank >= dist->nranks ||
+            (dist->mode != NSM_DIST_HYBRID && dist->mode != NSM_DIST_GLOBAL)) {
+            g_setup_err = "nsm_setup: bad nsm_dist";
+            return NSM_ERR_ARG;
+        }
+        rank = dist->rank;
+        nranks = dist->nranks;
+        for (int q = 0; q < nranks; ++q)
+            if (dist->row_offsets[q + 1] < dist->row_offsets[q] || dist->row_offsets[0] != 0) {
+                g_setup_err = "nsm_setup: row_offsets must start at 0 and ascend";
+                return NSM_ERR_DIST;
+            }
+        rb = dist->row_offsets[rank];
+        re = dist->row_offsets[rank + 1];
+        nglob = dist->row_offsets[nranks];
+        if (A->nrows != re - rb || A->ncols != nglob) {
+            g_setup_err = "nsm_setup: CSR block does not match the partition (rows or global columns)";
+            return NSM_ERR_DIST;
+        }
+    } else if (A->ncols != A->nrows) {
+        g_setup_err = "nsm_setup: A must be square on one rank";
+        return NSM_ERR_ARG;
     }
-    if (A->ncols != A->nrows) { g_setup_err = "nsm_setup: A must be square on one rank"; return NSM_ERR_ARG; }
     Split sa, sf;
     nsm_status st = build_split(A, rb, re, &sa, &g_setup_err);
     if (st != NSM_OK) return st;
@@ -179,6 +331,10 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         if (F->nrows != A->nrows || F->ncols != A->ncols) { g_setup_err = "nsm_setup: F shape differs from A"; return NSM_ERR_ARG; }
         st = build_split(F, rb, re, &sf, &g_setup_err);
         if (st != NSM_OK) { g_setup_err = "factor: " + g_setup_err; return st; }
+        if (sf.ghost_gid != sa.ghost_gid) {
+            g_setup_err = "nsm_setup: the factor couples to other ranks' columns that A does not";
+            return NSM_ERR_PATTERN;
+        }
     }
     if (cudaSetDevice(device) != cudaSuccess) { g_setup_err = "nsm_setup: cudaSetDevice failed"; return NSM_ERR_CUDA; }
     nsm_handle *h = new nsm_handle();
@@ -188,6 +344,9 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     h->n_ghost = sa.n_ghost;
     h->nnz_off = sa.nnz_off;
     h->nslices = (int)((sa.n + kSlice - 1) / kSlice);
+    h->rank = rank;
+    h->nranks = nranks;
+    h->mode = dist ? dist->mode : NSM_DIST_HYBRID;
     DevAlloc a{h};
     bool ok = a.get(&h->d, h->n) && upload(h->d, sa.d.data(), h->n) && upload_sell(a, sa.L, &h->L) &&
               upload_sell(a, sa.U, &h->U) && upload_sell(a, sa.LG, &h->LG) && upload_sell(a, sa.UG, &h->UG);
@@ -197,10 +356,45 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
              upload_sell(a, sf.U, &h->Us) && upload_sell(a, sf.LG, &h->LsG) && upload_sell(a, sf.UG, &h->UsG);
     }
     for (int i = 0; ok && i < 3; ++i) ok = a.get(&h->w[i], std::max<int64_t>(h->n, 1));
-    ok = ok && a.get(&h->ghost, std::max<int64_t>(h->n_ghost, 1)) && a.get(&h->flag, 1);
+    ok = ok && a.get(&h->flag, 1) && a.get(&h->ghost_null, 1);
     if (ok) {
         unsigned long long init = ULLONG_MAX;
         ok = cudaMemcpy(h->flag, &init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+    if (ok && nranks > 1) {
+        h->row_offsets.assign(dist->row_offsets, dist->row_offsets + nranks + 1);
+        h->ghost_gid = sa.ghost_gid;
+        h->recv_off.assign(nranks + 1, 0);
+        for (int q = 0; q <= nranks; ++q)
+            h->recv_off[q] = (int64_t)(std::lower_bound(h->ghost_gid.begin(), h->ghost_gid.end(), h->row_offsets[q]) -
+                                       h->ghost_gid.begin());
+        // slices whose rows couple to ghosts are "boundary", the rest "interior"
+        std::vector<int32_t> inner, bnd;
+        for (int s = 0; s < h->nslices; ++s) {
+            bool g = sa.LG.ptr[s + 1] > sa.LG.ptr[s] || sa.UG.ptr[s + 1] > sa.UG.ptr[s];
+            (g ? bnd : inner).push_back(s);
+        }
+        h->n_interior = (int)inner.size();
+        h->n_boundary = (int)bnd.size();
+        ok = a.get(&h->interior, h->n_interior) && upload(h->interior, inner.data(), h->n_interior) &&
+             a.get(&h->boundary, h->n_boundary) && upload(h->boundary, bnd.data(), h->n_boundary);
+        // neighbours we receive from (send side joins in nsm_halo_set_send)
+        for (int q = 0; q < nranks; ++q)
+            if (q != rank && h->recv_off[q + 1] > h->recv_off[q]) {
+                Peer p;
+                p.q = q;
+                h->peers.push_back(p);
+            }
+        h->flags_bytes = flags_bytes_for(nranks);
+        h->mailbox_bytes = h->flags_bytes + (size_t)2 * std::max<int64_t>(h->n_ghost, 1) * sizeof(double);
+        ok = ok && cudaMalloc(&h->mailbox, h->mailbox_bytes) == cudaSuccess &&
+             cudaMemset(h->mailbox, 0, h->mailbox_bytes) == cudaSuccess;
+        if (ok) {
+            h->device_bytes += (int64_t)h->mailbox_bytes;
+            h->mb_flags = (unsigned long long *)h->mailbox;
+            h->mb_data = (double *)((char *)h->mailbox + h->flags_bytes);
+        }
+        ok = ok && a.get(&h->d_dist_err, 1) && cudaMemset(h->d_dist_err, 0, sizeof(unsigned int)) == cudaSuccess;
     }
     if (!ok) {
         cudaGetLastError();
@@ -209,6 +403,102 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         return NSM_ERR_OOM;
     }
     *out = h;
+    return NSM_OK;
+}
+
+nsm_status nsm_halo_set_send(nsm_handle *h, int q, const int64_t *rows, int64_t count) {
+    if (!h || q < 0 || q >= h->nranks || q == h->rank || count < 0 || (count > 0 && !rows)) return NSM_ERR_ARG;
+    if (h->committed) { h->err = "nsm_halo_set_send after commit"; return NSM_ERR_STATE; }
+    Peer *p = find_peer(h, q);
+    if (!p) {
+        if (count == 0) return NSM_OK;
+        Peer np;
+        np.q = q;
+        h->peers.push_back(np);
+        std::sort(h->peers.begin(), h->peers.end(), [](const Peer &a, const Peer &b) { return a.q < b.q; });
+        p = find_peer(h, q);
+    }
+    p->send_rows.resize(count);
+    for (int64_t i = 0; i < count; ++i) {
+        int64_t l = rows[i] - h->row_begin;
+        if (l < 0 || l >= h->n) {
+            h->err = "nsm_halo_set_send: row " + std::to_string((long long)rows[i]) + " is not owned by this rank";
+            return NSM_ERR_DIST;
+        }
+        p->send_rows[i] = (int32_t)l;
+    }
+    p->send_set = true;
+    return NSM_OK;
+}
+
+nsm_status nsm_halo_mailbox(nsm_handle *h, void **base, void *ipc_handle, int64_t *recv_offsets) {
+    if (!h || h->nranks < 2) return NSM_ERR_STATE;
+    if (base) *base = h->mailbox;
+    if (ipc_handle) {
+        cudaIpcMemHandle_t ih;
+        cudaSetDevice(h->device);
+        cudaError_t e = cudaIpcGetMemHandle(&ih, h->mailbox);
+        if (e != cudaSuccess) return cuda_fail(h, e, "cudaIpcGetMemHandle");
+        std::memcpy(ipc_handle, &ih, sizeof(ih));
+    }
+    if (recv_offsets) std::copy(h->recv_off.begin(), h->recv_off.begin() + h->nranks, recv_offsets);
+    return NSM_OK;
+}
+
+static nsm_status connect_common(nsm_handle *h, int q, void *peer_base, int64_t peer_n_ghost,
+                                 int64_t peer_recv_off_for_us, void *ipc_base) {
+    Peer *p = find_peer(h, q);
+    if (!p) { h->err = "nsm_halo_connect: rank " + std::to_string(q) + " is not a neighbour"; return NSM_ERR_DIST; }
+    const size_t fb = flags_bytes_for(h->nranks);
+    p->remote_flags = (unsigned long long *)peer_base + h->rank;
+    p->remote_data = (double *)((char *)peer_base + fb) + peer_recv_off_for_us;
+    p->remote_stride = std::max<int64_t>(peer_n_ghost, 1);
+    p->ipc_base = ipc_base;
+    p->connected = true;
+    return NSM_OK;
+}
+
+nsm_status nsm_halo_connect(nsm_handle *h, int q, void *peer_base, int64_t peer_n_ghost, int64_t peer_recv_off) {
+    if (!h || !peer_base || q < 0 || q >= h->nranks) return NSM_ERR_ARG;
+    return connect_common(h, q, peer_base, peer_n_ghost, peer_recv_off, nullptr);
+}
+
+nsm_status nsm_halo_connect_ipc(nsm_handle *h, int q, const void *ipc_handle, int64_t peer_n_ghost,
+                                int64_t peer_recv_off) {
+    if (!h || !ipc_handle || q < 0 || q >= h->nranks) return NSM_ERR_ARG;
+    cudaSetDevice(h->device);
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, ipc_handle, sizeof(ih));
+    void *ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaIpcOpenMemHandle");
+    return connect_common(h, q, ptr, peer_n_ghost, peer_recv_off, ptr);
+}
+
+nsm_status nsm_halo_commit(nsm_handle *h) {
+    if (!h || h->nranks < 2) return NSM_ERR_STATE;
+    std::vector<PutDesc> desc;
+    std::vector<int> ids;
+    int blocks = 0;
+    DevAlloc a{h};
+    for (Peer &p : h->peers) {
+        if (!p.connected) { h->err = "nsm_halo_commit: neighbour " + std::to_string(p.q) + " not connected"; return NSM_ERR_DIST; }
+        int64_t cnt = (int64_t)p.send_rows.size();
+        if (!a.get(&p.d_send_rows, cnt) || !upload(p.d_send_rows, p.send_rows.data(), cnt)) return NSM_ERR_OOM;
+        PutDesc d{p.d_send_rows, cnt, p.remote_data, p.remote_stride, p.remote_flags, put_blocks(cnt), blocks};
+        blocks += d.nblocks;
+        desc.push_back(d);
+        ids.push_back(p.q);
+    }
+    h->put_grid = blocks;
+    int np = (int)desc.size();
+    if (np > 0) {
+        if (!a.get(&h->d_put, np) || !upload(h->d_put, desc.data(), np) || !a.get(&h->d_peer_ids, np) ||
+            !upload(h->d_peer_ids, ids.data(), np) || !a.get(&h->d_counters, np) ||
+            cudaMemset(h->d_counters, 0, np * sizeof(unsigned int)) != cudaSuccess)
+            return NSM_ERR_OOM;
+    }
+    h->committed = true;
     return NSM_OK;
 }
 
@@ -254,16 +544,11 @@ static nsm_status tri_solve(nsm_handle *h, bool lower, const double *r, double *
         return NSM_ERR_ARG;
     }
     cudaStream_t s = S(stream);
-    const Sell *T;
-    const double *dT;
-    if (h->has_ilu) { T = lower ? &h->Ls : &h->Us; dT = lower ? nullptr : h->dU; }
-    else { T = lower ? &h->L : &h->U; dT = h->d; }
-    if (k == 0) {
-        cudaError_t e = launch_scale(false, h->n, r, dT, x, h->flag, ++h->sweep_counter, s);
-        if (h->n > 0) ++h->launches;
-        return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "scale launch");
-    }
-    return run_sweeps(h, Stage{T, dT, r, k}, h->w[0], h->w[1], EPI_STORE, x, nullptr, nullptr, nullptr, s);
+    Stage stg;
+    if (h->has_ilu) stg = lower ? Stage{&h->Ls, &h->LsG, nullptr, r, k} : Stage{&h->Us, &h->UsG, h->dU, r, k};
+    else stg = lower ? Stage{&h->L, &h->LG, h->d, r, k} : Stage{&h->U, &h->UG, h->d, r, k};
+    if (k == 0) return scale_into(h, false, r, stg.dT, x, s);
+    return run_sweeps(h, stg, h->w[0], h->w[1], EPI_STORE, x, nullptr, nullptr, s);
 }
 
 nsm_status nsm_lsolve(nsm_handle *h, const double *r, double *x, int k, void *stream) {
@@ -294,43 +579,35 @@ nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, 
         }
         nsm_status st = NSM_OK;
         if (kind == NSM_PGS) {
-            // rows a3/a4: k_l sweeps g <- D^{-1}(r - L g), last one fused with x += g
-            if (k_l == 0) {
-                cudaError_t e = launch_scale(true, h->n, rhs, h->d, x, h->flag, ++h->sweep_counter, s);
-                if (h->n > 0) ++h->launches;
-                if (e != cudaSuccess) return cuda_fail(h, e, "scale launch");
-            } else {
-                st = run_sweeps(h, Stage{&h->L, h->d, rhs, k_l}, W0, W1, EPI_XADD, nullptr, x, nullptr, nullptr, s);
-            }
+            // rows a3/a4: k_l sweeps g <- D^{-1}(r - L g), the last fused with x += g
+            if (k_l == 0) st = scale_into(h, true, rhs, h->d, x, s);
+            else st = run_sweeps(h, Stage{&h->L, &h->LG, h->d, rhs, k_l}, W0, W1, EPI_XADD, nullptr, x, nullptr, s);
         } else {
             // row a5: y = sum_{j<=kL} (-Ls)^j r ; z = sum_{j<=kU} (-DU^{-1}Us)^j DU^{-1} y ; x += z
             const double *y = rhs;
-            double *ybuf = nullptr;
             if (k_l > 0) {
-                // L sweeps ping-pong in W0/W1; the last writes y (and z0 = y/dU if k_u >= 1
-                // is gathered on the fly by the first U sweep, so only y is stored)
-                ybuf = (k_l & 1) ? W0 : W1;
+                // L sweeps ping-pong in W0/W1; the last writes y (z^(0) = y/dU is
+                // recomputed in the first U sweep's gather, so only y is stored)
+                double *ybuf = (k_l & 1) ? W0 : W1;
                 if (k_u == 0)
-                    st = run_sweeps(h, Stage{&h->Ls, nullptr, rhs, k_l}, W0, W1, EPI_XADD_SCALE, nullptr, x, h->dU,
-                                    nullptr, s);
+                    st = run_sweeps(h, Stage{&h->Ls, &h->LsG, nullptr, rhs, k_l}, W0, W1, EPI_XADD_SCALE, nullptr, x,
+                                    h->dU, s);
                 else
-                    st = run_sweeps(h, Stage{&h->Ls, nullptr, rhs, k_l}, W0, W1, EPI_STORE, ybuf, nullptr, nullptr,
+                    st = run_sweeps(h, Stage{&h->Ls, &h->LsG, nullptr, rhs, k_l}, W0, W1, EPI_STORE, ybuf, nullptr,
                                     nullptr, s);
                 if (st != NSM_OK) return st;
                 y = ybuf;
             } else if (k_u == 0) {
-                cudaError_t e = launch_scale(true, h->n, rhs, h->dU, x, h->flag, ++h->sweep_counter, s);
-                if (h->n > 0) ++h->launches;
-                if (e != cudaSuccess) return cuda_fail(h, e, "scale launch");
+                st = scale_into(h, true, rhs, h->dU, x, s);
             }
-            if (k_u > 0) {
-                // scratch for the z ping-pong: the two work vectors not holding y
-                // (R is free once the L stage has consumed the residual)
+            if (st == NSM_OK && k_u > 0) {
+                // z ping-pong in the two work vectors not holding y (R is free
+                // once the L stage has consumed the residual)
                 double *za, *zb;
                 if (y == W0) { za = R; zb = W1; }
                 else if (y == W1) { za = R; zb = W0; }
                 else { za = W0; zb = W1; }
-                st = run_sweeps(h, Stage{&h->Us, h->dU, y, k_u}, za, zb, EPI_XADD, nullptr, x, nullptr, nullptr, s);
+                st = run_sweeps(h, Stage{&h->Us, &h->UsG, h->dU, y, k_u}, za, zb, EPI_XADD, nullptr, x, nullptr, s);
             }
         }
         if (st != NSM_OK) return st;
@@ -340,13 +617,23 @@ nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, 
 
 nsm_status nsm_check(nsm_handle *h, int64_t *first_bad_sweep, void *stream) {
     if (!h) return NSM_ERR_ARG;
+    cudaSetDevice(h->device);
     cudaError_t e = cudaStreamSynchronize(S(stream));
     if (e != cudaSuccess) return cuda_fail(h, e, "nsm_check");
     unsigned long long v = 0, init = ULLONG_MAX;
+    unsigned int derr = 0;
     e = cudaMemcpy(&v, h->flag, sizeof(v), cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(h->flag, &init, sizeof(init), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && h->d_dist_err) {
+        e = cudaMemcpy(&derr, h->d_dist_err, sizeof(derr), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemset(h->d_dist_err, 0, sizeof(unsigned int));
+    }
     if (e != cudaSuccess) return cuda_fail(h, e, "nsm_check");
     if (first_bad_sweep) *first_bad_sweep = v == ULLONG_MAX ? -1 : (int64_t)v;
+    if (derr) {
+        h->err = "halo exchange timed out waiting for a neighbour";
+        return NSM_ERR_DIST;
+    }
     if (v != ULLONG_MAX) {
         h->err = "non-finite value produced by sweep " + std::to_string((long long)v);
         return NSM_ERR_NONFINITE;

@@ -91,6 +91,28 @@ cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t st);
 cudaError_t launch_scale(bool xadd, int64_t n, const double *rhs, const double *d, double *out,
                          unsigned long long *flag, int64_t sweep_id, cudaStream_t st);
 
+// ---- halo exchange (halo.cu) --------------------------------------------------
+// One outgoing message: entries rows[0..count) of the sent vector go to
+// remote[parity * remote_stride + e] in the neighbour's mailbox; the last of
+// the nblocks blocks writing it publishes the exchange's sequence number at
+// remote_flag.  block0 = first block of this peer in the put grid.
+struct PutDesc {
+    const int32_t *rows;
+    int64_t count;
+    double *remote;
+    int64_t remote_stride;
+    unsigned long long *remote_flag;
+    int nblocks;
+    int block0;
+};
+
+int put_blocks(int64_t count);
+cudaError_t launch_halo_put(const PutDesc *desc, int npeers, int total_blocks, const double *src,
+                            const double *scale, int parity, unsigned long long seq, unsigned int *counters,
+                            cudaStream_t st);
+cudaError_t launch_halo_wait(const unsigned long long *flags, const int *peers, int npeers, unsigned long long seq,
+                             unsigned long long timeout_ns, unsigned int *dist_err, cudaStream_t st);
+
 // Host ILU(0) (nsm_ilu0).
 nsm_status ilu0_host(const nsm_csr *A, int64_t row_begin, double *fval, std::string *err);
 
