@@ -229,6 +229,16 @@ nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *hal
  * The pointer stays valid until the next call on the same handle. */
 const char *nsm_last_error(const nsm_handle *h);
 
+/* Handle options (not on the hot path; take effect for subsequent calls):
+ *   NSM_OPT_PIPELINE        1 (default) = bulk-copy pipelined kernels for
+ *                           contiguous slice ranges (cp.async.bulk + mbarrier,
+ *                           DESIGN.md §6); 0 = the plain register-blocked
+ *                           kernels.  Both give bit-identical results.
+ *   NSM_OPT_HALO_TIMEOUT_MS how long a halo wait spins before giving up and
+ *                           flagging NSM_ERR_DIST (default 20000). */
+typedef enum { NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1 } nsm_option;
+nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
+
 /* Frees all device memory of the handle (synchronises its device).  NULL ok. */
 void nsm_destroy(nsm_handle *h);
 

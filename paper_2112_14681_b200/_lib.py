@@ -19,7 +19,7 @@ _STATUS = {0: "NSM_OK", 1: "NSM_ERR_ARG", 2: "NSM_ERR_PATTERN", 3: "NSM_ERR_ZERO
 SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_spmv",
                   "nsm_check", "nsm_info", "nsm_stats", "nsm_last_error", "nsm_destroy", "nsm_halo_plan",
                   "nsm_halo_set_send", "nsm_halo_mailbox", "nsm_halo_connect_ipc", "nsm_halo_connect",
-                  "nsm_halo_commit"])
+                  "nsm_halo_commit", "nsm_set_option"])
 
 
 class NsmError(RuntimeError):
@@ -69,13 +69,14 @@ def load():
     L.nsm_halo_connect_ipc.argtypes = [vp, ci, vp, i64, i64]
     L.nsm_halo_connect.argtypes = [vp, ci, vp, i64, i64]
     L.nsm_halo_commit.argtypes = [vp]
+    L.nsm_set_option.argtypes = [vp, ci, i64]
     L.nsm_last_error.argtypes = [vp]
     L.nsm_last_error.restype = ctypes.c_char_p
     L.nsm_destroy.argtypes = [vp]
     L.nsm_destroy.restype = None
     for name in ["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
                  "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
-                 "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit"]:
+                 "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -296,6 +297,14 @@ class Smoother:
                 S._call(L.nsm_halo_connect(S._h, int(q), qbase, int(ranks[q].n_ghost), int(qoffs[S.rank])))
         for S in ranks:
             S._call(L.nsm_halo_commit(S._h))
+
+    def set_pipeline(self, enable: bool):
+        """Bulk-copy pipelined kernels (default) or the plain ones."""
+        self._call(load().nsm_set_option(self._h, 0, int(bool(enable))))
+
+    def set_halo_timeout(self, ms: int):
+        """How long a halo wait spins before reporting NSM_ERR_DIST."""
+        self._call(load().nsm_set_option(self._h, 1, int(ms)))
 
     def stats(self):
         """(kernel launches, halo exchanges) since setup."""

@@ -54,6 +54,8 @@ struct nsm_handle {
     std::vector<int64_t> row_offsets, ghost_gid, recv_off;  // recv_off[q]: first ghost owned by q
     int32_t *interior = nullptr, *boundary = nullptr;       // slice lists
     int n_interior = 0, n_boundary = 0;
+    int64_t interior_begin = -1, interior_end = -1;          // set if the interior list is one range
+    bool pipeline = true;                                    // bulk-copy pipelined kernels (stream.cu)
     void *mailbox = nullptr;           // [flags: nranks u64, padded][data: 2 x n_ghost f64]
     size_t mailbox_bytes = 0, flags_bytes = 0;
     unsigned long long *mb_flags = nullptr;
@@ -152,13 +154,21 @@ Peer *find_peer(nsm_handle *h, int q) {
 }
 
 // ---- one pass over the slices, with or without a halo exchange --------------
-// launch(list, count, with_ghost, ghost): run the kernel on a slice list.
+// A set of slices: an explicit list, and (if it is one contiguous range)
+// its bounds, which lets the bulk-copy pipelined kernels stream it.
+struct Slices {
+    const int32_t *list;
+    int count;
+    int64_t begin, end;  // begin < 0: not a single range
+};
+
+// launch(slices, with_ghost, ghost): run the kernel on a set of slices.
 // With an exchange of `src` (scaled by 1/scale if given): put -> interior
 // slices (overlap with the NVLink transfer) -> wait -> boundary slices.
 template <class F>
 nsm_status pass(nsm_handle *h, bool exchange, const double *src, const double *scale, cudaStream_t s, F launch) {
     if (!exchange || !distributed(h)) {
-        cudaError_t e = launch((const int32_t *)nullptr, h->nslices, false, (const double *)h->ghost_null);
+        cudaError_t e = launch(Slices{nullptr, h->nslices, 0, h->nslices}, false, (const double *)h->ghost_null);
         if (h->n > 0) ++h->launches;
         return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "kernel launch");
     }
@@ -173,14 +183,14 @@ nsm_status pass(nsm_handle *h, bool exchange, const double *src, const double *s
                                     h->d_counters, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "halo put");
     if (h->n_interior > 0) {
-        e = launch(h->interior, h->n_interior, false, ghost);
+        e = launch(Slices{h->interior, h->n_interior, h->interior_begin, h->interior_end}, false, ghost);
         ++h->launches;
         if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch (interior)");
     }
     e = launch_halo_wait(h->mb_flags, h->d_peer_ids, (int)h->peers.size(), seq, h->timeout_ns, h->d_dist_err, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "halo wait");
     if (h->n_boundary > 0) {
-        e = launch(h->boundary, h->n_boundary, true, ghost);
+        e = launch(Slices{h->boundary, h->n_boundary, -1, -1}, true, ghost);
         ++h->launches;
         if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch (boundary)");
     }
@@ -214,14 +224,15 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
         const double *xsrc = j == 1 ? st.rhs : gin;
         const double *xscale = j == 1 ? st.dT : nullptr;
         nsm_status r = pass(h, global, xsrc, xscale, s,
-                            [&](const int32_t *list, int cnt, bool with_ghost, const double *ghost) {
+                            [&](const Slices &sl, bool with_ghost, const double *ghost) {
                                 SweepArgs a{};
                                 a.n = h->n;
-                                a.nslices = cnt;
-                                a.list = list;
+                                a.nslices = sl.count;
+                                a.list = sl.list;
                                 a.T = st.T;
                                 a.TG = st.TG;
-                                a.has_ghost = with_ghost;
+                                // upper-triangle ghosts follow the local entries
+                                a.has_ghost = !with_ghost ? 0 : ((st.TG == &h->UG || st.TG == &h->UsG) ? 2 : 1);
                                 a.unit = st.dT == nullptr;
                                 a.epi = last ? last_epi : EPI_STORE;
                                 a.gin_scaled = j == 1;
@@ -235,6 +246,8 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 a.gout2 = nullptr;
                                 a.flag = h->flag;
                                 a.sweep_id = sid;
+                                if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(1, st.T->maxw))
+                                    return launch_sweep_tma(a, sl.begin, sl.end, s);
                                 return launch_sweep(a, s);
                             });
         if (r != NSM_OK) return r;
@@ -244,9 +257,11 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
 }
 
 nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double *out, bool spmv, cudaStream_t s) {
-    return pass(h, true, x, nullptr, s, [&](const int32_t *list, int cnt, bool with_ghost, const double *ghost) {
-        return launch_residual(spmv, h->n, cnt, list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost, out,
-                               s);
+    return pass(h, true, x, nullptr, s, [&](const Slices &sl, bool with_ghost, const double *ghost) {
+        if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(2, std::max(h->L.maxw, h->U.maxw)))
+            return launch_residual_tma(spmv, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, s);
+        return launch_residual(spmv, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
+                               out, s);
     });
 }
 
@@ -337,6 +352,10 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         }
     }
     if (cudaSetDevice(device) != cudaSuccess) { g_setup_err = "nsm_setup: cudaSetDevice failed"; return NSM_ERR_CUDA; }
+    // load every kernel now: a lazy load during a spinning halo wait would stall
+    preload_plain_kernels();
+    preload_tma_kernels();
+    preload_halo_kernels();
     nsm_handle *h = new nsm_handle();
     h->device = device;
     h->n = sa.n;
@@ -375,6 +394,10 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
             (g ? bnd : inner).push_back(s);
         }
         h->n_interior = (int)inner.size();
+        if (!inner.empty() && inner.back() - inner.front() + 1 == (int32_t)inner.size()) {
+            h->interior_begin = inner.front();
+            h->interior_end = inner.back() + 1;
+        }
         h->n_boundary = (int)bnd.size();
         ok = a.get(&h->interior, h->n_interior) && upload(h->interior, inner.data(), h->n_interior) &&
              a.get(&h->boundary, h->n_boundary) && upload(h->boundary, bnd.data(), h->n_boundary);
@@ -503,6 +526,18 @@ nsm_status nsm_halo_commit(nsm_handle *h) {
 }
 
 void nsm_destroy(nsm_handle *h) { free_handle(h); }
+
+nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
+    if (!h) return NSM_ERR_ARG;
+    switch (opt) {
+        case NSM_OPT_PIPELINE: h->pipeline = value != 0; return NSM_OK;
+        case NSM_OPT_HALO_TIMEOUT_MS:
+            if (value <= 0) return NSM_ERR_ARG;
+            h->timeout_ns = (unsigned long long)value * 1000000ull;
+            return NSM_OK;
+    }
+    return NSM_ERR_ARG;
+}
 
 nsm_status nsm_info(const nsm_handle *h, int64_t *n_local, int64_t *n_ghost, int64_t *nnz_offdiag,
                     int64_t *device_bytes) {

@@ -121,3 +121,11 @@ cudaError_t launch_halo_wait(const unsigned long long *flags, const int *peers, 
 }
 
 }  // namespace nsm
+
+namespace nsm {
+void preload_halo_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, k_halo_put);
+    cudaFuncGetAttributes(&a, k_halo_wait);
+}
+}  // namespace nsm

@@ -198,8 +198,11 @@ __global__ void __launch_bounds__(kThreads) k_sweep(int64_t n, int nslices, cons
     const double dn = ((EPI == EPI_STORE2 || EPI == EPI_XADD_SCALE) && row) ? __ldg(dnext + i) : 1.0;
     ct.gather_mul(gin);
     double acc = 0.0;
-    if (has_ghost) acc = accum(TG, s, lane, GatherPlain{ghost}, acc, pol);
+    // ghost couplings lie below the block for a lower triangle (has_ghost 1)
+    // and above it for an upper one (2): keep the ascending column order
+    if (has_ghost == 1) acc = accum(TG, s, lane, GatherPlain{ghost}, acc, pol);
     acc = ct.add(acc, T, gin, pol);
+    if (has_ghost == 2) acc = accum(TG, s, lane, GatherPlain{ghost}, acc, pol);
     if (!row) return;
     double v = __dsub_rn(ri, acc);
     if (!UNIT) v = __ddiv_rn(v, di);
@@ -307,4 +310,41 @@ cudaError_t launch_scale(bool xadd, int64_t n, const double *rhs, const double *
     return cudaGetLastError();
 }
 
+}  // namespace nsm
+
+// ---- eager loading ------------------------------------------------------------
+// CUDA loads kernels lazily on first launch, and a lazy load may wait for the
+// device to go idle.  A halo-wait kernel spinning on a neighbour's flag while
+// the host launches a not-yet-loaded kernel would then stall until the wait
+// times out, so multi-rank handles load every kernel up front.
+namespace nsm {
+namespace {
+template <class K>
+void touch(K k) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, k);
+}
+template <int CH>
+void touch_ch() {
+    touch(k_residual<OUT_R, CH>);
+    touch(k_residual<OUT_AX, CH>);
+    touch(k_sweep<true, EPI_STORE, GatherPlain, CH>);
+    touch(k_sweep<true, EPI_XADD, GatherPlain, CH>);
+    touch(k_sweep<true, EPI_XADD_SCALE, GatherPlain, CH>);
+    touch(k_sweep<false, EPI_STORE, GatherPlain, CH>);
+    touch(k_sweep<false, EPI_XADD, GatherPlain, CH>);
+    touch(k_sweep<false, EPI_XADD_SCALE, GatherPlain, CH>);
+    touch(k_sweep<false, EPI_STORE, GatherScaled, CH>);
+    touch(k_sweep<false, EPI_XADD, GatherScaled, CH>);
+    touch(k_sweep<false, EPI_XADD_SCALE, GatherScaled, CH>);
+}
+}  // namespace
+
+void preload_plain_kernels() {
+    touch_ch<4>();
+    touch_ch<8>();
+    touch_ch<16>();
+    touch(k_scale<true>);
+    touch(k_scale<false>);
+}
 }  // namespace nsm

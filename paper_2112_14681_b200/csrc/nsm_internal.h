@@ -72,7 +72,7 @@ struct SweepArgs {
     int nslices;
     const int32_t *list;     // slice list or nullptr (= all slices 0..nslices-1)
     const Sell *T, *TG;      // local strict triangle, ghost part (or nullptr)
-    bool has_ghost;
+    int has_ghost;           // 0: none, 1: TG columns precede T's (lower), 2: follow (upper)
     bool unit;               // unit diagonal: no division
     int epi;
     bool gin_scaled;         // gather rhs[c]/dT[c] instead of gin[c] (first sweep)
@@ -112,6 +112,17 @@ cudaError_t launch_halo_put(const PutDesc *desc, int npeers, int total_blocks, c
                             cudaStream_t st);
 cudaError_t launch_halo_wait(const unsigned long long *flags, const int *peers, int npeers, unsigned long long seq,
                              unsigned long long timeout_ns, unsigned int *dist_err, cudaStream_t st);
+
+// ---- bulk-copy pipelined kernels (stream.cu), contiguous slice ranges --------
+bool tma_ok(int np, int maxw);
+cudaError_t launch_residual_tma(bool spmv, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
+                                const double *d, const double *b, const double *x, double *out, cudaStream_t st);
+cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st);
+
+// Force-load every kernel of the library (see kernels.cu "eager loading").
+void preload_plain_kernels();
+void preload_tma_kernels();
+void preload_halo_kernels();
 
 // Host ILU(0) (nsm_ilu0).
 nsm_status ilu0_host(const nsm_csr *A, int64_t row_begin, double *fval, std::string *err);

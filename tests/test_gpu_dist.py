@@ -47,7 +47,7 @@ class VirtualRanks:
         for r in range(self.P):
             blk = A.rows(int(bounds[r]), int(bounds[r + 1]))
             F = None
-            if factors == "block":
+            if isinstance(factors, str) and factors == "block":
                 F = nsm.ilu0(blk, row_begin=int(bounds[r]))
             elif factors is not None:  # global factor values on A's pattern
                 F = factors[A.rowptr[bounds[r]]:A.rowptr[bounds[r + 1]]]

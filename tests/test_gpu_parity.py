@@ -64,12 +64,15 @@ SMALL = {
 }
 
 
-@pytest.fixture(scope="module", params=list(SMALL))
+@pytest.fixture(scope="module", params=[(c, p) for c in SMALL for p in ("pipelined", "plain")],
+                ids=lambda v: f"{v[0]}-{v[1]}")
 def case(request):
-    A = SMALL[request.param]()
+    name, pipe = request.param
+    A = SMALL[name]()
     F = oracle.ilu0(A)[2]
     S = nsm.Smoother(A, F)
-    yield request.param, A, F, S
+    S.set_pipeline(pipe == "pipelined")   # both kernel families must agree with the oracle
+    yield f"{name}/{pipe}", A, F, S
     S.close()
 
 
@@ -194,18 +197,19 @@ def test_errors_and_determinism():
 @pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
 def test_full_size_parity(cfg):
     """BASELINE.json configs at full size, in the launch configuration bench.py
-    times (one nsm_smooth per application); the oracle computes the whole
-    vector (a few seconds of CPU)."""
+    times (one nsm_smooth per application, both kernel families); the oracle
+    computes the whole vector (a few seconds of CPU)."""
     A = inputs.config_matrix(cfg)
     kind = {"C2": "ilu", "C3": "pgs", "C4": "ilu", "C5": "pgs"}[cfg]
     F = oracle.ilu0(A)[2] if kind == "ilu" else None
     b, x0 = inputs.uniform(0, A.nrows), inputs.uniform(1, A.nrows)
-    with nsm.Smoother(A, F) as S:
-        x = dev(x0)
-        S.smooth(dev(b), x, kind, nu=1, k_l=2, k_u=2)
-        got = host(x)
     if kind == "ilu":
         want = oracle.ilu_apply(A, (A.rowptr, A.col, F), b, x0, 2, 2)
     else:
         want = oracle.pgs_apply(A, b, x0, 2)
-    agree(got, want, cfg)
+    with nsm.Smoother(A, F) as S:
+        for pipe in (True, False):
+            S.set_pipeline(pipe)
+            x = dev(x0)
+            S.smooth(dev(b), x, kind, nu=1, k_l=2, k_u=2)
+            agree(host(x), want, f"{cfg} pipeline={pipe}")
