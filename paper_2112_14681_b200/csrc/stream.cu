@@ -1,23 +1,30 @@
-// stream.cu — TMA-bulk-pipelined variants of the residual and sweep kernels
-// (DESIGN.md §6 "v2: bulk-copy pipeline").
+// stream.cu — bulk-copy pipelined variants of the residual and sweep kernels
+// (DESIGN.md §6 "Kernels").
 //
 // The SELL value/index streams of a contiguous range of slices are moved
-// HBM -> shared memory by the bulk-copy engine (cp.async.bulk, completion on
-// an mbarrier), NST stages ahead of the consumers, so the DRAM stream never
-// waits for the consumers' second round trip (the x / g gathers through
-// L1/L2).  One producer warp (one elected lane) issues the copies; TS
-// consumer warps each own one slice (one thread per row) of the tile, read
-// their entries from shared memory (lane-contiguous, conflict-free), gather,
-// and accumulate in stored order — the same arithmetic sequence as the plain
-// kernels in kernels.cu, hence bit-identical results.
+// HBM -> shared memory by the bulk-copy (TMA) engine — cp.async.bulk with
+// completion on an mbarrier — NST stages ahead of the consumers, so the DRAM
+// stream does not stall while the consumers make their second round trip
+// (the x / g gathers through L1/L2).  One producer warp (one elected lane)
+// issues the copies; TS consumer warps each own one slice (one thread per
+// row) of the tile, pull a register chunk of CH entries of their row from
+// shared memory (lane-contiguous, conflict-free), issue all CH gathers
+// together, and accumulate in stored order — the same arithmetic sequence as
+// the plain kernels in kernels.cu and as the oracle, hence bit-identical
+// results.
 //
 // Tiles of TS consecutive slices are dealt round-robin to a persistent grid
-// (a multiple of the 148 SMs), so at any moment all CTAs stream neighbouring
-// tiles and the gathered vector windows stay L2-resident.
+// (a multiple of the SM count), so at any moment all CTAs stream
+// neighbouring tiles and the gathered vector windows stay L2-resident.  The
+// number of stages is chosen per matrix to maximise resident consumer warps
+// (occupancy from registers and shared memory), then pipeline depth.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "nsm_internal.h"
 
@@ -25,12 +32,10 @@ namespace nsm {
 
 namespace {
 
-constexpr int kTS = 8;                    // slices (warps) per tile
+constexpr int kTS = 8;                    // slices (consumer warps) per tile
 constexpr int kThreadsT = (kTS + 1) * 32; // + 1 producer warp
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -88,6 +93,17 @@ struct Layout {
     }
 };
 
+__device__ __forceinline__ void init_barriers(const Layout &Ly, char *sm) {
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < Ly.nst; ++st) {
+            mbar_init(Ly.full(sm) + st, 1);
+            mbar_init(Ly.empty(sm) + st, kTS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
 // Producer: stream the parts' segments of each of this CTA's tiles.
 template <int NP>
 __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellView (&P)[NP], int64_t s_begin,
@@ -118,27 +134,47 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
     }
 }
 
-// Sum over the lane's row of slice s from the staged copy (stored order).
-template <class G>
-__device__ __forceinline__ double staged_sum(const double *sv, const int32_t *sc, int64_t off, int w, int lane,
-                                             const G &g, double acc) {
-    const double *v = sv + off + lane;
-    const int32_t *c = sc + off + lane;
-    double prod[4];
-    int j = 0;
-    for (; j + 4 <= w; j += 4) {
+// Register chunk of one row taken from the staged copy: the first CH entries
+// (predicated on the slice width w) are read from shared memory, all their
+// gathers issued together, and multiplied; add() sums them in stored order
+// and continues with any entries beyond CH one by one.
+template <int CH>
+struct StagedChunk {
+    double v[CH];
+    int32_t c[CH];
+    const double *sv;
+    const int32_t *sc;
+    int w;
+    __device__ __forceinline__ void load(const double *sv_, const int32_t *sc_, int64_t off, int w_, int lane) {
+        sv = sv_ + off + lane;
+        sc = sc_ + off + lane;
+        w = w_;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) prod[u] = __dmul_rn(v[(j + u) * kSlice], g(c[(j + u) * kSlice]));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, prod[u]);
+        for (int j = 0; j < CH; ++j)
+            if (j < w) {
+                v[j] = sv[j * kSlice];
+                c[j] = sc[j * kSlice];
+            }
     }
-    for (; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn(v[j * kSlice], g(c[j * kSlice])));
-    return acc;
-}
+    template <class G>
+    __device__ __forceinline__ void gather_mul(const G &g) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) v[j] = __dmul_rn(v[j], g(c[j]));
+    }
+    template <class G>
+    __device__ __forceinline__ double add(double acc, const G &g) const {
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) acc = __dadd_rn(acc, v[j]);
+        for (int j = CH; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn(sv[j * kSlice], g(sc[j * kSlice])));
+        return acc;
+    }
+};
 
 enum { OUTT_R = 0, OUTT_AX = 1 };
 
-template <int OUT>
+template <int OUT, int CH>
 __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView L,
                                                             SellView U, const double *__restrict__ d,
                                                             const double *__restrict__ b,
@@ -148,14 +184,7 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
     const Layout Ly{nst, 2, cap};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < nst; ++st) {
-            mbar_init(Ly.full(sm) + st, 1);
-            mbar_init(Ly.empty(sm) + st, kTS);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
+    init_barriers(Ly, sm);
     if (warp == kTS) {
         if (lane == 0) {
             const SellView P[2] = {L, U};
@@ -186,19 +215,35 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
             uw = (int)((us1 - us) / kSlice);
         }
         mbar_wait(Ly.full(sm) + st, use & 1);
+        double acc = 0.0;
         if (has) {
-            double acc = 0.0;
-            acc = staged_sum(Ly.val(sm, st, 0), Ly.col(sm, st, 0), lo, lw, lane, gx, acc);
-            acc = __dadd_rn(acc, __dmul_rn(di, xi));
-            acc = staged_sum(Ly.val(sm, st, 1), Ly.col(sm, st, 1), uo, uw, lane, gx, acc);
-            if (row) out[i] = OUT == OUTT_R ? __dsub_rn(bi, acc) : acc;
+            if constexpr (CH <= 8) {  // both triangles' gathers in flight together
+                StagedChunk<CH> cl, cu;
+                cl.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), lo, lw, lane);
+                cu.load(Ly.val(sm, st, 1), Ly.col(sm, st, 1), uo, uw, lane);
+                cl.gather_mul(gx);
+                cu.gather_mul(gx);
+                acc = cl.add(acc, gx);
+                acc = __dadd_rn(acc, __dmul_rn(di, xi));
+                acc = cu.add(acc, gx);
+            } else {                  // wide rows: one triangle at a time (registers)
+                StagedChunk<CH> c;
+                c.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), lo, lw, lane);
+                c.gather_mul(gx);
+                acc = c.add(acc, gx);
+                acc = __dadd_rn(acc, __dmul_rn(di, xi));
+                c.load(Ly.val(sm, st, 1), Ly.col(sm, st, 1), uo, uw, lane);
+                c.gather_mul(gx);
+                acc = c.add(acc, gx);
+            }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(Ly.empty(sm) + st);
+        if (lane == 0) mbar_arrive(Ly.empty(sm) + st);  // the stage may be refilled
+        if (row) out[i] = OUT == OUTT_R ? __dsub_rn(bi, acc) : acc;
     }
 }
 
-template <bool UNIT, int EPI, class G>
+template <bool UNIT, int EPI, class G, int CH>
 __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView T,
                                                          const double *__restrict__ dT,
                                                          const double *__restrict__ rhs, G gin,
@@ -210,14 +255,7 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
     const Layout Ly{nst, 1, cap};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < nst; ++st) {
-            mbar_init(Ly.full(sm) + st, 1);
-            mbar_init(Ly.empty(sm) + st, kTS);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
+    init_barriers(Ly, sm);
     if (warp == kTS) {
         if (lane == 0) {
             const SellView P[1] = {T};
@@ -245,8 +283,16 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
             tw = (int)((ts1 - ts) / kSlice);
         }
         mbar_wait(Ly.full(sm) + st, use & 1);
+        double acc = 0.0;
+        if (has) {
+            StagedChunk<CH> ct;
+            ct.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), to, tw, lane);
+            ct.gather_mul(gin);
+            acc = ct.add(acc, gin);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(Ly.empty(sm) + st);
         if (row) {
-            const double acc = staged_sum(Ly.val(sm, st, 0), Ly.col(sm, st, 0), to, tw, lane, gin, 0.0);
             double v = __dsub_rn(ri, acc);
             if (!UNIT) v = __ddiv_rn(v, di);
             if (!isfinite(v)) atomicMin(flag, (unsigned long long)sweep_id);
@@ -254,34 +300,11 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
             if (EPI == EPI_XADD) x[i] = __dadd_rn(xi, v);
             if (EPI == EPI_XADD_SCALE) x[i] = __dadd_rn(xi, __ddiv_rn(v, dn));
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(Ly.empty(sm) + st);
     }
 }
 
 // ---- launch geometry ---------------------------------------------------------
-constexpr int64_t kSmemBudget = 200 * 1024;   // per CTA (opt-in max is 227 KB)
-
-struct Geo {
-    int nst = 0;
-    int64_t cap = 0;
-    size_t smem = 0;
-    bool ok = false;
-};
-
-Geo geometry(int np, int maxw) {
-    Geo g;
-    g.cap = (int64_t)kTS * kSlice * std::max(maxw, 1);
-    const int64_t stage = np * g.cap * 12;
-    for (int nst = 4; nst >= 2; --nst)
-        if (128 + nst * stage <= kSmemBudget) {
-            g.nst = nst;
-            break;
-        }
-    g.smem = (size_t)(128 + g.nst * stage);
-    g.ok = g.nst >= 2;
-    return g;
-}
+constexpr int64_t kSmemMax = 220 * 1024;  // per CTA (opt-in max 227 KB)
 
 int sm_count() {
     static int n = 0;
@@ -294,94 +317,159 @@ int sm_count() {
     return n;
 }
 
-template <class K>
-int grid_tma(K kernel, size_t smem, int64_t ntiles) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+inline int chunk_for_t(int maxw) { return maxw <= 4 ? 4 : (maxw <= 8 ? 8 : 16); }
+
+struct Geo {
+    int nst = 0;
+    int64_t cap = 0;
+    size_t smem = 0;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreadsT, smem);
-    per_sm = std::max(per_sm, 1);
-    return (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * per_sm);
+};
+
+// Stages per CTA: maximise resident consumer warps (capped at 32 per SM),
+// then the pipeline depth.  Cached per kernel and stage size.
+template <class K>
+Geo geometry(K kernel, int np, int maxw) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int64_t>, Geo> cache;
+    Geo g;
+    g.cap = (int64_t)kTS * kSlice * std::max(maxw, 1);
+    const int64_t stage = np * g.cap * 12;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair((const void *)kernel, stage);
+    auto itc = cache.find(key);
+    if (itc != cache.end()) return itc->second;
+    int best_warps = -1;
+    for (int nst = 2; nst <= 6; ++nst) {
+        const int64_t smem = 128 + nst * stage;
+        if (smem > kSmemMax) break;
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreadsT, (size_t)smem);
+        const int warps = std::min(per_sm * kTS, 32);
+        if (per_sm > 0 && warps >= best_warps) {  // ties: deeper pipeline
+            best_warps = warps;
+            g.nst = nst;
+            g.smem = (size_t)smem;
+            g.per_sm = per_sm;
+        }
+    }
+    if (g.nst) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    cache[key] = g;
+    return g;
 }
 
-template <bool UNIT, int EPI, class G>
-cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end, G gin, const Geo &g,
-                             cudaStream_t st) {
-    auto k = k_sweep_tma<UNIT, EPI, G>;
+template <class K>
+int grid_of(const Geo &g, int64_t ntiles) {
+    return (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(g.per_sm, 1));
+}
+
+template <int OUT, int CH>
+cudaError_t residual_tma_ch(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
+                            const double *d, const double *b, const double *x, double *out, cudaStream_t st) {
+    auto k = k_residual_tma<OUT, CH>;
+    const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw));
+    if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    const int grid = grid_tma(k, g.smem, ntiles);
-    k<<<grid, kThreadsT, g.smem, st>>>(a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs, gin, a.gout, a.x, a.dnext,
-                                       a.flag, a.sweep_id, g.nst, g.cap);
+    k<<<grid_of<decltype(k)>(g, ntiles), kThreadsT, g.smem, st>>>(n, s_begin, s_end, view(L), view(U), d, b, x, out,
+                                                                  g.nst, g.cap);
     return cudaGetLastError();
 }
 
-template <bool UNIT, int EPI>
-cudaError_t sweep_tma_epi(const SweepArgs &a, int64_t s_begin, int64_t s_end, const Geo &g, cudaStream_t st) {
+template <bool UNIT, int EPI, class G, int CH>
+cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end, G gin, cudaStream_t st) {
+    auto k = k_sweep_tma<UNIT, EPI, G, CH>;
+    const Geo g = geometry(k, 1, a.T->maxw);
+    if (!g.nst) return cudaErrorInvalidConfiguration;
+    const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
+    k<<<grid_of<decltype(k)>(g, ntiles), kThreadsT, g.smem, st>>>(a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs, gin,
+                                                                  a.gout, a.x, a.dnext, a.flag, a.sweep_id, g.nst,
+                                                                  g.cap);
+    return cudaGetLastError();
+}
+
+template <bool UNIT, int EPI, int CH>
+cudaError_t sweep_tma_g(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st) {
     if constexpr (!UNIT) {
-        if (a.gin_scaled) return sweep_tma_launch<UNIT, EPI>(a, s_begin, s_end, GatherScaledT{a.rhs, a.dT}, g, st);
+        if (a.gin_scaled)
+            return sweep_tma_launch<UNIT, EPI, GatherScaledT, CH>(a, s_begin, s_end, GatherScaledT{a.rhs, a.dT}, st);
     }
-    return sweep_tma_launch<UNIT, EPI>(a, s_begin, s_end, GatherPlainT{a.gin_scaled ? a.rhs : a.gin}, g, st);
+    return sweep_tma_launch<UNIT, EPI, GatherPlainT, CH>(a, s_begin, s_end,
+                                                          GatherPlainT{a.gin_scaled ? a.rhs : a.gin}, st);
+}
+
+template <bool UNIT, int EPI>
+cudaError_t sweep_tma_epi(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st) {
+    switch (chunk_for_t(a.T->maxw)) {
+        case 4: return sweep_tma_g<UNIT, EPI, 4>(a, s_begin, s_end, st);
+        case 8: return sweep_tma_g<UNIT, EPI, 8>(a, s_begin, s_end, st);
+        default: return sweep_tma_g<UNIT, EPI, 16>(a, s_begin, s_end, st);
+    }
 }
 
 }  // namespace
 
-bool tma_ok(int np, int maxw) { return geometry(np, maxw).ok; }
+// Shared memory of one stage must fit (two stages at least).
+bool tma_ok(int np, int maxw) {
+    const int64_t stage = np * (int64_t)kTS * kSlice * std::max(maxw, 1) * 12;
+    return 128 + 2 * stage <= kSmemMax;
+}
 
 cudaError_t launch_residual_tma(bool spmv, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
                                 const double *d, const double *b, const double *x, double *out, cudaStream_t st) {
     if (s_end <= s_begin) return cudaSuccess;
-    const Geo g = geometry(2, std::max(L.maxw, U.maxw));
-    const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    if (spmv) {
-        auto k = k_residual_tma<OUTT_AX>;
-        k<<<grid_tma(k, g.smem, ntiles), kThreadsT, g.smem, st>>>(n, s_begin, s_end, view(L), view(U), d, b, x, out,
-                                                                 g.nst, g.cap);
-    } else {
-        auto k = k_residual_tma<OUTT_R>;
-        k<<<grid_tma(k, g.smem, ntiles), kThreadsT, g.smem, st>>>(n, s_begin, s_end, view(L), view(U), d, b, x, out,
-                                                                 g.nst, g.cap);
-    }
-    return cudaGetLastError();
+    const int ch = chunk_for_t(std::max(L.maxw, U.maxw));
+#define NSM_RT(OUT)                                                                            \
+    (ch == 4 ? residual_tma_ch<OUT, 4>(n, s_begin, s_end, L, U, d, b, x, out, st)              \
+             : ch == 8 ? residual_tma_ch<OUT, 8>(n, s_begin, s_end, L, U, d, b, x, out, st)    \
+                       : residual_tma_ch<OUT, 16>(n, s_begin, s_end, L, U, d, b, x, out, st))
+    return spmv ? NSM_RT(OUTT_AX) : NSM_RT(OUTT_R);
+#undef NSM_RT
 }
 
 cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st) {
     if (s_end <= s_begin) return cudaSuccess;
-    const Geo g = geometry(1, a.T->maxw);
     if (a.unit) {
         switch (a.epi) {
-            case EPI_STORE: return sweep_tma_epi<true, EPI_STORE>(a, s_begin, s_end, g, st);
-            case EPI_XADD: return sweep_tma_epi<true, EPI_XADD>(a, s_begin, s_end, g, st);
-            default: return sweep_tma_epi<true, EPI_XADD_SCALE>(a, s_begin, s_end, g, st);
+            case EPI_STORE: return sweep_tma_epi<true, EPI_STORE>(a, s_begin, s_end, st);
+            case EPI_XADD: return sweep_tma_epi<true, EPI_XADD>(a, s_begin, s_end, st);
+            default: return sweep_tma_epi<true, EPI_XADD_SCALE>(a, s_begin, s_end, st);
         }
     }
     switch (a.epi) {
-        case EPI_STORE: return sweep_tma_epi<false, EPI_STORE>(a, s_begin, s_end, g, st);
-        case EPI_XADD: return sweep_tma_epi<false, EPI_XADD>(a, s_begin, s_end, g, st);
-        default: return sweep_tma_epi<false, EPI_XADD_SCALE>(a, s_begin, s_end, g, st);
+        case EPI_STORE: return sweep_tma_epi<false, EPI_STORE>(a, s_begin, s_end, st);
+        case EPI_XADD: return sweep_tma_epi<false, EPI_XADD>(a, s_begin, s_end, st);
+        default: return sweep_tma_epi<false, EPI_XADD_SCALE>(a, s_begin, s_end, st);
     }
 }
 
-}  // namespace nsm
-
-namespace nsm {
+// ---- eager loading (see kernels.cu) --------------------------------------------
 namespace {
 template <class K>
 void touch_t(K k) {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, k);
 }
+template <int CH>
+void touch_tma_ch() {
+    touch_t(k_residual_tma<OUTT_R, CH>);
+    touch_t(k_residual_tma<OUTT_AX, CH>);
+    touch_t(k_sweep_tma<true, EPI_STORE, GatherPlainT, CH>);
+    touch_t(k_sweep_tma<true, EPI_XADD, GatherPlainT, CH>);
+    touch_t(k_sweep_tma<true, EPI_XADD_SCALE, GatherPlainT, CH>);
+    touch_t(k_sweep_tma<false, EPI_STORE, GatherPlainT, CH>);
+    touch_t(k_sweep_tma<false, EPI_XADD, GatherPlainT, CH>);
+    touch_t(k_sweep_tma<false, EPI_XADD_SCALE, GatherPlainT, CH>);
+    touch_t(k_sweep_tma<false, EPI_STORE, GatherScaledT, CH>);
+    touch_t(k_sweep_tma<false, EPI_XADD, GatherScaledT, CH>);
+    touch_t(k_sweep_tma<false, EPI_XADD_SCALE, GatherScaledT, CH>);
+}
 }  // namespace
 
 void preload_tma_kernels() {
-    touch_t(k_residual_tma<OUTT_R>);
-    touch_t(k_residual_tma<OUTT_AX>);
-    touch_t(k_sweep_tma<true, EPI_STORE, GatherPlainT>);
-    touch_t(k_sweep_tma<true, EPI_XADD, GatherPlainT>);
-    touch_t(k_sweep_tma<true, EPI_XADD_SCALE, GatherPlainT>);
-    touch_t(k_sweep_tma<false, EPI_STORE, GatherPlainT>);
-    touch_t(k_sweep_tma<false, EPI_XADD, GatherPlainT>);
-    touch_t(k_sweep_tma<false, EPI_XADD_SCALE, GatherPlainT>);
-    touch_t(k_sweep_tma<false, EPI_STORE, GatherScaledT>);
-    touch_t(k_sweep_tma<false, EPI_XADD, GatherScaledT>);
-    touch_t(k_sweep_tma<false, EPI_XADD_SCALE, GatherScaledT>);
+    touch_tma_ch<4>();
+    touch_tma_ch<8>();
+    touch_tma_ch<16>();
 }
+
 }  // namespace nsm
