@@ -340,10 +340,12 @@ Geo geometry(K kernel, int np, int maxw) {
     auto itc = cache.find(key);
     if (itc != cache.end()) return itc->second;
     int best_warps = -1;
+    // the attribute is per kernel (shared by all handles): allow the maximum
+    // once; each launch passes its own dynamic size
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
     for (int nst = 2; nst <= 6; ++nst) {
         const int64_t smem = 128 + nst * stage;
         if (smem > kSmemMax) break;
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreadsT, (size_t)smem);
         const int warps = std::min(per_sm * kTS, 32);
@@ -354,7 +356,6 @@ Geo geometry(K kernel, int np, int maxw) {
             g.per_sm = per_sm;
         }
     }
-    if (g.nst) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     cache[key] = g;
     return g;
 }

@@ -1,0 +1,125 @@
+"""Pins of the oracle's AMG / GMRES driver (-m "not gpu"): the defining
+properties of each setup step checked independently of its implementation
+(brute-force independence, constant interpolation, Galerkin symmetry, exact
+coarse solve, GMRES against a direct solve)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+import inputs
+import oracle
+from oracle import amg
+
+
+def rand_fn(level, n):
+    return inputs.uniform(1000 + level, n, 0.0, 1.0)
+
+
+def test_strength_rule():
+    A = sp.csr_matrix(np.array([[4.0, -1.0, -0.2, 0.5], [-1.0, 4.0, 0.0, -3.0], [0.1, 0.0, 1.0, -0.1],
+                                [0.0, -2.0, -2.0, 5.0]]))
+    S = amg.strength(A, 0.25).toarray()
+    # row 0: max |off| = 1 -> keep |a| >= 0.25: cols 1 and 3 (|0.5|), not 2 (0.2)
+    assert S[0].tolist() == [0, 1, 0, 1]
+    assert S[1].tolist() == [1, 0, 0, 1]       # max 3: |-1| >= 0.75 is strong too
+    assert S[2].tolist() == [1, 0, 0, 1]
+    assert S[3].tolist() == [0, 1, 1, 0]
+
+
+def test_strength_rule_row1():
+    A = sp.csr_matrix(np.array([[2.0, -1.0, 0.0], [-1.0, 4.0, -3.0], [0.0, -1.0, 2.0]]))
+    S = amg.strength(A, 0.25).toarray()
+    assert S[1].tolist() == [1, 0, 1]  # |-1| >= 0.25 * 3
+
+
+@pytest.mark.parametrize("shape", [(9, 1, 1), (8, 8, 1), (5, 5, 4)])
+def test_pmis_independent_and_maximal(shape):
+    nx, ny, nz = shape
+    if ny == 1:
+        A = sp.diags([-np.ones(nx - 1), 2 * np.ones(nx), -np.ones(nx - 1)], [-1, 0, 1]).tocsr()
+    else:
+        A = inputs.laplace(nx, ny, nz).to_scipy()
+    S = amg.strength(A, 0.25)
+    cf = amg.pmis(S, rand_fn(0, A.shape[0]))
+    G = (S + S.T).toarray() > 0
+    C = np.nonzero(cf == 1)[0]
+    # independence in the symmetrised strong graph (brute force)
+    assert not np.any(G[np.ix_(C, C)])
+    # every F point with strong connections strongly depends on some C point
+    Sd = S.toarray() > 0
+    for i in np.nonzero(cf == 0)[0]:
+        if Sd[i].any():
+            assert Sd[i, C].any()
+    assert 0 < len(C) < A.shape[0]
+
+
+def test_bamg_interpolates_constants():
+    """For zero-row-sum rows (f = 1 is the near null space) the BAMG-direct
+    weights of every F point with strong C-neighbours sum to 1."""
+    N = 8
+    A = inputs.laplace(N, N, 1).to_scipy().tolil()
+    A.setdiag(0.0)
+    A = A.tocsr()
+    A = A - sp.diags(np.asarray(A.sum(1)).ravel())   # pure-Neumann 5-point: zero row sums
+    A = sp.csr_matrix(A)
+    S = amg.strength(A, 0.25)
+    cf = amg.pmis(S, rand_fn(0, A.shape[0]))
+    P = amg.bamg_direct(A, S, cf)
+    rs = np.asarray(P.sum(1)).ravel()
+    nonempty = np.diff(P.indptr) > 0
+    np.testing.assert_allclose(rs[nonempty], 1.0, rtol=0, atol=1e-12)
+    assert np.all(rs[cf == 1] == 1.0)
+
+
+def test_galerkin_symmetric_and_hierarchy_shrinks():
+    A = inputs.var27(10).to_scipy()
+    levels = amg.hierarchy(A, rand_fn, min_coarse=100)
+    assert len(levels) >= 3
+    for (Ak, Pk), (An, _) in zip(levels, levels[1:]):
+        assert An.shape[0] < Ak.shape[0]
+        np.testing.assert_allclose((An - An.T).toarray(), 0, atol=1e-9 * abs(An).max())
+        np.testing.assert_allclose((Pk.T @ Ak @ Pk - An).toarray(), 0, atol=1e-12 * abs(An).max())
+    assert levels[-1][0].shape[0] <= 100
+
+
+def test_single_level_vcycle_is_exact():
+    A = inputs.laplace(6, 6, 1).to_scipy()
+    levels = [(A, None)]
+    b = inputs.uniform(0, A.shape[0])
+    x = amg.vcycle(levels, None, b, lu=amg.coarse_lu(levels))
+    np.testing.assert_allclose(A @ x, b, rtol=1e-12, atol=1e-12)
+
+
+def test_vcycle_is_linear():
+    A = inputs.laplace(12, 12, 1).to_scipy()
+    levels = amg.hierarchy(A, rand_fn, min_coarse=20)
+    lu = amg.coarse_lu(levels)
+    sm = lambda lev, M, b, x, z: oracle.pgs_apply(M, b, x, 2, x_is_zero=z)
+    b1, b2 = inputs.uniform(0, A.shape[0]), inputs.uniform(1, A.shape[0])
+    v = amg.vcycle(levels, sm, b1 + 2 * b2, lu=lu)
+    w = amg.vcycle(levels, sm, b1, lu=lu) + 2 * amg.vcycle(levels, sm, b2, lu=lu)
+    np.testing.assert_allclose(v, w, rtol=1e-12, atol=1e-12)
+
+
+def test_gmres_identity_precond_matches_direct():
+    A = inputs.convdiff(5, rcm=False).to_scipy()
+    b = inputs.uniform(0, A.shape[0])
+    x, its, hist = amg.gmres(A, b, lambda v: v, tol=1e-12, maxit=200)
+    np.testing.assert_allclose(x, spla.spsolve(A.tocsc(), b), rtol=1e-9)
+    assert its <= A.shape[0]
+    assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) < 1e-11   # implicit == true residual
+
+
+def test_gmres_amg_pgs_poisson64():
+    """GMRES + V(1,1) C-AMG with pGS (k = 2) on 2-D Poisson 64 x 64 reaches
+    1e-8 in a handful of iterations (SPEC acceptance 6: <= 30)."""
+    A = inputs.config_matrix("C1").to_scipy()
+    levels = amg.hierarchy(A, rand_fn, min_coarse=100)
+    lu = amg.coarse_lu(levels)
+    sm = lambda lev, M, b, x, z: oracle.pgs_apply(M, b, x, 2, x_is_zero=z)
+    b = inputs.uniform(0, A.shape[0])
+    x, its, hist = amg.gmres(A, b, lambda v: amg.vcycle(levels, sm, v, lu=lu), tol=1e-8)
+    assert its <= 30
+    assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) < 1e-7
+    assert all(h2 <= h1 * (1 + 1e-12) for h1, h2 in zip(hist, hist[1:]))   # GMRES residuals never grow
