@@ -256,9 +256,9 @@ def run_nsm(args, rank, nranks, local_rank):
     launches = S.stats()[0] - launches0
     S.check()
     t_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
-    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=dev if not args.same_device else "cpu")
     if nranks > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)   # max over ranks
     t_ms = float(t.item())
     ms_step = t_ms / args.steps
     value = ab * nranks * args.steps / (t_ms * 1e-3) / 1e9
@@ -302,7 +302,8 @@ def run_nsm(args, rank, nranks, local_rank):
         xo.copy_(xd, non_blocking=True)
         e1.record(stream)
     barrier()
-    te = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in eev)], dtype=torch.float64, device=dev)
+    te = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in eev)], dtype=torch.float64,
+                      device=dev if not args.same_device else "cpu")
     if nranks > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = ab * nranks * args.steps / (float(te.item()) * 1e-3) / 1e9
@@ -356,10 +357,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--plain", action="store_true", help="plain register-blocked kernels instead of the bulk-copy pipelined ones")
+    ap.add_argument("--same-device", action="store_true",
+                    help="test mode: every rank on cuda:0 (halo over same-device IPC), gloo plumbing")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     nranks = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, nranks)
         return
@@ -367,7 +372,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_nsm(args, rank, nranks, local_rank)
     if nranks > 1:
         import torch.distributed as dist
