@@ -47,26 +47,32 @@ def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k
     every n-vector the kernel reads or writes once; gathered neighbour values
     are counted once (they hit L1/L2 after first touch)."""
     res = 12 * nnz_off + 32 * n + 8 * n_ghost           # A streams, d, x, b, write r
-    out = {"residual": res}
+    out = {}
     if kind == "pgs":
+        # with sweeps following, the residual pass also writes g0 = r / d
+        out["residual"] = res + (8 * n if k_l > 0 else 0)
         sw = []
         for j in range(1, k_l + 1):
-            b = 12 * nnz_l + 16 * n                       # L streams, rhs, d
-            b += 0 if j == 1 else 8 * n                   # previous iterate (first sweep recomputes r/d)
+            b = 12 * nnz_l + 24 * n                       # L streams, r, d, previous iterate (g0 first)
             b += 16 * n if j == k_l else 8 * n            # last: x read+write; else write g
             sw.append(b)
         if k_l == 0:
             sw.append(32 * n)                             # x += r/d
         out["sweeps"] = sw
     else:
+        out["residual"] = res
         sl, su = [], []
         for j in range(1, k_l + 1):
-            b = 12 * nnz_l + 8 * n + (0 if j == 1 else 8 * n) + 8 * n   # Ls, rhs, prev iterate, write y
+            b = 12 * nnz_l + 8 * n + (0 if j == 1 else 8 * n)   # Ls, r (the first iterate is r), prev iterate
             if j == k_l and k_u == 0:
-                b += 16 * n                               # dU, x read+write instead of the y write
+                b += 24 * n                               # dU, x read+write
+            elif j == k_l:
+                b += 24 * n                               # write y, dU, write z0 = y / dU
+            else:
+                b += 8 * n                                # write y
             sl.append(b)
         for j in range(1, k_u + 1):
-            b = 12 * nnz_u + 16 * n + (0 if j == 1 else 8 * n)  # Us, y, dU, prev iterate
+            b = 12 * nnz_u + 24 * n                       # Us, y, dU, previous iterate (z0 first)
             b += 16 * n if j == k_u else 8 * n
             su.append(b)
         if k_l == 0 and k_u == 0:

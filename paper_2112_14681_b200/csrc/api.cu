@@ -43,8 +43,8 @@ struct nsm_handle {
     bool has_ilu = false;
     double *dU = nullptr;
     Sell Ls, Us, LsG, UsG;
-    // workspace: three n-vectors, divergence flag
-    double *w[3] = {nullptr, nullptr, nullptr};
+    // workspace: four n-vectors (residual, ping-pong iterates, g^(0)), divergence flag
+    double *w[4] = {nullptr, nullptr, nullptr, nullptr};
     unsigned long long *flag = nullptr;
     int64_t sweep_counter = 0;
     int64_t launches = 0, exchanges = 0;
@@ -209,20 +209,23 @@ struct Stage {
     const double *dT;    // nullptr = unit diagonal
     const double *rhs;
     int k;
+    const double *g0 = nullptr;  // materialised g^(0) (else recomputed as rhs / dT)
 };
 
 nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB, int last_epi, double *last_out,
-                      double *x, const double *dnext, cudaStream_t s) {
+                      double *x, const double *dnext, cudaStream_t s, double *gout2 = nullptr) {
     const bool global = distributed(h) && h->mode == NSM_DIST_GLOBAL;
-    const double *gin = nullptr;
+    const double *gin = st.g0;
     for (int j = 1; j <= st.k; ++j) {
         const bool last = j == st.k;
         double *out = last ? last_out : ((j & 1) ? bufA : bufB);
         const int64_t sid = ++h->sweep_counter;
+        const bool scaled = j == 1 && !st.g0;
         // the ghost values a GLOBAL sweep needs are those of its input iterate:
-        // g^(0) = rhs / dT for the first sweep, the previous output after that
-        const double *xsrc = j == 1 ? st.rhs : gin;
-        const double *xscale = j == 1 ? st.dT : nullptr;
+        // g^(0) (materialised, or rhs / dT) for the first sweep, then the
+        // previous output
+        const double *xsrc = scaled ? st.rhs : gin;
+        const double *xscale = scaled ? st.dT : nullptr;
         nsm_status r = pass(h, global, xsrc, xscale, s,
                             [&](const Slices &sl, bool with_ghost, const double *ghost) {
                                 SweepArgs a{};
@@ -235,7 +238,7 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 a.has_ghost = !with_ghost ? 0 : ((st.TG == &h->UG || st.TG == &h->UsG) ? 2 : 1);
                                 a.unit = st.dT == nullptr;
                                 a.epi = last ? last_epi : EPI_STORE;
-                                a.gin_scaled = j == 1;
+                                a.gin_scaled = scaled;
                                 a.dT = st.dT;
                                 a.rhs = st.rhs;
                                 a.gin = gin;
@@ -243,7 +246,7 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 a.gout = out;
                                 a.x = x;
                                 a.dnext = dnext;
-                                a.gout2 = nullptr;
+                                a.gout2 = last ? gout2 : nullptr;
                                 a.flag = h->flag;
                                 a.sweep_id = sid;
                                 if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(1, st.T->maxw))
@@ -256,12 +259,14 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
     return NSM_OK;
 }
 
-nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double *out, bool spmv, cudaStream_t s) {
+// mode OUT_R: out = b - A x; OUT_AX: out = A x; OUT_RG: also out2 = out / d.
+nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double *out, int mode, cudaStream_t s,
+                         double *out2 = nullptr) {
     return pass(h, true, x, nullptr, s, [&](const Slices &sl, bool with_ghost, const double *ghost) {
         if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(2, std::max(h->L.maxw, h->U.maxw)))
-            return launch_residual_tma(spmv, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, s);
-        return launch_residual(spmv, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
-                               out, s);
+            return launch_residual_tma(mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, s);
+        return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
+                               out, out2, s);
     });
 }
 
@@ -374,7 +379,7 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         ok = a.get(&h->dU, h->n) && upload(h->dU, sf.d.data(), h->n) && upload_sell(a, sf.L, &h->Ls) &&
              upload_sell(a, sf.U, &h->Us) && upload_sell(a, sf.LG, &h->LsG) && upload_sell(a, sf.UG, &h->UsG);
     }
-    for (int i = 0; ok && i < 3; ++i) ok = a.get(&h->w[i], std::max<int64_t>(h->n, 1));
+    for (int i = 0; ok && i < 4; ++i) ok = a.get(&h->w[i], std::max<int64_t>(h->n, 1));
     ok = ok && a.get(&h->flag, 1) && a.get(&h->ghost_null, 1);
     if (ok) {
         unsigned long long init = ULLONG_MAX;
@@ -562,13 +567,13 @@ nsm_status nsm_residual(nsm_handle *h, const double *b, const double *x, double 
         h->err = "nsm_residual: NULL or aliased vector";
         return NSM_ERR_ARG;
     }
-    return residual_into(h, b, x, r, false, S(stream));
+    return residual_into(h, b, x, r, OUT_R, S(stream));
 }
 
 nsm_status nsm_spmv(nsm_handle *h, const double *x, double *y, void *stream) {
     if (!h) return NSM_ERR_ARG;
     if ((h->n > 0 && (!x || !y)) || overlap(x, y, h->n)) { h->err = "nsm_spmv: NULL or aliased vector"; return NSM_ERR_ARG; }
-    return residual_into(h, nullptr, x, y, true, S(stream));
+    return residual_into(h, nullptr, x, y, OUT_AX, S(stream));
 }
 
 static nsm_status tri_solve(nsm_handle *h, bool lower, const double *r, double *x, int k, void *stream) {
@@ -603,46 +608,55 @@ nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, 
     if (kind != NSM_PGS && kind != NSM_ILU0) { h->err = "nsm_smooth: unknown kind"; return NSM_ERR_ARG; }
     if (kind == NSM_ILU0 && !h->has_ilu) { h->err = "nsm_smooth: ILU0 requested on a handle without factors"; return NSM_ERR_STATE; }
     cudaStream_t s = S(stream);
-    double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2];
+    double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
     for (int it = 0; it < nu; ++it) {
         // row a2: residual; x == 0 => r = b exactly (reading R3)
-        const double *rhs = b;
-        if (!(it == 0 && x_is_zero)) {
-            nsm_status st = residual_into(h, b, x, R, false, s);
-            if (st != NSM_OK) return st;
-            rhs = R;
-        }
+        const bool fresh = it == 0 && x_is_zero;
+        const double *rhs = fresh ? b : R;
         nsm_status st = NSM_OK;
         if (kind == NSM_PGS) {
+            // the residual pass also writes g^(0) = r / d (eq:jr-initial-guess)
+            // when sweeps follow, so the first sweep gathers it instead of
+            // dividing per gathered entry
+            const bool rg = !fresh && k_l > 0;
+            if (!fresh) st = residual_into(h, b, x, R, rg ? OUT_RG : OUT_R, s, rg ? W2 : nullptr);
+            if (st != NSM_OK) return st;
             // rows a3/a4: k_l sweeps g <- D^{-1}(r - L g), the last fused with x += g
             if (k_l == 0) st = scale_into(h, true, rhs, h->d, x, s);
-            else st = run_sweeps(h, Stage{&h->L, &h->LG, h->d, rhs, k_l}, W0, W1, EPI_XADD, nullptr, x, nullptr, s);
+            else {
+                Stage sg{&h->L, &h->LG, h->d, rhs, k_l, rg ? W2 : nullptr};
+                st = run_sweeps(h, sg, W0, W1, EPI_XADD, nullptr, x, nullptr, s);
+            }
         } else {
+            if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
+            if (st != NSM_OK) return st;
             // row a5: y = sum_{j<=kL} (-Ls)^j r ; z = sum_{j<=kU} (-DU^{-1}Us)^j DU^{-1} y ; x += z
             const double *y = rhs;
+            const double *z0 = nullptr;
             if (k_l > 0) {
-                // L sweeps ping-pong in W0/W1; the last writes y (z^(0) = y/dU is
-                // recomputed in the first U sweep's gather, so only y is stored)
+                // L sweeps ping-pong in W0/W1; the last writes y and, when U
+                // sweeps follow, z^(0) = y / dU into W2 (EPI_STORE2)
                 double *ybuf = (k_l & 1) ? W0 : W1;
-                if (k_u == 0)
-                    st = run_sweeps(h, Stage{&h->Ls, &h->LsG, nullptr, rhs, k_l}, W0, W1, EPI_XADD_SCALE, nullptr, x,
-                                    h->dU, s);
-                else
-                    st = run_sweeps(h, Stage{&h->Ls, &h->LsG, nullptr, rhs, k_l}, W0, W1, EPI_STORE, ybuf, nullptr,
-                                    nullptr, s);
+                Stage sl{&h->Ls, &h->LsG, nullptr, rhs, k_l};
+                if (k_u == 0) st = run_sweeps(h, sl, W0, W1, EPI_XADD_SCALE, nullptr, x, h->dU, s);
+                else {
+                    st = run_sweeps(h, sl, W0, W1, EPI_STORE2, ybuf, nullptr, h->dU, s, W2);
+                    z0 = W2;
+                }
                 if (st != NSM_OK) return st;
                 y = ybuf;
             } else if (k_u == 0) {
                 st = scale_into(h, true, rhs, h->dU, x, s);
             }
             if (st == NSM_OK && k_u > 0) {
-                // z ping-pong in the two work vectors not holding y (R is free
-                // once the L stage has consumed the residual)
+                // z ping-pong in buffers holding neither y nor (for the first
+                // U sweep) z^(0)
                 double *za, *zb;
-                if (y == W0) { za = R; zb = W1; }
-                else if (y == W1) { za = R; zb = W0; }
+                if (y == W0) { za = W1; zb = W2; }
+                else if (y == W1) { za = W0; zb = W2; }
                 else { za = W0; zb = W1; }
-                st = run_sweeps(h, Stage{&h->Us, &h->UsG, h->dU, y, k_u}, za, zb, EPI_XADD, nullptr, x, nullptr, s);
+                st = run_sweeps(h, Stage{&h->Us, &h->UsG, h->dU, y, k_u, z0}, za, zb, EPI_XADD, nullptr, x, nullptr,
+                                s);
             }
         }
         if (st != NSM_OK) return st;

@@ -131,15 +131,16 @@ __device__ __forceinline__ bool slice_of(int nslices, const int32_t *list, int64
 
 // ---- residual / SpMV (row a2) ------------------------------------------------
 // acc_i = sum_{j ascending} a_ij x_j over LG (ghosts below), L, D, U, UG
-// (ghosts above); then  OUT_R: r = b - acc;  OUT_AX: y = acc.
-enum { OUT_R = 0, OUT_AX = 1 };
+// (ghosts above); then  OUT_R: r = b - acc;  OUT_AX: y = acc;  OUT_RG: r and
+// g^(0) = r / d (eq:jr-initial-guess) so the first sweep gathers g^(0)
+// instead of recomputing one division per gathered entry.
 
 template <int OUT, int CH>
 __global__ void __launch_bounds__(kThreads) k_residual(int64_t n, int nslices, const int32_t *__restrict__ list,
                                                        SellView LG, SellView L, SellView U, SellView UG, int has_ghost,
                                                        const double *__restrict__ d, const double *__restrict__ b,
                                                        const double *__restrict__ x, const double *__restrict__ ghost,
-                                                       double *__restrict__ out) {
+                                                       double *__restrict__ out, double *__restrict__ out2) {
     int64_t s;
     int lane;
     if (!slice_of(nslices, list, &s, &lane)) return;
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(int64_t n, int nslices, c
     cl.load(L, s, lane, pol);
     cu.load(U, s, lane, pol);
     const double di = row ? __ldg(d + i) : 0.0, xi = row ? __ldg(x + i) : 0.0;
-    const double bi = (OUT == OUT_R && row) ? __ldg(b + i) : 0.0;
+    const double bi = (OUT != OUT_AX && row) ? __ldg(b + i) : 0.0;
     cl.gather_mul(gx);
     cu.gather_mul(gx);
     // then sum in ascending column order: LG, L, D, U, UG
@@ -162,7 +163,14 @@ __global__ void __launch_bounds__(kThreads) k_residual(int64_t n, int nslices, c
     acc = __dadd_rn(acc, __dmul_rn(di, xi));
     acc = cu.add(acc, U, gx, pol);
     if (has_ghost) acc = accum(UG, s, lane, GatherPlain{ghost}, acc, pol);
-    if (row) out[i] = OUT == OUT_R ? __dsub_rn(bi, acc) : acc;
+    if (!row) return;
+    if (OUT == OUT_AX) {
+        out[i] = acc;
+    } else {
+        const double r = __dsub_rn(bi, acc);
+        out[i] = r;
+        if (OUT == OUT_RG) out2[i] = __ddiv_rn(r, di);
+    }
 }
 
 // ---- inner Jacobi sweep (rows a3, a4, a5) -----------------------------------
@@ -237,21 +245,23 @@ static inline int chunk_for(int maxw) { return maxw <= 4 ? 4 : (maxw <= 8 ? 8 : 
 template <int OUT, int CH>
 static void residual_ch(int64_t n, int nslices, const int32_t *list, const Sell &LG, const Sell &L, const Sell &U,
                         const Sell &UG, bool has_ghost, const double *d, const double *b, const double *x,
-                        const double *ghost, double *out, cudaStream_t st) {
+                        const double *ghost, double *out, double *out2, cudaStream_t st) {
     k_residual<OUT, CH><<<grid_for(nslices), kThreads, 0, st>>>(n, nslices, list, view(LG), view(L), view(U),
-                                                                view(UG), has_ghost, d, b, x, ghost, out);
+                                                                view(UG), has_ghost, d, b, x, ghost, out, out2);
 }
 
-cudaError_t launch_residual(bool spmv, int64_t n, int nslices, const int32_t *list, const Sell &LG, const Sell &L,
-                            const Sell &U, const Sell &UG, bool has_ghost, const double *d, const double *b,
-                            const double *x, const double *ghost, double *out, cudaStream_t st) {
+cudaError_t launch_residual(int out_mode, int64_t n, int nslices, const int32_t *list, const Sell &LG,
+                            const Sell &L, const Sell &U, const Sell &UG, bool has_ghost, const double *d,
+                            const double *b, const double *x, const double *ghost, double *out, double *out2,
+                            cudaStream_t st) {
     if (nslices <= 0) return cudaSuccess;
     const int ch = chunk_for(std::max(L.maxw, U.maxw));
-#define NSM_RES(OUT)                                                                                        \
-    (ch == 4 ? residual_ch<OUT, 4>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, st)      \
-             : ch == 8 ? residual_ch<OUT, 8>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, st) \
-                       : residual_ch<OUT, 16>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, st))
-    if (spmv) NSM_RES(OUT_AX);
+#define NSM_RES(OUT)                                                                                              \
+    (ch == 4 ? residual_ch<OUT, 4>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, st)      \
+             : ch == 8 ? residual_ch<OUT, 8>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, st) \
+                       : residual_ch<OUT, 16>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, st))
+    if (out_mode == OUT_AX) NSM_RES(OUT_AX);
+    else if (out_mode == OUT_RG) NSM_RES(OUT_RG);
     else NSM_RES(OUT_R);
 #undef NSM_RES
     return cudaGetLastError();
@@ -328,6 +338,7 @@ template <int CH>
 void touch_ch() {
     touch(k_residual<OUT_R, CH>);
     touch(k_residual<OUT_AX, CH>);
+    touch(k_residual<OUT_RG, CH>);
     touch(k_sweep<true, EPI_STORE, GatherPlain, CH>);
     touch(k_sweep<true, EPI_XADD, GatherPlain, CH>);
     touch(k_sweep<true, EPI_XADD_SCALE, GatherPlain, CH>);

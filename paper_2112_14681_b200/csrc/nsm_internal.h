@@ -84,9 +84,12 @@ struct SweepArgs {
     int64_t sweep_id;
 };
 
-cudaError_t launch_residual(bool spmv, int64_t n, int nslices, const int32_t *list, const Sell &LG, const Sell &L,
-                            const Sell &U, const Sell &UG, bool has_ghost, const double *d, const double *b,
-                            const double *x, const double *ghost, double *out, cudaStream_t st);
+// Residual kernel output modes.
+enum { OUT_R = 0, OUT_AX = 1, OUT_RG = 2 };
+cudaError_t launch_residual(int out_mode, int64_t n, int nslices, const int32_t *list, const Sell &LG,
+                            const Sell &L, const Sell &U, const Sell &UG, bool has_ghost, const double *d,
+                            const double *b, const double *x, const double *ghost, double *out, double *out2,
+                            cudaStream_t st);
 cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t st);
 cudaError_t launch_scale(bool xadd, int64_t n, const double *rhs, const double *d, double *out,
                          unsigned long long *flag, int64_t sweep_id, cudaStream_t st);
@@ -115,8 +118,9 @@ cudaError_t launch_halo_wait(const unsigned long long *flags, const int *peers, 
 
 // ---- bulk-copy pipelined kernels (stream.cu), contiguous slice ranges --------
 bool tma_ok(int np, int maxw);
-cudaError_t launch_residual_tma(bool spmv, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
-                                const double *d, const double *b, const double *x, double *out, cudaStream_t st);
+cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
+                                const Sell &U, const double *d, const double *b, const double *x, double *out,
+                                double *out2, cudaStream_t st);
 cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st);
 
 // Force-load every kernel of the library (see kernels.cu "eager loading").

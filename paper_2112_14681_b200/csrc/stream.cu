@@ -172,14 +172,13 @@ struct StagedChunk {
     }
 };
 
-enum { OUTT_R = 0, OUTT_AX = 1 };
 
 template <int OUT, int CH>
 __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView L,
                                                             SellView U, const double *__restrict__ d,
                                                             const double *__restrict__ b,
                                                             const double *__restrict__ x, double *__restrict__ out,
-                                                            int nst, int64_t cap) {
+                                                            double *__restrict__ out2, int nst, int64_t cap) {
     extern __shared__ __align__(128) char sm[];
     const Layout Ly{nst, 2, cap};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -203,7 +202,7 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
         const bool row = has && i < n;
         // per-row vectors and slice geometry: issued before waiting on the copy
         const double di = row ? __ldg(d + i) : 0.0, xi = row ? __ldg(x + i) : 0.0;
-        const double bi = (OUT == OUTT_R && row) ? __ldg(b + i) : 0.0;
+        const double bi = (OUT != OUT_AX && row) ? __ldg(b + i) : 0.0;
         int64_t lo = 0, uo = 0;
         int lw = 0, uw = 0;
         if (has) {
@@ -239,7 +238,15 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(Ly.empty(sm) + st);  // the stage may be refilled
-        if (row) out[i] = OUT == OUTT_R ? __dsub_rn(bi, acc) : acc;
+        if (row) {
+            if (OUT == OUT_AX) {
+                out[i] = acc;
+            } else {
+                const double r = __dsub_rn(bi, acc);
+                out[i] = r;
+                if (OUT == OUT_RG) out2[i] = __ddiv_rn(r, di);
+            }
+        }
     }
 }
 
@@ -248,7 +255,7 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
                                                          const double *__restrict__ dT,
                                                          const double *__restrict__ rhs, G gin,
                                                          double *__restrict__ gout, double *__restrict__ x,
-                                                         const double *__restrict__ dnext,
+                                                         const double *__restrict__ dnext, double *__restrict__ gout2,
                                                          unsigned long long *flag, int64_t sweep_id, int nst,
                                                          int64_t cap) {
     extern __shared__ __align__(128) char sm[];
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
         const double ri = row ? __ldg(rhs + i) : 0.0;
         const double di = (!UNIT && row) ? __ldg(dT + i) : 1.0;
         const double xi = ((EPI == EPI_XADD || EPI == EPI_XADD_SCALE) && row) ? x[i] : 0.0;
-        const double dn = (EPI == EPI_XADD_SCALE && row) ? __ldg(dnext + i) : 1.0;
+        const double dn = ((EPI == EPI_XADD_SCALE || EPI == EPI_STORE2) && row) ? __ldg(dnext + i) : 1.0;
         int64_t to = 0;
         int tw = 0;
         if (has) {
@@ -298,6 +305,7 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
             if (!isfinite(v)) atomicMin(flag, (unsigned long long)sweep_id);
             if (EPI == EPI_STORE) gout[i] = v;
             if (EPI == EPI_XADD) x[i] = __dadd_rn(xi, v);
+            if (EPI == EPI_STORE2) { gout[i] = v; gout2[i] = __ddiv_rn(v, dn); }
             if (EPI == EPI_XADD_SCALE) x[i] = __dadd_rn(xi, __ddiv_rn(v, dn));
         }
     }
@@ -367,13 +375,14 @@ int grid_of(const Geo &g, int64_t ntiles) {
 
 template <int OUT, int CH>
 cudaError_t residual_tma_ch(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
-                            const double *d, const double *b, const double *x, double *out, cudaStream_t st) {
+                            const double *d, const double *b, const double *x, double *out, double *out2,
+                            cudaStream_t st) {
     auto k = k_residual_tma<OUT, CH>;
     const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw));
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     k<<<grid_of<decltype(k)>(g, ntiles), kThreadsT, g.smem, st>>>(n, s_begin, s_end, view(L), view(U), d, b, x, out,
-                                                                  g.nst, g.cap);
+                                                                  out2, g.nst, g.cap);
     return cudaGetLastError();
 }
 
@@ -384,8 +393,8 @@ cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end,
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     k<<<grid_of<decltype(k)>(g, ntiles), kThreadsT, g.smem, st>>>(a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs, gin,
-                                                                  a.gout, a.x, a.dnext, a.flag, a.sweep_id, g.nst,
-                                                                  g.cap);
+                                                                  a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id,
+                                                                  g.nst, g.cap);
     return cudaGetLastError();
 }
 
@@ -416,15 +425,16 @@ bool tma_ok(int np, int maxw) {
     return 128 + 2 * stage <= kSmemMax;
 }
 
-cudaError_t launch_residual_tma(bool spmv, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
-                                const double *d, const double *b, const double *x, double *out, cudaStream_t st) {
+cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
+                                const Sell &U, const double *d, const double *b, const double *x, double *out,
+                                double *out2, cudaStream_t st) {
     if (s_end <= s_begin) return cudaSuccess;
     const int ch = chunk_for_t(std::max(L.maxw, U.maxw));
-#define NSM_RT(OUT)                                                                            \
-    (ch == 4 ? residual_tma_ch<OUT, 4>(n, s_begin, s_end, L, U, d, b, x, out, st)              \
-             : ch == 8 ? residual_tma_ch<OUT, 8>(n, s_begin, s_end, L, U, d, b, x, out, st)    \
-                       : residual_tma_ch<OUT, 16>(n, s_begin, s_end, L, U, d, b, x, out, st))
-    return spmv ? NSM_RT(OUTT_AX) : NSM_RT(OUTT_R);
+#define NSM_RT(OUT)                                                                                  \
+    (ch == 4 ? residual_tma_ch<OUT, 4>(n, s_begin, s_end, L, U, d, b, x, out, out2, st)              \
+             : ch == 8 ? residual_tma_ch<OUT, 8>(n, s_begin, s_end, L, U, d, b, x, out, out2, st)    \
+                       : residual_tma_ch<OUT, 16>(n, s_begin, s_end, L, U, d, b, x, out, out2, st))
+    return out_mode == OUT_AX ? NSM_RT(OUT_AX) : (out_mode == OUT_RG ? NSM_RT(OUT_RG) : NSM_RT(OUT_R));
 #undef NSM_RT
 }
 
@@ -434,6 +444,7 @@ cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end,
         switch (a.epi) {
             case EPI_STORE: return sweep_tma_epi<true, EPI_STORE>(a, s_begin, s_end, st);
             case EPI_XADD: return sweep_tma_epi<true, EPI_XADD>(a, s_begin, s_end, st);
+            case EPI_STORE2: return sweep_tma_epi<true, EPI_STORE2>(a, s_begin, s_end, st);
             default: return sweep_tma_epi<true, EPI_XADD_SCALE>(a, s_begin, s_end, st);
         }
     }
@@ -453,8 +464,10 @@ void touch_t(K k) {
 }
 template <int CH>
 void touch_tma_ch() {
-    touch_t(k_residual_tma<OUTT_R, CH>);
-    touch_t(k_residual_tma<OUTT_AX, CH>);
+    touch_t(k_residual_tma<OUT_R, CH>);
+    touch_t(k_residual_tma<OUT_AX, CH>);
+    touch_t(k_residual_tma<OUT_RG, CH>);
+    touch_t(k_sweep_tma<true, EPI_STORE2, GatherPlainT, CH>);
     touch_t(k_sweep_tma<true, EPI_STORE, GatherPlainT, CH>);
     touch_t(k_sweep_tma<true, EPI_XADD, GatherPlainT, CH>);
     touch_t(k_sweep_tma<true, EPI_XADD_SCALE, GatherPlainT, CH>);
