@@ -78,7 +78,7 @@ def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k
         if k_l == 0 and k_u == 0:
             sl.append(32 * n)
         out["l_sweeps"], out["u_sweeps"] = sl, su
-    out["total"] = res + sum(sum(v) for k, v in out.items() if isinstance(v, list))
+    out["total"] = out["residual"] + sum(sum(v) for k, v in out.items() if isinstance(v, list))
     return out
 
 

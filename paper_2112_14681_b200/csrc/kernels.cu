@@ -299,13 +299,13 @@ static void sweep_unit(const SweepArgs &a, cudaStream_t st) {
     switch (a.epi) {
         case EPI_STORE: sweep_epi<UNIT, EPI_STORE>(a, st); break;
         case EPI_XADD: sweep_epi<UNIT, EPI_XADD>(a, st); break;
+        case EPI_STORE2: sweep_epi<UNIT, EPI_STORE2>(a, st); break;
         default: sweep_epi<UNIT, EPI_XADD_SCALE>(a, st); break;
     }
 }
 
 cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t st) {
     if (a.nslices <= 0) return cudaSuccess;
-    if (a.epi == EPI_STORE2) return cudaErrorInvalidValue;  // reserved, not used by api.cu
     if (a.unit) sweep_unit<true>(a, st);
     else sweep_unit<false>(a, st);
     return cudaGetLastError();
@@ -342,6 +342,9 @@ void touch_ch() {
     touch(k_sweep<true, EPI_STORE, GatherPlain, CH>);
     touch(k_sweep<true, EPI_XADD, GatherPlain, CH>);
     touch(k_sweep<true, EPI_XADD_SCALE, GatherPlain, CH>);
+    touch(k_sweep<true, EPI_STORE2, GatherPlain, CH>);
+    touch(k_sweep<false, EPI_STORE2, GatherPlain, CH>);
+    touch(k_sweep<false, EPI_STORE2, GatherScaled, CH>);
     touch(k_sweep<false, EPI_STORE, GatherPlain, CH>);
     touch(k_sweep<false, EPI_XADD, GatherPlain, CH>);
     touch(k_sweep<false, EPI_XADD_SCALE, GatherPlain, CH>);

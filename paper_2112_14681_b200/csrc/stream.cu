@@ -451,6 +451,7 @@ cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end,
     switch (a.epi) {
         case EPI_STORE: return sweep_tma_epi<false, EPI_STORE>(a, s_begin, s_end, st);
         case EPI_XADD: return sweep_tma_epi<false, EPI_XADD>(a, s_begin, s_end, st);
+        case EPI_STORE2: return sweep_tma_epi<false, EPI_STORE2>(a, s_begin, s_end, st);
         default: return sweep_tma_epi<false, EPI_XADD_SCALE>(a, s_begin, s_end, st);
     }
 }
@@ -468,6 +469,8 @@ void touch_tma_ch() {
     touch_t(k_residual_tma<OUT_AX, CH>);
     touch_t(k_residual_tma<OUT_RG, CH>);
     touch_t(k_sweep_tma<true, EPI_STORE2, GatherPlainT, CH>);
+    touch_t(k_sweep_tma<false, EPI_STORE2, GatherPlainT, CH>);
+    touch_t(k_sweep_tma<false, EPI_STORE2, GatherScaledT, CH>);
     touch_t(k_sweep_tma<true, EPI_STORE, GatherPlainT, CH>);
     touch_t(k_sweep_tma<true, EPI_XADD, GatherPlainT, CH>);
     touch_t(k_sweep_tma<true, EPI_XADD_SCALE, GatherPlainT, CH>);
