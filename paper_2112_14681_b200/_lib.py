@@ -302,6 +302,10 @@ class Smoother:
         """Bulk-copy pipelined kernels (default) or the plain ones."""
         self._call(load().nsm_set_option(self._h, 0, int(bool(enable))))
 
+    def set_fused(self, enable: bool):
+        """One-pass fused pGS applications (default) or one kernel per pass."""
+        self._call(load().nsm_set_option(self._h, 2, int(bool(enable))))
+
     def set_halo_timeout(self, ms: int):
         """How long a halo wait spins before reporting NSM_ERR_DIST."""
         self._call(load().nsm_set_option(self._h, 1, int(ms)))

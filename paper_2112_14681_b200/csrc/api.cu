@@ -56,6 +56,13 @@ struct nsm_handle {
     int n_interior = 0, n_boundary = 0;
     int64_t interior_begin = -1, interior_end = -1;          // set if the interior list is one range
     bool pipeline = true;                                    // bulk-copy pipelined kernels (stream.cu)
+    // fused one-pass pGS (fused.cu), single rank
+    bool fused = true, fused_ready = false;
+    int fused_DL = 0, fused_DU = 0, fused_grid = 0;
+    int64_t fused_M = 0;
+    static constexpr int kFusedKmax = 8;
+    double *fused_ring = nullptr;
+    unsigned int *fused_sync = nullptr;
     void *mailbox = nullptr;           // [flags: nranks u64, padded][data: 2 x n_ghost f64]
     size_t mailbox_bytes = 0, flags_bytes = 0;
     unsigned long long *mb_flags = nullptr;
@@ -133,6 +140,8 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->d_counters);
     cudaFree(h->d_dist_err);
     cudaFree(h->ghost_null);
+    cudaFree(h->fused_ring);
+    cudaFree(h->fused_sync);
     delete h;
 }
 
@@ -361,6 +370,7 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     preload_plain_kernels();
     preload_tma_kernels();
     preload_halo_kernels();
+    preload_fused_kernels();
     nsm_handle *h = new nsm_handle();
     h->device = device;
     h->n = sa.n;
@@ -380,10 +390,23 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
              upload_sell(a, sf.U, &h->Us) && upload_sell(a, sf.LG, &h->LsG) && upload_sell(a, sf.UG, &h->UsG);
     }
     for (int i = 0; ok && i < 4; ++i) ok = a.get(&h->w[i], std::max<int64_t>(h->n, 1));
-    ok = ok && a.get(&h->flag, 1) && a.get(&h->ghost_null, 1);
+    ok = ok && a.get(&h->flag, 1) && a.get(&h->ghost_null, 1) && a.get(&h->d_dist_err, 1) &&
+         cudaMemset(h->d_dist_err, 0, sizeof(unsigned int)) == cudaSuccess;
     if (ok) {
         unsigned long long init = ULLONG_MAX;
         ok = cudaMemcpy(h->flag, &init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+    if (ok && nranks == 1 && h->n > 0 && fused_ok(h->L.maxw, h->U.maxw)) {
+        // rings and flags of the fused one-pass pGS application (fused.cu)
+        const int64_t tr = fused_tile_rows();
+        const int64_t ntiles = (h->n + tr - 1) / tr;
+        h->fused_DL = (int)((sa.bw_lower + tr - 1) / tr);
+        h->fused_DU = (int)((sa.bw_upper + tr - 1) / tr);
+        h->fused_grid = fused_grid(h->L.maxw, h->U.maxw);
+        h->fused_M = h->fused_DL + h->fused_DU + 2 * (int64_t)h->fused_grid + 4;
+        ok = a.get(&h->fused_ring, (int64_t)(nsm_handle::kFusedKmax + 1) * h->fused_M * tr) &&
+             a.get(&h->fused_sync, 64 + 2 * ntiles);
+        h->fused_ready = ok;
     }
     if (ok && nranks > 1) {
         h->row_offsets.assign(dist->row_offsets, dist->row_offsets + nranks + 1);
@@ -422,7 +445,6 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
             h->mb_flags = (unsigned long long *)h->mailbox;
             h->mb_data = (double *)((char *)h->mailbox + h->flags_bytes);
         }
-        ok = ok && a.get(&h->d_dist_err, 1) && cudaMemset(h->d_dist_err, 0, sizeof(unsigned int)) == cudaSuccess;
     }
     if (!ok) {
         cudaGetLastError();
@@ -536,6 +558,7 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
     if (!h) return NSM_ERR_ARG;
     switch (opt) {
         case NSM_OPT_PIPELINE: h->pipeline = value != 0; return NSM_OK;
+        case NSM_OPT_FUSED: h->fused = value != 0; return NSM_OK;
         case NSM_OPT_HALO_TIMEOUT_MS:
             if (value <= 0) return NSM_ERR_ARG;
             h->timeout_ns = (unsigned long long)value * 1000000ull;
@@ -618,6 +641,33 @@ nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, 
             // the residual pass also writes g^(0) = r / d (eq:jr-initial-guess)
             // when sweeps follow, so the first sweep gathers it instead of
             // dividing per gathered entry
+            if (h->fused_ready && h->fused && h->pipeline && k_l >= 1 && k_l <= nsm_handle::kFusedKmax) {
+                // rows a2-a4 in ONE pass over the matrix (fused.cu); x = 0 needs
+                // no special case: the residual phase then computes b exactly
+                FusedLaunch f{};
+                f.n = h->n;
+                f.L = &h->L;
+                f.U = &h->U;
+                f.d = h->d;
+                f.b = b;
+                f.x = x;
+                f.k = k_l;
+                f.DL = h->fused_DL;
+                f.DU = h->fused_DU;
+                f.M = h->fused_M;
+                f.ring = h->fused_ring;
+                f.sync = h->fused_sync;
+                f.grid = h->fused_grid;
+                f.flag = h->flag;
+                f.sweep_id0 = h->sweep_counter + 1;
+                h->sweep_counter += k_l + 1;
+                f.err = h->d_dist_err;
+                f.timeout_ns = h->timeout_ns;
+                cudaError_t e = launch_pgs_fused(f, s);
+                h->launches += 2;
+                if (e != cudaSuccess) return cuda_fail(h, e, "fused pGS launch");
+                continue;
+            }
             const bool rg = !fresh && k_l > 0;
             if (!fresh) st = residual_into(h, b, x, R, rg ? OUT_RG : OUT_R, s, rg ? W2 : nullptr);
             if (st != NSM_OK) return st;
@@ -680,7 +730,8 @@ nsm_status nsm_check(nsm_handle *h, int64_t *first_bad_sweep, void *stream) {
     if (e != cudaSuccess) return cuda_fail(h, e, "nsm_check");
     if (first_bad_sweep) *first_bad_sweep = v == ULLONG_MAX ? -1 : (int64_t)v;
     if (derr) {
-        h->err = "halo exchange timed out waiting for a neighbour";
+        h->err = (derr & 1u) ? "halo exchange timed out waiting for a neighbour"
+                             : "fused wavefront kernel timed out waiting for a lower tile";
         return NSM_ERR_DIST;
     }
     if (v != ULLONG_MAX) {

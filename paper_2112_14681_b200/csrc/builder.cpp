@@ -180,6 +180,15 @@ nsm_status build_split(const nsm_csr *A, int64_t rb, int64_t re, Split *out, std
     pack(n, cnt[P_LG], first[P_LG], ci, va, gm, &out->LG);
     pack(n, cnt[P_UG], first[P_UG], ci, va, gm, &out->UG);
     out->nnz_off = out->L.nnz + out->U.nnz + out->LG.nnz + out->UG.nnz;
+    // local lower / upper bandwidths (dependency distances of the fused kernel)
+    int64_t bwl = 0, bwu = 0;
+#pragma omp parallel for schedule(static) reduction(max : bwl, bwu)
+    for (int64_t i = 0; i < n; ++i) {
+        if (cnt[P_L][i] > 0) bwl = std::max(bwl, rb + i - ci[first[P_L][i]]);
+        if (cnt[P_U][i] > 0) bwu = std::max(bwu, ci[first[P_U][i] + cnt[P_U][i] - 1] - rb - i);
+    }
+    out->bw_lower = bwl;
+    out->bw_upper = bwu;
     return NSM_OK;
 }
 

@@ -55,6 +55,7 @@ struct Split {
     SellHost LG, UG;                  // couplings to ghost columns below / above the block
     std::vector<int64_t> ghost_gid;   // global id of ghost k (ascending)
     int64_t nnz_off = 0;
+    int64_t bw_lower = 0, bw_upper = 0;  // max (i - j) over L entries, max (j - i) over U entries
 };
 
 // Builds the SELL split of rows [row_begin, row_begin + n) of A.
@@ -122,6 +123,29 @@ cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_
                                 const Sell &U, const double *d, const double *b, const double *x, double *out,
                                 double *out2, cudaStream_t st);
 cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st);
+
+// ---- fused one-pass pGS application (fused.cu) ---------------------------------
+struct FusedLaunch {
+    int64_t n;
+    const Sell *L, *U;
+    const double *d, *b;
+    double *x;
+    int k;
+    int DL, DU;              // dependency distances in tiles of fused_tile_rows() rows
+    int64_t M;               // ring length in tiles
+    double *ring;            // (k + 1) * M * tile_rows doubles
+    unsigned int *sync;      // 64 + 2 * ntiles ints: dispenser, progress, write-back flags
+    int grid;
+    unsigned long long *flag;
+    int64_t sweep_id0;
+    unsigned int *err;
+    unsigned long long timeout_ns;
+};
+int fused_tile_rows();
+bool fused_ok(int maxwL, int maxwU);
+int fused_grid(int maxwL, int maxwU);
+cudaError_t launch_pgs_fused(const FusedLaunch &f, cudaStream_t st);
+void preload_fused_kernels();
 
 // Force-load every kernel of the library (see kernels.cu "eager loading").
 void preload_plain_kernels();

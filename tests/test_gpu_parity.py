@@ -64,14 +64,23 @@ SMALL = {
 }
 
 
-@pytest.fixture(scope="module", params=[(c, p) for c in SMALL for p in ("pipelined", "plain")],
-                ids=lambda v: f"{v[0]}-{v[1]}")
+KERNELS = ("fused", "pipelined", "plain")
+
+
+def set_kernels(S, mode):
+    """fused: one-pass wavefront pGS + pipelined kernels (default); pipelined:
+    one cp.async.bulk pipelined kernel per pass; plain: register-blocked."""
+    S.set_pipeline(mode != "plain")
+    S.set_fused(mode == "fused")
+
+
+@pytest.fixture(scope="module", params=[(c, p) for c in SMALL for p in KERNELS], ids=lambda v: f"{v[0]}-{v[1]}")
 def case(request):
     name, pipe = request.param
     A = SMALL[name]()
     F = oracle.ilu0(A)[2]
     S = nsm.Smoother(A, F)
-    S.set_pipeline(pipe == "pipelined")   # both kernel families must agree with the oracle
+    set_kernels(S, pipe)   # every kernel family must agree with the oracle
     yield f"{name}/{pipe}", A, F, S
     S.close()
 
@@ -208,8 +217,8 @@ def test_full_size_parity(cfg):
     else:
         want = oracle.pgs_apply(A, b, x0, 2)
     with nsm.Smoother(A, F) as S:
-        for pipe in (True, False):
-            S.set_pipeline(pipe)
+        for mode in KERNELS:
+            set_kernels(S, mode)
             x = dev(x0)
             S.smooth(dev(b), x, kind, nu=1, k_l=2, k_u=2)
-            agree(host(x), want, f"{cfg} pipeline={pipe}")
+            agree(host(x), want, f"{cfg} kernels={mode}")
