@@ -225,6 +225,7 @@ def run_nsm(args, rank, nranks, local_rank):
     F = nsm.ilu0(A, row_begin=A.row_begin) if kind == "ilu" else None
     S = nsm.Smoother(A, F, device=local_rank, rank=rank, nranks=nranks, row_offsets=offsets)
     S.set_pipeline(not args.plain)
+    S.set_fused(args.fused)
     if nranks > 1:
         S.connect(dist)
     nl, nu_, noff = split_counts(A)
@@ -336,7 +337,8 @@ def run_nsm(args, rank, nranks, local_rank):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "n_per_gpu": A.nrows, "nnz_per_gpu": A.nnz, "kind": kind, "k_l": k_l,
                        "k_u": k_u, "nu": 1, "partition": "z-slab rows" if nranks > 1 else "none",
-                       "kernels": "plain register-blocked" if args.plain else "cp.async.bulk pipelined (persistent)",
+                       "kernels": ("plain register-blocked" if args.plain else "cp.async.bulk pipelined (persistent)")
+                       + (", pGS fused into one wavefront pass" if args.fused and not args.plain and kind == "pgs" else ""),
                        "l2": "flushed before every timed step (256 MB read through L2)",
                        "bytes_per_step_per_gpu": ab, "frac_of_hbm_peak": round(value / nranks / peak, 4)},
             "ms_per_apply": round(ms_step, 4),
@@ -363,6 +365,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--plain", action="store_true", help="plain register-blocked kernels instead of the bulk-copy pipelined ones")
+    ap.add_argument("--fused", action="store_true", help="pGS as one fused wavefront pass (opt-in, latency-bound)")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: every rank on cuda:0 (halo over same-device IPC), gloo plumbing")
     args = ap.parse_args()

@@ -236,11 +236,12 @@ const char *nsm_last_error(const nsm_handle *h);
  *                           kernels.  Both give bit-identical results.
  *   NSM_OPT_HALO_TIMEOUT_MS how long a halo or wavefront wait spins before
  *                           giving up and flagging NSM_ERR_DIST (default 20000).
- *   NSM_OPT_FUSED           1 (default) = single-rank pGS applications with
- *                           1 <= k <= 8 run as ONE fused wavefront pass
- *                           (residual + k sweeps + x update, the matrix read
- *                           once); 0 = one kernel per pass.
- *                           Bit-identical results either way. */
+ *   NSM_OPT_FUSED           1 = single-rank pGS applications with 1 <= k <= 8
+ *                           run as ONE fused wavefront pass (residual + k
+ *                           sweeps + x update, the matrix read once;
+ *                           DESIGN.md §6); 0 (default) = one kernel per pass.
+ *                           Bit-identical results either way; the fused pass
+ *                           is currently latency-bound and slower. */
 typedef enum { NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 

@@ -57,7 +57,7 @@ struct nsm_handle {
     int64_t interior_begin = -1, interior_end = -1;          // set if the interior list is one range
     bool pipeline = true;                                    // bulk-copy pipelined kernels (stream.cu)
     // fused one-pass pGS (fused.cu), single rank
-    bool fused = true, fused_ready = false;
+    bool fused = false, fused_ready = false;  // opt-in: latency-bound so far
     int fused_DL = 0, fused_DU = 0, fused_grid = 0;
     int64_t fused_M = 0;
     static constexpr int kFusedKmax = 8;

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "nsm_internal.h"
 #include "ptx.cuh"
@@ -357,13 +358,15 @@ cudaError_t launch_pgs_fused(const FusedLaunch &f, cudaStream_t st) {
     p.err = f.err;
     p.timeout_ns = f.timeout_ns;
     p.nst = 2;
+    if (const char *e = getenv("NSM_FUSED_NST")) p.nst = std::max(1, atoi(e));  // DEBUG experiment
     p.capL = (int64_t)kRowsF * std::max(f.L->maxw, 1);
     p.capU = (int64_t)kRowsF * std::max(f.U->maxw, 1);
     // reset the dispenser and the progress flags
     cudaError_t e = cudaMemsetAsync(f.sync, 0, (64 + 2 * (size_t)p.ntiles) * sizeof(int), st);
     if (e != cudaSuccess) return e;
     const size_t smem = fused_smem(f.L->maxw, f.U->maxw, p.nst);
-    const int grid = (int)std::min<int64_t>(f.grid, p.ntiles);
+    int grid = (int)std::min<int64_t>(f.grid, p.ntiles);
+    if (const char *e = getenv("NSM_FUSED_GRID_DIV")) grid = std::max(1, grid / std::max(1, atoi(e)));  // DEBUG
     const int mw = std::max(f.L->maxw, f.U->maxw);
     e = mw <= 4 ? fused_launch<4>(p, smem, grid, st)
                 : (mw <= 8 ? fused_launch<8>(p, smem, grid, st) : fused_launch<16>(p, smem, grid, st));
