@@ -68,6 +68,14 @@ __device__ __forceinline__ uint64_t policy_evict_first_t() {
     return p;
 }
 
+// Programmatic dependent launch: the kernels are launched with
+// programmatic stream serialisation, so a kernel's CTAs may start while the
+// previous kernel drains.  Only the immutable matrix streams (the producer's
+// bulk copies) are touched before griddepcontrol.wait; everything produced
+// by the previous kernel (x, r, g, y, z) is read after it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 struct GatherPlainT {
     const double *__restrict__ g;
     __device__ __forceinline__ double operator()(int32_t c) const { return __ldg(g + c); }
@@ -132,6 +140,7 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
             }
         }
     }
+    pdl_trigger();  // all of this CTA's copies are issued: dependents may be scheduled
 }
 
 // Register chunk of one row taken from the staged copy: the first CH entries
@@ -192,6 +201,7 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
         return;
     }
     const GatherPlainT gx{x};
+    pdl_wait();  // x, b of the previous kernel
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int st = it % nst;
@@ -270,6 +280,7 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
         }
         return;
     }
+    pdl_wait();  // rhs, iterates, x of the previous kernels
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int st = it % nst;
@@ -373,6 +384,21 @@ int grid_of(const Geo &g, int64_t ntiles) {
     return (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(g.per_sm, 1));
 }
 
+template <class K, class... Args>
+cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreadsT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int OUT, int CH>
 cudaError_t residual_tma_ch(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
                             const double *d, const double *b, const double *x, double *out, double *out2,
@@ -381,9 +407,8 @@ cudaError_t residual_tma_ch(int64_t n, int64_t s_begin, int64_t s_end, const Sel
     const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw));
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    k<<<grid_of<decltype(k)>(g, ntiles), kThreadsT, g.smem, st>>>(n, s_begin, s_end, view(L), view(U), d, b, x, out,
-                                                                  out2, g.nst, g.cap);
-    return cudaGetLastError();
+    return launch_pdl(k, grid_of<decltype(k)>(g, ntiles), g.smem, st, n, s_begin, s_end, view(L), view(U), d, b, x,
+                      out, out2, g.nst, g.cap);
 }
 
 template <bool UNIT, int EPI, class G, int CH>
@@ -392,10 +417,8 @@ cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end,
     const Geo g = geometry(k, 1, a.T->maxw);
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    k<<<grid_of<decltype(k)>(g, ntiles), kThreadsT, g.smem, st>>>(a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs, gin,
-                                                                  a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id,
-                                                                  g.nst, g.cap);
-    return cudaGetLastError();
+    return launch_pdl(k, grid_of<decltype(k)>(g, ntiles), g.smem, st, a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs,
+                      gin, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id, g.nst, g.cap);
 }
 
 template <bool UNIT, int EPI, int CH>
