@@ -241,8 +241,12 @@ const char *nsm_last_error(const nsm_handle *h);
  *                           sweeps + x update, the matrix read once;
  *                           DESIGN.md §6); 0 (default) = one kernel per pass.
  *                           Bit-identical results either way; the fused pass
- *                           is currently latency-bound and slower. */
-typedef enum { NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2 } nsm_option;
+ *                           is currently latency-bound and slower.
+ *   NSM_OPT_PDL             1 (default) = launch the pipelined kernels with
+ *                           programmatic dependent launch (a kernel's matrix
+ *                           prefetch overlaps the previous kernel's drain);
+ *                           0 = plain stream order. */
+typedef enum { NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2, NSM_OPT_PDL = 3 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 
 /* Frees all device memory of the handle (synchronises its device).  NULL ok. */

@@ -306,6 +306,10 @@ class Smoother:
         """One-pass fused pGS applications (default) or one kernel per pass."""
         self._call(load().nsm_set_option(self._h, 2, int(bool(enable))))
 
+    def set_pdl(self, enable: bool):
+        """Programmatic dependent launch between consecutive pipelined kernels."""
+        self._call(load().nsm_set_option(self._h, 3, int(bool(enable))))
+
     def set_halo_timeout(self, ms: int):
         """How long a halo wait spins before reporting NSM_ERR_DIST."""
         self._call(load().nsm_set_option(self._h, 1, int(ms)))

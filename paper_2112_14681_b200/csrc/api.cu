@@ -56,6 +56,7 @@ struct nsm_handle {
     int n_interior = 0, n_boundary = 0;
     int64_t interior_begin = -1, interior_end = -1;          // set if the interior list is one range
     bool pipeline = true;                                    // bulk-copy pipelined kernels (stream.cu)
+    bool pdl = true;                                         // programmatic dependent launch for them
     // fused one-pass pGS (fused.cu), single rank
     bool fused = false, fused_ready = false;  // opt-in: latency-bound so far
     int fused_DL = 0, fused_DU = 0, fused_grid = 0;
@@ -258,6 +259,7 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 a.gout2 = last ? gout2 : nullptr;
                                 a.flag = h->flag;
                                 a.sweep_id = sid;
+                                a.pdl = h->pdl;
                                 if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(1, st.T->maxw))
                                     return launch_sweep_tma(a, sl.begin, sl.end, s);
                                 return launch_sweep(a, s);
@@ -273,7 +275,7 @@ nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double
                          double *out2 = nullptr) {
     return pass(h, true, x, nullptr, s, [&](const Slices &sl, bool with_ghost, const double *ghost) {
         if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(2, std::max(h->L.maxw, h->U.maxw)))
-            return launch_residual_tma(mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, s);
+            return launch_residual_tma(mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
         return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
                                out, out2, s);
     });
@@ -559,6 +561,7 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
     switch (opt) {
         case NSM_OPT_PIPELINE: h->pipeline = value != 0; return NSM_OK;
         case NSM_OPT_FUSED: h->fused = value != 0; return NSM_OK;
+        case NSM_OPT_PDL: h->pdl = value != 0; return NSM_OK;
         case NSM_OPT_HALO_TIMEOUT_MS:
             if (value <= 0) return NSM_ERR_ARG;
             h->timeout_ns = (unsigned long long)value * 1000000ull;

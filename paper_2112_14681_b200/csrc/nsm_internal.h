@@ -83,6 +83,7 @@ struct SweepArgs {
     double *gout2;
     unsigned long long *flag;
     int64_t sweep_id;
+    bool pdl;                // programmatic dependent launch (pipelined kernels)
 };
 
 // Residual kernel output modes.
@@ -121,7 +122,7 @@ cudaError_t launch_halo_wait(const unsigned long long *flags, const int *peers, 
 bool tma_ok(int np, int maxw);
 cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
                                 const Sell &U, const double *d, const double *b, const double *x, double *out,
-                                double *out2, cudaStream_t st);
+                                double *out2, bool pdl, cudaStream_t st);
 cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st);
 
 // ---- fused one-pass pGS application (fused.cu) ---------------------------------

@@ -385,7 +385,7 @@ int grid_of(const Geo &g, int64_t ntiles) {
 }
 
 template <class K, class... Args>
-cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
+cudaError_t launch_pdl(bool pdl, K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreadsT);
@@ -395,19 +395,19 @@ cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t st, Args...
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 template <int OUT, int CH>
 cudaError_t residual_tma_ch(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
                             const double *d, const double *b, const double *x, double *out, double *out2,
-                            cudaStream_t st) {
+                            bool pdl, cudaStream_t st) {
     auto k = k_residual_tma<OUT, CH>;
     const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw));
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    return launch_pdl(k, grid_of<decltype(k)>(g, ntiles), g.smem, st, n, s_begin, s_end, view(L), view(U), d, b, x,
+    return launch_pdl(pdl, k, grid_of<decltype(k)>(g, ntiles), g.smem, st, n, s_begin, s_end, view(L), view(U), d, b, x,
                       out, out2, g.nst, g.cap);
 }
 
@@ -417,7 +417,7 @@ cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end,
     const Geo g = geometry(k, 1, a.T->maxw);
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    return launch_pdl(k, grid_of<decltype(k)>(g, ntiles), g.smem, st, a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs,
+    return launch_pdl(a.pdl, k, grid_of<decltype(k)>(g, ntiles), g.smem, st, a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs,
                       gin, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id, g.nst, g.cap);
 }
 
@@ -450,13 +450,13 @@ bool tma_ok(int np, int maxw) {
 
 cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
                                 const Sell &U, const double *d, const double *b, const double *x, double *out,
-                                double *out2, cudaStream_t st) {
+                                double *out2, bool pdl, cudaStream_t st) {
     if (s_end <= s_begin) return cudaSuccess;
     const int ch = chunk_for_t(std::max(L.maxw, U.maxw));
 #define NSM_RT(OUT)                                                                                  \
-    (ch == 4 ? residual_tma_ch<OUT, 4>(n, s_begin, s_end, L, U, d, b, x, out, out2, st)              \
-             : ch == 8 ? residual_tma_ch<OUT, 8>(n, s_begin, s_end, L, U, d, b, x, out, out2, st)    \
-                       : residual_tma_ch<OUT, 16>(n, s_begin, s_end, L, U, d, b, x, out, out2, st))
+    (ch == 4 ? residual_tma_ch<OUT, 4>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st)              \
+             : ch == 8 ? residual_tma_ch<OUT, 8>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st)    \
+                       : residual_tma_ch<OUT, 16>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st))
     return out_mode == OUT_AX ? NSM_RT(OUT_AX) : (out_mode == OUT_RG ? NSM_RT(OUT_RG) : NSM_RT(OUT_R));
 #undef NSM_RT
 }
