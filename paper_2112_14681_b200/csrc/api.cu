@@ -380,6 +380,10 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     h->n_ghost = sa.n_ghost;
     h->nnz_off = sa.nnz_off;
     h->nslices = (int)((sa.n + kSlice - 1) / kSlice);
+    // PDL pays where kernels are short (C2: +5 %) and was measured to cost
+    // 14 % on 16.7 M-row 7-point sweeps (profiles/r01_v5_pdl.md): default on
+    // up to 8 M rows per rank
+    h->pdl = sa.n <= (int64_t)8 * 1024 * 1024;
     h->rank = rank;
     h->nranks = nranks;
     h->mode = dist ? dist->mode : NSM_DIST_HYBRID;
