@@ -226,7 +226,8 @@ def run_nsm(args, rank, nranks, local_rank):
     S = nsm.Smoother(A, F, device=local_rank, rank=rank, nranks=nranks, row_offsets=offsets)
     S.set_pipeline(not args.plain)
     S.set_fused(args.fused)
-    S.set_pdl(not args.no_pdl)
+    if args.pdl != "auto":
+        S.set_pdl(args.pdl == "on")
     if nranks > 1:
         S.connect(dist)
     nl, nu_, noff = split_counts(A)
@@ -366,7 +367,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--plain", action="store_true", help="plain register-blocked kernels instead of the bulk-copy pipelined ones")
-    ap.add_argument("--no-pdl", action="store_true", help="no programmatic dependent launch")
+    ap.add_argument("--pdl", default="auto", choices=["auto", "on", "off"],
+                    help="programmatic dependent launch (auto: the library's size-based default)")
     ap.add_argument("--fused", action="store_true", help="pGS as one fused wavefront pass (opt-in, latency-bound)")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: every rank on cuda:0 (halo over same-device IPC), gloo plumbing")
