@@ -60,8 +60,12 @@ typedef enum {
 } nsm_status;
 
 typedef enum {
-    NSM_PGS = 0,   /* polynomial Gauss-Seidel, §5.2 */
-    NSM_ILU0 = 1   /* ILU(0) with Jacobi-iterated L and U solves, §5.3 / Alg. 2 */
+    NSM_PGS = 0,          /* polynomial Gauss-Seidel, forward (M = D + L), §5.2 */
+    NSM_ILU0 = 1,         /* ILU(0) with Jacobi-iterated L and U solves, §5.3 / Alg. 2 */
+    NSM_PGS_BACKWARD = 2, /* polynomial GS with M = D + U (eq:one-stage backward) */
+    NSM_PGS_SYMMETRIC = 3,/* one forward then one backward pGS application per outer iteration */
+    NSM_L1_JACOBI = 4     /* l1-Jacobi, x += D_l1^{-1}(b - A x), D_l1 = a_ii + sum_{j!=i} |a_ij|
+                             (the paper's comparison smoother; definition) */
 } nsm_kind;
 
 typedef enum {
@@ -200,6 +204,9 @@ nsm_status nsm_usolve(nsm_handle *h, const double *r, double *x, int k_sweeps, v
  * P:L723-725; §8(a) rows a2-a6):
  *   NSM_PGS : x <- x + sum_{j<=k_l} (-D^{-1}L)^j D^{-1} (b - A x)     (k_u ignored)
  *   NSM_ILU0: x <- x + U~^{-1}_{k_u} L~^{-1}_{k_l} (b - A x)  (Jacobi-iterated factors)
+ *   NSM_PGS_BACKWARD: x <- x + sum_{j<=k_l} (-D^{-1}U)^j D^{-1} (b - A x)
+ *   NSM_PGS_SYMMETRIC: NSM_PGS then NSM_PGS_BACKWARD (each with its residual)
+ *   NSM_L1_JACOBI: x <- x + D_l1^{-1} (b - A x)                      (k_l, k_u ignored)
  * x_is_zero != 0 asserts x == 0 on entry, so the first residual is b and is
  * not computed (V-cycle pre-smoothing; exact).  b and x must not alias.
  * Requesting NSM_ILU0 on a handle set up without factors -> NSM_ERR_STATE.

@@ -46,6 +46,8 @@ def _L():
         _lib.orc_tri_direct.argtypes = [i64, vp, vp, vp, ci, ci, vp, ci, vp, vp]
         _lib.orc_pgs_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, ci, ci, vp]
         _lib.orc_gs_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, vp]
+        _lib.orc_pgs_backward_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, ci, ci, vp]
+        _lib.orc_l1_jacobi_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci]
         _lib.orc_ilu0.argtypes = [i64, vp, vp, vp, vp]
         _lib.orc_ilu_apply.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci, ci, ci, ci, ci, vp]
     return _lib
@@ -127,6 +129,35 @@ def pgs_apply(A, b, x, k, nu=1, x_is_zero=False, bounds=None):
     x = np.array(x, dtype=np.float64, copy=True)
     _check(_L().orc_pgs_apply(n, _p(rp), _p(ci), _p(va), _p(b), _p(x), int(k), int(nu), int(x_is_zero), nb, _p(bd)),
            "pgs_apply")
+    return x
+
+
+def pgs_backward_apply(A, b, x, k, nu=1, x_is_zero=False, bounds=None):
+    """Backward pGS (M = D + U); returns the new x."""
+    n, rp, ci, va = _csr(A)
+    nb, bd = _part(bounds)
+    b = _f64(b)
+    x = np.array(x, dtype=np.float64, copy=True)
+    _check(_L().orc_pgs_backward_apply(n, _p(rp), _p(ci), _p(va), _p(b), _p(x), int(k), int(nu), int(x_is_zero),
+                                       nb, _p(bd)), "pgs_backward_apply")
+    return x
+
+
+def pgs_symmetric_apply(A, b, x, k, nu=1, x_is_zero=False, bounds=None):
+    """nu x (forward pGS, then backward pGS)."""
+    x = np.array(x, dtype=np.float64, copy=True)
+    for it in range(nu):
+        x = pgs_apply(A, b, x, k, x_is_zero=x_is_zero and it == 0, bounds=bounds)
+        x = pgs_backward_apply(A, b, x, k, bounds=bounds)
+    return x
+
+
+def l1_jacobi_apply(A, b, x, nu=1, x_is_zero=False):
+    n, rp, ci, va = _csr(A)
+    b = _f64(b)
+    x = np.array(x, dtype=np.float64, copy=True)
+    _check(_L().orc_l1_jacobi_apply(n, _p(rp), _p(ci), _p(va), _p(b), _p(x), int(nu), int(x_is_zero)),
+           "l1_jacobi_apply")
     return x
 
 

@@ -169,6 +169,52 @@ int orc_pgs_apply(i64 n, const i64 *rp, const i64 *ci, const double *va, const d
     return rc;
 }
 
+/* Polynomial GS with the backward splitting M = D + U (eq:one-stage,
+ * P:L726-727 "M = U + D ... backward sweeps"), same Neumann construction
+ * with the upper triangle: x = x + sum_{j<=k} (-D^{-1}U)^j D^{-1} (b - A x). */
+int orc_pgs_backward_apply(i64 n, const i64 *rp, const i64 *ci, const double *va, const double *b,
+                           double *x, int k, int nu, int x_is_zero, int nblocks, const i64 *bounds) {
+    double *r = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    double *g = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    if (!r || !g) { free(r); free(g); return -1; }
+    int rc = 0;
+    for (int it = 0; it < nu && rc == 0; ++it) {
+        if (it == 0 && x_is_zero) memcpy(r, b, (size_t)n * sizeof(double));
+        else orc_residual(n, rp, ci, va, b, x, r);
+        rc = orc_tri_jacobi(n, rp, ci, va, 0, 0, r, k, nblocks, bounds, g);
+        if (rc) break;
+        for (i64 i = 0; i < n; ++i) x[i] = x[i] + g[i];
+    }
+    free(r); free(g);
+    return rc;
+}
+
+/* l1-Jacobi (named by the paper as the comparison smoother; the
+ * definition is hypre's as fixed by S:L354-359):
+ *   d_i = a_ii + sum_{j != i} |a_ij|  (ascending columns, summed from 0)
+ *   x = x + D_l1^{-1} (b - A x), nu times. */
+int orc_l1_jacobi_apply(i64 n, const i64 *rp, const i64 *ci, const double *va, const double *b, double *x,
+                        int nu, int x_is_zero) {
+    double *r = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    double *d = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    if (!r || !d) { free(r); free(d); return -1; }
+    int rc = diagonal(n, rp, ci, va, d);
+    if (rc) { free(r); free(d); return rc; }
+    for (i64 i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (i64 p = rp[i]; p < rp[i + 1]; ++p)
+            if (ci[p] != i) s = s + (va[p] < 0 ? -va[p] : va[p]);
+        d[i] = d[i] + s;
+    }
+    for (int it = 0; it < nu; ++it) {
+        if (it == 0 && x_is_zero) memcpy(r, b, (size_t)n * sizeof(double));
+        else orc_residual(n, rp, ci, va, b, x, r);
+        for (i64 i = 0; i < n; ++i) x[i] = x[i] + r[i] / d[i];
+    }
+    free(r); free(d);
+    return 0;
+}
+
 /* Classical (direct) forward Gauss-Seidel, nu sweeps: x = x + (D+L)^{-1}(b - Ax)
  * (eq:one-stage).  With a partition this is hypre's hybrid GS
  * (P:L733-741).  It is the exact operator pGS approximates (config C1). */

@@ -10,7 +10,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIBPATH = os.path.join(_HERE, "libnsm.so")
 _lib = None
 
-NSM_PGS, NSM_ILU0 = 0, 1
+NSM_PGS, NSM_ILU0, NSM_PGS_BACKWARD, NSM_PGS_SYMMETRIC, NSM_L1_JACOBI = 0, 1, 2, 3, 4
+KINDS = {"pgs": NSM_PGS, "ilu": NSM_ILU0, "ilu0": NSM_ILU0, "pgs_backward": NSM_PGS_BACKWARD,
+         "pgs_symmetric": NSM_PGS_SYMMETRIC, "l1_jacobi": NSM_L1_JACOBI}
 NSM_DIST_HYBRID, NSM_DIST_GLOBAL = 0, 1
 _STATUS = {0: "NSM_OK", 1: "NSM_ERR_ARG", 2: "NSM_ERR_PATTERN", 3: "NSM_ERR_ZERO_DIAG", 4: "NSM_ERR_NONFINITE",
            5: "NSM_ERR_CUDA", 6: "NSM_ERR_OOM", 7: "NSM_ERR_STATE", 8: "NSM_ERR_DIST"}
@@ -229,7 +231,7 @@ class Smoother:
         return x
 
     def smooth(self, b, x, kind="pgs", nu=1, k_l=2, k_u=None, x_is_zero=False, stream=None):
-        kd = {"pgs": NSM_PGS, "ilu": NSM_ILU0, "ilu0": NSM_ILU0}[kind] if isinstance(kind, str) else int(kind)
+        kd = KINDS[kind] if isinstance(kind, str) else int(kind)
         k_u = k_l if k_u is None else k_u
         self._call(load().nsm_smooth(self._h, kd, self._vec(b, "b"), self._vec(x, "x"), int(nu), int(k_l), int(k_u),
                                      int(bool(x_is_zero)), self._stream(stream)))

@@ -37,7 +37,7 @@ struct nsm_handle {
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
     // A = L + D + U (+ ghost couplings LG / UG)
-    double *d = nullptr;
+    double *d = nullptr, *dl1 = nullptr;  // diagonal; l1-Jacobi diagonal
     Sell L, U, LG, UG;
     // ILU(0) factors: unit-lower L = I + Ls, U = D_U (I + D_U^{-1} Us)
     bool has_ilu = false;
@@ -126,6 +126,7 @@ void free_handle(nsm_handle *h) {
     cudaDeviceSynchronize();
     for (Sell *s : {&h->L, &h->U, &h->LG, &h->UG, &h->Ls, &h->Us, &h->LsG, &h->UsG}) free_sell(*s);
     cudaFree(h->d);
+    cudaFree(h->dl1);
     cudaFree(h->dU);
     for (double *&p : h->w) cudaFree(p);
     cudaFree(h->flag);
@@ -388,7 +389,8 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     h->nranks = nranks;
     h->mode = dist ? dist->mode : NSM_DIST_HYBRID;
     DevAlloc a{h};
-    bool ok = a.get(&h->d, h->n) && upload(h->d, sa.d.data(), h->n) && upload_sell(a, sa.L, &h->L) &&
+    bool ok = a.get(&h->d, h->n) && upload(h->d, sa.d.data(), h->n) && a.get(&h->dl1, h->n) &&
+              upload(h->dl1, sa.dl1.data(), h->n) && upload_sell(a, sa.L, &h->L) &&
               upload_sell(a, sa.U, &h->U) && upload_sell(a, sa.LG, &h->LG) && upload_sell(a, sa.UG, &h->UG);
     if (ok && F) {
         h->has_ilu = true;
@@ -628,6 +630,86 @@ nsm_status nsm_usolve(nsm_handle *h, const double *r, double *x, int k, void *st
     return tri_solve(h, false, r, x, k, stream);
 }
 
+// One smoother application of the given kind (rows a2-a5).  fresh: x == 0 on
+// entry, so the residual is b (reading R3).
+static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, double *x, int k_l, int k_u, bool fresh,
+                             cudaStream_t s) {
+    double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
+    const double *rhs = fresh ? b : R;
+    nsm_status st = NSM_OK;
+    if (kind == NSM_L1_JACOBI) {
+        // l1-Jacobi: x += D_l1^{-1} (b - A x)
+        if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
+        return st != NSM_OK ? st : scale_into(h, true, rhs, h->dl1, x, s);
+    }
+    if (kind == NSM_PGS || kind == NSM_PGS_BACKWARD) {
+        const bool fwd = kind == NSM_PGS;
+        if (fwd && h->fused_ready && h->fused && h->pipeline && k_l >= 1 && k_l <= nsm_handle::kFusedKmax) {
+            // rows a2-a4 in ONE pass over the matrix (fused.cu); x = 0 needs
+            // no special case: the residual phase then computes b exactly
+            FusedLaunch f{};
+            f.n = h->n;
+            f.L = &h->L;
+            f.U = &h->U;
+            f.d = h->d;
+            f.b = b;
+            f.x = x;
+            f.k = k_l;
+            f.DL = h->fused_DL;
+            f.DU = h->fused_DU;
+            f.M = h->fused_M;
+            f.ring = h->fused_ring;
+            f.sync = h->fused_sync;
+            f.grid = h->fused_grid;
+            f.flag = h->flag;
+            f.sweep_id0 = h->sweep_counter + 1;
+            h->sweep_counter += k_l + 1;
+            f.err = h->d_dist_err;
+            f.timeout_ns = h->timeout_ns;
+            cudaError_t e = launch_pgs_fused(f, s);
+            h->launches += 2;
+            return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "fused pGS launch");
+        }
+        // the residual pass also writes g^(0) = r / d (eq:jr-initial-guess)
+        // when sweeps follow, so the first sweep gathers it instead of
+        // dividing per gathered entry
+        const bool rg = !fresh && k_l > 0;
+        if (!fresh) st = residual_into(h, b, x, R, rg ? OUT_RG : OUT_R, s, rg ? W2 : nullptr);
+        if (st != NSM_OK) return st;
+        // rows a3/a4: k_l sweeps g <- D^{-1}(r - T g) (T = L forward, U
+        // backward), the last fused with x += g
+        if (k_l == 0) return scale_into(h, true, rhs, h->d, x, s);
+        Stage sg = fwd ? Stage{&h->L, &h->LG, h->d, rhs, k_l, rg ? W2 : nullptr}
+                       : Stage{&h->U, &h->UG, h->d, rhs, k_l, rg ? W2 : nullptr};
+        return run_sweeps(h, sg, W0, W1, EPI_XADD, nullptr, x, nullptr, s);
+    }
+    // NSM_ILU0
+    if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
+    if (st != NSM_OK) return st;
+    // row a5: y = sum_{j<=kL} (-Ls)^j r ; z = sum_{j<=kU} (-DU^{-1}Us)^j DU^{-1} y ; x += z
+    const double *y = rhs;
+    const double *z0 = nullptr;
+    if (k_l > 0) {
+        // L sweeps ping-pong in W0/W1; the last writes y and, when U sweeps
+        // follow, z^(0) = y / dU into W2 (EPI_STORE2)
+        double *ybuf = (k_l & 1) ? W0 : W1;
+        Stage sl{&h->Ls, &h->LsG, nullptr, rhs, k_l};
+        if (k_u == 0) return run_sweeps(h, sl, W0, W1, EPI_XADD_SCALE, nullptr, x, h->dU, s);
+        st = run_sweeps(h, sl, W0, W1, EPI_STORE2, ybuf, nullptr, h->dU, s, W2);
+        if (st != NSM_OK) return st;
+        z0 = W2;
+        y = ybuf;
+    } else if (k_u == 0) {
+        return scale_into(h, true, rhs, h->dU, x, s);
+    }
+    // z ping-pong in buffers holding neither y nor (for the first U sweep) z^(0)
+    double *za, *zb;
+    if (y == W0) { za = W1; zb = W2; }
+    else if (y == W1) { za = W0; zb = W2; }
+    else { za = W0; zb = W1; }
+    return run_sweeps(h, Stage{&h->Us, &h->UsG, h->dU, y, k_u, z0}, za, zb, EPI_XADD, nullptr, x, nullptr, s);
+}
+
 nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, int nu, int k_l, int k_u,
                       int x_is_zero, void *stream) {
     if (!h) return NSM_ERR_ARG;
@@ -635,86 +717,17 @@ nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, 
         h->err = "nsm_smooth: bad argument (negative count, NULL or aliased vector)";
         return NSM_ERR_ARG;
     }
-    if (kind != NSM_PGS && kind != NSM_ILU0) { h->err = "nsm_smooth: unknown kind"; return NSM_ERR_ARG; }
+    if (kind < NSM_PGS || kind > NSM_L1_JACOBI) { h->err = "nsm_smooth: unknown kind"; return NSM_ERR_ARG; }
     if (kind == NSM_ILU0 && !h->has_ilu) { h->err = "nsm_smooth: ILU0 requested on a handle without factors"; return NSM_ERR_STATE; }
     cudaStream_t s = S(stream);
-    double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
     for (int it = 0; it < nu; ++it) {
-        // row a2: residual; x == 0 => r = b exactly (reading R3)
         const bool fresh = it == 0 && x_is_zero;
-        const double *rhs = fresh ? b : R;
-        nsm_status st = NSM_OK;
-        if (kind == NSM_PGS) {
-            // the residual pass also writes g^(0) = r / d (eq:jr-initial-guess)
-            // when sweeps follow, so the first sweep gathers it instead of
-            // dividing per gathered entry
-            if (h->fused_ready && h->fused && h->pipeline && k_l >= 1 && k_l <= nsm_handle::kFusedKmax) {
-                // rows a2-a4 in ONE pass over the matrix (fused.cu); x = 0 needs
-                // no special case: the residual phase then computes b exactly
-                FusedLaunch f{};
-                f.n = h->n;
-                f.L = &h->L;
-                f.U = &h->U;
-                f.d = h->d;
-                f.b = b;
-                f.x = x;
-                f.k = k_l;
-                f.DL = h->fused_DL;
-                f.DU = h->fused_DU;
-                f.M = h->fused_M;
-                f.ring = h->fused_ring;
-                f.sync = h->fused_sync;
-                f.grid = h->fused_grid;
-                f.flag = h->flag;
-                f.sweep_id0 = h->sweep_counter + 1;
-                h->sweep_counter += k_l + 1;
-                f.err = h->d_dist_err;
-                f.timeout_ns = h->timeout_ns;
-                cudaError_t e = launch_pgs_fused(f, s);
-                h->launches += 2;
-                if (e != cudaSuccess) return cuda_fail(h, e, "fused pGS launch");
-                continue;
-            }
-            const bool rg = !fresh && k_l > 0;
-            if (!fresh) st = residual_into(h, b, x, R, rg ? OUT_RG : OUT_R, s, rg ? W2 : nullptr);
-            if (st != NSM_OK) return st;
-            // rows a3/a4: k_l sweeps g <- D^{-1}(r - L g), the last fused with x += g
-            if (k_l == 0) st = scale_into(h, true, rhs, h->d, x, s);
-            else {
-                Stage sg{&h->L, &h->LG, h->d, rhs, k_l, rg ? W2 : nullptr};
-                st = run_sweeps(h, sg, W0, W1, EPI_XADD, nullptr, x, nullptr, s);
-            }
+        nsm_status st;
+        if (kind == NSM_PGS_SYMMETRIC) {
+            st = apply_once(h, NSM_PGS, b, x, k_l, k_u, fresh, s);
+            if (st == NSM_OK) st = apply_once(h, NSM_PGS_BACKWARD, b, x, k_l, k_u, false, s);
         } else {
-            if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
-            if (st != NSM_OK) return st;
-            // row a5: y = sum_{j<=kL} (-Ls)^j r ; z = sum_{j<=kU} (-DU^{-1}Us)^j DU^{-1} y ; x += z
-            const double *y = rhs;
-            const double *z0 = nullptr;
-            if (k_l > 0) {
-                // L sweeps ping-pong in W0/W1; the last writes y and, when U
-                // sweeps follow, z^(0) = y / dU into W2 (EPI_STORE2)
-                double *ybuf = (k_l & 1) ? W0 : W1;
-                Stage sl{&h->Ls, &h->LsG, nullptr, rhs, k_l};
-                if (k_u == 0) st = run_sweeps(h, sl, W0, W1, EPI_XADD_SCALE, nullptr, x, h->dU, s);
-                else {
-                    st = run_sweeps(h, sl, W0, W1, EPI_STORE2, ybuf, nullptr, h->dU, s, W2);
-                    z0 = W2;
-                }
-                if (st != NSM_OK) return st;
-                y = ybuf;
-            } else if (k_u == 0) {
-                st = scale_into(h, true, rhs, h->dU, x, s);
-            }
-            if (st == NSM_OK && k_u > 0) {
-                // z ping-pong in buffers holding neither y nor (for the first
-                // U sweep) z^(0)
-                double *za, *zb;
-                if (y == W0) { za = W1; zb = W2; }
-                else if (y == W1) { za = W0; zb = W2; }
-                else { za = W0; zb = W1; }
-                st = run_sweeps(h, Stage{&h->Us, &h->UsG, h->dU, y, k_u, z0}, za, zb, EPI_XADD, nullptr, x, nullptr,
-                                s);
-            }
+            st = apply_once(h, kind, b, x, k_l, k_u, fresh, s);
         }
         if (st != NSM_OK) return st;
     }

@@ -150,16 +150,20 @@ nsm_status build_split(const nsm_csr *A, int64_t rb, int64_t re, Split *out, std
     std::vector<int64_t> first[5];
     for (int k = 0; k < 5; ++k) { cnt[k].assign(n, 0); first[k].assign(n, 0); }
     out->d.assign(n, 0.0);
+    out->dl1.assign(n, 0.0);
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
         for (int k = 0; k < 5; ++k) first[k][i] = rp[i];
         int prev = -1;
+        double l1 = 0.0;  // sum of |a_ij|, j != i, ascending columns
         for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
             int k = classify(rb + i, ci[p], rb, re);
             if (k != prev) { first[k][i] = p; prev = k; }
             cnt[k][i]++;
             if (k == P_D) out->d[i] = va[p];
+            else l1 = l1 + std::fabs(va[p]);
         }
+        out->dl1[i] = out->d[i] + l1;
     }
     // ---- ghost columns (ascending global ids)
     std::vector<int64_t> &g = out->ghost_gid;

@@ -51,6 +51,7 @@ inline SellView view(const Sell &s) { return SellView{s.ptr, s.col, s.val}; }
 struct Split {
     int64_t n = 0, row_begin = 0, n_ghost = 0;
     std::vector<double> d;            // diagonal of A (or of U for factors)
+    std::vector<double> dl1;          // a_ii + sum_{j != i} |a_ij| (l1-Jacobi diagonal)
     SellHost L, U;                    // strict lower / upper, LOCAL columns
     SellHost LG, UG;                  // couplings to ghost columns below / above the block
     std::vector<int64_t> ghost_gid;   // global id of ghost k (ascending)

@@ -201,3 +201,26 @@ def test_two_process_ipc_same_device():
     for p in procs:
         p.join(timeout=120)
     assert res is True, res
+
+
+@pytest.mark.parametrize("mode", ["hybrid", "global"])
+@pytest.mark.parametrize("kind", ["pgs_backward", "pgs_symmetric", "l1_jacobi"])
+def test_dist_other_smoothers(mode, kind):
+    A = CASES["random_3"][0]()
+    bounds = CASES["random_3"][1]
+    m = nsm.NSM_DIST_HYBRID if mode == "hybrid" else nsm.NSM_DIST_GLOBAL
+    part = bounds if mode == "hybrid" else None
+    V = VirtualRanks(A, bounds, m)
+    b, x0 = inputs.uniform(0, A.nrows), inputs.uniform(1, A.nrows)
+    try:
+        bs, xs = V.split(b), V.split(x0)
+        V.run(lambda r, S: S.smooth(bs[r], xs[r], kind, nu=2, k_l=2))
+        if kind == "pgs_backward":
+            want = oracle.pgs_backward_apply(A, b, x0, 2, nu=2, bounds=part)
+        elif kind == "pgs_symmetric":
+            want = oracle.pgs_symmetric_apply(A, b, x0, 2, nu=2, bounds=part)
+        else:
+            want = oracle.l1_jacobi_apply(A, b, x0, nu=2)
+        agree(torch.cat(xs).cpu().numpy(), want, f"{mode} {kind}")
+    finally:
+        V.close()

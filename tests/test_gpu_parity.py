@@ -222,3 +222,24 @@ def test_full_size_parity(cfg):
             x = dev(x0)
             S.smooth(dev(b), x, kind, nu=1, k_l=2, k_u=2)
             agree(host(x), want, f"{cfg} kernels={mode}")
+
+
+ORACLE_APPLY = {
+    "pgs_backward": lambda A, b, x0, k, nu, xz: oracle.pgs_backward_apply(A, b, x0, k, nu=nu, x_is_zero=xz),
+    "pgs_symmetric": lambda A, b, x0, k, nu, xz: oracle.pgs_symmetric_apply(A, b, x0, k, nu=nu, x_is_zero=xz),
+    "l1_jacobi": lambda A, b, x0, k, nu, xz: oracle.l1_jacobi_apply(A, b, x0, nu=nu, x_is_zero=xz),
+}
+
+
+@pytest.mark.parametrize("kind,k,nu,xz", [("pgs_backward", 2, 1, False), ("pgs_backward", 0, 2, True),
+                                          ("pgs_backward", 3, 2, True), ("pgs_symmetric", 2, 2, False),
+                                          ("pgs_symmetric", 1, 1, True), ("l1_jacobi", 0, 3, False),
+                                          ("l1_jacobi", 0, 1, True)])
+def test_other_smoothers(case, kind, k, nu, xz):
+    """Backward / symmetric pGS and l1-Jacobi."""
+    name, A, F, S = case
+    b = inputs.uniform(0, A.nrows)
+    x0 = np.zeros(A.nrows) if xz else inputs.uniform(1, A.nrows)
+    x = dev(x0)
+    S.smooth(dev(b), x, kind, nu=nu, k_l=k, x_is_zero=xz)
+    agree(host(x), ORACLE_APPLY[kind](A, b, x0, k, nu, xz), f"{name} {kind} k={k} nu={nu} xz={xz}")

@@ -402,3 +402,59 @@ def test_zero_diagonal_error():
     A = inputs.CSR.from_scipy(sp.csr_matrix(np.array([[1.0, 1.0], [1.0, 0.0]])))
     with pytest.raises(oracle.OracleError):
         oracle.pgs_apply(A, np.ones(2), np.zeros(2), 1)
+
+
+# ------------------------------------------- backward / symmetric / l1-Jacobi
+@pytest.mark.parametrize("n", [4, 7])
+def test_backward_pgs_neumann_and_nilpotence(n):
+    """M = D + U: k sweeps = (k+1)-term Neumann series in
+    D^-1 U (dense powers); k = n-1 = backward substitution."""
+    A = inputs.random_dense(n, seed=300 + n, density=0.7)
+    M = dense(A)
+    D, L, U = split(M)
+    Dinv = np.diag(1.0 / np.diag(M))
+    b, x0 = inputs.uniform(0, n), inputs.uniform(1, n)
+    r = b - M @ x0
+    for k in range(n):
+        want = x0 + neumann_powers(Dinv @ U, Dinv @ r, k)
+        np.testing.assert_allclose(oracle.pgs_backward_apply(A, b, x0, k), want, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(oracle.pgs_backward_apply(A, b, x0, n - 1),
+                               x0 + sla.solve_triangular(np.triu(M), r, lower=False), rtol=1e-12, atol=1e-13)
+
+
+def test_symmetric_pgs_is_forward_then_backward_operator():
+    """Symmetric pGS error operator = E_back E_fwd with the dense Neumann
+    operators M_k^{-1} = S_k D^{-1} of each direction."""
+    n = 8
+    A = inputs.random_dense(n, seed=17, density=0.6)
+    M = dense(A)
+    D, L, U = split(M)
+    Dinv = np.diag(1.0 / np.diag(M))
+    k = 2
+    Mf = sum(np.linalg.matrix_power(-Dinv @ L, j) for j in range(k + 1)) @ Dinv
+    Mb = sum(np.linalg.matrix_power(-Dinv @ U, j) for j in range(k + 1)) @ Dinv
+    I = np.eye(n)
+    E = (I - Mb @ M) @ (I - Mf @ M)
+    x0 = inputs.uniform(1, n)
+    # b = 0: x_new = E x0
+    np.testing.assert_allclose(oracle.pgs_symmetric_apply(A, np.zeros(n), x0, k), E @ x0, rtol=1e-12, atol=1e-13)
+
+
+def test_l1_jacobi_properties():
+    # diagonal matrix: exact in one sweep
+    A = inputs.CSR.from_scipy(sp.diags(np.arange(1.0, 9.0)).tocsr())
+    b = inputs.uniform(0, 8)
+    np.testing.assert_allclose(oracle.l1_jacobi_apply(A, b, np.zeros(8)), b / np.arange(1.0, 9.0), rtol=1e-15)
+    # zero-row-sum interior rows of an M-matrix: D_l1 = 2 a_ii
+    A = inputs.var27(6)
+    M = dense(A)
+    x0 = inputs.uniform(1, A.nrows)
+    b = inputs.uniform(0, A.nrows)
+    dl1 = np.diag(M) + np.abs(M - np.diag(np.diag(M))).sum(1)
+    i = 2 + 6 * (2 + 6 * 2)
+    assert abs(dl1[i] - 2 * M[i, i]) < 1e-9 * M[i, i]
+    got = oracle.l1_jacobi_apply(A, b, x0)
+    np.testing.assert_allclose(got, x0 + (b - M @ x0) / dl1, rtol=1e-13, atol=1e-14)
+    # unconditionally convergent for SPD A (Baker et al. 2011): rho(I - D_l1^-1 A) < 1
+    rho = max(abs(np.linalg.eigvals(np.eye(A.nrows) - M / dl1[:, None])))
+    assert rho < 1.0
