@@ -362,7 +362,7 @@ Geo geometry(K kernel, int np, int maxw) {
     // the attribute is per kernel (shared by all handles): allow the maximum
     // once; each launch passes its own dynamic size
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-    for (int nst = 2; nst <= 6; ++nst) {
+    for (int nst = 1; nst <= 6; ++nst) {  // nst = 1: overlap comes from co-resident CTAs
         const int64_t smem = 128 + nst * stage;
         if (smem > kSmemMax) break;
         int per_sm = 0;
@@ -445,7 +445,7 @@ cudaError_t sweep_tma_epi(const SweepArgs &a, int64_t s_begin, int64_t s_end, cu
 // Shared memory of one stage must fit (two stages at least).
 bool tma_ok(int np, int maxw) {
     const int64_t stage = np * (int64_t)kTS * kSlice * std::max(maxw, 1) * 12;
-    return 128 + 2 * stage <= kSmemMax;
+    return 128 + stage <= kSmemMax;
 }
 
 cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
