@@ -256,6 +256,44 @@ const char *nsm_last_error(const nsm_handle *h);
 typedef enum { NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2, NSM_OPT_PDL = 3 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 
+/* ---- GPU-resident solver around the smoothers ---
+ * nsm_spmat: a general (rectangular) CSR matrix on the device for the AMG
+ * transfer operators; y = alpha * M x + beta * y.  HOST CSR in, device
+ * vectors at apply time. */
+typedef struct nsm_spmat nsm_spmat;
+nsm_status nsm_spmat_setup(nsm_spmat **out, const nsm_csr *M, int device);
+nsm_status nsm_spmat_apply(nsm_spmat *M, const double *x, double *y, double alpha, double beta, void *stream);
+void nsm_spmat_destroy(nsm_spmat *M);
+
+/* nsm_amg: one C-AMG V(nu_pre, nu_post) cycle
+ * over a hierarchy built by the caller: smoothers[l] (l < nlevels) are
+ * nsm handles of A_l (BORROWED: must outlive the nsm_amg), P[l] the HOST
+ * prolongation A_l -> A_{l+1} (n_l x n_{l+1}; R = P^T), coarse the
+ * HOST coarsest matrix A_{nlevels} (<= 8192 rows; inverted densely at setup
+ * with partial pivoting: the coarse direct solve).  nsm_amg_vcycle computes
+ * x = V(b) from x = 0: per level pre-smooth (x_is_zero), residual, restrict,
+ * recurse, prolong-add, post-smooth; b and x device, length n_0, distinct.
+ * Default smoother on every level: NSM_PGS, nu = 1/1, k = 2. */
+typedef struct nsm_amg nsm_amg;
+nsm_status nsm_amg_setup(nsm_amg **out, int nlevels, nsm_handle *const *smoothers, const nsm_csr *const *P,
+                         const nsm_csr *coarse, int device);
+nsm_status nsm_amg_set_smoother(nsm_amg *M, int level, nsm_kind kind, int nu_pre, int nu_post, int k_l, int k_u);
+nsm_status nsm_amg_vcycle(nsm_amg *M, const double *b, double *x, void *stream);
+void nsm_amg_destroy(nsm_amg *M);
+const char *nsm_solver_last_error(const nsm_amg *M);
+
+/* nsm_gmres: right-preconditioned one-reduce MGS-GMRES with lagged
+ * normalisation (Algorithm 1), x0 = 0, no restart.  Per
+ * iteration: w = A M u, ONE reduction [V, u]^T [u, w] (one device -> host
+ * read), projection with T = I - L (t_mode 0: the paper's truncated Neumann
+ * series) or T = (I + L)^{-1} (t_mode 1).  Stops when
+ * the implicit relative residual < tol or after maxit iterations.
+ * M = NULL: no preconditioner.  *iters = Krylov dimension m; hist (NULL or
+ * maxit + 1 entries) receives the implicit relative residuals.  b, x device,
+ * length n; synchronises `stream`.  Allocates (maxit + 1) n-vectors. */
+nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int maxit, double tol, int t_mode,
+                     int *iters, double *hist, void *stream);
+
 /* Frees all device memory of the handle (synchronises its device).  NULL ok. */
 void nsm_destroy(nsm_handle *h);
 

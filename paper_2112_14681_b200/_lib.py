@@ -21,7 +21,9 @@ _STATUS = {0: "NSM_OK", 1: "NSM_ERR_ARG", 2: "NSM_ERR_PATTERN", 3: "NSM_ERR_ZERO
 SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_spmv",
                   "nsm_check", "nsm_info", "nsm_stats", "nsm_last_error", "nsm_destroy", "nsm_halo_plan",
                   "nsm_halo_set_send", "nsm_halo_mailbox", "nsm_halo_connect_ipc", "nsm_halo_connect",
-                  "nsm_halo_commit", "nsm_set_option"])
+                  "nsm_halo_commit", "nsm_set_option", "nsm_spmat_setup", "nsm_spmat_apply",
+                  "nsm_spmat_destroy", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle", "nsm_amg_destroy",
+                  "nsm_solver_last_error", "nsm_gmres"])
 
 
 class NsmError(RuntimeError):
@@ -72,13 +74,27 @@ def load():
     L.nsm_halo_connect.argtypes = [vp, ci, vp, i64, i64]
     L.nsm_halo_commit.argtypes = [vp]
     L.nsm_set_option.argtypes = [vp, ci, i64]
+    L.nsm_spmat_setup.argtypes = [P(vp), P(_Csr), ci]
+    L.nsm_spmat_apply.argtypes = [vp, vp, vp, ctypes.c_double, ctypes.c_double, vp]
+    L.nsm_spmat_destroy.argtypes = [vp]
+    L.nsm_spmat_destroy.restype = None
+    L.nsm_amg_setup.argtypes = [P(vp), ci, vp, vp, P(_Csr), ci]
+    L.nsm_amg_set_smoother.argtypes = [vp, ci, ci, ci, ci, ci, ci]
+    L.nsm_amg_vcycle.argtypes = [vp, vp, vp, vp]
+    L.nsm_amg_destroy.argtypes = [vp]
+    L.nsm_amg_destroy.restype = None
+    L.nsm_solver_last_error.argtypes = [vp]
+    L.nsm_solver_last_error.restype = ctypes.c_char_p
+    L.nsm_gmres.argtypes = [vp, vp, vp, vp, ci, ctypes.c_double, ci, P(ci), vp, vp]
     L.nsm_last_error.argtypes = [vp]
     L.nsm_last_error.restype = ctypes.c_char_p
     L.nsm_destroy.argtypes = [vp]
     L.nsm_destroy.restype = None
     for name in ["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
                  "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
-                 "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option"]:
+                 "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
+                 "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
+                 "nsm_gmres"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -338,3 +354,112 @@ class Smoother:
 
     def __exit__(self, *a):
         self.close()
+
+
+# ----------------------------------------------------------- solver layer --
+def _solver_err(h=None) -> str:
+    m = load().nsm_solver_last_error(h)
+    return m.decode() if m else ""
+
+
+class SpMat:
+    """Device CSR (rectangular allowed): y = alpha * M x + beta * y."""
+
+    def __init__(self, M, device: int | None = None):
+        import torch
+        self._torch = torch
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        keep: list = []
+        cs = _csr_struct(M, keep)
+        h = ctypes.c_void_p()
+        st = load().nsm_spmat_setup(ctypes.byref(h), ctypes.byref(cs), self.device)
+        if st != 0:
+            raise NsmError(st, _solver_err())
+        self._h, self.shape = h, (int(M.nrows), int(M.ncols))
+
+    def apply(self, x, y=None, alpha=1.0, beta=0.0, stream=None):
+        torch = self._torch
+        if y is None:
+            y = torch.zeros(self.shape[0], dtype=torch.float64, device=f"cuda:{self.device}")
+        st = load().nsm_spmat_apply(self._h, x.data_ptr(), y.data_ptr(), float(alpha), float(beta),
+                                    torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream)
+        if st != 0:
+            raise NsmError(st, "nsm_spmat_apply")
+        return y
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().nsm_spmat_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Amg:
+    """GPU V-cycle over a caller-built hierarchy: smoothers = [Smoother of A_l],
+    P = [host CSR A_l -> A_{l+1}], coarse = host CSR of the coarsest matrix."""
+
+    def __init__(self, smoothers, P, coarse, device: int | None = None):
+        import torch
+        self._torch = torch
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.smoothers = list(smoothers)  # keep the borrowed handles alive
+        keep: list = []
+        nl = len(self.smoothers)
+        hs = (ctypes.c_void_p * max(nl, 1))(*[S._h for S in self.smoothers])
+        ps = [_csr_struct(p, keep) for p in P]
+        parr = (ctypes.POINTER(_Csr) * max(nl, 1))(*[ctypes.pointer(p) for p in ps])
+        cc = _csr_struct(coarse, keep)
+        h = ctypes.c_void_p()
+        st = load().nsm_amg_setup(ctypes.byref(h), nl, ctypes.cast(hs, ctypes.c_void_p),
+                                  ctypes.cast(parr, ctypes.c_void_p), ctypes.byref(cc), self.device)
+        if st != 0:
+            raise NsmError(st, _solver_err())
+        self._h = h
+        self.n = self.smoothers[0].n if nl else int(coarse.nrows)
+
+    def set_smoother(self, level, kind="pgs", nu_pre=1, nu_post=1, k_l=2, k_u=2):
+        kd = KINDS[kind] if isinstance(kind, str) else int(kind)
+        st = load().nsm_amg_set_smoother(self._h, int(level), kd, int(nu_pre), int(nu_post), int(k_l), int(k_u))
+        if st != 0:
+            raise NsmError(st, "nsm_amg_set_smoother")
+
+    def vcycle(self, b, x=None, stream=None):
+        torch = self._torch
+        x = torch.empty_like(b) if x is None else x
+        st = load().nsm_amg_vcycle(self._h, b.data_ptr(), x.data_ptr(),
+                                   torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream)
+        if st != 0:
+            raise NsmError(st, _solver_err(self._h))
+        return x
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().nsm_amg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gmres(A: "Smoother", b, amg: "Amg | None" = None, tol: float = 1e-5, maxit: int = 200, t_mode: str = "neumann",
+          stream=None):
+    """Algorithm 1 on the device.  Returns (x, iterations, implicit relres history)."""
+    import torch
+    x = torch.empty_like(b)
+    hist = np.zeros(maxit + 1)
+    its = ctypes.c_int()
+    tm = {"neumann": 0, "inverse": 1}[t_mode]
+    st = load().nsm_gmres(A._h, amg._h if amg is not None else None, b.data_ptr(), x.data_ptr(), int(maxit),
+                          float(tol), tm, ctypes.byref(its), hist.ctypes.data,
+                          torch.cuda.current_stream(A.device).cuda_stream if stream is None else stream)
+    if st != 0:
+        raise NsmError(st, _solver_err())
+    return x, its.value, hist[:its.value + 1]
