@@ -207,8 +207,9 @@ nsm_status nsm_usolve(nsm_handle *h, const double *r, double *x, int k_sweeps, v
  *   NSM_PGS_BACKWARD: x <- x + sum_{j<=k_l} (-D^{-1}U)^j D^{-1} (b - A x)
  *   NSM_PGS_SYMMETRIC: NSM_PGS then NSM_PGS_BACKWARD (each with its residual)
  *   NSM_L1_JACOBI: x <- x + D_l1^{-1} (b - A x)                      (k_l, k_u ignored)
- * x_is_zero != 0 asserts x == 0 on entry, so the first residual is b and is
- * not computed (V-cycle pre-smoothing; exact).  b and x must not alias.
+ * x_is_zero != 0: the first iteration takes x = 0 whatever x holds on entry
+ * (its contents are ignored and overwritten), so the first residual is b and
+ * is not computed (V-cycle pre-smoothing; exact).  b and x must not alias.
  * Requesting NSM_ILU0 on a handle set up without factors -> NSM_ERR_STATE.
  */
 nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, int nu, int k_l,

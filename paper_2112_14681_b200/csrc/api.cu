@@ -630,8 +630,9 @@ nsm_status nsm_usolve(nsm_handle *h, const double *r, double *x, int k, void *st
     return tri_solve(h, false, r, x, k, stream);
 }
 
-// One smoother application of the given kind (rows a2-a5).  fresh: x == 0 on
-// entry, so the residual is b (reading R3).
+// One smoother application of the given kind (rows a2-a5).  fresh: x is
+// taken as 0 (its contents are ignored), so the residual is b (reading R3)
+// and the last kernel STORES x instead of adding to it.
 static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, double *x, int k_l, int k_u, bool fresh,
                              cudaStream_t s) {
     double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
@@ -640,13 +641,15 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
     if (kind == NSM_L1_JACOBI) {
         // l1-Jacobi: x += D_l1^{-1} (b - A x)
         if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
-        return st != NSM_OK ? st : scale_into(h, true, rhs, h->dl1, x, s);
+        return st != NSM_OK ? st : scale_into(h, !fresh, rhs, h->dl1, x, s);
     }
     if (kind == NSM_PGS || kind == NSM_PGS_BACKWARD) {
         const bool fwd = kind == NSM_PGS;
         if (fwd && h->fused_ready && h->fused && h->pipeline && k_l >= 1 && k_l <= nsm_handle::kFusedKmax) {
-            // rows a2-a4 in ONE pass over the matrix (fused.cu); x = 0 needs
-            // no special case: the residual phase then computes b exactly
+            // rows a2-a4 in ONE pass over the matrix (fused.cu); with x = 0
+            // the residual phase computes b exactly
+            if (fresh && h->n > 0 && cudaMemsetAsync(x, 0, h->n * sizeof(double), s) != cudaSuccess)
+                return cuda_fail(h, cudaGetLastError(), "memset");
             FusedLaunch f{};
             f.n = h->n;
             f.L = &h->L;
@@ -678,10 +681,11 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
         if (st != NSM_OK) return st;
         // rows a3/a4: k_l sweeps g <- D^{-1}(r - T g) (T = L forward, U
         // backward), the last fused with x += g
-        if (k_l == 0) return scale_into(h, true, rhs, h->d, x, s);
+        if (k_l == 0) return scale_into(h, !fresh, rhs, h->d, x, s);
         Stage sg = fwd ? Stage{&h->L, &h->LG, h->d, rhs, k_l, rg ? W2 : nullptr}
                        : Stage{&h->U, &h->UG, h->d, rhs, k_l, rg ? W2 : nullptr};
-        return run_sweeps(h, sg, W0, W1, EPI_XADD, nullptr, x, nullptr, s);
+        return fresh ? run_sweeps(h, sg, W0, W1, EPI_STORE, x, nullptr, nullptr, s)
+                     : run_sweeps(h, sg, W0, W1, EPI_XADD, nullptr, x, nullptr, s);
     }
     // NSM_ILU0
     if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
@@ -694,20 +698,24 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
         // follow, z^(0) = y / dU into W2 (EPI_STORE2)
         double *ybuf = (k_l & 1) ? W0 : W1;
         Stage sl{&h->Ls, &h->LsG, nullptr, rhs, k_l};
-        if (k_u == 0) return run_sweeps(h, sl, W0, W1, EPI_XADD_SCALE, nullptr, x, h->dU, s);
+        if (k_u == 0)
+            return fresh ? run_sweeps(h, sl, W0, W1, EPI_STORE2, W2, nullptr, h->dU, s, x)   // x = y / dU
+                         : run_sweeps(h, sl, W0, W1, EPI_XADD_SCALE, nullptr, x, h->dU, s);
         st = run_sweeps(h, sl, W0, W1, EPI_STORE2, ybuf, nullptr, h->dU, s, W2);
         if (st != NSM_OK) return st;
         z0 = W2;
         y = ybuf;
     } else if (k_u == 0) {
-        return scale_into(h, true, rhs, h->dU, x, s);
+        return scale_into(h, !fresh, rhs, h->dU, x, s);
     }
     // z ping-pong in buffers holding neither y nor (for the first U sweep) z^(0)
     double *za, *zb;
     if (y == W0) { za = W1; zb = W2; }
     else if (y == W1) { za = W0; zb = W2; }
     else { za = W0; zb = W1; }
-    return run_sweeps(h, Stage{&h->Us, &h->UsG, h->dU, y, k_u, z0}, za, zb, EPI_XADD, nullptr, x, nullptr, s);
+    Stage su{&h->Us, &h->UsG, h->dU, y, k_u, z0};
+    return fresh ? run_sweeps(h, su, za, zb, EPI_STORE, x, nullptr, nullptr, s)
+                 : run_sweeps(h, su, za, zb, EPI_XADD, nullptr, x, nullptr, s);
 }
 
 nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, int nu, int k_l, int k_u,
