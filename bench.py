@@ -273,20 +273,32 @@ def run_nsm(args, rank, nranks, local_rank):
     value = ab * nranks * args.steps / (t_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
 
-    # ---- dominant kernel: the residual pass, timed alone through nsm_residual
+    # ---- dominant kernel: the residual pass, timed INSIDE the smoother steps
+    # with the library's in-stream event pairs (NSM_OPT_PROFILE), over a second
+    # run of the same steps (events around each pass perturb PDL overlap, so
+    # they stay out of the headline timed region)
+    S.set_profile(True)
+    for _ in range(args.steps):
+        flush_l2(flush)
+        step()
+    torch.cuda.synchronize()
+    prof = S.profile()
+    S.set_profile(False)
+    k_ms = prof["residual"][0] / max(prof["residual"][1], 1)
+    k_bytes = model["residual"]
+    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9
+    sweep_bytes = sum(sum(v) for kk, v in model.items() if isinstance(v, list))
+    sweep_ms = prof["sweep"][0] / args.steps
+    # and alone through nsm_residual (L2 flushed before each launch)
     r = torch.empty_like(b)
-    for _ in range(3):
-        S.residual(b, x, r)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
     for e0, e1 in kev:
         flush_l2(flush)
         e0.record(stream)
         S.residual(b, x, r)
         e1.record(stream)
     torch.cuda.synchronize()
-    k_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in kev]))
-    k_bytes = model["residual"]
-    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9
+    alone_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in kev]))
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -344,9 +356,14 @@ def run_nsm(args, rank, nranks, local_rank):
                        "l2": "flushed before every timed step (256 MB read through L2)",
                        "bytes_per_step_per_gpu": ab, "frac_of_hbm_peak": round(value / nranks / peak, 4)},
             "ms_per_apply": round(ms_step, 4),
-            "roofline": {"bound": "hbm", "kernel": "k_residual (r = b - A x)", "achieved": round(k_gbs, 1),
-                         "peak": peak, "unit": "GB/s", "frac": round(k_gbs / peak, 4), "traffic": traffic,
-                         "peak_source": peak_src, "bytes_per_launch": k_bytes, "ms_per_launch": round(k_ms, 4)},
+            "roofline": {"bound": "hbm", "kernel": "residual pass r = b - A x (k_residual_tma)",
+                         "achieved": round(k_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(k_gbs / peak, 4),
+                         "traffic": traffic, "peak_source": peak_src, "bytes_per_launch": k_bytes,
+                         "ms_per_launch": round(k_ms, 4), "timing": "in-step CUDA events (NSM_OPT_PROFILE)",
+                         "alone_ms": round(alone_ms, 4),
+                         "alone_frac": round(k_bytes / (alone_ms * 1e-3) / 1e9 / peak, 4),
+                         "sweeps_frac": round(sweep_bytes / (max(sweep_ms, 1e-9) * 1e-3) / 1e9 / peak, 4)
+                         if prof["sweep"][1] else None},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": 16 * A.nrows,
                     "d2h_bytes_per_step": 8 * A.nrows},

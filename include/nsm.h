@@ -233,6 +233,12 @@ nsm_status nsm_info(const nsm_handle *h, int64_t *n_local, int64_t *n_ghost, int
  * call) and halo exchanges it performed.  Host-side, no synchronisation. */
 nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *halo_exchanges);
 
+/* In-stream pass timing (after nsm_set_option(h, NSM_OPT_PROFILE, 1)):
+ * waits for the recorded events, returns the summed milliseconds and counts
+ * of residual passes (ms[0], count[0]) and sweep passes (ms[1], count[1])
+ * since the last call, and clears the records. */
+nsm_status nsm_profile(nsm_handle *h, double *ms, int64_t *count);
+
 /* Last error message: of `h`, or of the last failed setup when h == NULL.
  * The pointer stays valid until the next call on the same handle. */
 const char *nsm_last_error(const nsm_handle *h);
@@ -254,7 +260,11 @@ const char *nsm_last_error(const nsm_handle *h);
  *                           programmatic dependent launch (a kernel's matrix
  *                           prefetch overlaps the previous kernel's drain);
  *                           0 = plain stream order. */
-typedef enum { NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2, NSM_OPT_PDL = 3 } nsm_option;
+typedef enum {
+    NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2, NSM_OPT_PDL = 3,
+    NSM_OPT_PROFILE = 4 /* 1: record a CUDA event pair around every residual / sweep pass (up to
+                           4096 passes) for nsm_profile(); 0: off (default) */
+} nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 
 /* ---- GPU-resident solver around the smoothers ---

@@ -23,7 +23,7 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_us
                   "nsm_halo_set_send", "nsm_halo_mailbox", "nsm_halo_connect_ipc", "nsm_halo_connect",
                   "nsm_halo_commit", "nsm_set_option", "nsm_spmat_setup", "nsm_spmat_apply",
                   "nsm_spmat_destroy", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle", "nsm_amg_destroy",
-                  "nsm_solver_last_error", "nsm_gmres"])
+                  "nsm_solver_last_error", "nsm_gmres", "nsm_profile"])
 
 
 class NsmError(RuntimeError):
@@ -86,6 +86,7 @@ def load():
     L.nsm_solver_last_error.argtypes = [vp]
     L.nsm_solver_last_error.restype = ctypes.c_char_p
     L.nsm_gmres.argtypes = [vp, vp, vp, vp, ci, ctypes.c_double, ci, P(ci), vp, vp]
+    L.nsm_profile.argtypes = [vp, vp, vp]
     L.nsm_last_error.argtypes = [vp]
     L.nsm_last_error.restype = ctypes.c_char_p
     L.nsm_destroy.argtypes = [vp]
@@ -94,7 +95,7 @@ def load():
                  "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
                  "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
-                 "nsm_gmres"]:
+                 "nsm_gmres", "nsm_profile"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -327,6 +328,17 @@ class Smoother:
     def set_pdl(self, enable: bool):
         """Programmatic dependent launch between consecutive pipelined kernels."""
         self._call(load().nsm_set_option(self._h, 3, int(bool(enable))))
+
+    def set_profile(self, enable: bool):
+        """Record an event pair around every residual / sweep pass."""
+        self._call(load().nsm_set_option(self._h, 4, int(bool(enable))))
+
+    def profile(self):
+        """{'residual': (ms, count), 'sweep': (ms, count)} since the last call."""
+        ms = np.zeros(2)
+        cnt = np.zeros(2, dtype=np.int64)
+        self._call(load().nsm_profile(self._h, ms.ctypes.data, cnt.ctypes.data))
+        return {"residual": (float(ms[0]), int(cnt[0])), "sweep": (float(ms[1]), int(cnt[1]))}
 
     def set_halo_timeout(self, ms: int):
         """How long a halo wait spins before reporting NSM_ERR_DIST."""

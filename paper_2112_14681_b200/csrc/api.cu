@@ -57,6 +57,11 @@ struct nsm_handle {
     int64_t interior_begin = -1, interior_end = -1;          // set if the interior list is one range
     bool pipeline = true;                                    // bulk-copy pipelined kernels (stream.cu)
     bool pdl = true;                                         // programmatic dependent launch for them
+    // in-stream pass timing (NSM_OPT_PROFILE): event pool and records
+    bool profile = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> ev_kind;                                // kind of record i (events 2i, 2i+1)
+    int ev_used = 0;
     // fused one-pass pGS (fused.cu), single rank
     bool fused = false, fused_ready = false;  // opt-in: latency-bound so far
     int fused_DL = 0, fused_DU = 0, fused_grid = 0;
@@ -142,6 +147,7 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->d_counters);
     cudaFree(h->d_dist_err);
     cudaFree(h->ghost_null);
+    for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
     cudaFree(h->fused_ring);
     cudaFree(h->fused_sync);
     delete h;
@@ -176,8 +182,28 @@ struct Slices {
 // launch(slices, with_ghost, ghost): run the kernel on a set of slices.
 // With an exchange of `src` (scaled by 1/scale if given): put -> interior
 // slices (overlap with the NVLink transfer) -> wait -> boundary slices.
+// Optional in-stream timing of each pass (NSM_OPT_PROFILE): an event pair
+// around the pass, accumulated per kind by nsm_profile().
+struct ProfScope {
+    nsm_handle *h;
+    int kind;
+    cudaStream_t s;
+    int slot = -1;
+    ProfScope(nsm_handle *h_, int kind_, cudaStream_t s_) : h(h_), kind(kind_), s(s_) {
+        if (!h->profile || h->ev_used >= (int)h->ev_kind.size()) return;
+        slot = h->ev_used++;
+        h->ev_kind[slot] = kind;
+        cudaEventRecord(h->ev[2 * slot], s);
+    }
+    ~ProfScope() {
+        if (slot >= 0) cudaEventRecord(h->ev[2 * slot + 1], s);
+    }
+};
+
 template <class F>
-nsm_status pass(nsm_handle *h, bool exchange, const double *src, const double *scale, cudaStream_t s, F launch) {
+nsm_status pass(nsm_handle *h, bool exchange, const double *src, const double *scale, cudaStream_t s, F launch,
+                int prof_kind) {
+    ProfScope prof(h, prof_kind, s);
     if (!exchange || !distributed(h)) {
         cudaError_t e = launch(Slices{nullptr, h->nslices, 0, h->nslices}, false, (const double *)h->ghost_null);
         if (h->n > 0) ++h->launches;
@@ -264,7 +290,8 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(1, st.T->maxw))
                                     return launch_sweep_tma(a, sl.begin, sl.end, s);
                                 return launch_sweep(a, s);
-                            });
+                            },
+                            1);
         if (r != NSM_OK) return r;
         gin = out;
     }
@@ -279,7 +306,7 @@ nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double
             return launch_residual_tma(mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
         return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
                                out, out2, s);
-    });
+    }, 0);
 }
 
 nsm_status scale_into(nsm_handle *h, bool xadd, const double *rhs, const double *d, double *out, cudaStream_t s) {
@@ -568,6 +595,16 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
         case NSM_OPT_PIPELINE: h->pipeline = value != 0; return NSM_OK;
         case NSM_OPT_FUSED: h->fused = value != 0; return NSM_OK;
         case NSM_OPT_PDL: h->pdl = value != 0; return NSM_OK;
+        case NSM_OPT_PROFILE:
+            h->profile = value != 0;
+            if (h->profile && h->ev.empty()) {
+                cudaSetDevice(h->device);
+                h->ev.resize(2 * 4096);
+                for (cudaEvent_t &e : h->ev) cudaEventCreate(&e);
+                h->ev_kind.assign(4096, 0);
+            }
+            h->ev_used = 0;
+            return NSM_OK;
         case NSM_OPT_HALO_TIMEOUT_MS:
             if (value <= 0) return NSM_ERR_ARG;
             h->timeout_ns = (unsigned long long)value * 1000000ull;
@@ -583,6 +620,21 @@ nsm_status nsm_info(const nsm_handle *h, int64_t *n_local, int64_t *n_ghost, int
     if (n_ghost) *n_ghost = h->n_ghost;
     if (nnz_offdiag) *nnz_offdiag = h->nnz_off;
     if (device_bytes) *device_bytes = h->device_bytes;
+    return NSM_OK;
+}
+
+nsm_status nsm_profile(nsm_handle *h, double *ms, int64_t *count) {
+    if (!h || !ms || !count) return NSM_ERR_ARG;
+    for (int k = 0; k < 2; ++k) { ms[k] = 0.0; count[k] = 0; }
+    for (int i = 0; i < h->ev_used; ++i) {
+        float t = 0.f;
+        if (cudaEventSynchronize(h->ev[2 * i + 1]) != cudaSuccess ||
+            cudaEventElapsedTime(&t, h->ev[2 * i], h->ev[2 * i + 1]) != cudaSuccess)
+            return cuda_fail(h, cudaGetLastError(), "nsm_profile");
+        ms[h->ev_kind[i]] += t;
+        count[h->ev_kind[i]] += 1;
+    }
+    h->ev_used = 0;
     return NSM_OK;
 }
 
