@@ -114,3 +114,53 @@ def test_gmres_iteration_parity(case, t_mode):
             assert true < tol * 10
     finally:
         B.close()
+
+
+@pytest.mark.slow
+def test_solve_timing_table(tmp_path):
+    """Whole GMRES + C-AMG solve on the GPU (the paper's Table 6/7 metric,
+    P:L1351-1374) on a C3-shaped 27-point matrix, per smoother:
+    iterations to relres < 1e-5 and device solve time.  Informational: the
+    numbers are written to gpurun_out/solve_timing.json (profiles/ cites them)."""
+    import json
+    import os
+    import time
+    N = int(os.environ.get("NSM_SOLVE_N", "48"))
+    A = inputs.var27(N).to_scipy()
+    levels = amg.hierarchy(A, rand_fn, min_coarse=200)
+    nl = len(levels) - 1
+    S = [nsm.Smoother(inputs.CSR.from_scipy(levels[l][0]), oracle.ilu0(levels[l][0])[2] if l == 0 else None)
+         for l in range(nl)]
+    M = nsm.Amg(S, [inputs.CSR.from_scipy(levels[l][1]) for l in range(nl)], inputs.CSR.from_scipy(levels[-1][0]))
+    b = dev(inputs.uniform(0, A.shape[0]))
+    rows = []
+    variants = [("pGS k=1", "pgs", 1), ("pGS k=2", "pgs", 2), ("pGS k=3", "pgs", 3), ("symmetric pGS k=2", "pgs_symmetric", 2),
+                ("l1-Jacobi (2 sweeps)", "l1_jacobi", 0), ("ILU(0) k=3 finest + pGS k=2", "hybrid", 3)]
+    try:
+        for label, kind, k in variants:
+            for l in range(nl):
+                if kind == "hybrid":
+                    M.set_smoother(l, "ilu" if l == 0 else "pgs", 1, 1, k if l == 0 else 2, k if l == 0 else 2)
+                elif kind == "l1_jacobi":
+                    M.set_smoother(l, kind, 2, 2, 0, 0)
+                else:
+                    M.set_smoother(l, kind, 1, 1, k, k)
+            for t_mode in ("neumann", "inverse"):
+                nsm.gmres(S[0], b, M, tol=1e-5, t_mode=t_mode)          # warm-up
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                x, its, hist = nsm.gmres(S[0], b, M, tol=1e-5, t_mode=t_mode)
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+                rows.append({"smoother": label, "gmres_T": t_mode, "iterations": its, "solve_ms": round(dt * 1e3, 3),
+                             "final_implicit_relres": float(hist[-1])})
+        out = {"matrix": f"27-point variable coefficient {N}^3 (C3 shape)", "n": A.shape[0],
+               "levels": [lv[0].shape[0] for lv in levels], "rows": rows}
+        os.makedirs("gpurun_out", exist_ok=True)
+        with open("gpurun_out/solve_timing.json", "w") as f:
+            json.dump(out, f, indent=1)
+        assert all(r["iterations"] < 200 for r in rows)
+    finally:
+        M.close()
+        for s_ in S:
+            s_.close()
