@@ -116,35 +116,19 @@ def test_gmres_iteration_parity(case, t_mode):
         B.close()
 
 
-@pytest.mark.slow
-def test_solve_timing_table(tmp_path):
-    """Whole GMRES + C-AMG solve on the GPU (the paper's Table 6/7 metric,
-    P:L1351-1374) on a C3-shaped 27-point matrix, per smoother:
-    iterations to relres < 1e-5 and device solve time.  Informational: the
-    numbers are written to gpurun_out/solve_timing.json (profiles/ cites them)."""
-    import json
-    import os
+def _solve_table(A, variants, ilu_finest):
     import time
-    N = int(os.environ.get("NSM_SOLVE_N", "48"))
-    A = inputs.var27(N).to_scipy()
     levels = amg.hierarchy(A, rand_fn, min_coarse=200)
     nl = len(levels) - 1
-    S = [nsm.Smoother(inputs.CSR.from_scipy(levels[l][0]), oracle.ilu0(levels[l][0])[2] if l == 0 else None)
+    S = [nsm.Smoother(inputs.CSR.from_scipy(levels[l][0]), oracle.ilu0(levels[l][0])[2] if (l == 0 and ilu_finest) else None)
          for l in range(nl)]
     M = nsm.Amg(S, [inputs.CSR.from_scipy(levels[l][1]) for l in range(nl)], inputs.CSR.from_scipy(levels[-1][0]))
     b = dev(inputs.uniform(0, A.shape[0]))
     rows = []
-    variants = [("pGS k=1", "pgs", 1), ("pGS k=2", "pgs", 2), ("pGS k=3", "pgs", 3), ("symmetric pGS k=2", "pgs_symmetric", 2),
-                ("l1-Jacobi (2 sweeps)", "l1_jacobi", 0), ("ILU(0) k=3 finest + pGS k=2", "hybrid", 3)]
     try:
-        for label, kind, k in variants:
+        for label, per_level in variants:
             for l in range(nl):
-                if kind == "hybrid":
-                    M.set_smoother(l, "ilu" if l == 0 else "pgs", 1, 1, k if l == 0 else 2, k if l == 0 else 2)
-                elif kind == "l1_jacobi":
-                    M.set_smoother(l, kind, 2, 2, 0, 0)
-                else:
-                    M.set_smoother(l, kind, 1, 1, k, k)
+                M.set_smoother(l, *per_level(l))
             for t_mode in ("neumann", "inverse"):
                 nsm.gmres(S[0], b, M, tol=1e-5, t_mode=t_mode)          # warm-up
                 torch.cuda.synchronize()
@@ -154,13 +138,37 @@ def test_solve_timing_table(tmp_path):
                 dt = time.perf_counter() - t0
                 rows.append({"smoother": label, "gmres_T": t_mode, "iterations": its, "solve_ms": round(dt * 1e3, 3),
                              "final_implicit_relres": float(hist[-1])})
-        out = {"matrix": f"27-point variable coefficient {N}^3 (C3 shape)", "n": A.shape[0],
-               "levels": [lv[0].shape[0] for lv in levels], "rows": rows}
-        os.makedirs("gpurun_out", exist_ok=True)
-        with open("gpurun_out/solve_timing.json", "w") as f:
-            json.dump(out, f, indent=1)
-        assert all(r["iterations"] < 200 for r in rows)
     finally:
         M.close()
         for s_ in S:
             s_.close()
+    return {"n": A.shape[0], "levels": [lv[0].shape[0] for lv in levels], "rows": rows}
+
+
+@pytest.mark.slow
+def test_solve_timing_table():
+    """Whole GMRES + C-AMG solve on the GPU (the paper's Table 6/7 metric,
+    P:L1351-1374) per smoother: iterations to relres < 1e-5 and
+    solve time.  C3-shaped 27-point matrix with pGS / symmetric pGS /
+    l1-Jacobi (Table 6's smoothers); C4-shaped convection-diffusion (RCM)
+    with pGS vs ILU(0) on the finest level + pGS below (Table 7's hybrid
+    cycle).  Informational: written to gpurun_out/solve_timing.json."""
+    import json
+    import os
+    N3 = int(os.environ.get("NSM_SOLVE_N", "48"))
+    N4 = int(os.environ.get("NSM_SOLVE_N4", "32"))
+    pgs = lambda k: (lambda l: ("pgs", 1, 1, k, k))
+    t6 = _solve_table(inputs.var27(N3).to_scipy(), [
+        ("pGS k=1", pgs(1)), ("pGS k=2", pgs(2)), ("pGS k=3", pgs(3)),
+        ("symmetric pGS k=2", lambda l: ("pgs_symmetric", 1, 1, 2, 2)),
+        ("l1-Jacobi, 2 sweeps", lambda l: ("l1_jacobi", 2, 2, 0, 0))], False)
+    t7 = _solve_table(inputs.convdiff(N4).to_scipy(), [
+        ("pGS k=2", pgs(2)), ("pGS k=3", pgs(3)),
+        ("ILU(0) k=3 finest + pGS k=2", lambda l: ("ilu", 1, 1, 3, 3) if l == 0 else ("pgs", 1, 1, 2, 2)),
+        ("ILU(0) k=5 finest + pGS k=2", lambda l: ("ilu", 1, 1, 5, 5) if l == 0 else ("pgs", 1, 1, 2, 2))], True)
+    out = {"table6_like": dict(matrix=f"27-point variable coefficient {N3}^3 (C3 shape)", **t6),
+           "table7_like": dict(matrix=f"convection-diffusion {N4}^3 + RCM (C4 shape)", **t7)}
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/solve_timing.json", "w") as f:
+        json.dump(out, f, indent=1)
+    assert all(r["iterations"] < 200 for r in t6["rows"] + t7["rows"])
