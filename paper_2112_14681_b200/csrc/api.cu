@@ -319,6 +319,8 @@ size_t flags_bytes_for(int nranks) { return (((size_t)nranks * 8 + 255) / 256) *
 
 }  // namespace
 
+bool nsm::nsm_is_distributed(const nsm_handle *h) { return h && h->nranks > 1; }
+
 extern "C" {
 
 const char *nsm_last_error(const nsm_handle *h) { return h ? h->err.c_str() : g_setup_err.c_str(); }

@@ -154,6 +154,10 @@ void preload_plain_kernels();
 void preload_tma_kernels();
 void preload_halo_kernels();
 
+// True for handles of a multi-rank partition (their launches carry halo
+// sequence numbers and must not be captured into a replayed CUDA graph).
+bool nsm_is_distributed(const nsm_handle *h);
+
 // Host ILU(0) (nsm_ilu0).
 nsm_status ilu0_host(const nsm_csr *A, int64_t row_begin, double *fval, std::string *err);
 

@@ -402,6 +402,10 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
         g_solver_err = "nsm_gmres: device allocation failed";
         return NSM_ERR_OOM;
     }
+    cudaGraphExec_t gexec = nullptr;
+    bool use_graph = !nsm_is_distributed(A);
+    if (M)
+        for (nsm_handle *S : M->S) use_graph = use_graph && !nsm_is_distributed(S);
     auto precond = [&](const double *in, double *out) -> nsm_status {
         if (M) return nsm_amg_vcycle(M, in, out, s);
         return cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, s) == cudaSuccess ? NSM_OK
@@ -418,9 +422,35 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
     cudaMemcpyAsync(u, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
     for (int k = 0; k <= maxit && st == NSM_OK; ++k) {
         if (k < maxit) {
-            st = precond(u, z);                               // z = M u
-            if (st == NSM_OK) st = nsm_spmv(A, z, w, s);      // w = A M u   (step 5)
-            if (st != NSM_OK) break;
+            // step 5: w = A M u.  The V-cycle + SpMV is a fixed sequence of
+            // ~10 launches per level on fixed buffers (u -> z -> w), so it is
+            // captured once into a CUDA graph and replayed (single-rank
+            // handles only: a halo exchange bakes its sequence number in).
+            if (use_graph && !gexec) {
+                cudaGraph_t graph = nullptr;
+                bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                if (ok) {
+                    st = precond(u, z);
+                    if (st == NSM_OK) st = nsm_spmv(A, z, w, s);
+                    ok = cudaStreamEndCapture(s, &graph) == cudaSuccess && st == NSM_OK &&
+                         cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
+                    if (graph) cudaGraphDestroy(graph);
+                }
+                if (!ok) {  // fall back to plain launches
+                    cudaGetLastError();
+                    if (gexec) cudaGraphExecDestroy(gexec);
+                    gexec = nullptr;
+                    use_graph = false;
+                    st = NSM_OK;
+                }
+            }
+            if (gexec) {
+                if (cudaGraphLaunch(gexec, s) != cudaSuccess) { st = NSM_ERR_CUDA; break; }
+            } else {
+                st = precond(u, z);                               // z = M u
+                if (st == NSM_OK) st = nsm_spmv(A, z, w, s);      // w = A M u
+                if (st != NSM_OK) break;
+            }
         }
         // step 6: the single reduction [V_k, u]^T [u, w]
         k_multidot<<<nblk, kThr, 0, s>>>(n, k, V, u, k < maxit ? w : u, part);
@@ -493,6 +523,7 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
     }
     if (iters) *iters = m;
     if (hist) std::copy(hv.begin(), hv.end(), hist);
+    if (gexec) cudaGraphExecDestroy(gexec);
     cleanup();
     if (st != NSM_OK && g_solver_err.empty()) g_solver_err = "nsm_gmres: failed";
     return st;
