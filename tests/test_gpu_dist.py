@@ -224,3 +224,38 @@ def test_dist_other_smoothers(mode, kind):
         agree(torch.cat(xs).cpu().numpy(), want, f"{mode} {kind}")
     finally:
         V.close()
+
+
+@pytest.mark.parametrize("mode", ["hybrid", "global"])
+def test_eight_rank_slabs(mode):
+    """C5 shape: 8 z-slabs of a 7-point grid (each rank 20 x 20 x 6 rows),
+    pGS k = 2 and ILU(0) k = 2, nu = 2, all ranks exchanging over the
+    mailbox path at once."""
+    P, N = 8, 20
+    A = inputs.laplace(N, N, 6 * P)
+    n_loc = N * N * 6
+    bounds = list(range(0, P * n_loc + 1, n_loc))
+    b, x0 = inputs.uniform(0, A.nrows), inputs.uniform(1, A.nrows)
+    m = nsm.NSM_DIST_HYBRID if mode == "hybrid" else nsm.NSM_DIST_GLOBAL
+    part = bounds if mode == "hybrid" else None
+    V = VirtualRanks(A, bounds, m)
+    try:
+        bs, xs = V.split(b), V.split(x0)
+        V.run(lambda r, S: S.smooth(bs[r], xs[r], "pgs", nu=2, k_l=2))
+        agree(torch.cat(xs).cpu().numpy(), oracle.pgs_apply(A, b, x0, 2, nu=2, bounds=part), f"8 ranks {mode} pgs")
+    finally:
+        V.close()
+    if mode == "hybrid":
+        V = VirtualRanks(A, bounds, m, factors="block")
+        Fo = oracle.block_ilu0(A, bounds)
+    else:
+        Fg = oracle.ilu0(A)
+        V = VirtualRanks(A, bounds, m, factors=Fg[2])
+        Fo = Fg
+    try:
+        bs, xs = V.split(b), V.split(x0)
+        V.run(lambda r, S: S.smooth(bs[r], xs[r], "ilu", nu=2, k_l=2, k_u=2))
+        agree(torch.cat(xs).cpu().numpy(), oracle.ilu_apply(A, Fo, b, x0, 2, 2, nu=2, bounds=part),
+              f"8 ranks {mode} ilu")
+    finally:
+        V.close()
