@@ -129,6 +129,37 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
  */
 nsm_status nsm_ilu0(const nsm_csr *A, int64_t row_begin, double *fval);
 
+/*
+ * nsm_ilut — ILUT(droptol, lfil) factorisation on the host (Saad's
+ * dual-threshold ILU, "Compute A ~ LU with droptol and lfill imposed", Alg. 2
+ * P:L1024-1025; single rank).  Row i: pivots eliminated in ascending column
+ * order, L entries w_k / u_kk below droptol * ||a_i||_2 dropped, then every
+ * off-diagonal entry below that threshold dropped and the lfil largest of the
+ * L part and of the U part kept (ties: smaller column); the diagonal is kept.
+ * Output: factor CSR on its own pattern (strict lower = L_s, upper incl.
+ * diagonal = U), the layout nsm_setup takes as F.  rowptr (n+1) and *nnz are
+ * always written; colind / val (nnz entries, caller-allocated) may be NULL to
+ * query the size first.  Zero pivot -> NSM_ERR_ZERO_DIAG.
+ */
+nsm_status nsm_ilut(const nsm_csr *A, double droptol, int lfil, int64_t *rowptr, int64_t *nnz, int64_t *colind,
+                    double *val);
+
+/*
+ * nsm_ruiz — Ruiz scaling of the U part of a factor CSR (Alg. 2 P:L1032;
+ * P:L996-1008): max_iters rounds of sup-norm row/column equilibration, then an
+ * exact unit diagonal.  val (same pattern as F) receives L_s unchanged and
+ * U~ = diag(1/s_r) U diag(1/s_c); s_r, s_c (length n) receive the DIVISORS.
+ */
+nsm_status nsm_ruiz(const nsm_csr *F, int max_iters, double *val, double *s_r, double *s_c);
+
+/*
+ * nsm_set_ruiz — make NSM_ILU0 smoothing use the Ruiz form of Alg. 2: the
+ * handle's factor F must then hold U~ (nsm_ruiz output); after the L solve
+ * y~ = y / s_r, the U~ solve runs on the unit-diagonal U~, and x += v / s_c
+ * (P:L1032-1040).  s_r = s_c = NULL switches back.  Host arrays, length n.
+ */
+nsm_status nsm_set_ruiz(nsm_handle *h, const double *s_r, const double *s_c);
+
 /* ---- multi-GPU halo plan (setup time) ---------
  * A handle set up with nranks > 1 owns a "mailbox" (device memory: one flag
  * per source rank + two parity copies of its ghost array) that its

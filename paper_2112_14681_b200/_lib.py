@@ -23,7 +23,7 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_us
                   "nsm_halo_set_send", "nsm_halo_mailbox", "nsm_halo_connect_ipc", "nsm_halo_connect",
                   "nsm_halo_commit", "nsm_set_option", "nsm_spmat_setup", "nsm_spmat_apply",
                   "nsm_spmat_destroy", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle", "nsm_amg_destroy",
-                  "nsm_solver_last_error", "nsm_gmres", "nsm_profile"])
+                  "nsm_solver_last_error", "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz"])
 
 
 class NsmError(RuntimeError):
@@ -87,6 +87,9 @@ def load():
     L.nsm_solver_last_error.restype = ctypes.c_char_p
     L.nsm_gmres.argtypes = [vp, vp, vp, vp, ci, ctypes.c_double, ci, P(ci), vp, vp]
     L.nsm_profile.argtypes = [vp, vp, vp]
+    L.nsm_ilut.argtypes = [P(_Csr), ctypes.c_double, ci, vp, P(i64), vp, vp]
+    L.nsm_ruiz.argtypes = [P(_Csr), ci, vp, vp, vp]
+    L.nsm_set_ruiz.argtypes = [vp, vp, vp]
     L.nsm_last_error.argtypes = [vp]
     L.nsm_last_error.restype = ctypes.c_char_p
     L.nsm_destroy.argtypes = [vp]
@@ -95,7 +98,7 @@ def load():
                  "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
                  "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
-                 "nsm_gmres", "nsm_profile"]:
+                 "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -168,6 +171,49 @@ def exchange_plan(requests: dict, rank: int, nranks: int, all_gather_object) -> 
     allreq = [None] * nranks
     all_gather_object(allreq, {int(q): np.asarray(v, dtype=np.int64) for q, v in requests.items()})
     return {q: allreq[q][rank] for q in range(nranks) if q != rank and rank in allreq[q]}
+
+
+class FactorCSR:
+    """Host factor CSR (strict lower = L_s, upper incl. diagonal = U)."""
+
+    def __init__(self, nrows, rowptr, col, val):
+        self.nrows = self.ncols = int(nrows)
+        self.rowptr, self.col, self.val = rowptr, col, val
+
+
+def ilut(A, droptol: float, lfil: int) -> FactorCSR:
+    """Host ILUT(droptol, lfil) factors (nsm_ilut)."""
+    L = load()
+    keep: list = []
+    cs = _csr_struct(A, keep)
+    n = int(A.nrows)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    nnz = ctypes.c_int64()
+    st = L.nsm_ilut(ctypes.byref(cs), float(droptol), int(lfil), rp.ctypes.data, ctypes.byref(nnz), None, None)
+    if st != 0:
+        raise NsmError(st, _err(None))
+    col = np.zeros(nnz.value, dtype=np.int64)
+    val = np.zeros(nnz.value, dtype=np.float64)
+    st = L.nsm_ilut(ctypes.byref(cs), float(droptol), int(lfil), rp.ctypes.data, ctypes.byref(nnz),
+                    col.ctypes.data, val.ctypes.data)
+    if st != 0:
+        raise NsmError(st, _err(None))
+    return FactorCSR(n, rp, col, val)
+
+
+def ruiz(F, max_iters: int = 5):
+    """Ruiz scaling of the U part of a factor CSR (nsm_ruiz): returns
+    (FactorCSR with U~, s_r, s_c)."""
+    L = load()
+    keep: list = []
+    cs = _csr_struct(F, keep)
+    n = int(F.nrows)
+    val = np.zeros(int(F.rowptr[-1]), dtype=np.float64)
+    sr, sc = np.zeros(n), np.zeros(n)
+    st = L.nsm_ruiz(ctypes.byref(cs), int(max_iters), val.ctypes.data, sr.ctypes.data, sc.ctypes.data)
+    if st != 0:
+        raise NsmError(st, _err(None))
+    return FactorCSR(n, np.asarray(F.rowptr, np.int64), np.asarray(F.col, np.int64), val), sr, sc
 
 
 class Smoother:
@@ -316,6 +362,15 @@ class Smoother:
                 S._call(L.nsm_halo_connect(S._h, int(q), qbase, int(ranks[q].n_ghost), int(qoffs[S.rank])))
         for S in ranks:
             S._call(L.nsm_halo_commit(S._h))
+
+    def set_ruiz(self, s_r, s_c):
+        """Ruiz form of the ILU U solve (the factor must hold U~); None, None = off."""
+        if s_r is None:
+            self._call(load().nsm_set_ruiz(self._h, None, None))
+            return
+        sr = np.ascontiguousarray(s_r, dtype=np.float64)
+        sc = np.ascontiguousarray(s_c, dtype=np.float64)
+        self._call(load().nsm_set_ruiz(self._h, sr.ctypes.data, sc.ctypes.data))
 
     def set_pipeline(self, enable: bool):
         """Bulk-copy pipelined kernels (default) or the plain ones."""

@@ -42,6 +42,9 @@ struct nsm_handle {
     // ILU(0) factors: unit-lower L = I + Ls, U = D_U (I + D_U^{-1} Us)
     bool has_ilu = false;
     double *dU = nullptr;
+    // Ruiz-scaled U factor (Alg. 2 / NEXT-3): U~ = diag(1/s_r) U diag(1/s_c), unit diagonal
+    bool ruiz = false;
+    double *s_r = nullptr, *s_c = nullptr;
     Sell Ls, Us, LsG, UsG;
     // workspace: four n-vectors (residual, ping-pong iterates, g^(0)), divergence flag
     double *w[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -133,6 +136,8 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->d);
     cudaFree(h->dl1);
     cudaFree(h->dU);
+    cudaFree(h->s_r);
+    cudaFree(h->s_c);
     for (double *&p : h->w) cudaFree(p);
     cudaFree(h->flag);
     cudaFree(h->interior);
@@ -640,6 +645,40 @@ nsm_status nsm_profile(nsm_handle *h, double *ms, int64_t *count) {
     return NSM_OK;
 }
 
+nsm_status nsm_ilut(const nsm_csr *A, double droptol, int lfil, int64_t *rowptr, int64_t *nnz, int64_t *colind,
+                    double *val) {
+    if (!A || !rowptr || !nnz) { g_setup_err = "nsm_ilut: NULL argument"; return NSM_ERR_ARG; }
+    std::vector<int64_t> rp, ci;
+    std::vector<double> va;
+    nsm_status st = ilut_host(A, droptol, lfil, rp, ci, va, &g_setup_err);
+    if (st != NSM_OK) return st;
+    std::copy(rp.begin(), rp.end(), rowptr);
+    *nnz = (int64_t)ci.size();
+    if (colind) std::copy(ci.begin(), ci.end(), colind);
+    if (val) std::copy(va.begin(), va.end(), val);
+    return NSM_OK;
+}
+
+nsm_status nsm_ruiz(const nsm_csr *F, int max_iters, double *val, double *s_r, double *s_c) {
+    if (!F || !val || !s_r || !s_c) { g_setup_err = "nsm_ruiz: NULL argument"; return NSM_ERR_ARG; }
+    return ruiz_host(F, max_iters, val, s_r, s_c, &g_setup_err);
+}
+
+nsm_status nsm_set_ruiz(nsm_handle *h, const double *s_r, const double *s_c) {
+    if (!h || !h->has_ilu) return NSM_ERR_STATE;
+    cudaSetDevice(h->device);
+    if (!s_r || !s_c) {
+        h->ruiz = false;
+        return NSM_OK;
+    }
+    DevAlloc a{h};
+    if (!h->s_r && !(a.get(&h->s_r, std::max<int64_t>(h->n, 1)) && a.get(&h->s_c, std::max<int64_t>(h->n, 1))))
+        return NSM_ERR_OOM;
+    if (!upload(h->s_r, s_r, h->n) || !upload(h->s_c, s_c, h->n)) return cuda_fail(h, cudaGetLastError(), "nsm_set_ruiz");
+    h->ruiz = true;
+    return NSM_OK;
+}
+
 nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *halo_exchanges) {
     if (!h) return NSM_ERR_ARG;
     if (kernel_launches) *kernel_launches = h->launches;
@@ -744,6 +783,22 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
     // NSM_ILU0
     if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
     if (st != NSM_OK) return st;
+    if (h->ruiz) {
+        // Alg. 2 with Ruiz: y = L~^{-1} r; y~ = y / s_r; v = U~~^{-1} y~
+        // (unit diagonal); x += v / s_c
+        if (k_l > 0) {
+            double *ybuf = (k_l & 1) ? W0 : W1;
+            st = run_sweeps(h, Stage{&h->Ls, &h->LsG, nullptr, rhs, k_l}, W0, W1, EPI_STORE2, ybuf, nullptr, h->s_r, s,
+                            W2);
+        } else {
+            st = scale_into(h, false, rhs, h->s_r, W2, s);
+        }
+        if (st != NSM_OK) return st;
+        if (k_u == 0) return scale_into(h, !fresh, W2, h->s_c, x, s);
+        Stage su{&h->Us, &h->UsG, h->dU, W2, k_u, nullptr};
+        return fresh ? run_sweeps(h, su, W0, W1, EPI_STORE2, R, nullptr, h->s_c, s, x)
+                     : run_sweeps(h, su, W0, W1, EPI_XADD_SCALE, nullptr, x, h->s_c, s);
+    }
     // row a5: y = sum_{j<=kL} (-Ls)^j r ; z = sum_{j<=kU} (-DU^{-1}Us)^j DU^{-1} y ; x += z
     const double *y = rhs;
     const double *z0 = nullptr;

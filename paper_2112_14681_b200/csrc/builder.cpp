@@ -254,3 +254,147 @@ nsm_status ilu0_host(const nsm_csr *A, int64_t rb, double *fval, std::string *er
 }
 
 }  // namespace nsm
+
+// ---- ILUT(droptol, lfil) and Ruiz scaling (Alg. 2; NEXT-3) ----
+// Saad's dual-threshold ILUT, row by row: the pivots k < i of the working
+// row are eliminated in ascending column order (a min-heap, fill included);
+// w_k / u_kk below tau_i = droptol * ||a_i||_2 is dropped, otherwise row k of
+// U is subtracted; then off-diagonal entries below tau_i are dropped and the
+// lfil largest of the L part and of the U part kept (ties: smaller column).
+#include <queue>
+
+namespace nsm {
+
+nsm_status ilut_host(const nsm_csr *A, double droptol, int lfil, std::vector<int64_t> &rp_out,
+                     std::vector<int64_t> &ci_out, std::vector<double> &va_out, std::string *err) {
+    const int64_t n = A->nrows;
+    if (!A->rowptr || n < 0 || A->ncols != n || droptol < 0 || lfil < 0) { *err = "nsm_ilut: bad argument"; return NSM_ERR_ARG; }
+    std::vector<double> w(n, 0.0);
+    std::vector<char> present(n, 0);
+    std::vector<int64_t> nz;
+    // U rows kept for elimination: start offsets into (ucol, uval)
+    std::vector<int64_t> ustart(n + 1, 0), ucol;
+    std::vector<double> uval;
+    rp_out.assign(n + 1, 0);
+    ci_out.clear();
+    va_out.clear();
+    for (int64_t i = 0; i < n; ++i) {
+        double nrm2 = 0.0;
+        nz.clear();
+        std::priority_queue<int64_t, std::vector<int64_t>, std::greater<int64_t>> heap;
+        for (int64_t p = A->rowptr[i]; p < A->rowptr[i + 1]; ++p) {
+            const int64_t j = A->colind[p];
+            nrm2 = nrm2 + A->val[p] * A->val[p];
+            w[j] = A->val[p];
+            present[j] = 1;
+            nz.push_back(j);
+            if (j < i) heap.push(j);
+        }
+        const double tau = droptol * std::sqrt(nrm2);
+        std::vector<int64_t> dropped;
+        while (!heap.empty()) {
+            const int64_t k = heap.top();
+            heap.pop();
+            const double ukk = uval[ustart[k]];  // diagonal is the first entry of U row k
+            const double wk = w[k] / ukk;
+            if (std::fabs(wk) < tau) {
+                w[k] = 0.0;
+                dropped.push_back(k);
+                continue;
+            }
+            w[k] = wk;
+            for (int64_t q = ustart[k] + 1; q < ustart[k + 1]; ++q) {
+                const int64_t j = ucol[q];
+                if (!present[j]) {
+                    present[j] = 1;
+                    w[j] = 0.0;
+                    nz.push_back(j);
+                    if (j < i) heap.push(j);
+                }
+                w[j] = w[j] - wk * uval[q];
+            }
+        }
+        for (int64_t k : dropped) present[k] = 2;  // removed from the row
+        if (!present[i] || w[i] == 0.0) {
+            *err = "nsm_ilut: zero pivot at row " + std::to_string(i);
+            for (int64_t j : nz) { present[j] = 0; w[j] = 0.0; }
+            return NSM_ERR_ZERO_DIAG;
+        }
+        std::vector<std::pair<int64_t, double>> lpart, upart;
+        for (int64_t j : nz) {
+            if (present[j] != 1 || j == i) continue;
+            if (std::fabs(w[j]) < tau) continue;
+            (j < i ? lpart : upart).push_back({j, w[j]});
+        }
+        auto bigger = [](const std::pair<int64_t, double> &a, const std::pair<int64_t, double> &b) {
+            const double fa = std::fabs(a.second), fb = std::fabs(b.second);
+            return fa != fb ? fa > fb : a.first < b.first;
+        };
+        std::sort(lpart.begin(), lpart.end(), bigger);
+        std::sort(upart.begin(), upart.end(), bigger);
+        if ((int64_t)lpart.size() > lfil) lpart.resize(lfil);
+        if ((int64_t)upart.size() > lfil) upart.resize(lfil);
+        std::vector<std::pair<int64_t, double>> row(lpart);
+        row.push_back({i, w[i]});
+        row.insert(row.end(), upart.begin(), upart.end());
+        std::sort(row.begin(), row.end());
+        for (auto &e : row) { ci_out.push_back(e.first); va_out.push_back(e.second); }
+        rp_out[i + 1] = (int64_t)ci_out.size();
+        // U row i (diagonal first, then ascending columns)
+        ustart[i] = (int64_t)ucol.size();
+        ucol.push_back(i);
+        uval.push_back(w[i]);
+        for (auto &e : upart) (void)e;
+        std::vector<std::pair<int64_t, double>> us(upart);
+        std::sort(us.begin(), us.end());
+        for (auto &e : us) { ucol.push_back(e.first); uval.push_back(e.second); }
+        ustart[i + 1] = (int64_t)ucol.size();
+        for (int64_t j : nz) { present[j] = 0; w[j] = 0.0; }
+    }
+    return NSM_OK;
+}
+
+// Ruiz equilibration of the upper part (incl. diagonal) of a factor CSR, then
+// an exact unit diagonal; the scaling is returned as divisors s_r, s_c.
+nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, double *s_c, std::string *err) {
+    const int64_t n = F->nrows;
+    if (!F->rowptr || n < 0 || max_iters < 0) { *err = "nsm_ruiz: bad argument"; return NSM_ERR_ARG; }
+    const int64_t nnz = F->rowptr[n];
+    std::copy(F->val, F->val + nnz, v);
+    for (int64_t i = 0; i < n; ++i) { s_r[i] = 1.0; s_c[i] = 1.0; }
+    std::vector<double> rmax(n), cmax(n);
+    for (int it = 0; it < max_iters; ++it) {
+        std::fill(rmax.begin(), rmax.end(), 0.0);
+        std::fill(cmax.begin(), cmax.end(), 0.0);
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t p = F->rowptr[i]; p < F->rowptr[i + 1]; ++p) {
+                const int64_t j = F->colind[p];
+                if (j < i) continue;
+                rmax[i] = std::max(rmax[i], std::fabs(v[p]));
+                cmax[j] = std::max(cmax[j], std::fabs(v[p]));
+            }
+        for (int64_t i = 0; i < n; ++i) {
+            rmax[i] = rmax[i] == 0.0 ? 1.0 : std::sqrt(rmax[i]);
+            cmax[i] = cmax[i] == 0.0 ? 1.0 : std::sqrt(cmax[i]);
+        }
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t p = F->rowptr[i]; p < F->rowptr[i + 1]; ++p) {
+                const int64_t j = F->colind[p];
+                if (j >= i) v[p] = v[p] / rmax[i] / cmax[j];
+            }
+        for (int64_t i = 0; i < n; ++i) { s_r[i] = s_r[i] * rmax[i]; s_c[i] = s_c[i] * cmax[i]; }
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        double dg = 1.0;
+        bool has = false;
+        for (int64_t p = F->rowptr[i]; p < F->rowptr[i + 1]; ++p)
+            if (F->colind[p] == i) { dg = v[p]; has = true; }
+        if (!has || dg == 0.0) { *err = "nsm_ruiz: missing or zero diagonal at row " + std::to_string(i); return NSM_ERR_ZERO_DIAG; }
+        for (int64_t p = F->rowptr[i]; p < F->rowptr[i + 1]; ++p)
+            if (F->colind[p] >= i) v[p] = v[p] / dg;
+        s_r[i] = s_r[i] * dg;
+    }
+    return NSM_OK;
+}
+
+}  // namespace nsm

@@ -158,6 +158,11 @@ void preload_halo_kernels();
 // sequence numbers and must not be captured into a replayed CUDA graph).
 bool nsm_is_distributed(const nsm_handle *h);
 
+// Host ILUT(droptol, lfil) and Ruiz scaling of the U factor (NEXT-3).
+nsm_status ilut_host(const nsm_csr *A, double droptol, int lfil, std::vector<int64_t> &rp_out,
+                     std::vector<int64_t> &ci_out, std::vector<double> &va_out, std::string *err);
+nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, double *s_c, std::string *err);
+
 // Host ILU(0) (nsm_ilu0).
 nsm_status ilu0_host(const nsm_csr *A, int64_t row_begin, double *fval, std::string *err);
 
