@@ -82,6 +82,28 @@ def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k
     return out
 
 
+def floor_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k_l: int, k_u: int,
+                n_ghost: int = 0) -> dict:
+    """Bytes of one application at the data-movement floor (SURVEY.md §8(d)
+    "fused floor", without row pointers: SELL-32 has none): every stored
+    matrix entry the application needs read ONCE, every n-vector read or
+    written once.  These are also the algorithmic bytes of the phase-skewed
+    fused passes (fused.cu):
+      pGS, one pass:   A (12 nnz_off) + d, b, x read + x write         = 12 nnz_off + 32 n
+      ILU pass 1:      A + L_s + d, b, x, d_U read + y, z0 write      = 12 (nnz_off + nnz_L) + 48 n
+      ILU pass 2:      U_s + d_U, y, z0 read + x read and write        = 12 nnz_U + 40 n
+    With k = 0 (Jacobi) the per-pass model applies."""
+    if kind == "pgs":
+        if k_l == 0:
+            return {"passes": [], "total": algorithmic_bytes(kind, n, nnz_off, nnz_l, nnz_u, k_l, k_u, n_ghost)["total"]}
+        p = [12 * nnz_off + 32 * n + 8 * n_ghost]
+    else:
+        if k_l == 0 or k_u == 0:
+            return {"passes": [], "total": algorithmic_bytes(kind, n, nnz_off, nnz_l, nnz_u, k_l, k_u, n_ghost)["total"]}
+        p = [12 * (nnz_off + nnz_l) + 48 * n + 8 * n_ghost, 12 * nnz_u + 40 * n]
+    return {"passes": p, "total": sum(p)}
+
+
 def hbm_peak() -> tuple[float, str]:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -184,7 +206,7 @@ def run_reference(args, rank, nranks):
     import oracle
     A, offsets, kind, k_l, k_u, desc = build_workload(args.config, 0, 1)
     nl, nu_, noff = split_counts(A)
-    ab = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u)["total"]
+    ab = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u)["total"]   # same bytes as the default nsm path
     b, x0 = inputs.uniform(inputs.SEED_B, A.nrows), inputs.uniform(inputs.SEED_X0, A.nrows)
     F = oracle.ilu0(A) if kind == "ilu" else None
 
@@ -225,14 +247,15 @@ def run_nsm(args, rank, nranks, local_rank):
     F = nsm.ilu0(A, row_begin=A.row_begin) if kind == "ilu" else None
     S = nsm.Smoother(A, F, device=local_rank, rank=rank, nranks=nranks, row_offsets=offsets)
     S.set_pipeline(not args.plain)
-    S.set_fused(args.fused)
+    if args.fused != "default":
+        S.set_fused({"auto": 2, "on": 1, "off": 0}[args.fused])
     if args.pdl != "auto":
         S.set_pdl(args.pdl == "on")
     if nranks > 1:
         S.connect(dist)
     nl, nu_, noff = split_counts(A)
-    model = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost)
-    ab = model["total"]
+    model = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost)   # one kernel per pass
+    fmodel = floor_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost)       # fused passes / floor
     b = torch.from_numpy(inputs.uniform(inputs.SEED_B, A.nrows, idx0=A.row_begin)).to(dev)
     x0 = torch.from_numpy(inputs.uniform(inputs.SEED_X0, A.nrows, idx0=A.row_begin)).to(dev)
     x = x0.clone()
@@ -270,13 +293,13 @@ def run_nsm(args, rank, nranks, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)   # max over ranks
     t_ms = float(t.item())
     ms_step = t_ms / args.steps
-    value = ab * nranks * args.steps / (t_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
 
-    # ---- dominant kernel: the residual pass, timed INSIDE the smoother steps
-    # with the library's in-stream event pairs (NSM_OPT_PROFILE), over a second
-    # run of the same steps (events around each pass perturb PDL overlap, so
-    # they stay out of the headline timed region)
+    # ---- dominant kernel, timed INSIDE the smoother steps with the library's
+    # in-stream event pairs (NSM_OPT_PROFILE), over a second run of the same
+    # steps (events around each pass perturb PDL overlap, so they stay out of
+    # the headline timed region): the fused pass when the application ran
+    # fused, else the residual pass
     S.set_profile(True)
     for _ in range(args.steps):
         flush_l2(flush)
@@ -284,28 +307,45 @@ def run_nsm(args, rank, nranks, local_rank):
     torch.cuda.synchronize()
     prof = S.profile()
     S.set_profile(False)
-    k_ms = prof["residual"][0] / max(prof["residual"][1], 1)
-    k_bytes = model["residual"]
-    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9
-    sweep_bytes = sum(sum(v) for kk, v in model.items() if isinstance(v, list))
-    sweep_ms = prof["sweep"][0] / args.steps
-    # and alone through nsm_residual (L2 flushed before each launch)
-    r = torch.empty_like(b)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
-    for e0, e1 in kev:
-        flush_l2(flush)
-        e0.record(stream)
-        S.residual(b, x, r)
-        e1.record(stream)
-    torch.cuda.synchronize()
-    alone_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in kev]))
+    fused = prof["fused"][1] > 0
+    # algorithmic bytes of the path that ran (per-pass kernels or fused passes)
+    ab = fmodel["total"] if fused else model["total"]
+    value = ab * nranks * args.steps / (t_ms * 1e-3) / 1e9
+    floor_gbs = fmodel["total"] * nranks * args.steps / (t_ms * 1e-3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(args.config, {}).get("residual")
-            traffic = tr
+            traffic = json.load(f).get(args.config, {}).get("fused" if fused else "residual")
     except Exception:
         pass
+    if fused:
+        nlaunch = prof["fused"][1]
+        k_ms = prof["fused"][0] / nlaunch
+        k_bytes = fmodel["total"] * args.steps / nlaunch      # average over the pass kinds of a step
+        kernel_name = ("fused pGS pass: residual + k sweeps + x update (k_skew)" if kind == "pgs"
+                       else "fused ILU passes: residual + L sweeps; U sweeps + x update (k_skew)")
+        extra = {"passes_bytes": fmodel["passes"]}
+    else:
+        k_ms = prof["residual"][0] / max(prof["residual"][1], 1)
+        k_bytes = model["residual"]
+        kernel_name = "residual pass r = b - A x (k_residual_tma)"
+        sweep_bytes = sum(sum(v) for kk, v in model.items() if isinstance(v, list))
+        sweep_ms = prof["sweep"][0] / args.steps
+        extra = {"sweeps_frac": round(sweep_bytes / (max(sweep_ms, 1e-9) * 1e-3) / 1e9 / peak, 4)
+                 if prof["sweep"][1] else None}
+        # and alone through nsm_residual (L2 flushed before each launch)
+        r = torch.empty_like(b)
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for e0, e1 in kev:
+            flush_l2(flush)
+            e0.record(stream)
+            S.residual(b, x, r)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        alone_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in kev]))
+        extra.update({"alone_ms": round(alone_ms, 4),
+                      "alone_frac": round(k_bytes / (alone_ms * 1e-3) / 1e9 / peak, 4)})
+    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers
     bh = b.cpu().pin_memory()
@@ -351,19 +391,20 @@ def run_nsm(args, rank, nranks, local_rank):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "n_per_gpu": A.nrows, "nnz_per_gpu": A.nnz, "kind": kind, "k_l": k_l,
                        "k_u": k_u, "nu": 1, "partition": "z-slab rows" if nranks > 1 else "none",
-                       "kernels": ("plain register-blocked" if args.plain else "cp.async.bulk pipelined (persistent)")
-                       + (", pGS fused into one wavefront pass" if args.fused and not args.plain and kind == "pgs" else ""),
+                       "kernels": ("plain register-blocked, one kernel per pass" if args.plain else
+                                   ("phase-skewed fused passes (k_skew, cp.async.bulk pipelined, persistent)" if fused
+                                    else "cp.async.bulk pipelined (persistent), one kernel per pass")),
                        "l2": "flushed before every timed step (256 MB read through L2)",
-                       "bytes_per_step_per_gpu": ab, "frac_of_hbm_peak": round(value / nranks / peak, 4)},
+                       "bytes": ("algorithmic bytes of the path that ran (DESIGN.md §6): "
+                                 + ("fused passes = the floor" if fused else "one kernel per pass")),
+                       "bytes_per_step_per_gpu": ab, "floor_bytes_per_step_per_gpu": fmodel["total"],
+                       "floor_gbs": round(floor_gbs, 2),
+                       "frac_of_hbm_peak": round(value / nranks / peak, 4)},
             "ms_per_apply": round(ms_step, 4),
-            "roofline": {"bound": "hbm", "kernel": "residual pass r = b - A x (k_residual_tma)",
+            "roofline": {"bound": "hbm", "kernel": kernel_name,
                          "achieved": round(k_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(k_gbs / peak, 4),
-                         "traffic": traffic, "peak_source": peak_src, "bytes_per_launch": k_bytes,
-                         "ms_per_launch": round(k_ms, 4), "timing": "in-step CUDA events (NSM_OPT_PROFILE)",
-                         "alone_ms": round(alone_ms, 4),
-                         "alone_frac": round(k_bytes / (alone_ms * 1e-3) / 1e9 / peak, 4),
-                         "sweeps_frac": round(sweep_bytes / (max(sweep_ms, 1e-9) * 1e-3) / 1e9 / peak, 4)
-                         if prof["sweep"][1] else None},
+                         "traffic": traffic, "peak_source": peak_src, "bytes_per_launch": int(k_bytes),
+                         "ms_per_launch": round(k_ms, 4), "timing": "in-step CUDA events (NSM_OPT_PROFILE)", **extra},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": 16 * A.nrows,
                     "d2h_bytes_per_step": 8 * A.nrows},
@@ -386,7 +427,9 @@ def main():
     ap.add_argument("--plain", action="store_true", help="plain register-blocked kernels instead of the bulk-copy pipelined ones")
     ap.add_argument("--pdl", default="auto", choices=["auto", "on", "off"],
                     help="programmatic dependent launch (auto: the library's size-based default)")
-    ap.add_argument("--fused", action="store_true", help="pGS as one fused wavefront pass (opt-in, latency-bound)")
+    ap.add_argument("--fused", default="default", choices=["default", "auto", "on", "off"],
+                    help="phase-skewed fused passes (default: the library's default, per-pass kernels; "
+                         "auto: fused on large problems)")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: every rank on cuda:0 (halo over same-device IPC), gloo plumbing")
     args = ap.parse_args()

@@ -264,10 +264,17 @@ nsm_status nsm_info(const nsm_handle *h, int64_t *n_local, int64_t *n_ghost, int
  * call) and halo exchanges it performed.  Host-side, no synchronisation. */
 nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *halo_exchanges);
 
+/* Fused-pass synchronisation statistics since setup: work items whose
+ * consumer warps found the item not yet ready (its condition "all items <=
+ * w - Dw done", unmet) and had to wait, and the total time
+ * they waited in ns (one warp per CTA measures).  Synchronises the device. */
+nsm_status nsm_fused_stats(nsm_handle *h, int64_t *waits, int64_t *wait_ns);
+
 /* In-stream pass timing (after nsm_set_option(h, NSM_OPT_PROFILE, 1)):
  * waits for the recorded events, returns the summed milliseconds and counts
- * of residual passes (ms[0], count[0]) and sweep passes (ms[1], count[1])
- * since the last call, and clears the records. */
+ * of residual passes (ms[0], count[0]), sweep passes (ms[1], count[1]) and
+ * fused passes (ms[2], count[2]) since the last call, and clears the
+ * records.  `ms` and `count` have 3 entries. */
 nsm_status nsm_profile(nsm_handle *h, double *ms, int64_t *count);
 
 /* Last error message: of `h`, or of the last failed setup when h == NULL.
@@ -281,20 +288,32 @@ const char *nsm_last_error(const nsm_handle *h);
  *                           kernels.  Both give bit-identical results.
  *   NSM_OPT_HALO_TIMEOUT_MS how long a halo or wavefront wait spins before
  *                           giving up and flagging NSM_ERR_DIST (default 20000).
- *   NSM_OPT_FUSED           1 = single-rank pGS applications with 1 <= k <= 8
- *                           run as ONE fused wavefront pass (residual + k
- *                           sweeps + x update, the matrix read once;
- *                           DESIGN.md §6); 0 (default) = one kernel per pass.
- *                           Bit-identical results either way; the fused pass
- *                           is currently latency-bound and slower.
+ *   NSM_OPT_FUSED           single-rank applications as phase-skewed fused
+ *                           passes: pGS (forward / backward)
+ *                           = ONE pass (residual + k sweeps + x update, the
+ *                           matrix read from HBM once), ILU(0) = two passes
+ *                           (residual + k_l L sweeps ascending; k_u U sweeps
+ *                           + x update descending); needs 1 <= k <= 8.
+ *                           0 (default) = one kernel per pass; 1 = fused
+ *                           whenever possible; 2 = fused when the problem
+ *                           spans at least two skew distances (large
+ *                           problems).  Bit-identical results either way.
+ *                           The fused passes read ~2.4x fewer HBM bytes but
+ *                           are currently latency-bound and slower than the
+ *                           per-pass kernels.
+ *   NSM_OPT_FUSED_WINDOW    wait distance Dw of the fused passes in work
+ *                           items (0 = automatic, about the items in flight);
+ *                           a small value forces frequent waits and ring
+ *                           reuse (a test knob; slower).
  *   NSM_OPT_PDL             1 (default) = launch the pipelined kernels with
  *                           programmatic dependent launch (a kernel's matrix
  *                           prefetch overlaps the previous kernel's drain);
  *                           0 = plain stream order. */
 typedef enum {
     NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2, NSM_OPT_PDL = 3,
-    NSM_OPT_PROFILE = 4 /* 1: record a CUDA event pair around every residual / sweep pass (up to
-                           4096 passes) for nsm_profile(); 0: off (default) */
+    NSM_OPT_PROFILE = 4 /* 1: record a CUDA event pair around every residual / sweep / fused pass
+                           (up to 4096 passes) for nsm_profile(); 0: off (default) */,
+    NSM_OPT_FUSED_WINDOW = 5
 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 

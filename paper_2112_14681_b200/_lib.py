@@ -23,7 +23,8 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_us
                   "nsm_halo_set_send", "nsm_halo_mailbox", "nsm_halo_connect_ipc", "nsm_halo_connect",
                   "nsm_halo_commit", "nsm_set_option", "nsm_spmat_setup", "nsm_spmat_apply",
                   "nsm_spmat_destroy", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle", "nsm_amg_destroy",
-                  "nsm_solver_last_error", "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz"])
+                  "nsm_solver_last_error", "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz",
+                  "nsm_fused_stats"])
 
 
 class NsmError(RuntimeError):
@@ -87,6 +88,7 @@ def load():
     L.nsm_solver_last_error.restype = ctypes.c_char_p
     L.nsm_gmres.argtypes = [vp, vp, vp, vp, ci, ctypes.c_double, ci, P(ci), vp, vp]
     L.nsm_profile.argtypes = [vp, vp, vp]
+    L.nsm_fused_stats.argtypes = [vp, P(i64), P(i64)]
     L.nsm_ilut.argtypes = [P(_Csr), ctypes.c_double, ci, vp, P(i64), vp, vp]
     L.nsm_ruiz.argtypes = [P(_Csr), ci, vp, vp, vp]
     L.nsm_set_ruiz.argtypes = [vp, vp, vp]
@@ -98,7 +100,7 @@ def load():
                  "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
                  "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
-                 "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz"]:
+                 "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -376,9 +378,14 @@ class Smoother:
         """Bulk-copy pipelined kernels (default) or the plain ones."""
         self._call(load().nsm_set_option(self._h, 0, int(bool(enable))))
 
-    def set_fused(self, enable: bool):
-        """One-pass fused pGS applications (default) or one kernel per pass."""
-        self._call(load().nsm_set_option(self._h, 2, int(bool(enable))))
+    def set_fused(self, mode):
+        """Phase-skewed fused passes: False/0 off, True/1 whenever possible,
+        2 = automatic (the default: large problems)."""
+        self._call(load().nsm_set_option(self._h, 2, int(mode)))
+
+    def set_fused_window(self, items: int):
+        """Wait distance of the fused passes in work items (0 = automatic)."""
+        self._call(load().nsm_set_option(self._h, 5, int(items)))
 
     def set_pdl(self, enable: bool):
         """Programmatic dependent launch between consecutive pipelined kernels."""
@@ -389,11 +396,18 @@ class Smoother:
         self._call(load().nsm_set_option(self._h, 4, int(bool(enable))))
 
     def profile(self):
-        """{'residual': (ms, count), 'sweep': (ms, count)} since the last call."""
-        ms = np.zeros(2)
-        cnt = np.zeros(2, dtype=np.int64)
+        """{'residual' | 'sweep' | 'fused': (ms, count)} since the last call."""
+        ms = np.zeros(3)
+        cnt = np.zeros(3, dtype=np.int64)
         self._call(load().nsm_profile(self._h, ms.ctypes.data, cnt.ctypes.data))
-        return {"residual": (float(ms[0]), int(cnt[0])), "sweep": (float(ms[1]), int(cnt[1]))}
+        return {"residual": (float(ms[0]), int(cnt[0])), "sweep": (float(ms[1]), int(cnt[1])),
+                "fused": (float(ms[2]), int(cnt[2]))}
+
+    def fused_stats(self):
+        """(waits that had to spin, total spin ns) of the fused passes since setup."""
+        w, t = ctypes.c_int64(0), ctypes.c_int64(0)
+        self._call(load().nsm_fused_stats(self._h, ctypes.byref(w), ctypes.byref(t)))
+        return int(w.value), int(t.value)
 
     def set_halo_timeout(self, ms: int):
         """How long a halo wait spins before reporting NSM_ERR_DIST."""

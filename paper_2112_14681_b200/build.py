@@ -25,7 +25,7 @@ def sources() -> list[str]:
 
 
 def deps() -> list[str]:
-    return sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "nsm.h")]
+    return sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "nsm.h")]
 
 
 def stale() -> bool:

@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -65,13 +67,16 @@ struct nsm_handle {
     std::vector<cudaEvent_t> ev;
     std::vector<int> ev_kind;                                // kind of record i (events 2i, 2i+1)
     int ev_used = 0;
-    // fused one-pass pGS (fused.cu), single rank
-    bool fused = false, fused_ready = false;  // opt-in: latency-bound so far
-    int fused_DL = 0, fused_DU = 0, fused_grid = 0;
-    int64_t fused_M = 0;
+    // phase-skewed fused passes (fused.cu), single rank
+    int fused_mode = 0;                      // NSM_OPT_FUSED: 0 off (default), 1 on, 2 auto (large problems)
+    bool fused_ready = false;
+    int skew_dw = 0;                         // NSM_OPT_FUSED_WINDOW (0 = automatic)
+    int DLA = 0, DUA = 0, DLs = 0, DUs = 0;  // bandwidths in tiles of A and of the factors
     static constexpr int kFusedKmax = 8;
-    double *fused_ring = nullptr;
-    unsigned int *fused_sync = nullptr;
+    double *ring_r = nullptr, *ring_g = nullptr;
+    int64_t ring_r_tiles = 0, ring_g_tiles = 0;
+    SkewSync *skew_sync = nullptr;
+    unsigned long long *skew_prog = nullptr;  // per-CTA progress counters
     void *mailbox = nullptr;           // [flags: nranks u64, padded][data: 2 x n_ghost f64]
     size_t mailbox_bytes = 0, flags_bytes = 0;
     unsigned long long *mb_flags = nullptr;
@@ -153,8 +158,10 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->d_dist_err);
     cudaFree(h->ghost_null);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
-    cudaFree(h->fused_ring);
-    cudaFree(h->fused_sync);
+    cudaFree(h->ring_r);
+    cudaFree(h->ring_g);
+    cudaFree(h->skew_sync);
+    cudaFree(h->skew_prog);
     delete h;
 }
 
@@ -438,17 +445,49 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         unsigned long long init = ULLONG_MAX;
         ok = cudaMemcpy(h->flag, &init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
     }
-    if (ok && nranks == 1 && h->n > 0 && fused_ok(h->L.maxw, h->U.maxw)) {
-        // rings and flags of the fused one-pass pGS application (fused.cu)
-        const int64_t tr = fused_tile_rows();
-        const int64_t ntiles = (h->n + tr - 1) / tr;
-        h->fused_DL = (int)((sa.bw_lower + tr - 1) / tr);
-        h->fused_DU = (int)((sa.bw_upper + tr - 1) / tr);
-        h->fused_grid = fused_grid(h->L.maxw, h->U.maxw);
-        h->fused_M = h->fused_DL + h->fused_DU + 2 * (int64_t)h->fused_grid + 4;
-        ok = a.get(&h->fused_ring, (int64_t)(nsm_handle::kFusedKmax + 1) * h->fused_M * tr) &&
-             a.get(&h->fused_sync, 64 + 2 * ntiles);
-        h->fused_ready = ok;
+    if (ok && nranks == 1 && h->n > 0) {
+        // rings, done flags and launch state of the fused passes (fused.cu),
+        // sized for the largest shape any k <= kFusedKmax can need
+        const int64_t tr = skew_tile_rows();
+        auto tiles = [tr](int64_t bw) { return (int)((bw + tr - 1) / tr); };
+        h->DLA = tiles(sa.bw_lower);
+        h->DUA = tiles(sa.bw_upper);
+        h->DLs = F ? tiles(sf.bw_lower) : 0;
+        h->DUs = F ? tiles(sf.bw_upper) : 0;
+        int64_t mr = 0, mg = 0;
+        bool all = true;
+        auto need = [&](const SkewShape &sh) {
+            all = all && sh.ok;
+            mr = std::max(mr, sh.Mr);
+            mg = std::max(mg, sh.Mg);
+        };
+        const int K = nsm_handle::kFusedKmax;
+        const int mw = std::max(h->L.maxw, h->U.maxw);
+        need(skew_shape(SKEW_RESID, false, h->L.maxw, h->U.maxw, mw, K, h->n, std::max(h->DLA, h->DUA),
+                        std::max(h->DLA, h->DUA), 0));
+        need(skew_shape(SKEW_NONE, false, 0, 0, mw, K, h->n, std::max(h->DLA, h->DUA), 0, 0));
+        if (F) {
+            const int mwf = std::max(h->Ls.maxw, h->Us.maxw);
+            need(skew_shape(SKEW_RESID, true, h->L.maxw, h->U.maxw, h->Ls.maxw, K, h->n, h->DLs, h->DLA, 0));
+            need(skew_shape(SKEW_NONE, true, 0, 0, mwf, K, h->n, std::max(h->DLs, h->DUs), 0, 0));
+            need(skew_shape(SKEW_NONE, false, 0, 0, mwf, K, h->n, std::max(h->DLs, h->DUs), 0, 0));
+        }
+        if (all && getenv("NSM_DEBUG_FULL_RINGS")) {  // window experiments (tools/skew_exp.py) only
+            int64_t t = 1;
+            while (t * tr < h->n) t <<= 1;
+            mr = mg = t;
+        }
+        if (all) {
+            h->ring_r_tiles = std::max<int64_t>(mr, 1);
+            h->ring_g_tiles = std::max<int64_t>(mg, 1);
+            SkewSync init{};
+            init.epoch = 1;
+            ok = a.get(&h->ring_r, h->ring_r_tiles * tr) && a.get(&h->ring_g, (int64_t)K * h->ring_g_tiles * tr) &&
+                 a.get(&h->skew_sync, 1) && a.get(&h->skew_prog, 4096) &&
+                 cudaMemcpy(h->skew_sync, &init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess &&
+                 cudaMemset(h->skew_prog, 0, 4096 * sizeof(unsigned long long)) == cudaSuccess;
+            h->fused_ready = ok;
+        }
     }
     if (ok && nranks > 1) {
         h->row_offsets.assign(dist->row_offsets, dist->row_offsets + nranks + 1);
@@ -600,7 +639,14 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
     if (!h) return NSM_ERR_ARG;
     switch (opt) {
         case NSM_OPT_PIPELINE: h->pipeline = value != 0; return NSM_OK;
-        case NSM_OPT_FUSED: h->fused = value != 0; return NSM_OK;
+        case NSM_OPT_FUSED:
+            if (value < 0 || value > 2) return NSM_ERR_ARG;
+            h->fused_mode = (int)value;
+            return NSM_OK;
+        case NSM_OPT_FUSED_WINDOW:
+            if (value < 0 || value > INT_MAX) return NSM_ERR_ARG;
+            h->skew_dw = (int)value;
+            return NSM_OK;
         case NSM_OPT_PDL: h->pdl = value != 0; return NSM_OK;
         case NSM_OPT_PROFILE:
             h->profile = value != 0;
@@ -632,7 +678,7 @@ nsm_status nsm_info(const nsm_handle *h, int64_t *n_local, int64_t *n_ghost, int
 
 nsm_status nsm_profile(nsm_handle *h, double *ms, int64_t *count) {
     if (!h || !ms || !count) return NSM_ERR_ARG;
-    for (int k = 0; k < 2; ++k) { ms[k] = 0.0; count[k] = 0; }
+    for (int k = 0; k < 3; ++k) { ms[k] = 0.0; count[k] = 0; }
     for (int i = 0; i < h->ev_used; ++i) {
         float t = 0.f;
         if (cudaEventSynchronize(h->ev[2 * i + 1]) != cudaSuccess ||
@@ -676,6 +722,20 @@ nsm_status nsm_set_ruiz(nsm_handle *h, const double *s_r, const double *s_c) {
         return NSM_ERR_OOM;
     if (!upload(h->s_r, s_r, h->n) || !upload(h->s_c, s_c, h->n)) return cuda_fail(h, cudaGetLastError(), "nsm_set_ruiz");
     h->ruiz = true;
+    return NSM_OK;
+}
+
+nsm_status nsm_fused_stats(nsm_handle *h, int64_t *waits, int64_t *wait_ns) {
+    if (!h || !waits || !wait_ns) return NSM_ERR_ARG;
+    *waits = 0;
+    *wait_ns = 0;
+    if (!h->skew_sync) return NSM_OK;
+    cudaSetDevice(h->device);
+    SkewSync v{};
+    cudaError_t e = cudaMemcpy(&v, h->skew_sync, sizeof(v), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(h, e, "nsm_fused_stats");
+    *waits = (int64_t)v.waits;
+    *wait_ns = (int64_t)v.wait_ns;
     return NSM_OK;
 }
 
@@ -723,6 +783,81 @@ nsm_status nsm_usolve(nsm_handle *h, const double *r, double *x, int k, void *st
     return tri_solve(h, false, r, x, k, stream);
 }
 
+// One fused phase-skewed pass (fused.cu) if the handle allows it for this
+// shape: fused_mode 1 always, 2 (auto) when the problem spans at least two
+// skew distances.  *ran tells whether it was launched.
+static nsm_status skew_run(nsm_handle *h, SkewLaunch &L, bool unit, int DT, int DA, cudaStream_t s, bool *ran) {
+    *ran = false;
+    if (!h->fused_ready || h->fused_mode == 0 || !h->pipeline || L.k < 1 || L.k > nsm_handle::kFusedKmax ||
+        h->n == 0)
+        return NSM_OK;
+    const bool resid = L.ph0 == SKEW_RESID;
+    L.shape = skew_shape(L.ph0, unit, resid ? h->L.maxw : 0, resid ? h->U.maxw : 0, L.T->maxw, L.k, h->n, DT, DA,
+                         h->skew_dw);
+    const SkewShape &sh = L.shape;
+    if (!sh.ok || sh.Mr > h->ring_r_tiles || sh.Mg > h->ring_g_tiles || sh.grid > 4096) return NSM_OK;
+    if (h->fused_mode == 2 && sh.ntiles < 2 * (int64_t)sh.D) return NSM_OK;
+    L.n = h->n;
+    if (unit) L.dT = nullptr;
+    L.ring_r = h->ring_r;
+    L.ring_g = h->ring_g;
+    L.flag = h->flag;
+    L.sweep_id0 = h->sweep_counter + 1;
+    h->sweep_counter += L.k;
+    L.err = h->d_dist_err;
+    L.timeout_ns = h->timeout_ns;
+    L.sync = h->skew_sync;
+    L.prog = h->skew_prog;
+    ProfScope prof(h, 2, s);
+    // debug: per-unit timestamps of two CTAs, summarised on stderr
+    static unsigned long long *trace = nullptr;
+    static const bool want_trace = getenv("NSM_DEBUG_SKEW_TRACE") != nullptr;
+    if (want_trace && !trace) {
+        cudaMalloc(&trace, 2 * 3 * 2048 * 4 * sizeof(unsigned long long));
+    }
+    if (want_trace) cudaMemsetAsync(trace, 0, 2 * 3 * 2048 * 4 * sizeof(unsigned long long), s);
+    L.trace = want_trace ? trace : nullptr;
+    cudaError_t e = launch_skew(L, s);
+    if (want_trace && e == cudaSuccess) {
+        std::vector<unsigned long long> tb(2 * 3 * 2048 * 4);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(tb.data(), trace, tb.size() * 8, cudaMemcpyDeviceToHost);
+        for (int cta = 0; cta < 2; ++cta) {
+            const unsigned long long *C = tb.data() + (cta * 3 + 0) * 2048 * 4, *P = tb.data() + (cta * 3 + 1) * 2048 * 4;
+            const unsigned long long *Y = tb.data() + (cta * 3 + 2) * 2048 * 4;
+            unsigned long long t0 = C[0] ? C[0] : P[0], tend = 0;
+            double full_wait = 0, compute = 0, empty_wait = 0, issue = 0;
+            int nu = 0;
+            for (int u = 0; u < 2048 && C[u * 4 + 1]; ++u, ++nu) {
+                full_wait += (double)(C[u * 4 + 1] - C[u * 4 + 0]);
+                compute += (double)(C[u * 4 + 2] - C[u * 4 + 1]);
+                tend = C[u * 4 + 2];
+                if (P[u * 4 + 1]) {
+                    empty_wait += (double)(P[u * 4 + 1] - P[u * 4 + 0]);
+                    issue += (double)(P[u * 4 + 2] - P[u * 4 + 1]);
+                }
+            }
+            fprintf(stderr, "[skew trace] cta %d: %d units in %.1f us: consumer full-wait %.1f us, compute %.1f us; "
+                            "producer empty-wait %.1f us, issue %.1f us\n",
+                    cta, nu, (tend - t0) / 1e3, full_wait / 1e3, compute / 1e3, empty_wait / 1e3, issue / 1e3);
+            if (cta == 0)
+                for (int m = 0; m < 12; ++m)
+                    fprintf(stderr, "   item %-3d wanted %6.0f readied %6.0f idone-arrived(w0) %6.0f published %6.0f\n", m,
+                            (Y[m * 4 + 3] - t0) / 1.0, (Y[m * 4 + 0] - t0) / 1.0, (Y[m * 4 + 2] - t0) / 1.0,
+                            (Y[m * 4 + 1] - t0) / 1.0);
+            if (cta == 0)
+                for (int u = 0; u < 12 && u < nu; ++u)
+                    fprintf(stderr, "   u%-3d cons wait %6.0f..%6.0f done %6.0f empty-arrived %6.0f | prod %6.0f..%6.0f issued %6.0f\n", u,
+                            (C[u * 4] - t0) / 1.0, (C[u * 4 + 1] - t0) / 1.0, (C[u * 4 + 2] - t0) / 1.0, (C[u * 4 + 3] - t0) / 1.0,
+                            (P[u * 4] - t0) / 1.0, (P[u * 4 + 1] - t0) / 1.0, (P[u * 4 + 2] - t0) / 1.0);
+        }
+    }
+    ++h->launches;
+    if (e != cudaSuccess) return cuda_fail(h, e, "fused pass launch");
+    *ran = true;
+    return NSM_OK;
+}
+
 // One smoother application of the given kind (rows a2-a5).  fresh: x is
 // taken as 0 (its contents are ignored), so the residual is b (reading R3)
 // and the last kernel STORES x instead of adding to it.
@@ -731,6 +866,7 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
     double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
     const double *rhs = fresh ? b : R;
     nsm_status st = NSM_OK;
+    bool ran = false;
     if (kind == NSM_L1_JACOBI) {
         // l1-Jacobi: x += D_l1^{-1} (b - A x)
         if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
@@ -738,33 +874,35 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
     }
     if (kind == NSM_PGS || kind == NSM_PGS_BACKWARD) {
         const bool fwd = kind == NSM_PGS;
-        if (fwd && h->fused_ready && h->fused && h->pipeline && k_l >= 1 && k_l <= nsm_handle::kFusedKmax) {
-            // rows a2-a4 in ONE pass over the matrix (fused.cu); with x = 0
-            // the residual phase computes b exactly
-            if (fresh && h->n > 0 && cudaMemsetAsync(x, 0, h->n * sizeof(double), s) != cudaSuccess)
-                return cuda_fail(h, cudaGetLastError(), "memset");
-            FusedLaunch f{};
-            f.n = h->n;
-            f.L = &h->L;
-            f.U = &h->U;
-            f.d = h->d;
-            f.b = b;
-            f.x = x;
-            f.k = k_l;
-            f.DL = h->fused_DL;
-            f.DU = h->fused_DU;
-            f.M = h->fused_M;
-            f.ring = h->fused_ring;
-            f.sync = h->fused_sync;
-            f.grid = h->fused_grid;
-            f.flag = h->flag;
-            f.sweep_id0 = h->sweep_counter + 1;
-            h->sweep_counter += k_l + 1;
-            f.err = h->d_dist_err;
-            f.timeout_ns = h->timeout_ns;
-            cudaError_t e = launch_pgs_fused(f, s);
-            h->launches += 2;
-            return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "fused pGS launch");
+        if (k_l >= 1) {
+            // rows a2-a4 in ONE pass over the matrix: residual, k sweeps, x update
+            SkewLaunch L{};
+            L.desc = !fwd;
+            L.k = k_l;
+            L.T = fwd ? &h->L : &h->U;
+            L.dT = h->d;
+            if (!fresh) {
+                L.ph0 = SKEW_RESID;
+                L.A0 = &h->L;
+                L.A1 = &h->U;
+                L.dA = h->d;
+                L.b = b;
+                L.xin = x;
+                L.keep0 = fwd;   // the swept triangle is re-read by the later phases
+                L.keep1 = !fwd;
+                L.epi = SKEW_XADD;
+                L.x = x;
+            } else {
+                L.ph0 = SKEW_NONE;  // r = b, g(0) = b / d gathered on the fly
+                L.rhs = b;
+                L.g0 = b;
+                L.scaled_g0 = 1;
+                L.epi = SKEW_STORE;
+                L.out1 = x;
+            }
+            const int DT = fwd ? h->DLA : h->DUA;
+            st = skew_run(h, L, false, DT, DT, s, &ran);
+            if (st != NSM_OK || ran) return st;
         }
         // the residual pass also writes g^(0) = r / d (eq:jr-initial-guess)
         // when sweeps follow, so the first sweep gathers it instead of
@@ -780,42 +918,102 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
         return fresh ? run_sweeps(h, sg, W0, W1, EPI_STORE, x, nullptr, nullptr, s)
                      : run_sweeps(h, sg, W0, W1, EPI_XADD, nullptr, x, nullptr, s);
     }
-    // NSM_ILU0
-    if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
-    if (st != NSM_OK) return st;
-    if (h->ruiz) {
-        // Alg. 2 with Ruiz: y = L~^{-1} r; y~ = y / s_r; v = U~~^{-1} y~
-        // (unit diagonal); x += v / s_c
-        if (k_l > 0) {
-            double *ybuf = (k_l & 1) ? W0 : W1;
-            st = run_sweeps(h, Stage{&h->Ls, &h->LsG, nullptr, rhs, k_l}, W0, W1, EPI_STORE2, ybuf, nullptr, h->s_r, s,
-                            W2);
+    // NSM_ILU0, row a5: y = sum_{j<=kL} (-Ls)^j r ; z = sum_{j<=kU} (-DU^{-1}Us)^j DU^{-1} y ; x += z.
+    // With Ruiz (Alg. 2): y~ = y / s_r, v = U~^{-1} y~ (unit
+    // diagonal), x += v / s_c.
+    const bool ruiz = h->ruiz;
+    const double *y = nullptr, *z0 = nullptr;  // after the L stage: rhs of the U sweeps, materialised z^(0)
+    // ---- L stage (with the residual): one fused ascending pass
+    if (k_l >= 1 && !(ruiz && k_u == 0)) {
+        SkewLaunch L{};
+        L.desc = 0;
+        L.k = k_l;
+        L.T = &h->Ls;
+        if (!fresh) {
+            L.ph0 = SKEW_RESID;
+            L.A0 = &h->L;
+            L.A1 = &h->U;
+            L.dA = h->d;
+            L.b = b;
+            L.xin = x;
         } else {
-            st = scale_into(h, false, rhs, h->s_r, W2, s);
+            L.ph0 = SKEW_NONE;  // r = y(0) = b
+            L.rhs = b;
+            L.g0 = b;
         }
+        if (ruiz) { L.epi = SKEW_STORE_SCALE; L.out1 = W2; L.dn = h->s_r; }
+        else if (k_u >= 1) { L.epi = SKEW_STORE2; L.out1 = W0; L.out2 = W2; L.dn = h->dU; }
+        else if (fresh) { L.epi = SKEW_STORE_SCALE; L.out1 = x; L.dn = h->dU; }
+        else { L.epi = SKEW_XADD_SCALE; L.x = x; L.dn = h->dU; }
+        st = skew_run(h, L, true, h->DLs, h->DLA, s, &ran);
         if (st != NSM_OK) return st;
-        if (k_u == 0) return scale_into(h, !fresh, W2, h->s_c, x, s);
+        if (ran) {
+            if (!ruiz && k_u == 0) return NSM_OK;
+            y = ruiz ? W2 : W0;
+            z0 = ruiz ? nullptr : W2;
+        }
+    }
+    if (!y) {
+        if (!fresh) st = residual_into(h, b, x, R, OUT_R, s);
+        if (st != NSM_OK) return st;
+        if (ruiz) {
+            if (k_l > 0) {
+                double *ybuf = (k_l & 1) ? W0 : W1;
+                st = run_sweeps(h, Stage{&h->Ls, &h->LsG, nullptr, rhs, k_l}, W0, W1, EPI_STORE2, ybuf, nullptr,
+                                h->s_r, s, W2);
+            } else {
+                st = scale_into(h, false, rhs, h->s_r, W2, s);
+            }
+            if (st != NSM_OK) return st;
+            if (k_u == 0) return scale_into(h, !fresh, W2, h->s_c, x, s);
+            y = W2;
+        } else if (k_l > 0) {
+            // L sweeps ping-pong in W0/W1; the last writes y and, when U sweeps
+            // follow, z^(0) = y / dU into W2 (EPI_STORE2)
+            double *ybuf = (k_l & 1) ? W0 : W1;
+            Stage sl{&h->Ls, &h->LsG, nullptr, rhs, k_l};
+            if (k_u == 0)
+                return fresh ? run_sweeps(h, sl, W0, W1, EPI_STORE2, W2, nullptr, h->dU, s, x)   // x = y / dU
+                             : run_sweeps(h, sl, W0, W1, EPI_XADD_SCALE, nullptr, x, h->dU, s);
+            st = run_sweeps(h, sl, W0, W1, EPI_STORE2, ybuf, nullptr, h->dU, s, W2);
+            if (st != NSM_OK) return st;
+            z0 = W2;
+            y = ybuf;
+        } else if (k_u == 0) {
+            return scale_into(h, !fresh, rhs, h->dU, x, s);
+        } else {
+            y = rhs;
+        }
+    }
+    // ---- U stage: one fused descending pass
+    {
+        SkewLaunch L{};
+        L.ph0 = SKEW_NONE;
+        L.desc = 1;
+        L.k = k_u;
+        L.T = &h->Us;
+        L.dT = h->dU;
+        L.rhs = y;
+        L.g0 = z0 ? z0 : y;
+        L.scaled_g0 = z0 ? 0 : 1;
+        if (ruiz) {
+            L.dn = h->s_c;
+            if (fresh) { L.epi = SKEW_STORE_SCALE; L.out1 = x; }
+            else { L.epi = SKEW_XADD_SCALE; L.x = x; }
+        } else if (fresh) {
+            L.epi = SKEW_STORE;
+            L.out1 = x;
+        } else {
+            L.epi = SKEW_XADD;
+            L.x = x;
+        }
+        st = skew_run(h, L, false, h->DUs, 0, s, &ran);
+        if (st != NSM_OK || ran) return st;
+    }
+    if (ruiz) {
         Stage su{&h->Us, &h->UsG, h->dU, W2, k_u, nullptr};
         return fresh ? run_sweeps(h, su, W0, W1, EPI_STORE2, R, nullptr, h->s_c, s, x)
                      : run_sweeps(h, su, W0, W1, EPI_XADD_SCALE, nullptr, x, h->s_c, s);
-    }
-    // row a5: y = sum_{j<=kL} (-Ls)^j r ; z = sum_{j<=kU} (-DU^{-1}Us)^j DU^{-1} y ; x += z
-    const double *y = rhs;
-    const double *z0 = nullptr;
-    if (k_l > 0) {
-        // L sweeps ping-pong in W0/W1; the last writes y and, when U sweeps
-        // follow, z^(0) = y / dU into W2 (EPI_STORE2)
-        double *ybuf = (k_l & 1) ? W0 : W1;
-        Stage sl{&h->Ls, &h->LsG, nullptr, rhs, k_l};
-        if (k_u == 0)
-            return fresh ? run_sweeps(h, sl, W0, W1, EPI_STORE2, W2, nullptr, h->dU, s, x)   // x = y / dU
-                         : run_sweeps(h, sl, W0, W1, EPI_XADD_SCALE, nullptr, x, h->dU, s);
-        st = run_sweeps(h, sl, W0, W1, EPI_STORE2, ybuf, nullptr, h->dU, s, W2);
-        if (st != NSM_OK) return st;
-        z0 = W2;
-        y = ybuf;
-    } else if (k_u == 0) {
-        return scale_into(h, !fresh, rhs, h->dU, x, s);
     }
     // z ping-pong in buffers holding neither y nor (for the first U sweep) z^(0)
     double *za, *zb;
@@ -868,7 +1066,7 @@ nsm_status nsm_check(nsm_handle *h, int64_t *first_bad_sweep, void *stream) {
     if (first_bad_sweep) *first_bad_sweep = v == ULLONG_MAX ? -1 : (int64_t)v;
     if (derr) {
         h->err = (derr & 1u) ? "halo exchange timed out waiting for a neighbour"
-                             : "fused wavefront kernel timed out waiting for a lower tile";
+                             : "fused pass timed out waiting for an earlier work item";
         return NSM_ERR_DIST;
     }
     if (v != ULLONG_MAX) {

@@ -1,34 +1,72 @@
-// fused.cu — one-pass ("wavefront") polynomial Gauss-Seidel application
-// (DESIGN.md §6 "Fused wavefront kernel").
+// fused.cu — phase-skewed fused smoother passes (DESIGN.md §6 "Fused
+// phase-skewed passes"; SURVEY.md §7.3, §8(d) "fused floor").
 //
-// One launch computes  r = b - A x,  g^(0) = D^{-1} r,  k sweeps
-// g^(j) = D^{-1}(r - L g^(j-1))  and  x <- x + g^(k) while
-// reading the split matrix ONCE from HBM: tile t (256 rows) runs all k+1
-// phases back to back with its L and U slices held in shared memory (one
-// bulk copy), r and D in registers, and the inner iterates g^(j) published to
-// small L2-resident ring buffers.  Phase j of tile t needs g^(j-1) of the
-// rows within the lower bandwidth, i.e. of tiles [t - DL, t], so tiles are
-// dispatched IN ORDER to a persistent grid (atomic tile counter) and a tile
-// waits only for LOWER tiles' progress flags — the standard argument of
-// decoupled look-back: the lowest unfinished tile always progresses, so
-// there is no deadlock.
+// One launch computes a whole Jacobi-iterated triangular solve together with
+// the residual that feeds it, reading every matrix entry from HBM once:
 //
-// The new x of tile t cannot overwrite the old x while tiles up to t + DL
-// (whose residual reads it through L) or from t - DU (through U) have not
-// finished phase 0.  It goes to a ring buffer, and the CTA that processes
-// tile t + DL + 1 writes it back after checking those (lower) tiles' flags;
-// the last DL + 1 tiles are written back by a small tail kernel.
+//   pGS:   r = b - A x,  g(0) = D^{-1} r,
+//                       g(j) = D^{-1}(r - L g(j-1))  j = 1..k,   x += g(k)
+//   ILU pass 1 (Alg. 2, eq:LUiterMat P:L826-828):
+//                       r = b - A x,  y(0) = r,  y(j) = r - L_s y(j-1),
+//                       then y and z(0) = D_U^{-1} y are stored
+//   ILU pass 2 (LDU form P:L858-866, walked top-down):
+//                       z(j) = D_U^{-1}(y - U_s z(j-1)),   x += z(k)
 //
-// Every row is summed in the same order with the same IEEE operations as
-// the per-pass kernels and the oracle: the result is bit-identical.
-// All spin-waits are bounded (NSM_OPT_HALO_TIMEOUT_MS); a timeout sets an
-// error flag reported by nsm_check (NSM_ERR_DIST) instead of hanging.
+// (backward pGS, is pGS with U and a top-down walk).
+//
+// Schedule.  Rows are cut into tiles of 256 (8 SELL-32 slices).  Phase j of
+// tile u needs phase j-1 of tiles [u - DT, u] (DT: the triangle's bandwidth
+// in tiles), so a plain wavefront serialises the phases of each tile.
+// Instead, WORK ITEM w bundles phase j0 of tile w, phase j0+1 of tile w-D,
+// ..., phase k of tile w-(k-j0)D: every dependency of item w lies in items
+// [w - D - DT, w - D], at least D - DT = Dw items back.  Items are dealt
+// round-robin to a cooperative (co-resident) grid, item w to CTA w mod G,
+// and each CTA runs its items in order.  Before item w starts, all items
+// <= w - Dw must be done (one condition per item, tracked by per-item done
+// flags and a shared watermark); with Dw above the grid size it is almost
+// always already true.  The iterates g(j) of the last few thousand tiles
+// live in L2-resident ring buffers indexed by (row & mask); the triangle
+// slices a later phase re-reads are fetched with an L2 evict_normal policy,
+// the rest evict_first, so HBM sees the matrix about once.
+//
+// Warp roles (one CTA = 8 consumer warps + producer warp + sync warp):
+//   producer  stages, per unit, the tile's matrix slices, the per-slice
+//             offsets and the tile's immutable vector segments (d, b, x, ...)
+//             HBM/L2 -> shared memory with cp.async.bulk (mbarrier pipeline);
+//   sync      runs one item ahead of the consumers: waits for "items <= w -
+//             Dw done" and signals a shared-memory barrier; when the
+//             consumers finish an item it publishes the item's done flag
+//             (fence + st.release);
+//   consumers one slice per warp, one row per thread: no global
+//             synchronisation on their path.
+//
+// Ring and in-place-x safety (all with the single wait "items <= w-Dw done"):
+//   * g(j) slot of tile u is reused by tile u+Mg: its last reader is item
+//     u + DT + (j+1-j0)D  <=  w - Dw   when Mg >= D + DT + Dw;
+//   * r slot: last reader item u + (k-j0)D  <=  w - Dw  when Mr >= kD + Dw;
+//   * x of tile u is overwritten by item u + kD, after every residual that
+//     reads it (tiles up to u + DA, DA = A's bandwidth) when kD - DA >= Dw.
+// D = Dw + max(DT, DA) satisfies all three for k >= 1.
+//
+// Deadlock freedom: all CTAs are co-resident (cooperative launch); an item
+// depends only on items at least Dw lower; a sync warp waits for item w +
+// G's condition only after publishing item w, and G < Dw, so the lowest
+// unpublished item always makes progress.  Waits are bounded
+// (NSM_OPT_HALO_TIMEOUT_MS) and flag an error instead of hanging.  The
+// launch state (watermark, epoch of the done flags) is reset by the last CTA
+// to leave, so launches are self-contained and may be captured into graphs.
+//
+// Arithmetic: every row sum uses the operations and order of the per-pass
+// kernels (and of the oracle): results are bit-identical.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "nsm_internal.h"
 #include "ptx.cuh"
@@ -39,85 +77,107 @@ namespace {
 
 constexpr int kTSF = 8;                     // slices (consumer warps) per tile
 constexpr int kRowsF = kTSF * kSlice;       // 256 rows per tile
-constexpr int kThreadsF = (kTSF + 1) * 32;  // + 1 producer warp
-constexpr int kConsumers = kTSF * 32;
+constexpr int kWarpP = kTSF, kWarpS = kTSF + 1;
+constexpr int kThreadsF = (kTSF + 2) * 32;  // + producer warp + sync warp
+constexpr int kMaxStages = 8;
+constexpr int kSlots = 4;                   // item slots of the ready / done barriers
+constexpr int kNVec = 4;                    // vector segments staged per unit
+constexpr int kHeader = 256 + kMaxStages * 2 * kTSF * 8;  // barriers + per-stage slice offsets
+constexpr int64_t kSmemMaxF = 220 * 1024;
+constexpr int64_t kVecBytes = (int64_t)kRowsF * 8;
 
-struct FusedParams {
-    int64_t n, nslices, ntiles;
-    SellView L, U;
-    const double *d, *b;
-    double *x;
-    int k;
-    int DL, DU;              // dependency distances in tiles
-    int64_t M;               // ring length in tiles
-    double *ring;            // k + 1 rings of M * 256 doubles: g^(0..k-1), new x
-    unsigned int *counter;   // tile dispenser
-    int *prog;               // [ntiles]: number of finished phases of the tile
-    int *wb;                 // [ntiles]: new x written back
+struct SkewParams {
+    int64_t n, nslices, ntiles, nitems;
+    int desc;                 // walk tiles top-down (logical tile u = physical ntiles-1-u)
+    int k, j0, D, Dw;         // sweeps; first phase (0: residual, 1: none); skew; wait distance
+    int epi, scaled_g0, vec_bulk;
+    SellView A0, A1;          // phase 0: residual parts (strict lower, strict upper of A)
+    SellView T;               // swept triangle
+    const double *dA, *b, *xin;
+    const double *dT, *rhs, *g0;
+    double *x, *out1, *out2;
+    const double *dn;
+    double *ring_r, *ring_g;
+    int64_t rmask, gmask, gstride;
     unsigned long long *flag;
     int64_t sweep_id0;
     unsigned int *err;
     unsigned long long timeout_ns;
-    int nst;
-    int64_t capL, capU;      // staged entries per stage per part
+    SkewSync *sync;
+    unsigned long long *prog;   // per-CTA progress counters
+    int nst, keep0, keep1;
+    int64_t cap0, cap1, stage_bytes;
+    unsigned long long *trace;  // debug (NSM_DEBUG_SKEW_TRACE): per-unit timestamps of two CTAs
 };
-
-struct FLayout {
-    int nst;
-    int64_t capL, capU;
-    __device__ __forceinline__ uint64_t *full(char *s) const { return (uint64_t *)s; }
-    __device__ __forceinline__ uint64_t *empty(char *s) const { return (uint64_t *)s + nst; }
-    __device__ __forceinline__ int *tile_id(char *s) const { return (int *)(s + 16 * nst); }
-    __device__ __forceinline__ char *stage(char *s, int st) const {
-        return s + 256 + (int64_t)st * (capL + capU) * 12;
-    }
-    __device__ __forceinline__ double *lval(char *s, int st) const { return (double *)stage(s, st); }
-    __device__ __forceinline__ int32_t *lcol(char *s, int st) const { return (int32_t *)(stage(s, st) + capL * 8); }
-    __device__ __forceinline__ double *uval(char *s, int st) const { return (double *)(stage(s, st) + capL * 12); }
-    __device__ __forceinline__ int32_t *ucol(char *s, int st) const {
-        return (int32_t *)(stage(s, st) + capL * 12 + capU * 8);
-    }
-};
-
-// Warp-wide: wait until flags[v] >= need for every v in [lo, hi] (clamped to
-// [0, ...]).  Loads are issued in batches so one check costs about one L2
-// round trip; acquire ordering by a fence afterwards.  Bounded by a timeout.
-__device__ __forceinline__ void wait_flags(const int *flags, int64_t lo, int64_t hi, int need, const FusedParams &p,
-                                           int lane) {
-    lo = lo < 0 ? 0 : lo;
-    if (hi < lo) return;
-    const uint64_t t0 = ptx::globaltimer_ns();
-    for (int64_t base = lo; base <= hi; base += 32 * 8) {
-        while (true) {
-            int mn = INT_MAX;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int64_t v = base + (int64_t)u * 32 + lane;
-                if (v <= hi) mn = min(mn, __ldcv(flags + v));
-            }
-            if (__all_sync(0xffffffffu, mn >= need)) break;
-            if (ptx::globaltimer_ns() - t0 > p.timeout_ns) {
-                if (lane == 0) atomicOr(p.err, 2u);
-                return;
-            }
-            __nanosleep(100);
-        }
-    }
-    __threadfence();
+constexpr int kTraceUnits = 2048;
+__device__ __forceinline__ void trace_at(const SkewParams &p, int role, int unit, int slot) {
+    if (!p.trace || unit >= kTraceUnits) return;
+    const int cta = blockIdx.x == 0 ? 0 : (blockIdx.x == gridDim.x / 2 ? 1 : -1);
+    if (cta < 0) return;
+    p.trace[((cta * 3 + role) * kTraceUnits + unit) * 4 + slot] = ptx::globaltimer_ns();
 }
 
-__device__ __forceinline__ double *ring_at(const FusedParams &p, int which, int64_t tile) {
-    return p.ring + ((int64_t)which * p.M + tile % p.M) * kRowsF;
+// shared memory: [full x8][empty x8][ready x4][idone x4] ... [slice offsets][stages]
+__device__ __forceinline__ uint64_t *full_bar(char *s) { return (uint64_t *)s; }
+__device__ __forceinline__ uint64_t *empty_bar(char *s) { return (uint64_t *)s + kMaxStages; }
+__device__ __forceinline__ uint64_t *ready_bar(char *s) { return (uint64_t *)s + 2 * kMaxStages; }
+__device__ __forceinline__ uint64_t *idone_bar(char *s) { return (uint64_t *)s + 2 * kMaxStages + kSlots; }
+__device__ __forceinline__ unsigned int *pubcnt(char *s) { return (unsigned int *)((uint64_t *)s + 2 * kMaxStages + 2 * kSlots); }
+// {offset within the stage's part, width} of slice `sl` of part `pt` in stage `st`
+__device__ __forceinline__ int2 *slice_info(char *s, int st, int pt) {
+    return (int2 *)(s + 256) + (st * 2 + pt) * kTSF;
 }
+__device__ __forceinline__ char *stage_ptr(char *s, const SkewParams &p, int st) {
+    return s + kHeader + (int64_t)st * p.stage_bytes;
+}
+
+// Which vector segments a unit stages (slot order): phase 0: dA, b, xin;
+// phase j >= 1: dT (non-unit), rhs (given vector), x (last, x-update
+// epilogue), dn (last, scaling epilogue).
+struct VecSet {
+    const double *v[kNVec];
+    int n;
+};
+template <int PH0, bool UNIT>
+__device__ __forceinline__ VecSet unit_vectors(const SkewParams &p, int j) {
+    VecSet vs{};
+    if (PH0 == SKEW_RESID && j == 0) {
+        vs.v[0] = p.dA; vs.v[1] = p.b; vs.v[2] = p.xin; vs.n = 3;
+        return vs;
+    }
+    const bool last = j == p.k;
+    int n = 0;
+    if (!UNIT) vs.v[n++] = p.dT;
+    if (PH0 != SKEW_RESID) vs.v[n++] = p.rhs;
+    if (last && (p.epi == SKEW_XADD || p.epi == SKEW_XADD_SCALE)) vs.v[n++] = p.x;
+    if (last && (p.epi == SKEW_STORE2 || p.epi == SKEW_XADD_SCALE || p.epi == SKEW_STORE_SCALE)) vs.v[n++] = p.dn;
+    vs.n = n;
+    return vs;
+}
+
+struct GFull {
+    const double *__restrict__ g;
+    __device__ __forceinline__ double operator()(int32_t c) const { return __ldg(g + c); }
+};
+struct GScaled {
+    const double *__restrict__ g;
+    const double *__restrict__ d;
+    __device__ __forceinline__ double operator()(int32_t c) const { return __ddiv_rn(__ldg(g + c), __ldg(d + c)); }
+};
+struct GRing {  // written by other CTAs during this launch: L2 only
+    const double *base;
+    uint32_t mask;
+    __device__ __forceinline__ double operator()(int32_t c) const { return __ldcg(base + ((uint32_t)c & mask)); }
+};
 
 template <int CH>
-struct FChunk {
+struct Chunk {
     double v[CH];
     int32_t c[CH];
     const double *sv;
     const int32_t *sc;
     int w;
-    __device__ __forceinline__ void load(const double *sv_, const int32_t *sc_, int64_t off, int w_, int lane) {
+    __device__ __forceinline__ void load(const double *sv_, const int32_t *sc_, int off, int w_, int lane) {
         sv = sv_ + off + lane;
         sc = sc_ + off + lane;
         w = w_;
@@ -128,263 +188,615 @@ struct FChunk {
                 c[j] = sc[j * kSlice];
             }
     }
+    template <class G>
+    __device__ __forceinline__ void gather_mul(const G &g) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) v[j] = __dmul_rn(v[j], g(c[j]));
+    }
+    template <class G>
+    __device__ __forceinline__ double add(double acc, const G &g) const {
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) acc = __dadd_rn(acc, v[j]);
+        for (int j = CH; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn(sv[j * kSlice], g(sc[j * kSlice])));
+        return acc;
+    }
 };
 
-// sum of v_j * g(c_j) over the row, in stored order (products first)
 template <int CH, class G>
-__device__ __forceinline__ double row_sum(const double *sv, const int32_t *sc, int64_t off, int w, int lane,
-                                          const G &g, double acc) {
-    FChunk<CH> ch;
-    ch.load(sv, sc, off, w, lane);
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-        if (j < w) ch.v[j] = __dmul_rn(ch.v[j], g(ch.c[j]));
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-        if (j < w) acc = __dadd_rn(acc, ch.v[j]);
-    for (int j = CH; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn(ch.sv[j * kSlice], g(ch.sc[j * kSlice])));
-    return acc;
+__device__ __forceinline__ double tri_sum(const double *sv, const int32_t *sc, int2 info, int lane, const G &g) {
+    Chunk<CH> ch;
+    ch.load(sv, sc, info.x, info.y, lane);
+    ch.gather_mul(g);
+    return ch.add(0.0, g);
 }
 
-template <int CH>
-__global__ void __launch_bounds__(kThreadsF, 2) k_pgs_fused(FusedParams p) {
+// Completion is tracked per CTA: prog[c] = (epoch << 32) | items of CTA c
+// done (CTA c owns items c, c + G, c + 2G, ... and finishes them in order).
+// All items <= t are done iff t < F = min_c (c + done_c * G): the sync warp
+// reads the G counters in one parallel sweep and keeps F until it no
+// longer suffices.
+__device__ __forceinline__ int64_t read_frontier(const SkewParams &p, unsigned int epoch, int lane) {
+    const int64_t G = gridDim.x;
+    int64_t f = INT64_MAX;
+    for (int64_t c = lane; c < G; c += 32) {
+        // relaxed: an acquire load would invalidate the SM's L1 on every
+        // poll; the caller fences once when the condition holds
+        const unsigned long long v = ptx::ld_relaxed_gpu_u64(p.prog + c);
+        const int64_t cnt = (unsigned int)(v >> 32) == epoch ? (int64_t)(v & 0xffffffffull) : 0;
+        f = min(f, c + cnt * G);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) f = min(f, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)f, o));
+    return f;
+}
+
+// One unit: phase j of logical tile u, slice `warp`, row `lane`.  Row, slice
+// and ring indices are 32-bit (a rank holds < 2^31 rows: columns are int32).
+template <int PH0, bool UNIT, int CH>
+__device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, int64_t w, int j, int warp,
+                                         int lane) {
+    char *stg = stage_ptr(sm, p, st);
+    const int u = (int)(w - (int64_t)(j - p.j0) * p.D);
+    const int tp = p.desc ? (int)p.ntiles - 1 - u : u;
+    const int s = tp * kTSF + warp;
+    const bool has = s < (int)p.nslices;
+    const int i = s * kSlice + lane;
+    const bool row = has && i < (int)p.n;
+    // vectors from the stage (full tile, aligned) or from global memory
+    const bool vs = p.vec_bulk && (int64_t)(tp + 1) * kRowsF <= p.n;
+    const int rl = warp * kSlice + lane;   // row within the tile
+    const double *sv = (const double *)(stg + (p.cap0 + p.cap1) * 12) + rl;
+    auto vec = [&](int slot, const double *g) -> double {
+        return vs ? sv[slot * kRowsF] : (row ? __ldg(g + i) : 0.0);
+    };
+    const double *v0 = (const double *)stg;
+    const int32_t *c0 = (const int32_t *)(stg + p.cap0 * 8);
+    const uint32_t rmask = (uint32_t)p.rmask, gmask = (uint32_t)p.gmask;
+    if (PH0 == SKEW_RESID && j == 0) {
+        // phase 0: r = b - A x (A = L + D + U, ascending column order), g(0)
+        const double di = row ? vec(0, p.dA) : 1.0, bi = vec(1, p.b), xi = vec(2, p.xin);
+        const double *v1 = (const double *)(stg + p.cap0 * 12);
+        const int32_t *c1 = (const int32_t *)(stg + p.cap0 * 12 + p.cap1 * 8);
+        double acc = 0.0;
+        if (has) {
+            const int2 il = slice_info(sm, st, 0)[warp], iu = slice_info(sm, st, 1)[warp];
+            const GFull gx{p.xin};
+            if constexpr (CH <= 8) {
+                Chunk<CH> cl, cu;
+                cl.load(v0, c0, il.x, il.y, lane);
+                cu.load(v1, c1, iu.x, iu.y, lane);
+                cl.gather_mul(gx);
+                cu.gather_mul(gx);
+                acc = cl.add(acc, gx);
+                acc = __dadd_rn(acc, __dmul_rn(di, xi));
+                acc = cu.add(acc, gx);
+            } else {
+                Chunk<CH> c;
+                c.load(v0, c0, il.x, il.y, lane);
+                c.gather_mul(gx);
+                acc = c.add(acc, gx);
+                acc = __dadd_rn(acc, __dmul_rn(di, xi));
+                c.load(v1, c1, iu.x, iu.y, lane);
+                c.gather_mul(gx);
+                acc = c.add(acc, gx);
+            }
+        }
+        if (row) {
+            const double r = __dsub_rn(bi, acc);
+            p.ring_r[(uint32_t)i & rmask] = r;
+            if (!UNIT) p.ring_g[(uint32_t)i & gmask] = __ddiv_rn(r, di);  // eq:jr-initial-guess
+        }
+        return;
+    }
+    // phase j >= 1: v = (rhs - T g(j-1)) / dT   (eq:jacobi, eq:LUiterMat)
+    // staged slots: [dT (non-unit)] [rhs (given)] [x (x update)] [dn (scaling)]
+    const bool last = j == p.k;
+    const bool xadd = last && (p.epi == SKEW_XADD || p.epi == SKEW_XADD_SCALE);
+    const bool scale = last && (p.epi == SKEW_STORE2 || p.epi == SKEW_XADD_SCALE || p.epi == SKEW_STORE_SCALE);
+    const int s_rhs = UNIT ? 0 : 1;
+    const int s_x = s_rhs + (PH0 == SKEW_RESID ? 0 : 1);
+    const int s_dn = s_x + (xadd ? 1 : 0);
+    const double di = UNIT ? 1.0 : (row ? vec(0, p.dT) : 1.0);
+    const double ri = PH0 == SKEW_RESID ? (row ? __ldcg(p.ring_r + ((uint32_t)i & rmask)) : 0.0) : vec(s_rhs, p.rhs);
+    const double xi = xadd ? vec(s_x, p.x) : 0.0;
+    const double dn = scale ? vec(s_dn, p.dn) : 1.0;
+    double acc = 0.0;
+    if (has) {
+        const int2 it = slice_info(sm, st, 0)[warp];
+        if (PH0 == SKEW_NONE && j == 1) {
+            if (p.scaled_g0) acc = tri_sum<CH>(v0, c0, it, lane, GScaled{p.g0, p.dT});
+            else acc = tri_sum<CH>(v0, c0, it, lane, GFull{p.g0});
+        } else if (PH0 == SKEW_RESID && UNIT && j == 1) {
+            acc = tri_sum<CH>(v0, c0, it, lane, GRing{p.ring_r, rmask});  // y(0) = r
+        } else {
+            acc = tri_sum<CH>(v0, c0, it, lane, GRing{p.ring_g + (int64_t)(j - 1) * p.gstride, gmask});
+        }
+    }
+    if (!row) return;
+    double v = __dsub_rn(ri, acc);
+    if (!UNIT) v = __ddiv_rn(v, di);
+    if (!isfinite(v)) atomicMin(p.flag, (unsigned long long)(p.sweep_id0 + j - 1));
+    if (!last) {
+        p.ring_g[(int64_t)j * p.gstride + ((uint32_t)i & gmask)] = v;
+        return;
+    }
+    switch (p.epi) {
+        case SKEW_STORE: p.out1[i] = v; break;
+        case SKEW_XADD: p.x[i] = __dadd_rn(xi, v); break;
+        case SKEW_STORE2: p.out1[i] = v; p.out2[i] = __ddiv_rn(v, dn); break;
+        case SKEW_XADD_SCALE: p.x[i] = __dadd_rn(xi, __ddiv_rn(v, dn)); break;
+        default: p.out1[i] = __ddiv_rn(v, dn); break;  // SKEW_STORE_SCALE
+    }
+}
+
+// Unit sequence of a CTA: items w = blockIdx.x + m G in order, each with units
+// q = qa..qb (phase j0 + q on logical tile w - qD), qa = max(0, ceil((w - T +
+// 1) / D)), qb = min(floor(w / D), k - j0).  Division-free: the quotients
+// are carried along as w grows by G.
+struct UnitGen {
+    int64_t w, T, D, G, nitems;
+    int64_t quo, rem;     // w = quo D + rem
+    int64_t x2, quo2, rem2; // x2 = w - T + D; floor(x2 / D) once x2 >= 0
+    int nph;
+    int64_t q, qa, qb;
+    bool valid;
+    // skip = true: position on the first unit (producer); false: on item
+    // blockIdx.x whether or not it has units (consumers walk every item)
+    __device__ __forceinline__ void init(const SkewParams &p, bool skip) {
+        G = gridDim.x;
+        w = blockIdx.x;
+        T = p.ntiles;
+        D = p.D;
+        nitems = p.nitems;
+        nph = p.k - p.j0;
+        quo = w / D;
+        rem = w - quo * D;
+        x2 = w - T + D;
+        quo2 = x2 >= 0 ? x2 / D : 0;
+        rem2 = x2 >= 0 ? x2 - quo2 * D : 0;
+        item();
+        if (skip) first_unit();
+    }
+    __device__ __forceinline__ void item() {
+        qb = min(quo, (int64_t)nph);
+        qa = x2 >= 0 ? quo2 : 0;
+    }
+    __device__ __forceinline__ void advance_item() {
+        w += G;
+        rem += G;
+        while (rem >= D) { rem -= D; ++quo; }
+        const bool was_neg = x2 < 0;
+        x2 += G;
+        if (x2 >= 0) {
+            if (was_neg) {
+                quo2 = x2 / D;  // once
+                rem2 = x2 - quo2 * D;
+            } else {
+                rem2 += G;
+                while (rem2 >= D) { rem2 -= D; ++quo2; }
+            }
+        }
+        item();
+    }
+    // first unit of the current or a later item (skipping items without units)
+    __device__ __forceinline__ void first_unit() {
+        while (w < nitems && qa > qb) advance_item();
+        valid = w < nitems;
+        q = qa;
+    }
+    __device__ __forceinline__ void next() {
+        if (++q <= qb) return;
+        advance_item();
+        first_unit();
+    }
+};
+
+// Slice pointers of a unit's parts: lanes 0..8 part 0, lanes 16..24 part 1.
+template <int PH0>
+__device__ __forceinline__ int64_t unit_ptrs(const SkewParams &p, int64_t w, int64_t q, int lane) {
+    const int j = p.j0 + (int)q;
+    const int64_t u = w - q * p.D;
+    const int64_t tp = p.desc ? p.ntiles - 1 - u : u;
+    const int64_t s0 = tp * kTSF, s1 = min(s0 + kTSF, p.nslices);
+    const bool ph0 = PH0 == SKEW_RESID && j == 0;
+    int64_t pv = 0;
+    if (lane <= kTSF) pv = __ldg((ph0 ? p.A0.ptr : p.T.ptr) + min(s0 + lane, s1));
+    else if (ph0 && lane >= 16 && lane <= 16 + kTSF) pv = __ldg(p.A1.ptr + min(s0 + lane - 16, s1));
+    return pv;
+}
+
+constexpr int kPre = 4;  // units whose slice pointers the producer has in flight
+
+template <int PH0, bool UNIT>
+__device__ __forceinline__ void stage_unit(const SkewParams &p, char *sm, int it, int64_t w, int64_t q, int64_t pv,
+                                           uint64_t pol_first, uint64_t pol_keep, int lane) {
+    const int st = it % p.nst;
+    if (lane == 0) trace_at(p, 1, it, 0);
+    if (it >= p.nst) ptx::mbar_wait(empty_bar(sm) + st, ((uint32_t)(it / p.nst) - 1) & 1);
+    if (lane == 0) trace_at(p, 1, it, 1);
+    const int j = p.j0 + (int)q;
+    const int64_t u = w - q * p.D;
+    const int64_t tp = p.desc ? p.ntiles - 1 - u : u;
+    const bool ph0 = PH0 == SKEW_RESID && j == 0;
+    const SellView &P0 = ph0 ? p.A0 : p.T;
+    const int64_t pnext = __shfl_down_sync(0xffffffffu, pv, 1);
+    const int64_t pbase0 = __shfl_sync(0xffffffffu, pv, 0), pend0 = __shfl_sync(0xffffffffu, pv, kTSF);
+    const int64_t pbase1 = __shfl_sync(0xffffffffu, pv, 16), pend1 = __shfl_sync(0xffffffffu, pv, 16 + kTSF);
+    if (lane < kTSF) slice_info(sm, st, 0)[lane] = make_int2((int)(pv - pbase0), (int)((pnext - pv) / kSlice));
+    if (ph0 && lane >= 16 && lane < 16 + kTSF)
+        slice_info(sm, st, 1)[lane - 16] = make_int2((int)(pv - pbase1), (int)((pnext - pv) / kSlice));
+    __syncwarp();
+    if (lane == 0) {
+        char *sp = stage_ptr(sm, p, st);
+        uint64_t *bar = full_bar(sm) + st;
+        const VecSet V = unit_vectors<PH0, UNIT>(p, j);
+        const bool vs = p.vec_bulk && (tp + 1) * kRowsF <= p.n;
+        uint32_t bytes = (uint32_t)((pend0 - pbase0) * 12 + (ph0 ? (pend1 - pbase1) * 12 : 0));
+        if (vs) bytes += (uint32_t)(V.n * kVecBytes);
+        ptx::mbar_expect_tx(bar, bytes);
+        const uint64_t pol0 = ph0 ? (p.keep0 ? pol_keep : pol_first) : (j < p.k ? pol_keep : pol_first);
+        if (pend0 > pbase0) {
+            ptx::bulk_g2s(sp, P0.val + pbase0, (uint32_t)((pend0 - pbase0) * 8), bar, pol0);
+            ptx::bulk_g2s(sp + p.cap0 * 8, P0.col + pbase0, (uint32_t)((pend0 - pbase0) * 4), bar, pol0);
+        }
+        if (ph0 && pend1 > pbase1) {
+            const uint64_t pol1 = p.keep1 ? pol_keep : pol_first;
+            ptx::bulk_g2s(sp + p.cap0 * 12, p.A1.val + pbase1, (uint32_t)((pend1 - pbase1) * 8), bar, pol1);
+            ptx::bulk_g2s(sp + p.cap0 * 12 + p.cap1 * 8, p.A1.col + pbase1, (uint32_t)((pend1 - pbase1) * 4), bar,
+                          pol1);
+        }
+        if (vs) {
+#pragma unroll
+            for (int v = 0; v < kNVec; ++v)
+                if (v < V.n)
+                    ptx::bulk_g2s(sp + (p.cap0 + p.cap1) * 12 + v * kVecBytes, V.v[v] + tp * kRowsF,
+                                  (uint32_t)kVecBytes, bar, pol_keep);
+        }
+    }
+    __syncwarp();
+}
+
+// Producer: walks the unit sequence with the slice pointers of the next kPre
+// units already loading (their latency would otherwise serialise every unit).
+template <int PH0, bool UNIT>
+__device__ __forceinline__ void produce(const SkewParams &p, char *sm, int lane) {
+    const uint64_t pol_first = ptx::policy_evict_first(), pol_keep = ptx::policy_evict_normal();
+    UnitGen gen;
+    gen.init(p, true);
+    int64_t pw[kPre], pq[kPre], pv[kPre];
+    bool ok[kPre];
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+        ok[k] = gen.valid;
+        pw[k] = gen.w;
+        pq[k] = gen.q;
+        pv[k] = ok[k] ? unit_ptrs<PH0>(p, pw[k], pq[k], lane) : 0;
+        if (gen.valid) gen.next();
+    }
+    for (int it = 0; ok[0]; it += kPre) {
+#pragma unroll
+        for (int k = 0; k < kPre; ++k) {
+            if (!ok[k]) break;
+            stage_unit<PH0, UNIT>(p, sm, it + k, pw[k], pq[k], pv[k], pol_first, pol_keep, lane);
+            // refill slot k with the unit kPre ahead
+            ok[k] = gen.valid;
+            pw[k] = gen.w;
+            pq[k] = gen.q;
+            pv[k] = ok[k] ? unit_ptrs<PH0>(p, pw[k], pq[k], lane) : 0;
+            if (gen.valid) gen.next();
+        }
+    }
+}
+
+// Sync warp: signals "ready" for this CTA's items in order, once every item
+// <= w - Dw is done and the item's barrier slot is free (the consumers
+// finished item m - (kSlots-1)).  The progress counters are polled with
+// relaxed loads, and not at all while the condition still includes this
+// CTA's own unpublished item.  (Publication is done by the consumers: the
+// last warp to finish an item.)
+__device__ __forceinline__ void sync_role(const SkewParams &p, char *sm, unsigned int epoch, int lane) {
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    const int64_t nmine = c < p.nitems ? (p.nitems - c + G - 1) / G : 0;
+    int64_t F = 0;  // all items < F are known to be done
+    for (int64_t m = 0; m < nmine; ++m) {
+        if (m >= kSlots - 1) {
+            const int64_t mo = m - (kSlots - 1);  // slot reuse: that item is finished here
+            ptx::mbar_wait(idone_bar(sm) + (mo % kSlots), (uint32_t)(mo / kSlots) & 1);
+        }
+        const int64_t tgt = c + m * G - p.Dw;
+        if (tgt >= F) {
+            const uint64_t t0 = ptx::globaltimer_ns();
+            while (true) {
+                // own items before m are finished (the wait above) but maybe
+                // not yet published: the frontier may lag by our own counter
+                F = read_frontier(p, epoch, lane);
+                // No acquire fence on success: a gpu-scope acquire invalidates the
+                // SM's whole L1 (CCTL.IVALL), which the neighbour gathers live
+                // on.  Everything another CTA wrote in this launch (the ring
+                // buffers) is read with ld.global.cg from L2, the GPU's point
+                // of coherence, after this relaxed load observed a counter
+                // the writer published with a release reduction (its ring
+                // stores were performed at L2 first); the readers' loads are
+                // issued only after the ready barrier, i.e. after it.
+                if (tgt < F) break;
+                if (ptx::globaltimer_ns() - t0 > p.timeout_ns) {
+                    if (lane == 0) atomicOr(p.err, 2u);
+                    F = INT64_MAX;  // give up: let the consumers drain
+                    break;
+                }
+                __nanosleep(32);
+            }
+        }
+        if (lane == 0) {
+            trace_at(p, 2, (int)m, 0);  // item made ready
+            ptx::mbar_arrive(ready_bar(sm) + (m % kSlots));
+        }
+        __syncwarp();
+    }
+}
+
+template <int PH0, bool UNIT, int CH>
+__global__ void __launch_bounds__(kThreadsF, CH <= 4 ? 3 : (CH <= 8 ? 2 : 1)) k_skew(const __grid_constant__ SkewParams p) {
     extern __shared__ __align__(128) char sm[];
-    const FLayout Ly{p.nst, p.capL, p.capU};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned int epoch = *(volatile unsigned int *)&p.sync->epoch;
     if (threadIdx.x == 0) {
         for (int st = 0; st < p.nst; ++st) {
-            ptx::mbar_init(Ly.full(sm) + st, 1);
-            ptx::mbar_init(Ly.empty(sm) + st, kTSF);
+            ptx::mbar_init(full_bar(sm) + st, 1);
+            ptx::mbar_init(empty_bar(sm) + st, kTSF);
+        }
+        for (int sl = 0; sl < kSlots; ++sl) {
+            ptx::mbar_init(ready_bar(sm) + sl, 1);
+            ptx::mbar_init(idone_bar(sm) + sl, kTSF);
+            pubcnt(sm)[sl] = 0;
         }
         ptx::mbar_init_fence();
     }
     __syncthreads();
 
-    if (warp == kTSF) {  // ---- producer: claim tiles in order, stream their L and U slices
-        if (lane != 0) return;
-        const uint64_t pol = ptx::policy_evict_first();
-        for (int it = 0;; ++it) {
-            const int st = it % p.nst;
-            const uint32_t use = (uint32_t)(it / p.nst);
-            if (it >= p.nst) ptx::mbar_wait(Ly.empty(sm) + st, (use - 1) & 1);
-            const int64_t t = atomicAdd(p.counter, 1u);
-            Ly.tile_id(sm)[st] = (int)t;
-            if (t >= p.ntiles) {
-                ptx::mbar_arrive(Ly.full(sm) + st);
-                return;
+    if (warp == kWarpP) {
+        produce<PH0, UNIT>(p, sm, lane);
+    } else if (warp == kWarpS) {
+        sync_role(p, sm, epoch, lane);
+    } else {
+        int it = 0;
+        int64_t m = 0;
+        UnitGen gen;
+        gen.init(p, false);  // item-level walk (items without units included)
+        for (int64_t w = blockIdx.x; w < p.nitems; w += gridDim.x, ++m) {
+            if (w != (int64_t)blockIdx.x) gen.advance_item();
+            const int64_t qa = gen.qa, qb = gen.qb;
+            if (warp == 0 && lane == 0) trace_at(p, 2, (int)m, 3);  // consumers want item m
+            {
+                uint64_t *rb = ready_bar(sm) + (m % kSlots);
+                const uint32_t par = (uint32_t)(m / kSlots) & 1;
+                if (warp == 0 && !ptx::mbar_test(rb, par)) {  // statistics: consumers stalled on readiness
+                    const uint64_t t0 = ptx::globaltimer_ns();
+                    ptx::mbar_wait(rb, par);
+                    if (lane == 0) {
+                        atomicAdd(&p.sync->waits, 1ull);
+                        atomicAdd(&p.sync->wait_ns, ptx::globaltimer_ns() - t0);
+                    }
+                }
+                ptx::mbar_wait(rb, par);
             }
-            const int64_t s0 = t * kTSF, s1 = min(s0 + kTSF, p.nslices);
-            const int64_t lb = __ldg(p.L.ptr + s0), le = __ldg(p.L.ptr + s1);
-            const int64_t ub = __ldg(p.U.ptr + s0), ue = __ldg(p.U.ptr + s1);
-            ptx::mbar_expect_tx(Ly.full(sm) + st, (uint32_t)((le - lb + ue - ub) * 12));
-            if (le > lb) {
-                ptx::bulk_g2s(Ly.lval(sm, st), p.L.val + lb, (uint32_t)((le - lb) * 8), Ly.full(sm) + st, pol);
-                ptx::bulk_g2s(Ly.lcol(sm, st), p.L.col + lb, (uint32_t)((le - lb) * 4), Ly.full(sm) + st, pol);
+            for (int64_t q = qa; q <= qb; ++q, ++it) {
+                const int st = it % p.nst;
+                if (warp == 0 && lane == 0) trace_at(p, 0, it, 0);
+                ptx::mbar_wait(full_bar(sm) + st, (uint32_t)(it / p.nst) & 1);
+                if (warp == 0 && lane == 0) trace_at(p, 0, it, 1);
+                run_unit<PH0, UNIT, CH>(p, sm, st, w, p.j0 + (int)q, warp, lane);
+                __syncwarp();
+                if (warp == 0 && lane == 0) trace_at(p, 0, it, 2);
+                if (lane == 0) ptx::mbar_arrive(empty_bar(sm) + st);
+                if (warp == 0 && lane == 0) trace_at(p, 0, it, 3);
             }
-            if (ue > ub) {
-                ptx::bulk_g2s(Ly.uval(sm, st), p.U.val + ub, (uint32_t)((ue - ub) * 8), Ly.full(sm) + st, pol);
-                ptx::bulk_g2s(Ly.ucol(sm, st), p.U.col + ub, (uint32_t)((ue - ub) * 4), Ly.full(sm) + st, pol);
+            __syncwarp();
+            if (lane == 0) {
+                ptx::mbar_arrive(idone_bar(sm) + (m % kSlots));
+                if (warp == 0) trace_at(p, 2, (int)m, 2);
+                // the last warp to finish item m publishes "m + 1 items done";
+                // acq_rel at CTA scope makes the other warps' stores happen
+                // before this warp's release (cumulativity), max keeps the
+                // counter monotone if a later item's publication overtakes
+                const unsigned int prev = ptx::atom_add_acqrel_cta_shared(pubcnt(sm) + (m % kSlots), 1u);
+                if (prev == (unsigned int)((m / kSlots + 1) * kTSF - 1)) {
+                    trace_at(p, 2, (int)m, 1);  // item published
+                    ptx::red_max_release_gpu_u64(p.prog + blockIdx.x,
+                                                 ((unsigned long long)epoch << 32) | (unsigned long long)(m + 1));
+                }
             }
         }
     }
-
-    // ---- consumers: one slice (32 rows) per warp, one row per thread
-    for (int it = 0;; ++it) {
-        const int st = it % p.nst;
-        const uint32_t use = (uint32_t)(it / p.nst);
-        ptx::mbar_wait(Ly.full(sm) + st, use & 1);
-        const int64_t t = Ly.tile_id(sm)[st];
-        if (t >= p.ntiles) return;
-        const int64_t s0 = t * kTSF, s = s0 + warp;
-        const bool has = s < p.nslices;
-        const int64_t i = s * kSlice + lane;
-        const bool row = has && i < p.n;
-        const double di = row ? __ldg(p.d + i) : 1.0;
-        const double bi = row ? __ldg(p.b + i) : 0.0;
-        const double xi = row ? __ldg(p.x + i) : 0.0;
-        int64_t lo = 0, uo = 0;
-        int lw = 0, uw = 0;
-        if (has) {
-            const int64_t l0 = __ldg(p.L.ptr + s0), ls = __ldg(p.L.ptr + s), ls1 = __ldg(p.L.ptr + s + 1);
-            const int64_t u0 = __ldg(p.U.ptr + s0), us = __ldg(p.U.ptr + s), us1 = __ldg(p.U.ptr + s + 1);
-            lo = ls - l0;
-            lw = (int)((ls1 - ls) / kSlice);
-            uo = us - u0;
-            uw = (int)((us1 - us) / kSlice);
-        }
-        // ring slots of tile t may be reused once tile t - M is fully done
-        // and written back (tiles below t: no deadlock)
-        if (warp == 0 && t >= p.M) {
-            wait_flags(p.prog, t - p.M, t - p.M + p.DL, p.k + 1, p, lane);
-            wait_flags(p.wb, t - p.M, t - p.M, 1, p, lane);
-        }
-        // phase 0: residual r = b - A x (x is the input: its overwrite is deferred)
-        const double *lv = Ly.lval(sm, st), *uv = Ly.uval(sm, st);
-        const int32_t *lc = Ly.lcol(sm, st), *uc = Ly.ucol(sm, st);
-        const double *x = p.x;
-        auto gx = [x](int32_t c) { return __ldg(x + c); };
-        double acc = 0.0;
-        if (has) {
-            acc = row_sum<CH>(lv, lc, lo, lw, lane, gx, acc);
-            acc = __dadd_rn(acc, __dmul_rn(di, xi));
-            acc = row_sum<CH>(uv, uc, uo, uw, lane, gx, acc);
-        }
-        const double ri = __dsub_rn(bi, acc);
-        double g = __ddiv_rn(ri, di);
-        if (row && !isfinite(g)) atomicMin(p.flag, (unsigned long long)p.sweep_id0);
-        ptx::bar_sync(1, kConsumers);  // ring-reuse wait (warp 0) done; U slices no longer needed
-        if (row) ring_at(p, 0, t)[i - t * kRowsF] = g;
-        for (int ph = 1; ph <= p.k; ++ph) {
-            ptx::bar_sync(1, kConsumers);
-            if (threadIdx.x == 0) {
-                __threadfence();
-                ptx::st_release_gpu(p.prog + t, ph);  // phase ph-1 of tile t done
-            }
-            if (warp == 0) wait_flags(p.prog, t - p.DL, t - 1, ph, p, lane);
-            ptx::bar_sync(1, kConsumers);
-            const double *gp = p.ring + (int64_t)(ph - 1) * p.M * kRowsF;
-            const int64_t M = p.M;
-            auto gg = [gp, M](int32_t c) {
-                const int64_t tc = c / kRowsF;
-                return __ldcg(gp + (tc % M) * kRowsF + (c - tc * kRowsF));
-            };
-            double a2 = 0.0;
-            if (has) a2 = row_sum<CH>(lv, lc, lo, lw, lane, gg, a2);
-            g = __ddiv_rn(__dsub_rn(ri, a2), di);
-            if (row && !isfinite(g)) atomicMin(p.flag, (unsigned long long)(p.sweep_id0 + ph));
-            if (ph < p.k) {
-                if (row) ring_at(p, ph, t)[i - t * kRowsF] = g;
-            } else if (row) {
-                ring_at(p, p.k, t)[i - t * kRowsF] = __dadd_rn(xi, g);  // new x, written back later
-            }
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(Ly.empty(sm) + st);  // L/U slices consumed
-        ptx::bar_sync(1, kConsumers);
-        if (threadIdx.x == 0) {
+    // ---- the last CTA out resets the launch state for the next launch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(&p.sync->exits, 1u);
+        if (prev == gridDim.x - 1) {
+            p.sync->wmark = 0;
+            p.sync->exits = 0;
+            p.sync->epoch = epoch + 1 == 0 ? 1 : epoch + 1;
             __threadfence();
-            ptx::st_release_gpu(p.prog + t, p.k + 1);
-        }
-        // deferred write-back of tile w = t - DL - 1: every tile reading old
-        // x[w] in its residual (w - DU .. w + DL = t - 1) has finished phase 0
-        const int64_t w = t - p.DL - 1;
-        if (w >= 0) {
-            if (warp == 0) {
-                wait_flags(p.prog, w - p.DU, t - 1, 1, p, lane);
-                wait_flags(p.prog, w, w, p.k + 1, p, lane);
-            }
-            ptx::bar_sync(1, kConsumers);
-            const int64_t iw = w * kRowsF + threadIdx.x;
-            if (iw < p.n) p.x[iw] = __ldcg(ring_at(p, p.k, w) + threadIdx.x);
-            ptx::bar_sync(1, kConsumers);
-            if (threadIdx.x == 0) {
-                __threadfence();
-                ptx::st_release_gpu(p.wb + w, 1);
-            }
         }
     }
 }
 
-// write back the new x of the last tiles (nobody above them to do it)
-__global__ void k_fused_tail(int64_t n, int64_t w0, int64_t ntiles, int64_t M, const double *xring, double *x) {
-    const int64_t i = w0 * kRowsF + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || i >= ntiles * kRowsF) return;
-    const int64_t tl = i / kRowsF;
-    x[i] = xring[(tl % M) * kRowsF + (i - tl * kRowsF)];
+// ---- host side -----------------------------------------------------------------
+template <int PH0, bool UNIT, int CH>
+const void *kernel_ptr() {
+    return (const void *)k_skew<PH0, UNIT, CH>;
 }
 
-template <int CH>
-cudaError_t fused_launch(const FusedParams &p, size_t smem, int grid, cudaStream_t st) {
-    k_pgs_fused<CH><<<grid, kThreadsF, smem, st>>>(p);
-    return cudaGetLastError();
+const void *pick(int ph0, bool unit, int ch) {
+#define NSM_PK(P, U)                                                                               \
+    (ch == 4 ? kernel_ptr<P, U, 4>() : ch == 8 ? kernel_ptr<P, U, 8>() : kernel_ptr<P, U, 16>())
+    if (ph0 == SKEW_RESID) return unit ? NSM_PK(SKEW_RESID, true) : NSM_PK(SKEW_RESID, false);
+    return unit ? NSM_PK(SKEW_NONE, true) : NSM_PK(SKEW_NONE, false);
+#undef NSM_PK
 }
 
-int occupancy_fused(int ch, size_t smem) {
-    int per = 0;
-    auto f = [&](auto k) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreadsF, smem);
-    };
-    if (ch == 4) f(k_pgs_fused<4>);
-    else if (ch == 8) f(k_pgs_fused<8>);
-    else f(k_pgs_fused<16>);
-    return per;
+int sm_count_f() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
 }
+
+struct GeoF {
+    int nst = 0, per_sm = 0;
+    size_t smem = 0;
+};
+
+// stages: maximise resident consumer warps (<= 32 per SM, <= 4 CTAs), then depth
+GeoF geometry_f(const void *k, int64_t stage_bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int64_t>, GeoF> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(k, stage_bytes);
+    auto itc = cache.find(key);
+    if (itc != cache.end()) return itc->second;
+    GeoF g;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxF);
+    // experiment knobs (tools/skew_exp.py): cap stages / CTAs per SM
+    static const int max_nst = getenv("NSM_DEBUG_SKEW_NST") ? atoi(getenv("NSM_DEBUG_SKEW_NST")) : kMaxStages;
+    static const int max_per = getenv("NSM_DEBUG_SKEW_PERSM") ? atoi(getenv("NSM_DEBUG_SKEW_PERSM")) : 4;
+    int best = -1;
+    for (int nst = 2; nst <= std::min(kMaxStages, max_nst); ++nst) {
+        const int64_t smem = kHeader + nst * stage_bytes;
+        if (smem > kSmemMaxF) break;
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreadsF, (size_t)smem);
+        per = std::min(per, max_per);
+        const int warps = std::min(per * kTSF, 32);
+        if (per > 0 && warps >= best) {
+            best = warps;
+            g.nst = nst;
+            g.per_sm = per;
+            g.smem = (size_t)smem;
+        }
+    }
+    cache[key] = g;
+    return g;
+}
+
+int64_t pow2_at_least(int64_t v) {
+    int64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+inline int chunk_for(int maxw) { return maxw <= 4 ? 4 : (maxw <= 8 ? 8 : 16); }
 
 }  // namespace
 
-// ---- host side -----------------------------------------------------------------
-int fused_tile_rows() { return kRowsF; }
+int skew_tile_rows() { return kRowsF; }
 
-size_t fused_smem(int maxwL, int maxwU, int nst) {
-    const int64_t capL = (int64_t)kRowsF * std::max(maxwL, 1), capU = (int64_t)kRowsF * std::max(maxwU, 1);
-    return 256 + (size_t)nst * (capL + capU) * 12;
+// Shape of one launch (grid, stages, skew, rings); the same function sizes the
+// handle's buffers at setup (upper bound over k <= kmax) and each launch.
+SkewShape skew_shape(int ph0, bool unit, int maxw0, int maxw1, int maxwT, int k, int64_t n, int DT, int DA,
+                     int dw_override) {
+    SkewShape sh;
+    const int64_t cap0 = (int64_t)kRowsF * std::max({ph0 == SKEW_RESID ? maxw0 : 0, maxwT, 1});
+    const int64_t cap1 = ph0 == SKEW_RESID ? (int64_t)kRowsF * std::max(maxw1, 1) : 0;
+    const int ch = chunk_for(std::max({ph0 == SKEW_RESID ? std::max(maxw0, maxw1) : 0, maxwT}));
+    const void *kern = pick(ph0, unit, ch);
+    // staged vector segments: phase 0 dA, b, x; later phases dT, rhs, x, dn
+    const int nvec = ph0 == SKEW_RESID ? 3 : (unit ? 0 : 1) + 3;
+    const int64_t stage_bytes = ((cap0 + cap1) * 12 + nvec * kVecBytes + 127) / 128 * 128;
+    const GeoF g = geometry_f(kern, stage_bytes);
+    if (!g.nst) return sh;
+    sh.ok = true;
+    sh.kernel = kern;
+    sh.nst = g.nst;
+    sh.smem = g.smem;
+    sh.cap0 = cap0;
+    sh.cap1 = cap1;
+    sh.stage_bytes = stage_bytes;
+    sh.ntiles = (n + kRowsF - 1) / kRowsF;
+    sh.grid = (int)std::min<int64_t>((int64_t)sm_count_f() * g.per_sm, std::max<int64_t>(sh.ntiles, 1));
+    const int j0 = ph0 == SKEW_RESID ? 0 : 1;
+    const int units = k - j0 + 1;
+    // wait distance: two rounds of the grid (CTAs run their items in
+    // lockstep rounds; a wait blocks only on a CTA a full round behind)
+    (void)units;
+    sh.Dw = dw_override > 0 ? dw_override : 2 * sh.grid;
+    sh.D = sh.Dw + std::max(DT, ph0 == SKEW_RESID ? DA : 0);
+    sh.nitems = sh.ntiles + (int64_t)(k - j0) * sh.D;
+    const int64_t tiles_pow2 = pow2_at_least(std::max<int64_t>(sh.ntiles, 1));
+    sh.Mr = ph0 == SKEW_RESID ? std::min(pow2_at_least((int64_t)k * sh.D + sh.Dw), tiles_pow2) : 0;
+    sh.Mg = std::min(pow2_at_least((int64_t)sh.D + DT + sh.Dw), tiles_pow2);
+    return sh;
 }
 
-bool fused_ok(int maxwL, int maxwU) { return fused_smem(maxwL, maxwU, 2) <= 220 * 1024; }
-
-// Grid size (resident CTAs) for the persistent launch.
-int fused_grid(int maxwL, int maxwU) {
-    const int ch = std::max(maxwL, maxwU) <= 4 ? 4 : (std::max(maxwL, maxwU) <= 8 ? 8 : 16);
-    const size_t smem = fused_smem(maxwL, maxwU, 2);
-    int per = std::max(occupancy_fused(ch, smem), 1);
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms * per;
-}
-
-cudaError_t launch_pgs_fused(const FusedLaunch &f, cudaStream_t st) {
-    FusedParams p{};
-    p.n = f.n;
-    p.nslices = (f.n + kSlice - 1) / kSlice;
-    p.ntiles = (f.n + kRowsF - 1) / kRowsF;
-    if (p.ntiles == 0) return cudaSuccess;
-    p.L = view(*f.L);
-    p.U = view(*f.U);
-    p.d = f.d;
-    p.b = f.b;
-    p.x = f.x;
-    p.k = f.k;
-    p.DL = f.DL;
-    p.DU = f.DU;
-    p.M = f.M;
-    p.ring = f.ring;
-    p.counter = f.sync;
-    p.prog = (int *)(f.sync + 64);
-    p.wb = p.prog + p.ntiles;
-    p.flag = f.flag;
-    p.sweep_id0 = f.sweep_id0;
-    p.err = f.err;
-    p.timeout_ns = f.timeout_ns;
-    p.nst = 2;
-    if (const char *e = getenv("NSM_FUSED_NST")) p.nst = std::max(1, atoi(e));  // DEBUG experiment
-    p.capL = (int64_t)kRowsF * std::max(f.L->maxw, 1);
-    p.capU = (int64_t)kRowsF * std::max(f.U->maxw, 1);
-    // reset the dispenser and the progress flags
-    cudaError_t e = cudaMemsetAsync(f.sync, 0, (64 + 2 * (size_t)p.ntiles) * sizeof(int), st);
-    if (e != cudaSuccess) return e;
-    const size_t smem = fused_smem(f.L->maxw, f.U->maxw, p.nst);
-    int grid = (int)std::min<int64_t>(f.grid, p.ntiles);
-    if (const char *e = getenv("NSM_FUSED_GRID_DIV")) grid = std::max(1, grid / std::max(1, atoi(e)));  // DEBUG
-    const int mw = std::max(f.L->maxw, f.U->maxw);
-    e = mw <= 4 ? fused_launch<4>(p, smem, grid, st)
-                : (mw <= 8 ? fused_launch<8>(p, smem, grid, st) : fused_launch<16>(p, smem, grid, st));
-    if (e != cudaSuccess) return e;
-    const int64_t w0 = std::max<int64_t>(0, p.ntiles - p.DL - 1);
-    const int64_t rows = std::min<int64_t>(f.n - w0 * kRowsF, (p.ntiles - w0) * kRowsF);
-    if (rows > 0)
-        k_fused_tail<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(f.n, w0, p.ntiles, p.M,
-                                                                     f.ring + (int64_t)p.k * p.M * kRowsF, f.x);
-    return cudaGetLastError();
+cudaError_t launch_skew(const SkewLaunch &L, cudaStream_t st) {
+    const SkewShape &sh = L.shape;
+    if (!sh.ok) return cudaErrorInvalidConfiguration;
+    if (L.n == 0) return cudaSuccess;
+    SkewParams p{};
+    p.n = L.n;
+    p.nslices = (L.n + kSlice - 1) / kSlice;
+    p.ntiles = sh.ntiles;
+    p.nitems = sh.nitems;
+    p.desc = L.desc;
+    p.k = L.k;
+    p.j0 = L.ph0 == SKEW_RESID ? 0 : 1;
+    p.D = sh.D;
+    p.Dw = sh.Dw;
+    p.epi = L.epi;
+    p.scaled_g0 = L.scaled_g0;
+    if (L.A0) p.A0 = view(*L.A0);
+    if (L.A1) p.A1 = view(*L.A1);
+    p.T = view(*L.T);
+    p.dA = L.dA;
+    p.b = L.b;
+    p.xin = L.xin;
+    p.dT = L.dT;
+    p.rhs = L.rhs;
+    p.g0 = L.g0;
+    p.x = L.x;
+    p.out1 = L.out1;
+    p.out2 = L.out2;
+    p.dn = L.dn;
+    p.ring_r = L.ring_r;
+    p.ring_g = L.ring_g;
+    p.rmask = sh.Mr * kRowsF - 1;
+    p.gmask = sh.Mg * kRowsF - 1;
+    p.gstride = sh.Mg * kRowsF;
+    p.flag = L.flag;
+    p.sweep_id0 = L.sweep_id0;
+    p.err = L.err;
+    p.timeout_ns = L.timeout_ns;
+    p.sync = L.sync;
+    p.prog = L.prog;
+    p.nst = sh.nst;
+    p.keep0 = L.keep0;
+    p.keep1 = L.keep1;
+    p.cap0 = sh.cap0;
+    p.cap1 = sh.cap1;
+    p.stage_bytes = sh.stage_bytes;
+    // vector segments go through the bulk-copy engine when 16-byte aligned
+    auto al = [](const void *q) { return q == nullptr || ((uintptr_t)q & 15) == 0; };
+    p.trace = L.trace;
+    p.vec_bulk = al(p.dA) && al(p.b) && al(p.xin) && al(p.dT) && al(p.rhs) && al(p.x) && al(p.dn);
+    static const bool novec = getenv("NSM_DEBUG_SKEW_NOVEC") != nullptr;  // experiment knob
+    if (novec) p.vec_bulk = 0;
+    void *args[] = {&p};
+    // cooperative: all CTAs co-resident (the item schedule relies on it)
+    return cudaLaunchCooperativeKernel(sh.kernel, dim3((unsigned)sh.grid), dim3(kThreadsF), args, sh.smem, st);
 }
 
 void preload_fused_kernels() {
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, k_pgs_fused<4>);
-    cudaFuncGetAttributes(&a, k_pgs_fused<8>);
-    cudaFuncGetAttributes(&a, k_pgs_fused<16>);
-    cudaFuncGetAttributes(&a, k_fused_tail);
+    for (int ph0 : {SKEW_RESID, SKEW_NONE})
+        for (bool unit : {false, true})
+            for (int ch : {4, 8, 16}) cudaFuncGetAttributes(&a, pick(ph0, unit, ch));
 }
 
 }  // namespace nsm

@@ -126,27 +126,55 @@ cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_
                                 double *out2, bool pdl, cudaStream_t st);
 cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st);
 
-// ---- fused one-pass pGS application (fused.cu) ---------------------------------
-struct FusedLaunch {
+// ---- phase-skewed fused passes (fused.cu) ---------------------------------------
+enum { SKEW_RESID = 0, SKEW_NONE = 1 };  // phase 0 = residual r = b - A x; none (rhs, g(0) given)
+enum { SKEW_STORE = 0, SKEW_XADD = 1, SKEW_STORE2 = 2, SKEW_XADD_SCALE = 3, SKEW_STORE_SCALE = 4 };
+
+// Launch state in device memory (zeroed at setup except epoch = 1; reset by
+// the last CTA of every launch).
+struct SkewSync {
+    unsigned long long ctr, wmark;  // (reserved)
+    unsigned int epoch;         // tag of the progress counters in the current launch
+    unsigned int exits;         // CTAs finished
+    unsigned long long waits;   // statistics (cumulative, nsm_fused_stats): item waits that had to spin,
+    unsigned long long wait_ns; //   and their total spin time
+};
+
+struct SkewShape {
+    bool ok = false;
+    const void *kernel = nullptr;
+    int nst = 0, grid = 0, D = 0, Dw = 0;
+    size_t smem = 0;
+    int64_t cap0 = 0, cap1 = 0, stage_bytes = 0, ntiles = 0, nitems = 0;
+    int64_t Mr = 0, Mg = 0;     // ring lengths in tiles (powers of two)
+};
+
+// ph0 = SKEW_RESID: maxw0 / maxw1 = widths of A's strict lower / upper parts;
+// DT = bandwidth of the swept triangle in tiles, DA = A's (for the in-place x);
+// dw_override > 0 replaces the automatic wait distance (tests).
+SkewShape skew_shape(int ph0, bool unit, int maxw0, int maxw1, int maxwT, int k, int64_t n, int DT, int DA,
+                     int dw_override);
+int skew_tile_rows();
+
+struct SkewLaunch {
+    SkewShape shape;
     int64_t n;
-    const Sell *L, *U;
-    const double *d, *b;
-    double *x;
-    int k;
-    int DL, DU;              // dependency distances in tiles of fused_tile_rows() rows
-    int64_t M;               // ring length in tiles
-    double *ring;            // (k + 1) * M * tile_rows doubles
-    unsigned int *sync;      // 64 + 2 * ntiles ints: dispenser, progress, write-back flags
-    int grid;
+    int ph0, desc, k, epi, scaled_g0, keep0, keep1;
+    const Sell *A0, *A1, *T;
+    const double *dA, *b, *xin;     // phase 0
+    const double *dT, *rhs, *g0;    // sweeps (rhs, g0: full vectors when ph0 = SKEW_NONE)
+    double *x, *out1, *out2;
+    const double *dn;
+    double *ring_r, *ring_g;
     unsigned long long *flag;
     int64_t sweep_id0;
     unsigned int *err;
     unsigned long long timeout_ns;
+    SkewSync *sync;
+    unsigned long long *prog;       // >= grid per-CTA progress counters (zeroed at setup)
+    unsigned long long *trace;      // debug timestamps or nullptr
 };
-int fused_tile_rows();
-bool fused_ok(int maxwL, int maxwU);
-int fused_grid(int maxwL, int maxwU);
-cudaError_t launch_pgs_fused(const FusedLaunch &f, cudaStream_t st);
+cudaError_t launch_skew(const SkewLaunch &L, cudaStream_t st);
 void preload_fused_kernels();
 
 // Force-load every kernel of the library (see kernels.cu "eager loading").

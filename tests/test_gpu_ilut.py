@@ -36,12 +36,14 @@ def test_ruiz_ilu_smooth_bitwise(mat, kl, ku, fresh):
     S = nsm.Smoother(A, Fr)
     try:
         S.set_ruiz(sr, sc)
-        for pipe in (True, False):
-            S.set_pipeline(pipe)
+        for mode in ("fused", "fusedw1", "pipelined", "plain"):
+            S.set_pipeline(mode != "plain")
+            S.set_fused(1 if mode.startswith("fused") else 0)
+            S.set_fused_window(1 if mode == "fusedw1" else 0)
             x = dev(np.full(n, np.nan) if fresh else x0)
             S.smooth(dev(b), x, "ilu", 2, kl, ku, x_is_zero=fresh)
             got = x.cpu().numpy()
-            assert np.array_equal(got, want), (mat, kl, ku, fresh, pipe, np.max(np.abs(got - want)))
+            assert np.array_equal(got, want), (mat, kl, ku, fresh, mode, np.max(np.abs(got - want)))
         S.check()
     finally:
         S.close()
@@ -57,8 +59,10 @@ def test_ilut_factors_unscaled_bitwise(mat):
     want = oracle.ilu_apply(A, (F.rowptr, F.col, F.val), b, x0, 3, 3, nu=1)
     S = nsm.Smoother(A, F)
     try:
-        x = dev(x0)
-        S.smooth(dev(b), x, "ilu", 1, 3, 3)
-        assert np.array_equal(x.cpu().numpy(), want)
+        for fused in (1, 0):
+            S.set_fused(fused)
+            x = dev(x0)
+            S.smooth(dev(b), x, "ilu", 1, 3, 3)
+            assert np.array_equal(x.cpu().numpy(), want), f"fused={fused}"
     finally:
         S.close()

@@ -70,14 +70,18 @@ SMALL = {
 }
 
 
-KERNELS = ("fused", "pipelined", "plain")
+KERNELS = ("fused", "fusedw1", "pipelined", "plain")
 
 
 def set_kernels(S, mode):
-    """fused: one-pass wavefront pGS + pipelined kernels (default); pipelined:
-    one cp.async.bulk pipelined kernel per pass; plain: register-blocked."""
+    """fused: phase-skewed fused passes wherever possible (pGS one pass, ILU
+    two) + pipelined kernels; fusedw1: the same with wait distance 1 (every
+    item waits for its predecessor, rings wrap after a few tiles: stresses the
+    synchronisation); pipelined: one cp.async.bulk pipelined kernel per pass;
+    plain: register-blocked."""
     S.set_pipeline(mode != "plain")
-    S.set_fused(mode == "fused")
+    S.set_fused(1 if mode.startswith("fused") else 0)
+    S.set_fused_window(1 if mode == "fusedw1" else 0)
 
 
 @pytest.fixture(scope="module", params=[(c, p) for c in SMALL for p in KERNELS], ids=lambda v: f"{v[0]}-{v[1]}")
