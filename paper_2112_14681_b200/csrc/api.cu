@@ -796,7 +796,7 @@ static nsm_status skew_run(nsm_handle *h, SkewLaunch &L, bool unit, int DT, int 
                          h->skew_dw);
     const SkewShape &sh = L.shape;
     if (!sh.ok || sh.Mr > h->ring_r_tiles || sh.Mg > h->ring_g_tiles || sh.grid > 4096) return NSM_OK;
-    if (h->fused_mode == 2 && sh.ntiles < 2 * (int64_t)sh.D) return NSM_OK;
+    if (h->fused_mode == 2 && sh.nbig < 2 * (int64_t)sh.D) return NSM_OK;
     L.n = h->n;
     if (unit) L.dT = nullptr;
     L.ring_r = h->ring_r;

@@ -88,6 +88,8 @@ constexpr int64_t kVecBytes = (int64_t)kRowsF * 8;
 
 struct SkewParams {
     int64_t n, nslices, ntiles, nitems;
+    int64_t nbig;             // scheduling tiles of B x 256 rows (items, D, rings count these)
+    int B;
     int desc;                 // walk tiles top-down (logical tile u = physical ntiles-1-u)
     int k, j0, D, Dw;         // sweeps; first phase (0: residual, 1: none); skew; wait distance
     int epi, scaled_g0, vec_bulk;
@@ -234,12 +236,16 @@ __device__ __forceinline__ int64_t read_frontier(const SkewParams &p, unsigned i
 
 // One unit: phase j of logical tile u, slice `warp`, row `lane`.  Row, slice
 // and ring indices are 32-bit (a rank holds < 2^31 rows: columns are int32).
+// The stage is released (empty barrier) as soon as its shared-memory data is
+// consumed, before the results are stored.
 template <int PH0, bool UNIT, int CH>
-__device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, int64_t w, int j, int warp,
+__device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, int tp, int j, int warp,
                                          int lane) {
     char *stg = stage_ptr(sm, p, st);
-    const int u = (int)(w - (int64_t)(j - p.j0) * p.D);
-    const int tp = p.desc ? (int)p.ntiles - 1 - u : u;
+    auto release_stage = [&]() {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(empty_bar(sm) + st);
+    };
     const int s = tp * kTSF + warp;
     const bool has = s < (int)p.nslices;
     const int i = s * kSlice + lane;
@@ -283,6 +289,7 @@ __device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, 
                 acc = c.add(acc, gx);
             }
         }
+        release_stage();
         if (row) {
             const double r = __dsub_rn(bi, acc);
             p.ring_r[(uint32_t)i & rmask] = r;
@@ -314,6 +321,7 @@ __device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, 
             acc = tri_sum<CH>(v0, c0, it, lane, GRing{p.ring_g + (int64_t)(j - 1) * p.gstride, gmask});
         }
     }
+    release_stage();
     if (!row) return;
     double v = __dsub_rn(ri, acc);
     if (!UNIT) v = __ddiv_rn(v, di);
@@ -347,7 +355,7 @@ struct UnitGen {
     __device__ __forceinline__ void init(const SkewParams &p, bool skip) {
         G = gridDim.x;
         w = blockIdx.x;
-        T = p.ntiles;
+        T = p.nbig;
         D = p.D;
         nitems = p.nitems;
         nph = p.k - p.j0;
@@ -395,10 +403,7 @@ struct UnitGen {
 
 // Slice pointers of a unit's parts: lanes 0..8 part 0, lanes 16..24 part 1.
 template <int PH0>
-__device__ __forceinline__ int64_t unit_ptrs(const SkewParams &p, int64_t w, int64_t q, int lane) {
-    const int j = p.j0 + (int)q;
-    const int64_t u = w - q * p.D;
-    const int64_t tp = p.desc ? p.ntiles - 1 - u : u;
+__device__ __forceinline__ int64_t unit_ptrs(const SkewParams &p, int64_t tp, int j, int lane) {
     const int64_t s0 = tp * kTSF, s1 = min(s0 + kTSF, p.nslices);
     const bool ph0 = PH0 == SKEW_RESID && j == 0;
     int64_t pv = 0;
@@ -410,15 +415,12 @@ __device__ __forceinline__ int64_t unit_ptrs(const SkewParams &p, int64_t w, int
 constexpr int kPre = 4;  // units whose slice pointers the producer has in flight
 
 template <int PH0, bool UNIT>
-__device__ __forceinline__ void stage_unit(const SkewParams &p, char *sm, int it, int64_t w, int64_t q, int64_t pv,
+__device__ __forceinline__ void stage_unit(const SkewParams &p, char *sm, int it, int64_t tp, int j, int64_t pv,
                                            uint64_t pol_first, uint64_t pol_keep, int lane) {
     const int st = it % p.nst;
     if (lane == 0) trace_at(p, 1, it, 0);
     if (it >= p.nst) ptx::mbar_wait(empty_bar(sm) + st, ((uint32_t)(it / p.nst) - 1) & 1);
     if (lane == 0) trace_at(p, 1, it, 1);
-    const int j = p.j0 + (int)q;
-    const int64_t u = w - q * p.D;
-    const int64_t tp = p.desc ? p.ntiles - 1 - u : u;
     const bool ph0 = PH0 == SKEW_RESID && j == 0;
     const SellView &P0 = ph0 ? p.A0 : p.T;
     const int64_t pnext = __shfl_down_sync(0xffffffffu, pv, 1);
@@ -460,32 +462,57 @@ __device__ __forceinline__ void stage_unit(const SkewParams &p, char *sm, int it
 
 // Producer: walks the unit sequence with the slice pointers of the next kPre
 // units already loading (their latency would otherwise serialise every unit).
+// Sub-unit walk: each unit (w, q) covers big tile u = w - qD, i.e. the
+// 256-row tiles u B .. u B + B - 1 (those < ntiles), in that order.
+struct SubGen {
+    UnitGen g;
+    int b;
+    __device__ __forceinline__ int64_t tile(const SkewParams &p) const {
+        const int64_t t = (g.w - g.q * p.D) * p.B + b;
+        return p.desc ? p.ntiles - 1 - t : t;
+    }
+    __device__ __forceinline__ int j(const SkewParams &p) const { return p.j0 + (int)g.q; }
+    __device__ __forceinline__ void init(const SkewParams &p) {
+        g.init(p, true);
+        b = 0;
+    }
+    __device__ __forceinline__ void next(const SkewParams &p) {
+        ++b;
+        if (b < p.B && (g.w - g.q * p.D) * p.B + b < p.ntiles) return;
+        b = 0;
+        g.next();
+    }
+};
+
+// Producer: walks the sub-unit sequence with the slice pointers of the next
+// kPre sub-units already loading (their latency would otherwise serialise
+// every unit).
 template <int PH0, bool UNIT>
 __device__ __forceinline__ void produce(const SkewParams &p, char *sm, int lane) {
     const uint64_t pol_first = ptx::policy_evict_first(), pol_keep = ptx::policy_evict_normal();
-    UnitGen gen;
-    gen.init(p, true);
-    int64_t pw[kPre], pq[kPre], pv[kPre];
+    SubGen gen;
+    gen.init(p);
+    int64_t ptp[kPre], pv[kPre];
+    int pj[kPre];
     bool ok[kPre];
 #pragma unroll
     for (int k = 0; k < kPre; ++k) {
-        ok[k] = gen.valid;
-        pw[k] = gen.w;
-        pq[k] = gen.q;
-        pv[k] = ok[k] ? unit_ptrs<PH0>(p, pw[k], pq[k], lane) : 0;
-        if (gen.valid) gen.next();
+        ok[k] = gen.g.valid;
+        ptp[k] = ok[k] ? gen.tile(p) : 0;
+        pj[k] = gen.j(p);
+        pv[k] = ok[k] ? unit_ptrs<PH0>(p, ptp[k], pj[k], lane) : 0;
+        if (gen.g.valid) gen.next(p);
     }
     for (int it = 0; ok[0]; it += kPre) {
 #pragma unroll
         for (int k = 0; k < kPre; ++k) {
             if (!ok[k]) break;
-            stage_unit<PH0, UNIT>(p, sm, it + k, pw[k], pq[k], pv[k], pol_first, pol_keep, lane);
-            // refill slot k with the unit kPre ahead
-            ok[k] = gen.valid;
-            pw[k] = gen.w;
-            pq[k] = gen.q;
-            pv[k] = ok[k] ? unit_ptrs<PH0>(p, pw[k], pq[k], lane) : 0;
-            if (gen.valid) gen.next();
+            stage_unit<PH0, UNIT>(p, sm, it + k, ptp[k], pj[k], pv[k], pol_first, pol_keep, lane);
+            ok[k] = gen.g.valid;
+            ptp[k] = ok[k] ? gen.tile(p) : 0;
+            pj[k] = gen.j(p);
+            pv[k] = ok[k] ? unit_ptrs<PH0>(p, ptp[k], pj[k], lane) : 0;
+            if (gen.g.valid) gen.next(p);
         }
     }
 }
@@ -582,16 +609,17 @@ __global__ void __launch_bounds__(kThreadsF, CH <= 4 ? 3 : (CH <= 8 ? 2 : 1)) k_
                 }
                 ptx::mbar_wait(rb, par);
             }
-            for (int64_t q = qa; q <= qb; ++q, ++it) {
-                const int st = it % p.nst;
-                if (warp == 0 && lane == 0) trace_at(p, 0, it, 0);
-                ptx::mbar_wait(full_bar(sm) + st, (uint32_t)(it / p.nst) & 1);
-                if (warp == 0 && lane == 0) trace_at(p, 0, it, 1);
-                run_unit<PH0, UNIT, CH>(p, sm, st, w, p.j0 + (int)q, warp, lane);
-                __syncwarp();
-                if (warp == 0 && lane == 0) trace_at(p, 0, it, 2);
-                if (lane == 0) ptx::mbar_arrive(empty_bar(sm) + st);
-                if (warp == 0 && lane == 0) trace_at(p, 0, it, 3);
+            for (int64_t q = qa; q <= qb; ++q) {
+                const int64_t t0 = (w - q * p.D) * p.B;
+                for (int b = 0; b < p.B && t0 + b < p.ntiles; ++b, ++it) {
+                    const int st = it % p.nst;
+                    const int tp = (int)(p.desc ? p.ntiles - 1 - (t0 + b) : t0 + b);
+                    if (warp == 0 && lane == 0) trace_at(p, 0, it, 0);
+                    ptx::mbar_wait(full_bar(sm) + st, (uint32_t)(it / p.nst) & 1);
+                    if (warp == 0 && lane == 0) trace_at(p, 0, it, 1);
+                    run_unit<PH0, UNIT, CH>(p, sm, st, tp, p.j0 + (int)q, warp, lane);
+                    if (warp == 0 && lane == 0) trace_at(p, 0, it, 2);
+                }
             }
             __syncwarp();
             if (lane == 0) {
@@ -720,18 +748,25 @@ SkewShape skew_shape(int ph0, bool unit, int maxw0, int maxw1, int maxwT, int k,
     sh.cap1 = cap1;
     sh.stage_bytes = stage_bytes;
     sh.ntiles = (n + kRowsF - 1) / kRowsF;
-    sh.grid = (int)std::min<int64_t>((int64_t)sm_count_f() * g.per_sm, std::max<int64_t>(sh.ntiles, 1));
+    // B consecutive 256-row tiles per scheduling tile: the per-item
+    // synchronisation is paid once per B tiles of every phase
+    static const int env_b = getenv("NSM_DEBUG_SKEW_B") ? atoi(getenv("NSM_DEBUG_SKEW_B")) : 0;
+    int B = env_b > 0 ? env_b : 8;
+    while (B > 1 && (B & (B - 1))) --B;  // power of two (ring masks)
+    sh.B = B;
+    sh.nbig = (sh.ntiles + B - 1) / B;
+    sh.grid = (int)std::min<int64_t>((int64_t)sm_count_f() * g.per_sm, std::max<int64_t>(sh.nbig, 1));
     const int j0 = ph0 == SKEW_RESID ? 0 : 1;
-    const int units = k - j0 + 1;
+    const int DTb = (DT + B - 1) / B, DAb = (DA + B - 1) / B;
     // wait distance: two rounds of the grid (CTAs run their items in
     // lockstep rounds; a wait blocks only on a CTA a full round behind)
-    (void)units;
     sh.Dw = dw_override > 0 ? dw_override : 2 * sh.grid;
-    sh.D = sh.Dw + std::max(DT, ph0 == SKEW_RESID ? DA : 0);
-    sh.nitems = sh.ntiles + (int64_t)(k - j0) * sh.D;
-    const int64_t tiles_pow2 = pow2_at_least(std::max<int64_t>(sh.ntiles, 1));
-    sh.Mr = ph0 == SKEW_RESID ? std::min(pow2_at_least((int64_t)k * sh.D + sh.Dw), tiles_pow2) : 0;
-    sh.Mg = std::min(pow2_at_least((int64_t)sh.D + DT + sh.Dw), tiles_pow2);
+    sh.D = sh.Dw + std::max(DTb, ph0 == SKEW_RESID ? DAb : 0);
+    sh.nitems = sh.nbig + (int64_t)(k - j0) * sh.D;
+    const int64_t big_pow2 = pow2_at_least(std::max<int64_t>(sh.nbig, 1));
+    // ring lengths, reported in 256-row tiles
+    sh.Mr = ph0 == SKEW_RESID ? std::min(pow2_at_least((int64_t)k * sh.D + sh.Dw), big_pow2) * B : 0;
+    sh.Mg = std::min(pow2_at_least((int64_t)sh.D + DTb + sh.Dw), big_pow2) * B;
     return sh;
 }
 
@@ -744,6 +779,8 @@ cudaError_t launch_skew(const SkewLaunch &L, cudaStream_t st) {
     p.nslices = (L.n + kSlice - 1) / kSlice;
     p.ntiles = sh.ntiles;
     p.nitems = sh.nitems;
+    p.nbig = sh.nbig;
+    p.B = sh.B;
     p.desc = L.desc;
     p.k = L.k;
     p.j0 = L.ph0 == SKEW_RESID ? 0 : 1;

@@ -146,7 +146,9 @@ struct SkewShape {
     int nst = 0, grid = 0, D = 0, Dw = 0;
     size_t smem = 0;
     int64_t cap0 = 0, cap1 = 0, stage_bytes = 0, ntiles = 0, nitems = 0;
-    int64_t Mr = 0, Mg = 0;     // ring lengths in tiles (powers of two)
+    int64_t Mr = 0, Mg = 0;     // ring lengths in 256-row tiles (powers of two)
+    int B = 1;                  // 256-row tiles per scheduling tile
+    int64_t nbig = 0;           // scheduling tiles
 };
 
 // ph0 = SKEW_RESID: maxw0 / maxw1 = widths of A's strict lower / upper parts;
