@@ -419,7 +419,7 @@ __device__ __forceinline__ void stage_unit(const SkewParams &p, char *sm, int it
                                            uint64_t pol_first, uint64_t pol_keep, int lane) {
     const int st = it % p.nst;
     if (lane == 0) trace_at(p, 1, it, 0);
-    if (it >= p.nst) ptx::mbar_wait(empty_bar(sm) + st, ((uint32_t)(it / p.nst) - 1) & 1);
+    if (it >= p.nst) ptx::mbar_wait_sleep(empty_bar(sm) + st, ((uint32_t)(it / p.nst) - 1) & 1);
     if (lane == 0) trace_at(p, 1, it, 1);
     const bool ph0 = PH0 == SKEW_RESID && j == 0;
     const SellView &P0 = ph0 ? p.A0 : p.T;
@@ -530,7 +530,7 @@ __device__ __forceinline__ void sync_role(const SkewParams &p, char *sm, unsigne
     for (int64_t m = 0; m < nmine; ++m) {
         if (m >= kSlots - 1) {
             const int64_t mo = m - (kSlots - 1);  // slot reuse: that item is finished here
-            ptx::mbar_wait(idone_bar(sm) + (mo % kSlots), (uint32_t)(mo / kSlots) & 1);
+            ptx::mbar_wait_sleep(idone_bar(sm) + (mo % kSlots), (uint32_t)(mo / kSlots) & 1);
         }
         const int64_t tgt = c + m * G - p.Dw;
         if (tgt >= F) {
@@ -601,13 +601,13 @@ __global__ void __launch_bounds__(kThreadsF, CH <= 4 ? 3 : (CH <= 8 ? 2 : 1)) k_
                 const uint32_t par = (uint32_t)(m / kSlots) & 1;
                 if (warp == 0 && !ptx::mbar_test(rb, par)) {  // statistics: consumers stalled on readiness
                     const uint64_t t0 = ptx::globaltimer_ns();
-                    ptx::mbar_wait(rb, par);
+                    ptx::mbar_wait_sleep(rb, par);
                     if (lane == 0) {
                         atomicAdd(&p.sync->waits, 1ull);
                         atomicAdd(&p.sync->wait_ns, ptx::globaltimer_ns() - t0);
                     }
                 }
-                ptx::mbar_wait(rb, par);
+                ptx::mbar_wait_sleep(rb, par);
             }
             for (int64_t q = qa; q <= qb; ++q) {
                 const int64_t t0 = (w - q * p.D) * p.B;
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kThreadsF, CH <= 4 ? 3 : (CH <= 8 ? 2 : 1)) k_
                     const int st = it % p.nst;
                     const int tp = (int)(p.desc ? p.ntiles - 1 - (t0 + b) : t0 + b);
                     if (warp == 0 && lane == 0) trace_at(p, 0, it, 0);
-                    ptx::mbar_wait(full_bar(sm) + st, (uint32_t)(it / p.nst) & 1);
+                    ptx::mbar_wait_sleep(full_bar(sm) + st, (uint32_t)(it / p.nst) & 1);
                     if (warp == 0 && lane == 0) trace_at(p, 0, it, 1);
                     run_unit<PH0, UNIT, CH>(p, sm, st, tp, p.j0 + (int)q, warp, lane);
                     if (warp == 0 && lane == 0) trace_at(p, 0, it, 2);

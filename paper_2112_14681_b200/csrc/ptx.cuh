@@ -32,6 +32,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// blocking wait with a suspend-time hint: the waiting warp sleeps in hardware
+// (until the phase completes or the hint expires) instead of spinning on
+// try_wait, leaving issue slots to the warps doing work
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
 // one try_wait: returns when the phase completes or a hardware time limit passes
 __device__ __forceinline__ uint32_t mbar_try(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
