@@ -49,6 +49,7 @@ def _L():
         _lib.orc_pgs_backward_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, ci, ci, vp]
         _lib.orc_l1_jacobi_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci]
         _lib.orc_ilu0.argtypes = [i64, vp, vp, vp, vp]
+        _lib.orc_ilu0_fixed_point.argtypes = [i64, vp, vp, vp, ci, vp]
         _lib.orc_ilu_apply.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci, ci, ci, ci, ci, vp]
     return _lib
 
@@ -176,6 +177,15 @@ def ilu0(A):
     n, rp, ci, va = _csr(A)
     w = np.empty_like(va)
     _check(_L().orc_ilu0(n, _p(rp), _p(ci), _p(va), _p(w)), "ilu0")
+    return rp, ci, w
+
+
+def ilu0_fixed_point(A, sweeps):
+    """Chow-Patel fixed-point ILU(0) after `sweeps` synchronous sweeps (reading
+    R19); (rowptr, col, val) on A's pattern, the ilu0 layout."""
+    n, rp, ci, va = _csr(A)
+    w = np.empty_like(va)
+    _check(_L().orc_ilu0_fixed_point(n, _p(rp), _p(ci), _p(va), int(sweeps), _p(w)), "ilu0_fixed_point")
     return rp, ci, w
 
 

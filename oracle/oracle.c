@@ -279,6 +279,70 @@ int orc_ilu0(i64 n, const i64 *rp, const i64 *ci, const double *va, double *w) {
 }
 
 /*
+ * Chow-Patel fixed-point ILU(0) — the set-up algorithm the paper names as
+ * future work ("fixed-point iteration algorithms of Chow and
+ * Patel [Chow2015] ... to compute the ILU(0) ... factorizations").  The paper
+ * does not restate it; this is the standard definition (reading R19):
+ * the ILU(0) factors are the solution of the nonlinear equations
+ *     (L U)_ij = a_ij   for every (i,j) in S = pattern(A),  L unit lower,
+ * written as the fixed point
+ *     l_ij = ( a_ij - sum_{k<j} l_ik u_kj ) / u_jj     (i > j)
+ *     u_ij =   a_ij - sum_{k<i} l_ik u_kj              (i <= j)
+ * (sums over k with (i,k), (k,j) in S, ascending k, one subtraction each) and
+ * iterated SYNCHRONOUSLY: every entry of sweep s+1 uses only sweep-s values.
+ * Initial guess (reading R19): l_ij = a_ij / a_jj, u_ij = a_ij.
+ * Output layout as orc_ilu0 (strict lower = L_s, upper incl. diagonal = U).
+ * Pinned in tests/test_oracle_chow_patel.py: n sweeps reproduce orc_ilu0
+ * (Saad's IKJ ILU(0)) bit for bit; the 1-D closed form becomes exact one
+ * entry per sweep.
+ */
+int orc_ilu0_fixed_point(i64 n, const i64 *rp, const i64 *ci, const double *va, int sweeps, double *w) {
+    i64 nnz = rp[n];
+    i64 *dpos = (i64 *)malloc((size_t)(n > 0 ? n : 1) * sizeof(i64));
+    double *old = (double *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(double));
+    if (!dpos || !old) { free(dpos); free(old); return -1; }
+    for (i64 i = 0; i < n; ++i) {
+        dpos[i] = -1;
+        for (i64 p = rp[i]; p < rp[i + 1]; ++p) if (ci[p] == i) dpos[i] = p;
+        if (dpos[i] < 0 || va[dpos[i]] == 0.0) { free(dpos); free(old); return (int)(-(2 + i)); }
+    }
+    /* initial guess */
+    for (i64 i = 0; i < n; ++i)
+        for (i64 p = rp[i]; p < rp[i + 1]; ++p) {
+            i64 j = ci[p];
+            w[p] = (j < i) ? va[p] / va[dpos[j]] : va[p];
+        }
+    int rc = 0;
+    for (int s = 0; s < sweeps && rc == 0; ++s) {
+        memcpy(old, w, (size_t)nnz * sizeof(double));
+        for (i64 i = 0; i < n && rc == 0; ++i) {
+            for (i64 p = rp[i]; p < rp[i + 1]; ++p) {
+                i64 j = ci[p];
+                i64 m = j < i ? j : i;          /* k < min(i, j) */
+                double sum = va[p];
+                for (i64 q = rp[i]; q < rp[i + 1]; ++q) {
+                    i64 k = ci[q];              /* l_ik, ascending k */
+                    if (k >= m) break;
+                    for (i64 t = rp[k]; t < rp[k + 1]; ++t) {  /* u_kj, if (k,j) in S */
+                        if (ci[t] == j) { sum = sum - old[q] * old[t]; break; }
+                        if (ci[t] > j) break;
+                    }
+                }
+                if (j < i) {
+                    double ujj = old[dpos[j]];
+                    if (ujj == 0.0) { rc = (int)(-(2 + j)); break; }
+                    w[p] = sum / ujj;
+                } else {
+                    w[p] = sum;
+                }
+            }
+        }
+    }
+    free(dpos); free(old);
+    return rc;
+}
+
+/*
  * ILU smoother with Jacobi-iterated triangular solves, nu outer iterations
  * (Algorithm 2, with LDU row scaling of U in place of Ruiz,
  * P:L1012-1013):
