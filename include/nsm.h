@@ -130,6 +130,24 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
 nsm_status nsm_ilu0(const nsm_csr *A, int64_t row_begin, double *fval);
 
 /*
+ * nsm_ilu0_fixed_point — ILU(0) factor values computed ON THE GPU by
+ * Chow-Patel fixed-point sweeps (the set-up algorithm the paper plans for
+ * reducing C-AMG set-up cost; reading
+ * R19).  The factors solve (LU)_ij = a_ij on pattern(A) (L unit lower); each
+ * synchronous sweep updates every entry from the previous sweep,
+ *   l_ij = (a_ij - sum_{k<j} l_ik u_kj) / u_jj,   u_ij = a_ij - sum_{k<i} l_ik u_kj,
+ * starting from l_ij = a_ij / a_jj, u_ij = a_ij.  `sweeps` = 0 returns that
+ * initial guess; once `sweeps` reaches the dependency depth of the pattern
+ * the result equals nsm_ilu0 bit for bit (same operations, same order); a
+ * few sweeps give the approximate factors Chow and Patel use.  A is HOST CSR,
+ * fval (length nnz(A), caller-allocated HOST memory) receives the values in
+ * nsm_ilu0's layout (row_begin / off-block entries as there).  Runs on
+ * `device`, synchronous.  Missing or zero diagonal, or a zero u_jj during the
+ * sweeps -> NSM_ERR_ZERO_DIAG; unsorted columns -> NSM_ERR_PATTERN.
+ */
+nsm_status nsm_ilu0_fixed_point(const nsm_csr *A, int64_t row_begin, int sweeps, double *fval, int device);
+
+/*
  * nsm_ilut — ILUT(droptol, lfil) factorisation on the host (Saad's
  * dual-threshold ILU, "Compute A ~ LU with droptol and lfill imposed", Alg. 2
  * P:L1024-1025; single rank).  Row i: pivots eliminated in ascending column

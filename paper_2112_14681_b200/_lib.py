@@ -18,7 +18,7 @@ _STATUS = {0: "NSM_OK", 1: "NSM_ERR_ARG", 2: "NSM_ERR_PATTERN", 3: "NSM_ERR_ZERO
            5: "NSM_ERR_CUDA", 6: "NSM_ERR_OOM", 7: "NSM_ERR_STATE", 8: "NSM_ERR_DIST"}
 
 # every symbol include/nsm.h declares (tests check the .so exports them)
-SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_spmv",
+SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_spmv",
                   "nsm_check", "nsm_info", "nsm_stats", "nsm_last_error", "nsm_destroy", "nsm_halo_plan",
                   "nsm_halo_set_send", "nsm_halo_mailbox", "nsm_halo_connect_ipc", "nsm_halo_connect",
                   "nsm_halo_commit", "nsm_set_option", "nsm_spmat_setup", "nsm_spmat_apply",
@@ -60,6 +60,7 @@ def load():
     P = ctypes.POINTER
     L.nsm_setup.argtypes = [P(vp), P(_Csr), P(_Csr), P(_Dist), ci]
     L.nsm_ilu0.argtypes = [P(_Csr), i64, vp]
+    L.nsm_ilu0_fixed_point.argtypes = [P(_Csr), i64, ci, vp, ci]
     L.nsm_residual.argtypes = [vp, vp, vp, vp, vp]
     L.nsm_spmv.argtypes = [vp, vp, vp, vp]
     L.nsm_lsolve.argtypes = [vp, vp, vp, ci, vp]
@@ -96,7 +97,7 @@ def load():
     L.nsm_last_error.restype = ctypes.c_char_p
     L.nsm_destroy.argtypes = [vp]
     L.nsm_destroy.restype = None
-    for name in ["nsm_setup", "nsm_ilu0", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
+    for name in ["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
                  "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
                  "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
@@ -139,6 +140,19 @@ def ilu0(A, row_begin: int = 0) -> np.ndarray:
     cs = _csr_struct(A, keep)
     out = np.empty(int(A.rowptr[-1]), dtype=np.float64)
     st = L.nsm_ilu0(ctypes.byref(cs), int(row_begin), out.ctypes.data)
+    if st != 0:
+        raise NsmError(st, _err(None))
+    return out
+
+
+def ilu0_fixed_point(A, sweeps: int, row_begin: int = 0, device: int = 0) -> np.ndarray:
+    """ILU(0) values computed on the GPU by `sweeps` Chow-Patel fixed-point
+    sweeps (nsm_ilu0_fixed_point; nsm_ilu0's layout)."""
+    L = load()
+    keep: list = []
+    cs = _csr_struct(A, keep)
+    out = np.empty(int(A.rowptr[-1]), dtype=np.float64)
+    st = L.nsm_ilu0_fixed_point(ctypes.byref(cs), int(row_begin), int(sweeps), out.ctypes.data, int(device))
     if st != 0:
         raise NsmError(st, _err(None))
     return out

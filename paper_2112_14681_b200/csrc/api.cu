@@ -342,6 +342,11 @@ nsm_status nsm_ilu0(const nsm_csr *A, int64_t row_begin, double *fval) {
     return ilu0_host(A, row_begin, fval, &g_setup_err);
 }
 
+nsm_status nsm_ilu0_fixed_point(const nsm_csr *A, int64_t row_begin, int sweeps, double *fval, int device) {
+    if (!A || !fval) { g_setup_err = "nsm_ilu0_fixed_point: NULL argument"; return NSM_ERR_ARG; }
+    return ilu0_fixed_point_device(A, row_begin, sweeps, fval, device, &g_setup_err);
+}
+
 nsm_status nsm_halo_plan(const nsm_csr *A, const nsm_dist *dist, int64_t *recv_counts, int64_t *ghost_rows,
                          int64_t *n_ghost) {
     if (!A || !dist || dist->nranks < 1 || !dist->row_offsets || !recv_counts || !n_ghost) {

@@ -193,6 +193,10 @@ nsm_status ilut_host(const nsm_csr *A, double droptol, int lfil, std::vector<int
                      std::vector<int64_t> &ci_out, std::vector<double> &va_out, std::string *err);
 nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, double *s_c, std::string *err);
 
+// ILU(0) by Chow-Patel fixed-point sweeps on the GPU (nsm_ilu0_fixed_point).
+nsm_status ilu0_fixed_point_device(const nsm_csr *A, int64_t row_begin, int sweeps, double *fval, int device,
+                                   std::string *err);
+
 // Host ILU(0) (nsm_ilu0).
 nsm_status ilu0_host(const nsm_csr *A, int64_t row_begin, double *fval, std::string *err);
 
