@@ -8,6 +8,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIBPATH = os.path.join(_HERE, "libnsm.so")
+if os.environ.get("NSM_LIB_VARIANT"):   # build experiments (build.py --variant): an alternative in-tree build
+    _LIBPATH = os.path.join(_HERE, f"libnsm_{os.environ['NSM_LIB_VARIANT']}.so")
 _lib = None
 
 NSM_PGS, NSM_ILU0, NSM_PGS_BACKWARD, NSM_PGS_SYMMETRIC, NSM_L1_JACOBI = 0, 1, 2, 3, 4

@@ -75,14 +75,16 @@ namespace nsm {
 
 namespace {
 
-constexpr int kTSF = 8;                     // slices (consumer warps) per tile
-constexpr int kRowsF = kTSF * kSlice;       // 256 rows per tile
-constexpr int kWarpP = kTSF, kWarpS = kTSF + 1;
-constexpr int kThreadsF = (kTSF + 2) * 32;  // + producer warp + sync warp
+constexpr int kWarpsC = 8;                  // consumer warps
+constexpr int kRPT = 1;                     // rows per consumer thread (2 measured slower: spills)
+constexpr int kTSF = kWarpsC * kRPT;        // slices per tile
+constexpr int kRowsF = kTSF * kSlice;       // 512 rows per tile
+constexpr int kWarpP = kWarpsC, kWarpS = kWarpsC + 1;
+constexpr int kThreadsF = (kWarpsC + 2) * 32;  // + producer warp + sync warp
 constexpr int kMaxStages = 8;
 constexpr int kSlots = 4;                   // item slots of the ready / done barriers
 constexpr int kNVec = 4;                    // vector segments staged per unit
-constexpr int kHeader = 256 + kMaxStages * 2 * kTSF * 8;  // barriers + per-stage slice offsets
+constexpr int kHeader = 384 + kMaxStages * 2 * kTSF * 8;  // barriers, unit descriptors, per-stage slice offsets
 constexpr int64_t kSmemMaxF = 220 * 1024;
 constexpr int64_t kVecBytes = (int64_t)kRowsF * 8;
 
@@ -127,8 +129,16 @@ __device__ __forceinline__ uint64_t *idone_bar(char *s) { return (uint64_t *)s +
 __device__ __forceinline__ unsigned int *pubcnt(char *s) { return (unsigned int *)((uint64_t *)s + 2 * kMaxStages + 2 * kSlots); }
 // {offset within the stage's part, width} of slice `sl` of part `pt` in stage `st`
 __device__ __forceinline__ int2 *slice_info(char *s, int st, int pt) {
-    return (int2 *)(s + 256) + (st * 2 + pt) * kTSF;
+    return (int2 *)(s + 384) + (st * 2 + pt) * kTSF;
 }
+// per-stage unit descriptor written by the producer: physical 256-row tile
+// (-1: an item without units), phase, flags
+enum { U_FIRST = 1, U_LAST = 2, U_END = 4 };
+struct UDesc {
+    int tp;
+    short j, flags;
+};
+__device__ __forceinline__ UDesc *udesc(char *s) { return (UDesc *)(s + 256); }
 __device__ __forceinline__ char *stage_ptr(char *s, const SkewParams &p, int st) {
     return s + kHeader + (int64_t)st * p.stage_bytes;
 }
@@ -234,67 +244,96 @@ __device__ __forceinline__ int64_t read_frontier(const SkewParams &p, unsigned i
     return f;
 }
 
-// One unit: phase j of logical tile u, slice `warp`, row `lane`.  Row, slice
-// and ring indices are 32-bit (a rank holds < 2^31 rows: columns are int32).
-// The stage is released (empty barrier) as soon as its shared-memory data is
-// consumed, before the results are stored.
+// One unit: phase j of physical tile tp; consumer warp `warp` owns slices
+// warp + 8h (h < kRPT), one row of each per thread: the rows' loads and
+// gathers are issued together.  Row, slice and ring indices are 32-bit (a
+// rank holds < 2^31 rows: columns are int32).  The stage is released (empty
+// barrier) as soon as its shared-memory data is consumed, before the results
+// are stored.
 template <int PH0, bool UNIT, int CH>
 __device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, int tp, int j, int warp,
                                          int lane) {
     char *stg = stage_ptr(sm, p, st);
+    int i[kRPT], rl[kRPT];
+    bool has[kRPT], row[kRPT];
+#pragma unroll
+    for (int h = 0; h < kRPT; ++h) {
+        const int sl = warp + h * kWarpsC;   // slice within the tile
+        const int s = tp * kTSF + sl;
+        has[h] = s < (int)p.nslices;
+        i[h] = s * kSlice + lane;
+        row[h] = has[h] && i[h] < (int)p.n;
+        rl[h] = sl * kSlice + lane;
+    }
+    // vectors from the stage (full tile, aligned) or from global memory
+    const bool vs = p.vec_bulk && (int64_t)(tp + 1) * kRowsF <= p.n;
+    const double *svec = (const double *)(stg + (p.cap0 + p.cap1) * 12);
+    auto vec = [&](int slot, const double *g, int h) -> double {
+        return vs ? svec[slot * kRowsF + rl[h]] : (row[h] ? __ldg(g + i[h]) : 0.0);
+    };
     auto release_stage = [&]() {
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(empty_bar(sm) + st);
-    };
-    const int s = tp * kTSF + warp;
-    const bool has = s < (int)p.nslices;
-    const int i = s * kSlice + lane;
-    const bool row = has && i < (int)p.n;
-    // vectors from the stage (full tile, aligned) or from global memory
-    const bool vs = p.vec_bulk && (int64_t)(tp + 1) * kRowsF <= p.n;
-    const int rl = warp * kSlice + lane;   // row within the tile
-    const double *sv = (const double *)(stg + (p.cap0 + p.cap1) * 12) + rl;
-    auto vec = [&](int slot, const double *g) -> double {
-        return vs ? sv[slot * kRowsF] : (row ? __ldg(g + i) : 0.0);
     };
     const double *v0 = (const double *)stg;
     const int32_t *c0 = (const int32_t *)(stg + p.cap0 * 8);
     const uint32_t rmask = (uint32_t)p.rmask, gmask = (uint32_t)p.gmask;
     if (PH0 == SKEW_RESID && j == 0) {
         // phase 0: r = b - A x (A = L + D + U, ascending column order), g(0)
-        const double di = row ? vec(0, p.dA) : 1.0, bi = vec(1, p.b), xi = vec(2, p.xin);
         const double *v1 = (const double *)(stg + p.cap0 * 12);
         const int32_t *c1 = (const int32_t *)(stg + p.cap0 * 12 + p.cap1 * 8);
-        double acc = 0.0;
-        if (has) {
-            const int2 il = slice_info(sm, st, 0)[warp], iu = slice_info(sm, st, 1)[warp];
-            const GFull gx{p.xin};
-            if constexpr (CH <= 8) {
-                Chunk<CH> cl, cu;
-                cl.load(v0, c0, il.x, il.y, lane);
-                cu.load(v1, c1, iu.x, iu.y, lane);
-                cl.gather_mul(gx);
-                cu.gather_mul(gx);
-                acc = cl.add(acc, gx);
-                acc = __dadd_rn(acc, __dmul_rn(di, xi));
-                acc = cu.add(acc, gx);
-            } else {
+        const GFull gx{p.xin};
+        double di[kRPT], bi[kRPT], xi[kRPT], acc[kRPT];
+#pragma unroll
+        for (int h = 0; h < kRPT; ++h) {
+            di[h] = row[h] ? vec(0, p.dA, h) : 1.0;
+            bi[h] = vec(1, p.b, h);
+            xi[h] = vec(2, p.xin, h);
+            acc[h] = 0.0;
+        }
+        if constexpr (CH <= 8) {
+            Chunk<CH> cl[kRPT], cu[kRPT];
+#pragma unroll
+            for (int h = 0; h < kRPT; ++h) {
+                const int sl = warp + h * kWarpsC;
+                const int2 il = slice_info(sm, st, 0)[sl], iu = slice_info(sm, st, 1)[sl];
+                cl[h].load(v0, c0, il.x, has[h] ? il.y : 0, lane);
+                cu[h].load(v1, c1, iu.x, has[h] ? iu.y : 0, lane);
+            }
+#pragma unroll
+            for (int h = 0; h < kRPT; ++h) {
+                cl[h].gather_mul(gx);
+                cu[h].gather_mul(gx);
+            }
+#pragma unroll
+            for (int h = 0; h < kRPT; ++h) {
+                acc[h] = cl[h].add(acc[h], gx);
+                acc[h] = __dadd_rn(acc[h], __dmul_rn(di[h], xi[h]));
+                acc[h] = cu[h].add(acc[h], gx);
+            }
+        } else {
+#pragma unroll
+            for (int h = 0; h < kRPT; ++h) {
+                const int sl = warp + h * kWarpsC;
+                const int2 il = slice_info(sm, st, 0)[sl], iu = slice_info(sm, st, 1)[sl];
                 Chunk<CH> c;
-                c.load(v0, c0, il.x, il.y, lane);
+                c.load(v0, c0, il.x, has[h] ? il.y : 0, lane);
                 c.gather_mul(gx);
-                acc = c.add(acc, gx);
-                acc = __dadd_rn(acc, __dmul_rn(di, xi));
-                c.load(v1, c1, iu.x, iu.y, lane);
+                acc[h] = c.add(acc[h], gx);
+                acc[h] = __dadd_rn(acc[h], __dmul_rn(di[h], xi[h]));
+                c.load(v1, c1, iu.x, has[h] ? iu.y : 0, lane);
                 c.gather_mul(gx);
-                acc = c.add(acc, gx);
+                acc[h] = c.add(acc[h], gx);
             }
         }
         release_stage();
-        if (row) {
-            const double r = __dsub_rn(bi, acc);
-            p.ring_r[(uint32_t)i & rmask] = r;
-            if (!UNIT) p.ring_g[(uint32_t)i & gmask] = __ddiv_rn(r, di);  // eq:jr-initial-guess
-        }
+#pragma unroll
+        for (int h = 0; h < kRPT; ++h)
+            if (row[h]) {
+                const double r = __dsub_rn(bi[h], acc[h]);
+                p.ring_r[(uint32_t)i[h] & rmask] = r;
+                if (!UNIT) p.ring_g[(uint32_t)i[h] & gmask] = __ddiv_rn(r, di[h]);  // eq:jr-initial-guess
+            }
         return;
     }
     // phase j >= 1: v = (rhs - T g(j-1)) / dT   (eq:jacobi, eq:LUiterMat)
@@ -305,37 +344,53 @@ __device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, 
     const int s_rhs = UNIT ? 0 : 1;
     const int s_x = s_rhs + (PH0 == SKEW_RESID ? 0 : 1);
     const int s_dn = s_x + (xadd ? 1 : 0);
-    const double di = UNIT ? 1.0 : (row ? vec(0, p.dT) : 1.0);
-    const double ri = PH0 == SKEW_RESID ? (row ? __ldcg(p.ring_r + ((uint32_t)i & rmask)) : 0.0) : vec(s_rhs, p.rhs);
-    const double xi = xadd ? vec(s_x, p.x) : 0.0;
-    const double dn = scale ? vec(s_dn, p.dn) : 1.0;
-    double acc = 0.0;
-    if (has) {
-        const int2 it = slice_info(sm, st, 0)[warp];
-        if (PH0 == SKEW_NONE && j == 1) {
-            if (p.scaled_g0) acc = tri_sum<CH>(v0, c0, it, lane, GScaled{p.g0, p.dT});
-            else acc = tri_sum<CH>(v0, c0, it, lane, GFull{p.g0});
-        } else if (PH0 == SKEW_RESID && UNIT && j == 1) {
-            acc = tri_sum<CH>(v0, c0, it, lane, GRing{p.ring_r, rmask});  // y(0) = r
-        } else {
-            acc = tri_sum<CH>(v0, c0, it, lane, GRing{p.ring_g + (int64_t)(j - 1) * p.gstride, gmask});
+    double di[kRPT], ri[kRPT], xi[kRPT], dn[kRPT], acc[kRPT];
+#pragma unroll
+    for (int h = 0; h < kRPT; ++h) {
+        di[h] = UNIT ? 1.0 : (row[h] ? vec(0, p.dT, h) : 1.0);
+        ri[h] = PH0 == SKEW_RESID ? (row[h] ? __ldcg(p.ring_r + ((uint32_t)i[h] & rmask)) : 0.0)
+                                  : vec(s_rhs, p.rhs, h);
+        xi[h] = xadd ? vec(s_x, p.x, h) : 0.0;
+        dn[h] = scale ? vec(s_dn, p.dn, h) : 1.0;
+    }
+    auto sweep_sum = [&](const auto &g) {
+        Chunk<CH> ct[kRPT];
+#pragma unroll
+        for (int h = 0; h < kRPT; ++h) {
+            const int2 it = slice_info(sm, st, 0)[warp + h * kWarpsC];
+            ct[h].load(v0, c0, it.x, has[h] ? it.y : 0, lane);
         }
+#pragma unroll
+        for (int h = 0; h < kRPT; ++h) ct[h].gather_mul(g);
+#pragma unroll
+        for (int h = 0; h < kRPT; ++h) acc[h] = ct[h].add(0.0, g);
+    };
+    if (PH0 == SKEW_NONE && j == 1) {
+        if (p.scaled_g0) sweep_sum(GScaled{p.g0, p.dT});
+        else sweep_sum(GFull{p.g0});
+    } else if (PH0 == SKEW_RESID && UNIT && j == 1) {
+        sweep_sum(GRing{p.ring_r, rmask});  // y(0) = r
+    } else {
+        sweep_sum(GRing{p.ring_g + (int64_t)(j - 1) * p.gstride, gmask});
     }
     release_stage();
-    if (!row) return;
-    double v = __dsub_rn(ri, acc);
-    if (!UNIT) v = __ddiv_rn(v, di);
-    if (!isfinite(v)) atomicMin(p.flag, (unsigned long long)(p.sweep_id0 + j - 1));
-    if (!last) {
-        p.ring_g[(int64_t)j * p.gstride + ((uint32_t)i & gmask)] = v;
-        return;
-    }
-    switch (p.epi) {
-        case SKEW_STORE: p.out1[i] = v; break;
-        case SKEW_XADD: p.x[i] = __dadd_rn(xi, v); break;
-        case SKEW_STORE2: p.out1[i] = v; p.out2[i] = __ddiv_rn(v, dn); break;
-        case SKEW_XADD_SCALE: p.x[i] = __dadd_rn(xi, __ddiv_rn(v, dn)); break;
-        default: p.out1[i] = __ddiv_rn(v, dn); break;  // SKEW_STORE_SCALE
+#pragma unroll
+    for (int h = 0; h < kRPT; ++h) {
+        if (!row[h]) continue;
+        double v = __dsub_rn(ri[h], acc[h]);
+        if (!UNIT) v = __ddiv_rn(v, di[h]);
+        if (!isfinite(v)) atomicMin(p.flag, (unsigned long long)(p.sweep_id0 + j - 1));
+        if (!last) {
+            p.ring_g[(int64_t)j * p.gstride + ((uint32_t)i[h] & gmask)] = v;
+            continue;
+        }
+        switch (p.epi) {
+            case SKEW_STORE: p.out1[i[h]] = v; break;
+            case SKEW_XADD: p.x[i[h]] = __dadd_rn(xi[h], v); break;
+            case SKEW_STORE2: p.out1[i[h]] = v; p.out2[i[h]] = __ddiv_rn(v, dn[h]); break;
+            case SKEW_XADD_SCALE: p.x[i[h]] = __dadd_rn(xi[h], __ddiv_rn(v, dn[h])); break;
+            default: p.out1[i[h]] = __ddiv_rn(v, dn[h]); break;  // SKEW_STORE_SCALE
+        }
     }
 }
 
@@ -402,33 +457,35 @@ struct UnitGen {
 };
 
 // Slice pointers of a unit's parts: lanes 0..8 part 0, lanes 16..24 part 1.
+// Slice pointers of a unit's parts: lane l <= kTSF holds ptr[s0 + l] of part 0
+// (.x) and, for phase 0, of part 1 (.y).
 template <int PH0>
-__device__ __forceinline__ int64_t unit_ptrs(const SkewParams &p, int64_t tp, int j, int lane) {
+__device__ __forceinline__ longlong2 unit_ptrs(const SkewParams &p, int64_t tp, int j, int lane) {
     const int64_t s0 = tp * kTSF, s1 = min(s0 + kTSF, p.nslices);
     const bool ph0 = PH0 == SKEW_RESID && j == 0;
-    int64_t pv = 0;
-    if (lane <= kTSF) pv = __ldg((ph0 ? p.A0.ptr : p.T.ptr) + min(s0 + lane, s1));
-    else if (ph0 && lane >= 16 && lane <= 16 + kTSF) pv = __ldg(p.A1.ptr + min(s0 + lane - 16, s1));
+    longlong2 pv = make_longlong2(0, 0);
+    if (lane <= kTSF) {
+        pv.x = __ldg((ph0 ? p.A0.ptr : p.T.ptr) + min(s0 + lane, s1));
+        if (ph0) pv.y = __ldg(p.A1.ptr + min(s0 + lane, s1));
+    }
     return pv;
 }
 
-constexpr int kPre = 4;  // units whose slice pointers the producer has in flight
+constexpr int kPre = 2;  // records whose slice pointers the producer has in flight
 
 template <int PH0, bool UNIT>
-__device__ __forceinline__ void stage_unit(const SkewParams &p, char *sm, int it, int64_t tp, int j, int64_t pv,
+__device__ __forceinline__ void stage_unit(const SkewParams &p, char *sm, int st, int64_t tp, int j, longlong2 pvv,
                                            uint64_t pol_first, uint64_t pol_keep, int lane) {
-    const int st = it % p.nst;
-    if (lane == 0) trace_at(p, 1, it, 0);
-    if (it >= p.nst) ptx::mbar_wait_sleep(empty_bar(sm) + st, ((uint32_t)(it / p.nst) - 1) & 1);
-    if (lane == 0) trace_at(p, 1, it, 1);
     const bool ph0 = PH0 == SKEW_RESID && j == 0;
     const SellView &P0 = ph0 ? p.A0 : p.T;
-    const int64_t pnext = __shfl_down_sync(0xffffffffu, pv, 1);
+    const int64_t pv = pvv.x, pw = pvv.y;
+    const int64_t pnext = __shfl_down_sync(0xffffffffu, pv, 1), wnext = __shfl_down_sync(0xffffffffu, pw, 1);
     const int64_t pbase0 = __shfl_sync(0xffffffffu, pv, 0), pend0 = __shfl_sync(0xffffffffu, pv, kTSF);
-    const int64_t pbase1 = __shfl_sync(0xffffffffu, pv, 16), pend1 = __shfl_sync(0xffffffffu, pv, 16 + kTSF);
-    if (lane < kTSF) slice_info(sm, st, 0)[lane] = make_int2((int)(pv - pbase0), (int)((pnext - pv) / kSlice));
-    if (ph0 && lane >= 16 && lane < 16 + kTSF)
-        slice_info(sm, st, 1)[lane - 16] = make_int2((int)(pv - pbase1), (int)((pnext - pv) / kSlice));
+    const int64_t pbase1 = __shfl_sync(0xffffffffu, pw, 0), pend1 = __shfl_sync(0xffffffffu, pw, kTSF);
+    if (lane < kTSF) {
+        slice_info(sm, st, 0)[lane] = make_int2((int)(pv - pbase0), (int)((pnext - pv) / kSlice));
+        if (ph0) slice_info(sm, st, 1)[lane] = make_int2((int)(pw - pbase1), (int)((wnext - pw) / kSlice));
+    }
     __syncwarp();
     if (lane == 0) {
         char *sp = stage_ptr(sm, p, st);
@@ -460,60 +517,115 @@ __device__ __forceinline__ void stage_unit(const SkewParams &p, char *sm, int it
     __syncwarp();
 }
 
-// Producer: walks the unit sequence with the slice pointers of the next kPre
-// units already loading (their latency would otherwise serialise every unit).
-// Sub-unit walk: each unit (w, q) covers big tile u = w - qD, i.e. the
-// 256-row tiles u B .. u B + B - 1 (those < ntiles), in that order.
-struct SubGen {
+// Record sequence of a CTA: for each of its items w = blockIdx.x + m G, the
+// sub-units (unit (w, q) = big tile u = w - qD = 256-row tiles uB .. uB+B-1
+// below ntiles, phase j0 + q), or one empty record for an item without units.
+struct Seq {
     UnitGen g;
+    int64_t q;
     int b;
-    __device__ __forceinline__ int64_t tile(const SkewParams &p) const {
-        const int64_t t = (g.w - g.q * p.D) * p.B + b;
-        return p.desc ? p.ntiles - 1 - t : t;
+    int64_t tp;
+    int j, flags;
+    bool valid;
+    __device__ __forceinline__ void settle(const SkewParams &p) {
+        valid = g.w < p.nitems;
+        if (!valid) return;
+        if (g.qa > g.qb) {
+            tp = -1;
+            j = 0;
+            flags = U_FIRST | U_LAST;
+            return;
+        }
+        const int64_t t = (g.w - q * p.D) * p.B + b;
+        tp = p.desc ? p.ntiles - 1 - t : t;
+        j = p.j0 + (int)q;
+        const bool lastb = b + 1 >= p.B || t + 1 >= p.ntiles;
+        flags = (q == g.qa && b == 0 ? U_FIRST : 0) | (q == g.qb && lastb ? U_LAST : 0);
     }
-    __device__ __forceinline__ int j(const SkewParams &p) const { return p.j0 + (int)g.q; }
     __device__ __forceinline__ void init(const SkewParams &p) {
-        g.init(p, true);
+        g.init(p, false);
+        q = g.qa;
         b = 0;
+        settle(p);
     }
     __device__ __forceinline__ void next(const SkewParams &p) {
-        ++b;
-        if (b < p.B && (g.w - g.q * p.D) * p.B + b < p.ntiles) return;
+        if (tp >= 0) {
+            const int64_t t = (g.w - q * p.D) * p.B + b;
+            if (b + 1 < p.B && t + 1 < p.ntiles) {
+                ++b;
+                settle(p);
+                return;
+            }
+            b = 0;
+            if (q < g.qb) {
+                ++q;
+                settle(p);
+                return;
+            }
+        }
+        g.advance_item();
+        q = g.qa;
         b = 0;
-        g.next();
+        settle(p);
     }
 };
 
-// Producer: walks the sub-unit sequence with the slice pointers of the next
-// kPre sub-units already loading (their latency would otherwise serialise
-// every unit).
+// Producer: walks the record sequence with the slice pointers of the next
+// kPre records already loading (their latency would otherwise serialise
+// every unit); writes each record's descriptor into its stage.
 template <int PH0, bool UNIT>
 __device__ __forceinline__ void produce(const SkewParams &p, char *sm, int lane) {
     const uint64_t pol_first = ptx::policy_evict_first(), pol_keep = ptx::policy_evict_normal();
-    SubGen gen;
-    gen.init(p);
-    int64_t ptp[kPre], pv[kPre];
-    int pj[kPre];
+    Seq seq;
+    seq.init(p);
+    int64_t ptp[kPre];
+    longlong2 pv[kPre];
+    int pj[kPre], pf[kPre];
     bool ok[kPre];
 #pragma unroll
     for (int k = 0; k < kPre; ++k) {
-        ok[k] = gen.g.valid;
-        ptp[k] = ok[k] ? gen.tile(p) : 0;
-        pj[k] = gen.j(p);
-        pv[k] = ok[k] ? unit_ptrs<PH0>(p, ptp[k], pj[k], lane) : 0;
-        if (gen.g.valid) gen.next(p);
+        ok[k] = seq.valid;
+        ptp[k] = seq.tp;
+        pj[k] = seq.j;
+        pf[k] = seq.flags;
+        pv[k] = (ok[k] && seq.tp >= 0) ? unit_ptrs<PH0>(p, ptp[k], pj[k], lane) : make_longlong2(0, 0);
+        if (seq.valid) seq.next(p);
     }
-    for (int it = 0; ok[0]; it += kPre) {
+    int st = 0;
+    uint32_t round = 0;
+    auto next_stage = [&]() {
+        if (++st == p.nst) { st = 0; ++round; }
+    };
+    auto wait_free = [&]() {
+        if (round > 0) ptx::mbar_wait_sleep(empty_bar(sm) + st, (round - 1) & 1);
+    };
+    bool more = ok[0];
+    while (more) {
 #pragma unroll
         for (int k = 0; k < kPre; ++k) {
-            if (!ok[k]) break;
-            stage_unit<PH0, UNIT>(p, sm, it + k, ptp[k], pj[k], pv[k], pol_first, pol_keep, lane);
-            ok[k] = gen.g.valid;
-            ptp[k] = ok[k] ? gen.tile(p) : 0;
-            pj[k] = gen.j(p);
-            pv[k] = ok[k] ? unit_ptrs<PH0>(p, ptp[k], pj[k], lane) : 0;
-            if (gen.g.valid) gen.next(p);
+            if (!ok[k]) { more = false; break; }
+            wait_free();
+            if (lane == 0) udesc(sm)[st] = UDesc{(int)ptp[k], (short)pj[k], (short)pf[k]};
+            if (ptp[k] >= 0) {
+                stage_unit<PH0, UNIT>(p, sm, st, ptp[k], pj[k], pv[k], pol_first, pol_keep, lane);
+            } else {
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(full_bar(sm) + st);
+            }
+            next_stage();
+            ok[k] = seq.valid;
+            ptp[k] = seq.tp;
+            pj[k] = seq.j;
+            pf[k] = seq.flags;
+            pv[k] = (ok[k] && seq.tp >= 0) ? unit_ptrs<PH0>(p, ptp[k], pj[k], lane) : make_longlong2(0, 0);
+            if (seq.valid) seq.next(p);
         }
+    }
+    // end of the sequence
+    wait_free();
+    if (lane == 0) {
+        udesc(sm)[st] = UDesc{-1, 0, (short)U_END};
+        ptx::mbar_arrive(full_bar(sm) + st);
     }
 }
 
@@ -565,18 +677,21 @@ __device__ __forceinline__ void sync_role(const SkewParams &p, char *sm, unsigne
 }
 
 template <int PH0, bool UNIT, int CH>
-__global__ void __launch_bounds__(kThreadsF, CH <= 4 ? 3 : (CH <= 8 ? 2 : 1)) k_skew(const __grid_constant__ SkewParams p) {
+#ifndef NSM_SKEW_MINB4
+#define NSM_SKEW_MINB4 2  // CTAs per SM the CH = 4 variants are register-budgeted for
+#endif
+__global__ void __launch_bounds__(kThreadsF, CH <= 4 ? NSM_SKEW_MINB4 : (CH <= 8 ? 2 : 1)) k_skew(const __grid_constant__ SkewParams p) {
     extern __shared__ __align__(128) char sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned int epoch = *(volatile unsigned int *)&p.sync->epoch;
     if (threadIdx.x == 0) {
         for (int st = 0; st < p.nst; ++st) {
             ptx::mbar_init(full_bar(sm) + st, 1);
-            ptx::mbar_init(empty_bar(sm) + st, kTSF);
+            ptx::mbar_init(empty_bar(sm) + st, kWarpsC);
         }
         for (int sl = 0; sl < kSlots; ++sl) {
             ptx::mbar_init(ready_bar(sm) + sl, 1);
-            ptx::mbar_init(idone_bar(sm) + sl, kTSF);
+            ptx::mbar_init(idone_bar(sm) + sl, kWarpsC);
             pubcnt(sm)[sl] = 0;
         }
         ptx::mbar_init_fence();
@@ -588,54 +703,58 @@ __global__ void __launch_bounds__(kThreadsF, CH <= 4 ? 3 : (CH <= 8 ? 2 : 1)) k_
     } else if (warp == kWarpS) {
         sync_role(p, sm, epoch, lane);
     } else {
+        // consumers: follow the producer's descriptors (stage and parity
+        // tracked incrementally); item boundaries come with the flags
+        int st = 0;
+        uint32_t par = 0;
+        int64_t m = -1;
         int it = 0;
-        int64_t m = 0;
-        UnitGen gen;
-        gen.init(p, false);  // item-level walk (items without units included)
-        for (int64_t w = blockIdx.x; w < p.nitems; w += gridDim.x, ++m) {
-            if (w != (int64_t)blockIdx.x) gen.advance_item();
-            const int64_t qa = gen.qa, qb = gen.qb;
-            if (warp == 0 && lane == 0) trace_at(p, 2, (int)m, 3);  // consumers want item m
-            {
+        while (true) {
+            if (warp == 0 && lane == 0) trace_at(p, 0, it, 0);
+            ptx::mbar_wait_sleep(full_bar(sm) + st, par);
+            if (warp == 0 && lane == 0) trace_at(p, 0, it, 1);
+            const UDesc un = udesc(sm)[st];
+            if (un.flags & U_END) break;
+            if (un.flags & U_FIRST) {
+                ++m;
                 uint64_t *rb = ready_bar(sm) + (m % kSlots);
-                const uint32_t par = (uint32_t)(m / kSlots) & 1;
-                if (warp == 0 && !ptx::mbar_test(rb, par)) {  // statistics: consumers stalled on readiness
+                const uint32_t rpar = (uint32_t)(m / kSlots) & 1;
+                if (warp == 0 && !ptx::mbar_test(rb, rpar)) {  // statistics: consumers stalled on readiness
                     const uint64_t t0 = ptx::globaltimer_ns();
-                    ptx::mbar_wait_sleep(rb, par);
+                    ptx::mbar_wait_sleep(rb, rpar);
                     if (lane == 0) {
                         atomicAdd(&p.sync->waits, 1ull);
                         atomicAdd(&p.sync->wait_ns, ptx::globaltimer_ns() - t0);
                     }
                 }
-                ptx::mbar_wait_sleep(rb, par);
+                ptx::mbar_wait_sleep(rb, rpar);
             }
-            for (int64_t q = qa; q <= qb; ++q) {
-                const int64_t t0 = (w - q * p.D) * p.B;
-                for (int b = 0; b < p.B && t0 + b < p.ntiles; ++b, ++it) {
-                    const int st = it % p.nst;
-                    const int tp = (int)(p.desc ? p.ntiles - 1 - (t0 + b) : t0 + b);
-                    if (warp == 0 && lane == 0) trace_at(p, 0, it, 0);
-                    ptx::mbar_wait_sleep(full_bar(sm) + st, (uint32_t)(it / p.nst) & 1);
-                    if (warp == 0 && lane == 0) trace_at(p, 0, it, 1);
-                    run_unit<PH0, UNIT, CH>(p, sm, st, tp, p.j0 + (int)q, warp, lane);
-                    if (warp == 0 && lane == 0) trace_at(p, 0, it, 2);
+            if (un.tp >= 0) {
+                run_unit<PH0, UNIT, CH>(p, sm, st, un.tp, un.j, warp, lane);  // releases the stage
+            } else {
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(empty_bar(sm) + st);
+            }
+            if (warp == 0 && lane == 0) trace_at(p, 0, it, 2);
+            if (un.flags & U_LAST) {
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(idone_bar(sm) + (m % kSlots));
+                    if (warp == 0) trace_at(p, 2, (int)m, 2);
+                    // the last warp to finish item m publishes "m + 1 items done";
+                    // acq_rel at CTA scope makes the other warps' stores happen
+                    // before this warp's release (cumulativity), max keeps the
+                    // counter monotone if a later item's publication overtakes
+                    const unsigned int prev = ptx::atom_add_acqrel_cta_shared(pubcnt(sm) + (m % kSlots), 1u);
+                    if (prev == (unsigned int)((m / kSlots + 1) * kWarpsC - 1)) {
+                        trace_at(p, 2, (int)m, 1);  // item published
+                        ptx::red_max_release_gpu_u64(p.prog + blockIdx.x,
+                                                     ((unsigned long long)epoch << 32) | (unsigned long long)(m + 1));
+                    }
                 }
             }
-            __syncwarp();
-            if (lane == 0) {
-                ptx::mbar_arrive(idone_bar(sm) + (m % kSlots));
-                if (warp == 0) trace_at(p, 2, (int)m, 2);
-                // the last warp to finish item m publishes "m + 1 items done";
-                // acq_rel at CTA scope makes the other warps' stores happen
-                // before this warp's release (cumulativity), max keeps the
-                // counter monotone if a later item's publication overtakes
-                const unsigned int prev = ptx::atom_add_acqrel_cta_shared(pubcnt(sm) + (m % kSlots), 1u);
-                if (prev == (unsigned int)((m / kSlots + 1) * kTSF - 1)) {
-                    trace_at(p, 2, (int)m, 1);  // item published
-                    ptx::red_max_release_gpu_u64(p.prog + blockIdx.x,
-                                                 ((unsigned long long)epoch << 32) | (unsigned long long)(m + 1));
-                }
-            }
+            if (++st == p.nst) { st = 0; par ^= 1; }
+            ++it;
         }
     }
     // ---- the last CTA out resets the launch state for the next launch
@@ -702,7 +821,7 @@ GeoF geometry_f(const void *k, int64_t stage_bytes) {
         int per = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreadsF, (size_t)smem);
         per = std::min(per, max_per);
-        const int warps = std::min(per * kTSF, 32);
+        const int warps = std::min(per * kWarpsC, 32);
         if (per > 0 && warps >= best) {
             best = warps;
             g.nst = nst;
