@@ -291,7 +291,12 @@ __device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, 
             xi[h] = vec(2, p.xin, h);
             acc[h] = 0.0;
         }
-        if constexpr (CH <= 8) {
+#ifndef NSM_SKEW_SEQ_RESID
+        constexpr bool both = CH <= 8;  // both triangles' gathers in flight together
+#else
+        constexpr bool both = false;    // experiment: one triangle at a time (fewer registers)
+#endif
+        if constexpr (both) {
             Chunk<CH> cl[kRPT], cu[kRPT];
 #pragma unroll
             for (int h = 0; h < kRPT; ++h) {
