@@ -318,7 +318,9 @@ const char *nsm_last_error(const nsm_handle *h);
  *                           problems).  Bit-identical results either way.
  *                           The fused passes read ~2.4x fewer HBM bytes but
  *                           are currently latency-bound and slower than the
- *                           per-pass kernels.
+ *                           per-pass kernels.  Switching it
+ *                           on allocates the passes' L2 ring buffers (up to
+ *                           ~9 n-vectors; NSM_ERR_OOM if that fails).
  *   NSM_OPT_FUSED_WINDOW    wait distance Dw of the fused passes in work
  *                           items (0 = automatic, about the items in flight);
  *                           a small value forces frequent waits and ring

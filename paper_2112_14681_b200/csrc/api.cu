@@ -69,7 +69,7 @@ struct nsm_handle {
     int ev_used = 0;
     // phase-skewed fused passes (fused.cu), single rank
     int fused_mode = 0;                      // NSM_OPT_FUSED: 0 off (default), 1 on, 2 auto (large problems)
-    bool fused_ready = false;
+    bool fused_ready = false, fused_possible = false;  // rings allocated / single rank
     int skew_dw = 0;                         // NSM_OPT_FUSED_WINDOW (0 = automatic)
     int DLA = 0, DUA = 0, DLs = 0, DUs = 0;  // bandwidths in tiles of A and of the factors
     static constexpr int kFusedKmax = 8;
@@ -331,6 +331,54 @@ size_t flags_bytes_for(int nranks) { return (((size_t)nranks * 8 + 255) / 256) *
 
 }  // namespace
 
+// Rings, progress counters and launch state of the fused passes, sized for
+// the largest shape any k <= kFusedKmax can need (single rank; once).
+static nsm_status fused_alloc(nsm_handle *h) {
+    if (h->fused_ready || !h->fused_possible) return NSM_OK;
+    cudaSetDevice(h->device);
+    const int64_t tr = skew_tile_rows();
+    int64_t mr = 0, mg = 0;
+    bool all = true;
+    auto need = [&](const SkewShape &sh) {
+        all = all && sh.ok;
+        mr = std::max(mr, sh.Mr);
+        mg = std::max(mg, sh.Mg);
+    };
+    const int K = nsm_handle::kFusedKmax;
+    const int mw = std::max(h->L.maxw, h->U.maxw);
+    need(skew_shape(SKEW_RESID, false, h->L.maxw, h->U.maxw, mw, K, h->n, std::max(h->DLA, h->DUA),
+                    std::max(h->DLA, h->DUA), 0));
+    need(skew_shape(SKEW_NONE, false, 0, 0, mw, K, h->n, std::max(h->DLA, h->DUA), 0, 0));
+    if (h->has_ilu) {
+        const int mwf = std::max(h->Ls.maxw, h->Us.maxw);
+        need(skew_shape(SKEW_RESID, true, h->L.maxw, h->U.maxw, h->Ls.maxw, K, h->n, h->DLs, h->DLA, 0));
+        need(skew_shape(SKEW_NONE, true, 0, 0, mwf, K, h->n, std::max(h->DLs, h->DUs), 0, 0));
+        need(skew_shape(SKEW_NONE, false, 0, 0, mwf, K, h->n, std::max(h->DLs, h->DUs), 0, 0));
+    }
+    if (!all) return NSM_OK;  // shapes that do not fit shared memory: per-pass kernels
+    if (getenv("NSM_DEBUG_FULL_RINGS")) {  // window experiments (tools/skew_exp.py) only
+        int64_t t = 1;
+        while (t * tr < h->n) t <<= 1;
+        mr = mg = t;
+    }
+    h->ring_r_tiles = std::max<int64_t>(mr, 1);
+    h->ring_g_tiles = std::max<int64_t>(mg, 1);
+    SkewSync init{};
+    init.epoch = 1;
+    DevAlloc a{h};
+    const bool ok = a.get(&h->ring_r, h->ring_r_tiles * tr) && a.get(&h->ring_g, (int64_t)K * h->ring_g_tiles * tr) &&
+                    a.get(&h->skew_sync, 1) && a.get(&h->skew_prog, 4096) &&
+                    cudaMemcpy(h->skew_sync, &init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess &&
+                    cudaMemset(h->skew_prog, 0, 4096 * sizeof(unsigned long long)) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        h->err = "NSM_OPT_FUSED: device allocation of the fused-pass rings failed";
+        return NSM_ERR_OOM;
+    }
+    h->fused_ready = true;
+    return NSM_OK;
+}
+
 bool nsm::nsm_is_distributed(const nsm_handle *h) { return h && h->nranks > 1; }
 
 extern "C" {
@@ -451,48 +499,15 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         ok = cudaMemcpy(h->flag, &init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
     }
     if (ok && nranks == 1 && h->n > 0) {
-        // rings, done flags and launch state of the fused passes (fused.cu),
-        // sized for the largest shape any k <= kFusedKmax can need
+        // dependency distances of the fused passes (fused.cu); their rings are
+        // allocated when NSM_OPT_FUSED is switched on (fused_alloc)
         const int64_t tr = skew_tile_rows();
         auto tiles = [tr](int64_t bw) { return (int)((bw + tr - 1) / tr); };
         h->DLA = tiles(sa.bw_lower);
         h->DUA = tiles(sa.bw_upper);
         h->DLs = F ? tiles(sf.bw_lower) : 0;
         h->DUs = F ? tiles(sf.bw_upper) : 0;
-        int64_t mr = 0, mg = 0;
-        bool all = true;
-        auto need = [&](const SkewShape &sh) {
-            all = all && sh.ok;
-            mr = std::max(mr, sh.Mr);
-            mg = std::max(mg, sh.Mg);
-        };
-        const int K = nsm_handle::kFusedKmax;
-        const int mw = std::max(h->L.maxw, h->U.maxw);
-        need(skew_shape(SKEW_RESID, false, h->L.maxw, h->U.maxw, mw, K, h->n, std::max(h->DLA, h->DUA),
-                        std::max(h->DLA, h->DUA), 0));
-        need(skew_shape(SKEW_NONE, false, 0, 0, mw, K, h->n, std::max(h->DLA, h->DUA), 0, 0));
-        if (F) {
-            const int mwf = std::max(h->Ls.maxw, h->Us.maxw);
-            need(skew_shape(SKEW_RESID, true, h->L.maxw, h->U.maxw, h->Ls.maxw, K, h->n, h->DLs, h->DLA, 0));
-            need(skew_shape(SKEW_NONE, true, 0, 0, mwf, K, h->n, std::max(h->DLs, h->DUs), 0, 0));
-            need(skew_shape(SKEW_NONE, false, 0, 0, mwf, K, h->n, std::max(h->DLs, h->DUs), 0, 0));
-        }
-        if (all && getenv("NSM_DEBUG_FULL_RINGS")) {  // window experiments (tools/skew_exp.py) only
-            int64_t t = 1;
-            while (t * tr < h->n) t <<= 1;
-            mr = mg = t;
-        }
-        if (all) {
-            h->ring_r_tiles = std::max<int64_t>(mr, 1);
-            h->ring_g_tiles = std::max<int64_t>(mg, 1);
-            SkewSync init{};
-            init.epoch = 1;
-            ok = a.get(&h->ring_r, h->ring_r_tiles * tr) && a.get(&h->ring_g, (int64_t)K * h->ring_g_tiles * tr) &&
-                 a.get(&h->skew_sync, 1) && a.get(&h->skew_prog, 4096) &&
-                 cudaMemcpy(h->skew_sync, &init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess &&
-                 cudaMemset(h->skew_prog, 0, 4096 * sizeof(unsigned long long)) == cudaSuccess;
-            h->fused_ready = ok;
-        }
+        h->fused_possible = true;
     }
     if (ok && nranks > 1) {
         h->row_offsets.assign(dist->row_offsets, dist->row_offsets + nranks + 1);
@@ -647,7 +662,7 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
         case NSM_OPT_FUSED:
             if (value < 0 || value > 2) return NSM_ERR_ARG;
             h->fused_mode = (int)value;
-            return NSM_OK;
+            return value ? fused_alloc(h) : NSM_OK;
         case NSM_OPT_FUSED_WINDOW:
             if (value < 0 || value > INT_MAX) return NSM_ERR_ARG;
             h->skew_dw = (int)value;
