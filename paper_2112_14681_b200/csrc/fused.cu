@@ -176,10 +176,14 @@ struct GScaled {
     const double *__restrict__ d;
     __device__ __forceinline__ double operator()(int32_t c) const { return __ddiv_rn(__ldg(g + c), __ldg(d + c)); }
 };
-struct GRing {  // written by other CTAs during this launch: L2 only
+// Ring buffers are written by other CTAs during the launch: plain (L1-
+// allocating) loads, made coherent by the acquire fence the sync warp issues
+// before it releases each item (it invalidates the SM's L1; within the item
+// neighbouring rows then share L1 lines).
+struct GRing {
     const double *base;
     uint32_t mask;
-    __device__ __forceinline__ double operator()(int32_t c) const { return __ldcg(base + ((uint32_t)c & mask)); }
+    __device__ __forceinline__ double operator()(int32_t c) const { return base[(uint32_t)c & mask]; }
 };
 
 template <int CH>
@@ -353,7 +357,7 @@ __device__ __forceinline__ void run_unit(const SkewParams &p, char *sm, int st, 
 #pragma unroll
     for (int h = 0; h < kRPT; ++h) {
         di[h] = UNIT ? 1.0 : (row[h] ? vec(0, p.dT, h) : 1.0);
-        ri[h] = PH0 == SKEW_RESID ? (row[h] ? __ldcg(p.ring_r + ((uint32_t)i[h] & rmask)) : 0.0)
+        ri[h] = PH0 == SKEW_RESID ? (row[h] ? p.ring_r[(uint32_t)i[h] & rmask] : 0.0)
                                   : vec(s_rhs, p.rhs, h);
         xi[h] = xadd ? vec(s_x, p.x, h) : 0.0;
         dn[h] = scale ? vec(s_dn, p.dn, h) : 1.0;
@@ -656,14 +660,6 @@ __device__ __forceinline__ void sync_role(const SkewParams &p, char *sm, unsigne
                 // own items before m are finished (the wait above) but maybe
                 // not yet published: the frontier may lag by our own counter
                 F = read_frontier(p, epoch, lane);
-                // No acquire fence on success: a gpu-scope acquire invalidates the
-                // SM's whole L1 (CCTL.IVALL), which the neighbour gathers live
-                // on.  Everything another CTA wrote in this launch (the ring
-                // buffers) is read with ld.global.cg from L2, the GPU's point
-                // of coherence, after this relaxed load observed a counter
-                // the writer published with a release reduction (its ring
-                // stores were performed at L2 first); the readers' loads are
-                // issued only after the ready barrier, i.e. after it.
                 if (tgt < F) break;
                 if (ptx::globaltimer_ns() - t0 > p.timeout_ns) {
                     if (lane == 0) atomicOr(p.err, 2u);
@@ -673,6 +669,10 @@ __device__ __forceinline__ void sync_role(const SkewParams &p, char *sm, unsigne
                 __nanosleep(32);
             }
         }
+        // acquire: the frontier was read with relaxed loads; one gpu-scope
+        // fence per item (it also invalidates the SM's L1, so the consumers'
+        // L1-cached ring reads of this item see what the counters published)
+        __threadfence();
         if (lane == 0) {
             trace_at(p, 2, (int)m, 0);  // item made ready
             ptx::mbar_arrive(ready_bar(sm) + (m % kSlots));
