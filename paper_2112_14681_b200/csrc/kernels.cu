@@ -79,7 +79,9 @@ __device__ __forceinline__ double accum(const SellView P, int64_t s, int lane, c
 // (memory-level parallelism: all value/index requests of a row are in
 // flight together), multiplied by their gathered operands as they arrive,
 // then summed in stored order.  Entries beyond CH (rows wider than the
-// chunk) continue with the plain loop, so the summation order is unchanged.
+// chunk: coarse AMG levels) follow in further chunks of CH — their gathers
+// again issued together, their products again added one by one in stored
+// order — so the summation order (and every rounding) is unchanged.
 template <int CH>
 struct Chunk {
     double v[CH];
@@ -109,9 +111,17 @@ struct Chunk {
 #pragma unroll
         for (int j = 0; j < CH; ++j)
             if (j < w) acc = __dadd_rn(acc, v[j]);
-        for (int j = CH; j < w; ++j) {
-            const int64_t p = base + (int64_t)j * kSlice;
-            acc = __dadd_rn(acc, __dmul_rn(ld_stream(P.val + p, pol), g(ld_stream(P.col + p, pol))));
+        for (int j0 = CH; j0 < w; j0 += CH) {
+            double pr[CH];
+#pragma unroll
+            for (int t = 0; t < CH; ++t)
+                if (j0 + t < w) {
+                    const int64_t p = base + (int64_t)(j0 + t) * kSlice;
+                    pr[t] = __dmul_rn(ld_stream(P.val + p, pol), g(ld_stream(P.col + p, pol)));
+                }
+#pragma unroll
+            for (int t = 0; t < CH; ++t)
+                if (j0 + t < w) acc = __dadd_rn(acc, pr[t]);
         }
         return acc;
     }

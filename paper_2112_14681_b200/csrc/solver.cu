@@ -32,8 +32,18 @@ __global__ void __launch_bounds__(kThr) k_csr_spmv(int64_t nrows, const int64_t 
     const int64_t i = (int64_t)blockIdx.x * kThr + threadIdx.x;
     if (i >= nrows) return;
     double s = 0.0;
-    for (int64_t p = __ldg(rp + i), e = __ldg(rp + i + 1); p < e; ++p)
-        s = __dadd_rn(s, __dmul_rn(__ldg(va + p), __ldg(x + __ldg(ci + p))));
+    // chunks of 8 entries: loads and gathers issued together, products added
+    // in ascending column order (the order of the one-by-one loop)
+    constexpr int C = 8;
+    for (int64_t p0 = __ldg(rp + i), e = __ldg(rp + i + 1); p0 < e; p0 += C) {
+        double pr[C];
+#pragma unroll
+        for (int t = 0; t < C; ++t)
+            if (p0 + t < e) pr[t] = __dmul_rn(__ldg(va + p0 + t), __ldg(x + __ldg(ci + p0 + t)));
+#pragma unroll
+        for (int t = 0; t < C; ++t)
+            if (p0 + t < e) s = __dadd_rn(s, pr[t]);
+    }
     const double v = __dmul_rn(alpha, s);
     y[i] = beta == 0.0 ? v : __dadd_rn(v, __dmul_rn(beta, y[i]));
 }
