@@ -843,33 +843,28 @@ static nsm_status skew_run(nsm_handle *h, SkewLaunch &L, bool unit, int DT, int 
         cudaStreamSynchronize(s);
         cudaMemcpy(tb.data(), trace, tb.size() * 8, cudaMemcpyDeviceToHost);
         for (int cta = 0; cta < 2; ++cta) {
-            const unsigned long long *C = tb.data() + (cta * 3 + 0) * 2048 * 4, *P = tb.data() + (cta * 3 + 1) * 2048 * 4;
+            // consumer warp 0: slot 0 full-wait start, 1 data ready, 2 unit done;
+            // per item: slot 0 made ready, 1 published
+            const unsigned long long *C = tb.data() + (cta * 3 + 0) * 2048 * 4;
             const unsigned long long *Y = tb.data() + (cta * 3 + 2) * 2048 * 4;
-            unsigned long long t0 = C[0] ? C[0] : P[0], tend = 0;
-            double full_wait = 0, compute = 0, empty_wait = 0, issue = 0;
+            const unsigned long long t0 = C[0];
+            double full_wait = 0, compute = 0, gaps = 0;
             int nu = 0;
-            for (int u = 0; u < 2048 && C[u * 4 + 1]; ++u, ++nu) {
+            for (int u = 0; u < 2048 && C[u * 4 + 2]; ++u, ++nu) {
                 full_wait += (double)(C[u * 4 + 1] - C[u * 4 + 0]);
                 compute += (double)(C[u * 4 + 2] - C[u * 4 + 1]);
-                tend = C[u * 4 + 2];
-                if (P[u * 4 + 1]) {
-                    empty_wait += (double)(P[u * 4 + 1] - P[u * 4 + 0]);
-                    issue += (double)(P[u * 4 + 2] - P[u * 4 + 1]);
-                }
+                if (u > 0) gaps += (double)(C[u * 4 + 0] - C[u * 4 - 2]);
             }
-            fprintf(stderr, "[skew trace] cta %d: %d units in %.1f us: consumer full-wait %.1f us, compute %.1f us; "
-                            "producer empty-wait %.1f us, issue %.1f us\n",
-                    cta, nu, (tend - t0) / 1e3, full_wait / 1e3, compute / 1e3, empty_wait / 1e3, issue / 1e3);
-            if (cta == 0)
-                for (int m = 0; m < 12; ++m)
-                    fprintf(stderr, "   item %-3d wanted %6.0f readied %6.0f idone-arrived(w0) %6.0f published %6.0f\n", m,
-                            (Y[m * 4 + 3] - t0) / 1.0, (Y[m * 4 + 0] - t0) / 1.0, (Y[m * 4 + 2] - t0) / 1.0,
-                            (Y[m * 4 + 1] - t0) / 1.0);
-            if (cta == 0)
-                for (int u = 0; u < 12 && u < nu; ++u)
-                    fprintf(stderr, "   u%-3d cons wait %6.0f..%6.0f done %6.0f empty-arrived %6.0f | prod %6.0f..%6.0f issued %6.0f\n", u,
-                            (C[u * 4] - t0) / 1.0, (C[u * 4 + 1] - t0) / 1.0, (C[u * 4 + 2] - t0) / 1.0, (C[u * 4 + 3] - t0) / 1.0,
-                            (P[u * 4] - t0) / 1.0, (P[u * 4 + 1] - t0) / 1.0, (P[u * 4 + 2] - t0) / 1.0);
+            fprintf(stderr, "[skew trace] cta %d: %d units: full-wait %.1f us, unit work %.1f us, between units %.1f us\n",
+                    cta, nu, full_wait / 1e3, compute / 1e3, gaps / 1e3);
+            if (cta == 0) {
+                for (int m = 0; m < 6; ++m)
+                    fprintf(stderr, "   item %d ready at %.0f ns, published at %.0f ns\n", m,
+                            Y[m * 4] ? (double)(Y[m * 4] - t0) : -1.0, Y[m * 4 + 1] ? (double)(Y[m * 4 + 1] - t0) : -1.0);
+                for (int u = 0; u < 8 && u < nu; ++u)
+                    fprintf(stderr, "   unit %d: wait %.0f..%.0f done %.0f ns\n", u, (double)(C[u * 4] - t0),
+                            (double)(C[u * 4 + 1] - t0), (double)(C[u * 4 + 2] - t0));
+            }
         }
     }
     ++h->launches;
