@@ -371,7 +371,11 @@ const char *nsm_solver_last_error(const nsm_amg *M);
  * the implicit relative residual < tol or after maxit iterations.
  * M = NULL: no preconditioner.  *iters = Krylov dimension m; hist (NULL or
  * maxit + 1 entries) receives the implicit relative residuals.  b, x device,
- * length n; synchronises `stream`.  Allocates (maxit + 1) n-vectors. */
+ * length n; synchronises `stream`.  Workspace (the Krylov basis, grown in
+ * blocks of columns as the iteration needs them, pinned host buffers, the
+ * captured V-cycle graph) is kept in M across calls and freed by
+ * nsm_amg_destroy; with M = NULL it is allocated and freed per call.  One M
+ * must not be used by concurrent nsm_gmres calls. */
 nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int maxit, double tol, int t_mode,
                      int *iters, double *hist, void *stream);
 

@@ -135,8 +135,33 @@ struct nsm_spmat {
     double *va = nullptr;
 };
 
+// GMRES workspace, kept across nsm_gmres calls (in the preconditioner object):
+// the Krylov basis grows on demand, host buffers are pinned, and the captured
+// V-cycle + SpMV graph is reused until the operator, the stream or a smoother
+// setting changes.
+struct GmresWs {
+    int device = 0;
+    int64_t n = -1;
+    int cap = 0;                       // basis columns allocated
+    int m1cap = 0;                     // reduction buffers sized for this many columns
+    int nblk = 1;
+    double *V = nullptr, *u = nullptr, *w = nullptr, *z = nullptr, *part = nullptr, *red = nullptr, *hd = nullptr;
+    double *hred = nullptr, *hh = nullptr;  // pinned host mirrors
+    cudaGraphExec_t gexec = nullptr;
+    const nsm_handle *gA = nullptr;    // what the graph was captured for
+    cudaStream_t gs = nullptr;
+    bool stale = true;
+    void release() {
+        cudaFree(V); cudaFree(u); cudaFree(w); cudaFree(z); cudaFree(part); cudaFree(red); cudaFree(hd);
+        cudaFreeHost(hred); cudaFreeHost(hh);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        *this = GmresWs();
+    }
+};
+
 struct nsm_amg {
     int device = 0, nlevels = 0;
+    GmresWs ws;
     std::vector<nsm_handle *> S;          // borrowed smoother handles, levels 0 .. nlevels-1
     std::vector<nsm_spmat *> P, R;        // owned transfer operators
     std::vector<int64_t> n;               // level sizes 0 .. nlevels
@@ -299,6 +324,7 @@ void nsm_amg_destroy(nsm_amg *M) {
     for (double *p : M->x) cudaFree(p);
     for (double *p : M->r) cudaFree(p);
     cudaFree(M->Minv);
+    M->ws.release();
     delete M;
 }
 
@@ -376,6 +402,7 @@ nsm_status nsm_amg_setup(nsm_amg **out, int nlevels, nsm_handle *const *smoother
 nsm_status nsm_amg_set_smoother(nsm_amg *M, int level, nsm_kind kind, int nu_pre, int nu_post, int k_l, int k_u) {
     if (!M || level < 0 || level >= M->nlevels || nu_pre < 0 || nu_post < 0 || k_l < 0 || k_u < 0) return NSM_ERR_ARG;
     M->cfg[level] = nsm_amg::Cfg{kind, nu_pre, nu_post, k_l, k_u};
+    M->ws.stale = true;  // the captured V-cycle graph no longer matches
     return NSM_OK;
 }
 
@@ -398,21 +425,59 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
     int64_t n = 0;
     nsm_info(A, &n, nullptr, nullptr, nullptr);
     const int m1 = maxit + 1;
-    double *V = nullptr, *u = nullptr, *w = nullptr, *z = nullptr, *part = nullptr, *red = nullptr, *hd = nullptr;
-    const int nblk = (int)std::min<int64_t>(1184, std::max<int64_t>(1, n / 2048));
-    auto cleanup = [&]() { cudaFree(V); cudaFree(u); cudaFree(w); cudaFree(z); cudaFree(part); cudaFree(red); cudaFree(hd); };
-    if (cudaMalloc(&V, (size_t)m1 * std::max<int64_t>(n, 1) * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&u, std::max<int64_t>(n, 1) * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&w, std::max<int64_t>(n, 1) * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&z, std::max<int64_t>(n, 1) * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&part, (size_t)nblk * 2 * (m1 + 1) * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&red, 2 * (size_t)(m1 + 1) * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&hd, (size_t)(m1 + 1) * sizeof(double)) != cudaSuccess) {
-        cleanup();
+    GmresWs local;
+    GmresWs &W = M ? M->ws : local;   // persistent with a preconditioner object
+    auto grow = [&](int cols) -> bool {  // basis capacity >= cols (keeps columns 0 .. cap-1)
+        if (cols <= W.cap) return true;
+        const int nc = std::min(m1, std::max(cols, std::max(32, 2 * W.cap)));
+        double *nv = nullptr;
+        if (cudaMalloc(&nv, (size_t)nc * std::max<int64_t>(n, 1) * sizeof(double)) != cudaSuccess) return false;
+        if (W.V && W.cap > 0 &&
+            cudaMemcpyAsync(nv, W.V, (size_t)W.cap * n * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return false;
+        cudaStreamSynchronize(s);
+        cudaFree(W.V);
+        W.V = nv;
+        W.cap = nc;
+        return true;
+    };
+    bool ok = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (W.n != n || W.device != dev) {   // new operator size or device: start over
+        W.release();
+        W.n = n;
+        W.device = dev;
+        W.nblk = (int)std::min<int64_t>(1184, std::max<int64_t>(1, n / 2048));
+        ok = cudaMalloc(&W.u, std::max<int64_t>(n, 1) * sizeof(double)) == cudaSuccess &&
+             cudaMalloc(&W.w, std::max<int64_t>(n, 1) * sizeof(double)) == cudaSuccess &&
+             cudaMalloc(&W.z, std::max<int64_t>(n, 1) * sizeof(double)) == cudaSuccess;
+    }
+    if (ok && W.m1cap < m1) {
+        cudaFree(W.part); cudaFree(W.red); cudaFree(W.hd); cudaFreeHost(W.hred); cudaFreeHost(W.hh);
+        W.part = W.red = W.hd = W.hred = W.hh = nullptr;
+        ok = cudaMalloc(&W.part, (size_t)W.nblk * 2 * (m1 + 1) * sizeof(double)) == cudaSuccess &&
+             cudaMalloc(&W.red, 2 * (size_t)(m1 + 1) * sizeof(double)) == cudaSuccess &&
+             cudaMalloc(&W.hd, (size_t)(m1 + 1) * sizeof(double)) == cudaSuccess &&
+             cudaMallocHost(&W.hred, 2 * (size_t)(m1 + 1) * sizeof(double)) == cudaSuccess &&
+             cudaMallocHost(&W.hh, (size_t)(m1 + 1) * sizeof(double)) == cudaSuccess;
+        W.m1cap = ok ? m1 : 0;
+    }
+    ok = ok && grow(std::min(m1, 32));
+    if (!ok) {
+        cudaGetLastError();
+        if (!M) local.release();
         g_solver_err = "nsm_gmres: device allocation failed";
         return NSM_ERR_OOM;
     }
-    cudaGraphExec_t gexec = nullptr;
+    double *V = W.V, *u = W.u, *w = W.w, *z = W.z, *part = W.part, *red = W.red, *hd = W.hd;
+    const int nblk = W.nblk;
+    auto cleanup = [&]() { if (!M) local.release(); };
+    if (W.gexec && (W.stale || W.gA != A || W.gs != s)) {
+        cudaGraphExecDestroy(W.gexec);
+        W.gexec = nullptr;
+    }
+    cudaGraphExec_t &gexec = W.gexec;
     bool use_graph = !nsm_is_distributed(A);
     if (M)
         for (nsm_handle *S : M->S) use_graph = use_graph && !nsm_is_distributed(S);
@@ -422,7 +487,8 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
                                                                                                        : NSM_ERR_CUDA;
     };
     std::vector<double> Lm((size_t)m1 * m1, 0.0), H((size_t)m1 * maxit, 0.0), cs(maxit), sn(maxit), g(m1 + 1, 0.0);
-    std::vector<double> hred(2 * (m1 + 1)), zc, h;
+    std::vector<double> zc, h;
+    double *hred = W.hred;
     auto Hat = [&](int i, int j) -> double & { return H[(size_t)i * maxit + j]; };
     nsm_status st = NSM_OK;
     double beta = 0.0;
@@ -444,6 +510,9 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
                     if (st == NSM_OK) st = nsm_spmv(A, z, w, s);
                     ok = cudaStreamEndCapture(s, &graph) == cudaSuccess && st == NSM_OK &&
                          cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
+                    W.gA = A;
+                    W.gs = s;
+                    W.stale = false;
                     if (graph) cudaGraphDestroy(graph);
                 }
                 if (!ok) {  // fall back to plain launches
@@ -465,7 +534,7 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
         // step 6: the single reduction [V_k, u]^T [u, w]
         k_multidot<<<nblk, kThr, 0, s>>>(n, k, V, u, k < maxit ? w : u, part);
         k_sum_parts<<<(2 * (k + 1) + 127) / 128, 128, 0, s>>>(nblk, 2 * (k + 1), part, red);
-        cudaMemcpyAsync(hred.data(), red, 2 * (k + 1) * sizeof(double), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(hred, red, 2 * (k + 1) * sizeof(double), cudaMemcpyDeviceToHost, s);
         if (cudaStreamSynchronize(s) != cudaSuccess) { st = NSM_ERR_CUDA; break; }
         const double nu = hred[2 * k], mu = hred[2 * k + 1];
         const double rho = std::sqrt(nu);                     // step 7 (lagged norm)
@@ -490,6 +559,8 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
         }
         if (rho == 0.0) { m = k; break; }                     // exact solution (happy breakdown)
         // step 8: v_k = u / rho
+        if (!grow(k + 1)) { st = NSM_ERR_OOM; break; }
+        V = W.V;
         k_scal<<<blocks(n), kThr, 0, s>>>(n, 1.0 / rho, u, V + (size_t)k * n);
         // steps 9-11: z = [c, mu/rho] / rho, L row k = a / rho, h = T z
         zc.assign(k + 1, 0.0);
@@ -510,7 +581,8 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
             Hat(i, k) = acc;
         }
         // step 12: u = w / rho - V_{k+1} h
-        cudaMemcpyAsync(hd, h.data(), (k + 1) * sizeof(double), cudaMemcpyHostToDevice, s);
+        std::copy(h.begin(), h.end(), W.hh);
+        cudaMemcpyAsync(hd, W.hh, (k + 1) * sizeof(double), cudaMemcpyHostToDevice, s);
         k_multiaxpy<<<blocks(n), kThr, 0, s>>>(n, k + 1, V, hd, 1.0 / rho, w, u);
         if (cudaGetLastError() != cudaSuccess) { st = NSM_ERR_CUDA; break; }
     }
@@ -523,7 +595,8 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
             y[i] = acc / Hat(i, i);
         }
         for (double &v : y) v = -v;                            // multiaxpy subtracts
-        cudaMemcpyAsync(hd, y.data(), m * sizeof(double), cudaMemcpyHostToDevice, s);
+        std::copy(y.begin(), y.end(), W.hh);
+        cudaMemcpyAsync(hd, W.hh, m * sizeof(double), cudaMemcpyHostToDevice, s);
         k_multiaxpy<<<blocks(n), kThr, 0, s>>>(n, m, V, hd, 0.0, nullptr, u);
         st = precond(u, x);
         if (cudaStreamSynchronize(s) != cudaSuccess) st = NSM_ERR_CUDA;
@@ -533,7 +606,6 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
     }
     if (iters) *iters = m;
     if (hist) std::copy(hv.begin(), hv.end(), hist);
-    if (gexec) cudaGraphExecDestroy(gexec);
     cleanup();
     if (st != NSM_OK && g_solver_err.empty()) g_solver_err = "nsm_gmres: failed";
     return st;
