@@ -299,7 +299,8 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 a.flag = h->flag;
                                 a.sweep_id = sid;
                                 a.pdl = h->pdl;
-                                if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(1, st.T->maxw))
+                                if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(1, st.T->maxw) &&
+                                    !wide_rows(st.T->maxw, h->nslices))
                                     return launch_sweep_tma(a, sl.begin, sl.end, s);
                                 return launch_sweep(a, s);
                             },
@@ -314,7 +315,8 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
 nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double *out, int mode, cudaStream_t s,
                          double *out2 = nullptr) {
     return pass(h, true, x, nullptr, s, [&](const Slices &sl, bool with_ghost, const double *ghost) {
-        if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(2, std::max(h->L.maxw, h->U.maxw)))
+        if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(2, std::max(h->L.maxw, h->U.maxw)) &&
+            !wide_rows(std::max(h->L.maxw, h->U.maxw), h->nslices))
             return launch_residual_tma(mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
         return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
                                out, out2, s);

@@ -231,6 +231,107 @@ __global__ void __launch_bounds__(kThreads) k_sweep(int64_t n, int nslices, cons
     if (EPI == EPI_XADD_SCALE) x[i] = __dadd_rn(xi, __ddiv_rn(v, dn));
 }
 
+// ---- wide rows (coarse AMG levels): one warp per row --------------------------
+// Galerkin rows have 50-100+ entries while the levels are small (a few to a
+// few hundred slices), so one thread per row leaves the SMs idle and each
+// thread walks a long dependent chain.  Here the 32 lanes form the products of
+// 32 consecutive entries of ONE row at once (their gathers in flight
+// together) and every lane then adds them in stored order through shuffles —
+// the same sequence of IEEE operations as the thread-per-row kernels, so the
+// results are bit-identical.  Padding entries (val 0) take part exactly as
+// there.
+template <class G>
+__device__ __forceinline__ double accum_row_warp(const SellView P, int64_t s, int rr, int lane, const G &g,
+                                                 double acc) {
+    const int64_t b = __ldg(P.ptr + s), e = __ldg(P.ptr + s + 1);
+    const int w = (int)((e - b) / kSlice);
+    for (int j0 = 0; j0 < w; j0 += 32) {
+        const int j = j0 + lane;
+        double pr = 0.0;
+        if (j < w) {
+            const int64_t p = b + (int64_t)j * kSlice + rr;
+            pr = __dmul_rn(__ldg(P.val + p), g(__ldg(P.col + p)));
+        }
+        const int m = min(32, w - j0);
+        for (int t = 0; t < m; ++t) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, pr, t));
+    }
+    return acc;
+}
+
+__device__ __forceinline__ bool row_of(int nslices, const int32_t *list, int64_t *s, int *rr) {
+    const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    if (gw >= (int64_t)nslices * kSlice) return false;
+    const int64_t k = gw / kSlice;
+    *s = list ? (int64_t)list[k] : k;
+    *rr = (int)(gw - k * kSlice);
+    return true;
+}
+
+template <int OUT>
+__global__ void __launch_bounds__(kThreads) k_residual_wide(int64_t n, int nslices, const int32_t *__restrict__ list,
+                                                            SellView LG, SellView L, SellView U, SellView UG,
+                                                            int has_ghost, const double *__restrict__ d,
+                                                            const double *__restrict__ b,
+                                                            const double *__restrict__ x,
+                                                            const double *__restrict__ ghost,
+                                                            double *__restrict__ out, double *__restrict__ out2) {
+    int64_t s;
+    int rr;
+    if (!row_of(nslices, list, &s, &rr)) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = s * kSlice + rr;
+    if (i >= n) return;  // whole warp
+    const GatherPlain gx{x};
+    double acc = 0.0;
+    if (has_ghost) acc = accum_row_warp(LG, s, rr, lane, GatherPlain{ghost}, acc);
+    acc = accum_row_warp(L, s, rr, lane, gx, acc);
+    const double di = __ldg(d + i);
+    acc = __dadd_rn(acc, __dmul_rn(di, __ldg(x + i)));
+    acc = accum_row_warp(U, s, rr, lane, gx, acc);
+    if (has_ghost) acc = accum_row_warp(UG, s, rr, lane, GatherPlain{ghost}, acc);
+    if (lane != 0) return;
+    if (OUT == OUT_AX) {
+        out[i] = acc;
+    } else {
+        const double r = __dsub_rn(__ldg(b + i), acc);
+        out[i] = r;
+        if (OUT == OUT_RG) out2[i] = __ddiv_rn(r, di);
+    }
+}
+
+template <bool UNIT, int EPI, class G>
+__global__ void __launch_bounds__(kThreads) k_sweep_wide(int64_t n, int nslices, const int32_t *__restrict__ list,
+                                                         SellView T, SellView TG, int has_ghost,
+                                                         const double *__restrict__ dT,
+                                                         const double *__restrict__ rhs, G gin,
+                                                         const double *__restrict__ ghost, double *__restrict__ gout,
+                                                         double *__restrict__ x, const double *__restrict__ dnext,
+                                                         double *__restrict__ gout2, unsigned long long *flag,
+                                                         int64_t sweep_id) {
+    int64_t s;
+    int rr;
+    if (!row_of(nslices, list, &s, &rr)) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = s * kSlice + rr;
+    if (i >= n) return;
+    double acc = 0.0;
+    if (has_ghost == 1) acc = accum_row_warp(TG, s, rr, lane, GatherPlain{ghost}, acc);
+    acc = accum_row_warp(T, s, rr, lane, gin, acc);
+    if (has_ghost == 2) acc = accum_row_warp(TG, s, rr, lane, GatherPlain{ghost}, acc);
+    if (lane != 0) return;
+    double v = __dsub_rn(__ldg(rhs + i), acc);
+    if (!UNIT) v = __ddiv_rn(v, __ldg(dT + i));
+    flag_nonfinite(v, flag, sweep_id);
+    if (EPI == EPI_STORE) gout[i] = v;
+    if (EPI == EPI_XADD) x[i] = __dadd_rn(x[i], v);
+    if (EPI == EPI_STORE2) { gout[i] = v; gout2[i] = __ddiv_rn(v, __ldg(dnext + i)); }
+    if (EPI == EPI_XADD_SCALE) x[i] = __dadd_rn(x[i], __ddiv_rn(v, __ldg(dnext + i)));
+}
+
+inline unsigned grid_wide(int nslices) {
+    return (unsigned)(((int64_t)nslices * kSlice + (kThreads / 32) - 1) / (kThreads / 32));
+}
+
 // ---- diagonal scaling:  out = rhs / d  or  x += rhs / d  (k = 0 cases) -------
 template <bool XADD>
 __global__ void __launch_bounds__(kThreads) k_scale(int64_t n, const double *__restrict__ rhs,
@@ -248,6 +349,10 @@ inline unsigned grid_for(int nslices) { return (unsigned)((nslices + kSlicesPerC
 }  // namespace
 
 // ---------------------------------------------------------------- launchers --
+// Rows wider than 24 entries on a small level (<= 4096 rows: too few slices
+// to fill the GPU one thread per row): warp per row.
+bool wide_rows(int maxw, int64_t nslices) { return maxw > 24 && nslices * kSlice <= 4096; }
+
 // Register chunk CH: the smallest of 4 / 8 / 16 covering the widest slice
 // (wider rows continue in the plain loop).
 static inline int chunk_for(int maxw) { return maxw <= 4 ? 4 : (maxw <= 8 ? 8 : 16); }
@@ -265,6 +370,16 @@ cudaError_t launch_residual(int out_mode, int64_t n, int nslices, const int32_t 
                             const double *b, const double *x, const double *ghost, double *out, double *out2,
                             cudaStream_t st) {
     if (nslices <= 0) return cudaSuccess;
+    if (wide_rows(std::max(L.maxw, U.maxw), nslices)) {
+        const SellView lg = view(LG), l = view(L), u = view(U), ug = view(UG);
+        if (out_mode == OUT_AX)
+            k_residual_wide<OUT_AX><<<grid_wide(nslices), kThreads, 0, st>>>(n, nslices, list, lg, l, u, ug, has_ghost, d, b, x, ghost, out, out2);
+        else if (out_mode == OUT_RG)
+            k_residual_wide<OUT_RG><<<grid_wide(nslices), kThreads, 0, st>>>(n, nslices, list, lg, l, u, ug, has_ghost, d, b, x, ghost, out, out2);
+        else
+            k_residual_wide<OUT_R><<<grid_wide(nslices), kThreads, 0, st>>>(n, nslices, list, lg, l, u, ug, has_ghost, d, b, x, ghost, out, out2);
+        return cudaGetLastError();
+    }
     const int ch = chunk_for(std::max(L.maxw, U.maxw));
 #define NSM_RES(OUT)                                                                                              \
     (ch == 4 ? residual_ch<OUT, 4>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, st)      \
@@ -296,7 +411,28 @@ static void sweep_ch(const SweepArgs &a, cudaStream_t st) {
 }
 
 template <bool UNIT, int EPI>
+static void sweep_wide(const SweepArgs &a, cudaStream_t st) {
+    const dim3 g(grid_wide(a.nslices));
+    const SellView TG = a.TG ? view(*a.TG) : SellView{nullptr, nullptr, nullptr};
+    if constexpr (!UNIT) {
+        if (a.gin_scaled) {
+            k_sweep_wide<UNIT, EPI, GatherScaled><<<g, kThreads, 0, st>>>(
+                a.n, a.nslices, a.list, view(*a.T), TG, a.has_ghost, a.dT, a.rhs, GatherScaled{a.rhs, a.dT}, a.ghost,
+                a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
+            return;
+        }
+    }
+    k_sweep_wide<UNIT, EPI, GatherPlain><<<g, kThreads, 0, st>>>(
+        a.n, a.nslices, a.list, view(*a.T), TG, a.has_ghost, a.dT, a.rhs, GatherPlain{a.gin_scaled ? a.rhs : a.gin},
+        a.ghost, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
+}
+
+template <bool UNIT, int EPI>
 static void sweep_epi(const SweepArgs &a, cudaStream_t st) {
+    if (wide_rows(a.T->maxw, a.nslices)) {
+        sweep_wide<UNIT, EPI>(a, st);
+        return;
+    }
     switch (chunk_for(a.T->maxw)) {
         case 4: sweep_ch<UNIT, EPI, 4>(a, st); break;
         case 8: sweep_ch<UNIT, EPI, 8>(a, st); break;
@@ -344,6 +480,23 @@ void touch(K k) {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, k);
 }
+void touch_wide() {
+    touch(k_residual_wide<OUT_R>);
+    touch(k_residual_wide<OUT_AX>);
+    touch(k_residual_wide<OUT_RG>);
+    touch(k_sweep_wide<true, EPI_STORE, GatherPlain>);
+    touch(k_sweep_wide<true, EPI_XADD, GatherPlain>);
+    touch(k_sweep_wide<true, EPI_XADD_SCALE, GatherPlain>);
+    touch(k_sweep_wide<true, EPI_STORE2, GatherPlain>);
+    touch(k_sweep_wide<false, EPI_STORE2, GatherPlain>);
+    touch(k_sweep_wide<false, EPI_STORE2, GatherScaled>);
+    touch(k_sweep_wide<false, EPI_STORE, GatherPlain>);
+    touch(k_sweep_wide<false, EPI_XADD, GatherPlain>);
+    touch(k_sweep_wide<false, EPI_XADD_SCALE, GatherPlain>);
+    touch(k_sweep_wide<false, EPI_STORE, GatherScaled>);
+    touch(k_sweep_wide<false, EPI_XADD, GatherScaled>);
+    touch(k_sweep_wide<false, EPI_XADD_SCALE, GatherScaled>);
+}
 template <int CH>
 void touch_ch() {
     touch(k_residual<OUT_R, CH>);
@@ -365,6 +518,7 @@ void touch_ch() {
 }  // namespace
 
 void preload_plain_kernels() {
+    touch_wide();
     touch_ch<4>();
     touch_ch<8>();
     touch_ch<16>();

@@ -48,6 +48,29 @@ __global__ void __launch_bounds__(kThr) k_csr_spmv(int64_t nrows, const int64_t 
     y[i] = beta == 0.0 ? v : __dadd_rn(v, __dmul_rn(beta, y[i]));
 }
 
+// the same for small operators with wide rows (restriction R = P^T onto a
+// coarse level): one warp per row, products of 32 entries at once, added in
+// ascending column order through shuffles (bit-identical to k_csr_spmv)
+__global__ void __launch_bounds__(kThr) k_csr_spmv_wide(int64_t nrows, const int64_t *__restrict__ rp,
+                                                        const int32_t *__restrict__ ci,
+                                                        const double *__restrict__ va, const double *__restrict__ x,
+                                                        double *__restrict__ y, double alpha, double beta) {
+    const int64_t i = ((int64_t)blockIdx.x * kThr + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= nrows) return;
+    double s = 0.0;
+    const int64_t b = __ldg(rp + i), e = __ldg(rp + i + 1);
+    for (int64_t p0 = b; p0 < e; p0 += 32) {
+        const int64_t p = p0 + lane;
+        const double pr = p < e ? __dmul_rn(__ldg(va + p), __ldg(x + __ldg(ci + p))) : 0.0;
+        const int m = (int)(e - p0 < 32 ? e - p0 : 32);
+        for (int t = 0; t < m; ++t) s = __dadd_rn(s, __shfl_sync(0xffffffffu, pr, t));
+    }
+    if (lane != 0) return;
+    const double v = __dmul_rn(alpha, s);
+    y[i] = beta == 0.0 ? v : __dadd_rn(v, __dmul_rn(beta, y[i]));
+}
+
 // y = Minv x, dense row-major n x n (coarse-level solve): one warp per row
 __global__ void __launch_bounds__(kThr) k_dense_gemv(int n, const double *__restrict__ Minv,
                                                      const double *__restrict__ x, double *__restrict__ y) {
@@ -129,7 +152,7 @@ inline unsigned blocks(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + k
 // ------------------------------------------------------------ sparse matrix --
 struct nsm_spmat {
     int device = 0;
-    int64_t nrows = 0, ncols = 0, nnz = 0;
+    int64_t nrows = 0, ncols = 0, nnz = 0, maxrow = 0;
     int64_t *rp = nullptr;
     int32_t *ci = nullptr;
     double *va = nullptr;
@@ -227,6 +250,7 @@ nsm_status spmat_from_host(const nsm_csr *M, int device, nsm_spmat **out, std::s
     S->nrows = M->nrows;
     S->ncols = M->ncols;
     S->nnz = nnz;
+    for (int64_t i = 0; i < M->nrows; ++i) S->maxrow = std::max(S->maxrow, M->rowptr[i + 1] - M->rowptr[i]);
     bool ok = cudaMalloc(&S->rp, (M->nrows + 1) * sizeof(int64_t)) == cudaSuccess &&
               cudaMalloc(&S->ci, std::max<int64_t>(nnz, 1) * sizeof(int32_t)) == cudaSuccess &&
               cudaMalloc(&S->va, std::max<int64_t>(nnz, 1) * sizeof(double)) == cudaSuccess &&
@@ -244,7 +268,10 @@ nsm_status spmat_from_host(const nsm_csr *M, int device, nsm_spmat **out, std::s
 
 cudaError_t spmat_apply(const nsm_spmat *M, const double *x, double *y, double alpha, double beta, cudaStream_t s) {
     if (M->nrows == 0) return cudaSuccess;
-    k_csr_spmv<<<blocks(M->nrows), kThr, 0, s>>>(M->nrows, M->rp, M->ci, M->va, x, y, alpha, beta);
+    if (M->maxrow > 24 && M->nrows <= 4096)  // few, wide rows: warp per row
+        k_csr_spmv_wide<<<blocks(M->nrows * 32), kThr, 0, s>>>(M->nrows, M->rp, M->ci, M->va, x, y, alpha, beta);
+    else
+        k_csr_spmv<<<blocks(M->nrows), kThr, 0, s>>>(M->nrows, M->rp, M->ci, M->va, x, y, alpha, beta);
     return cudaGetLastError();
 }
 
