@@ -248,6 +248,14 @@ nsm_status pass(nsm_handle *h, bool exchange, const double *src, const double *s
     return NSM_OK;
 }
 
+// Bulk-copy pipelined kernels for contiguous slice ranges, unless the rows
+// are too wide to stage or the level is small with wide rows (warp-per-row
+// kernels).  (Plain kernels on mid-sized AMG levels, 50K-300K rows, were
+// measured 15-40 % slower: profiles/r01_solver_solve_timing.md.)
+bool use_pipelined(const nsm_handle *h, const Slices &sl, bool with_ghost, int np, int maxw) {
+    return h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(np, maxw) && !wide_rows(maxw, h->nslices);
+}
+
 // One stage of a Jacobi-iterated triangular solve: k >= 1 sweeps on T from
 // g^(0) = rhs / dT (recomputed in the first sweep's gather), the final
 // iterate written with epilogue last_epi.  bufA/bufB: ping-pong scratch.
@@ -299,8 +307,7 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 a.flag = h->flag;
                                 a.sweep_id = sid;
                                 a.pdl = h->pdl;
-                                if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(1, st.T->maxw) &&
-                                    !wide_rows(st.T->maxw, h->nslices))
+                                if (use_pipelined(h, sl, with_ghost, 1, st.T->maxw))
                                     return launch_sweep_tma(a, sl.begin, sl.end, s);
                                 return launch_sweep(a, s);
                             },
@@ -315,8 +322,7 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
 nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double *out, int mode, cudaStream_t s,
                          double *out2 = nullptr) {
     return pass(h, true, x, nullptr, s, [&](const Slices &sl, bool with_ghost, const double *ghost) {
-        if (h->pipeline && sl.begin >= 0 && !with_ghost && tma_ok(2, std::max(h->L.maxw, h->U.maxw)) &&
-            !wide_rows(std::max(h->L.maxw, h->U.maxw), h->nslices))
+        if (use_pipelined(h, sl, with_ghost, 2, std::max(h->L.maxw, h->U.maxw)))
             return launch_residual_tma(mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
         return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
                                out, out2, s);
