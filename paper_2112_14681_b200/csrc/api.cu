@@ -325,12 +325,12 @@ nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double
         if (use_pipelined(h, sl, with_ghost, 2, std::max(h->L.maxw, h->U.maxw)))
             return launch_residual_tma(mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
         return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
-                               out, out2, s);
+                               out, out2, h->pdl, s);
     }, 0);
 }
 
 nsm_status scale_into(nsm_handle *h, bool xadd, const double *rhs, const double *d, double *out, cudaStream_t s) {
-    cudaError_t e = launch_scale(xadd, h->n, rhs, d, out, h->flag, ++h->sweep_counter, s);
+    cudaError_t e = launch_scale(xadd, h->n, rhs, d, out, h->flag, ++h->sweep_counter, h->pdl, s);
     if (h->n > 0) ++h->launches;
     return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "scale launch");
 }

@@ -139,6 +139,15 @@ __device__ __forceinline__ bool slice_of(int nslices, const int32_t *list, int64
     return true;
 }
 
+// Programmatic dependent launch (launches with pdl = true): a kernel may be
+// scheduled while its predecessor drains; it waits for the predecessor's
+// completion (and memory) before touching ANY memory, then lets its own
+// dependents be scheduled.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 // ---- residual / SpMV (row a2) ------------------------------------------------
 // acc_i = sum_{j ascending} a_ij x_j over LG (ghosts below), L, D, U, UG
 // (ghosts above); then  OUT_R: r = b - acc;  OUT_AX: y = acc;  OUT_RG: r and
@@ -151,6 +160,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(int64_t n, int nslices, c
                                                        const double *__restrict__ d, const double *__restrict__ b,
                                                        const double *__restrict__ x, const double *__restrict__ ghost,
                                                        double *__restrict__ out, double *__restrict__ out2) {
+    pdl_enter();
     int64_t s;
     int lane;
     if (!slice_of(nslices, list, &s, &lane)) return;
@@ -202,6 +212,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep(int64_t n, int nslices, cons
                                                     double *__restrict__ gout, double *__restrict__ x,
                                                     const double *__restrict__ dnext, double *__restrict__ gout2,
                                                     unsigned long long *flag, int64_t sweep_id) {
+    pdl_enter();
     int64_t s;
     int lane;
     if (!slice_of(nslices, list, &s, &lane)) return;
@@ -275,6 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_residual_wide(int64_t n, int nslic
                                                             const double *__restrict__ x,
                                                             const double *__restrict__ ghost,
                                                             double *__restrict__ out, double *__restrict__ out2) {
+    pdl_enter();
     int64_t s;
     int rr;
     if (!row_of(nslices, list, &s, &rr)) return;
@@ -308,6 +320,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep_wide(int64_t n, int nslices,
                                                          double *__restrict__ x, const double *__restrict__ dnext,
                                                          double *__restrict__ gout2, unsigned long long *flag,
                                                          int64_t sweep_id) {
+    pdl_enter();
     int64_t s;
     int rr;
     if (!row_of(nslices, list, &s, &rr)) return;
@@ -337,6 +350,7 @@ template <bool XADD>
 __global__ void __launch_bounds__(kThreads) k_scale(int64_t n, const double *__restrict__ rhs,
                                                     const double *__restrict__ d, double *__restrict__ out,
                                                     unsigned long long *flag, int64_t sweep_id) {
+    pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     if (i >= n) return;
     const double v = d ? __ddiv_rn(__ldg(rhs + i), __ldg(d + i)) : __ldg(rhs + i);
@@ -345,6 +359,20 @@ __global__ void __launch_bounds__(kThreads) k_scale(int64_t n, const double *__r
 }
 
 inline unsigned grid_for(int nslices) { return (unsigned)((nslices + kSlicesPerCta - 1) / kSlicesPerCta); }
+
+template <class K, class... Args>
+void launch_k(bool pdl, K kernel, unsigned grid, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 
 }  // namespace
 
@@ -360,31 +388,32 @@ static inline int chunk_for(int maxw) { return maxw <= 4 ? 4 : (maxw <= 8 ? 8 : 
 template <int OUT, int CH>
 static void residual_ch(int64_t n, int nslices, const int32_t *list, const Sell &LG, const Sell &L, const Sell &U,
                         const Sell &UG, bool has_ghost, const double *d, const double *b, const double *x,
-                        const double *ghost, double *out, double *out2, cudaStream_t st) {
-    k_residual<OUT, CH><<<grid_for(nslices), kThreads, 0, st>>>(n, nslices, list, view(LG), view(L), view(U),
-                                                                view(UG), has_ghost, d, b, x, ghost, out, out2);
+                        const double *ghost, double *out, double *out2, bool pdl, cudaStream_t st) {
+    launch_k(pdl, k_residual<OUT, CH>, grid_for(nslices), st, n, nslices, list, view(LG), view(L), view(U),
+             view(UG), (int)has_ghost, d, b, x, ghost, out, out2);
 }
 
 cudaError_t launch_residual(int out_mode, int64_t n, int nslices, const int32_t *list, const Sell &LG,
                             const Sell &L, const Sell &U, const Sell &UG, bool has_ghost, const double *d,
                             const double *b, const double *x, const double *ghost, double *out, double *out2,
-                            cudaStream_t st) {
+                            bool pdl, cudaStream_t st) {
     if (nslices <= 0) return cudaSuccess;
     if (wide_rows(std::max(L.maxw, U.maxw), nslices)) {
         const SellView lg = view(LG), l = view(L), u = view(U), ug = view(UG);
+        const int hg = has_ghost;
         if (out_mode == OUT_AX)
-            k_residual_wide<OUT_AX><<<grid_wide(nslices), kThreads, 0, st>>>(n, nslices, list, lg, l, u, ug, has_ghost, d, b, x, ghost, out, out2);
+            launch_k(pdl, k_residual_wide<OUT_AX>, grid_wide(nslices), st, n, nslices, list, lg, l, u, ug, hg, d, b, x, ghost, out, out2);
         else if (out_mode == OUT_RG)
-            k_residual_wide<OUT_RG><<<grid_wide(nslices), kThreads, 0, st>>>(n, nslices, list, lg, l, u, ug, has_ghost, d, b, x, ghost, out, out2);
+            launch_k(pdl, k_residual_wide<OUT_RG>, grid_wide(nslices), st, n, nslices, list, lg, l, u, ug, hg, d, b, x, ghost, out, out2);
         else
-            k_residual_wide<OUT_R><<<grid_wide(nslices), kThreads, 0, st>>>(n, nslices, list, lg, l, u, ug, has_ghost, d, b, x, ghost, out, out2);
+            launch_k(pdl, k_residual_wide<OUT_R>, grid_wide(nslices), st, n, nslices, list, lg, l, u, ug, hg, d, b, x, ghost, out, out2);
         return cudaGetLastError();
     }
     const int ch = chunk_for(std::max(L.maxw, U.maxw));
 #define NSM_RES(OUT)                                                                                              \
-    (ch == 4 ? residual_ch<OUT, 4>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, st)      \
-             : ch == 8 ? residual_ch<OUT, 8>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, st) \
-                       : residual_ch<OUT, 16>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, st))
+    (ch == 4 ? residual_ch<OUT, 4>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, pdl, st)      \
+             : ch == 8 ? residual_ch<OUT, 8>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, pdl, st) \
+                       : residual_ch<OUT, 16>(n, nslices, list, LG, L, U, UG, has_ghost, d, b, x, ghost, out, out2, pdl, st))
     if (out_mode == OUT_AX) NSM_RES(OUT_AX);
     else if (out_mode == OUT_RG) NSM_RES(OUT_RG);
     else NSM_RES(OUT_R);
@@ -398,14 +427,14 @@ static void sweep_ch(const SweepArgs &a, cudaStream_t st) {
     SellView TG = a.TG ? view(*a.TG) : SellView{nullptr, nullptr, nullptr};
     if constexpr (!UNIT) {
         if (a.gin_scaled) {
-            k_sweep<UNIT, EPI, GatherScaled, CH><<<g, kThreads, 0, st>>>(
+            launch_k(a.pdl, k_sweep<UNIT, EPI, GatherScaled, CH>, g.x, st,
                 a.n, a.nslices, a.list, view(*a.T), TG, a.has_ghost, a.dT, a.rhs, GatherScaled{a.rhs, a.dT}, a.ghost,
                 a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
             return;
         }
     }
     // unit diagonal: g^(0) = rhs itself
-    k_sweep<UNIT, EPI, GatherPlain, CH><<<g, kThreads, 0, st>>>(
+    launch_k(a.pdl, k_sweep<UNIT, EPI, GatherPlain, CH>, g.x, st,
         a.n, a.nslices, a.list, view(*a.T), TG, a.has_ghost, a.dT, a.rhs, GatherPlain{a.gin_scaled ? a.rhs : a.gin},
         a.ghost, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
 }
@@ -416,13 +445,13 @@ static void sweep_wide(const SweepArgs &a, cudaStream_t st) {
     const SellView TG = a.TG ? view(*a.TG) : SellView{nullptr, nullptr, nullptr};
     if constexpr (!UNIT) {
         if (a.gin_scaled) {
-            k_sweep_wide<UNIT, EPI, GatherScaled><<<g, kThreads, 0, st>>>(
+            launch_k(a.pdl, k_sweep_wide<UNIT, EPI, GatherScaled>, g.x, st,
                 a.n, a.nslices, a.list, view(*a.T), TG, a.has_ghost, a.dT, a.rhs, GatherScaled{a.rhs, a.dT}, a.ghost,
                 a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
             return;
         }
     }
-    k_sweep_wide<UNIT, EPI, GatherPlain><<<g, kThreads, 0, st>>>(
+    launch_k(a.pdl, k_sweep_wide<UNIT, EPI, GatherPlain>, g.x, st,
         a.n, a.nslices, a.list, view(*a.T), TG, a.has_ghost, a.dT, a.rhs, GatherPlain{a.gin_scaled ? a.rhs : a.gin},
         a.ghost, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id);
 }
@@ -458,11 +487,11 @@ cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t st) {
 }
 
 cudaError_t launch_scale(bool xadd, int64_t n, const double *rhs, const double *d, double *out,
-                         unsigned long long *flag, int64_t sweep_id, cudaStream_t st) {
+                         unsigned long long *flag, int64_t sweep_id, bool pdl, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     unsigned g = (unsigned)((n + kThreads - 1) / kThreads);
-    if (xadd) k_scale<true><<<g, kThreads, 0, st>>>(n, rhs, d, out, flag, sweep_id);
-    else k_scale<false><<<g, kThreads, 0, st>>>(n, rhs, d, out, flag, sweep_id);
+    if (xadd) launch_k(pdl, k_scale<true>, g, st, n, rhs, d, out, flag, sweep_id);
+    else launch_k(pdl, k_scale<false>, g, st, n, rhs, d, out, flag, sweep_id);
     return cudaGetLastError();
 }
 

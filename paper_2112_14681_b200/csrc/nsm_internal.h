@@ -92,13 +92,13 @@ enum { OUT_R = 0, OUT_AX = 1, OUT_RG = 2 };
 cudaError_t launch_residual(int out_mode, int64_t n, int nslices, const int32_t *list, const Sell &LG,
                             const Sell &L, const Sell &U, const Sell &UG, bool has_ghost, const double *d,
                             const double *b, const double *x, const double *ghost, double *out, double *out2,
-                            cudaStream_t st);
+                            bool pdl, cudaStream_t st);
 cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t st);
 // Wide rows on a small level (coarse AMG levels): the plain launchers use one
 // warp per row; the pipelined kernels are not used for them.
 bool wide_rows(int maxw, int64_t nslices);
 cudaError_t launch_scale(bool xadd, int64_t n, const double *rhs, const double *d, double *out,
-                         unsigned long long *flag, int64_t sweep_id, cudaStream_t st);
+                         unsigned long long *flag, int64_t sweep_id, bool pdl, cudaStream_t st);
 
 // ---- halo exchange (halo.cu) --------------------------------------------------
 // One outgoing message: entries rows[0..count) of the sent vector go to

@@ -24,11 +24,32 @@ namespace {
 
 constexpr int kThr = 256;
 
+// programmatic dependent launch (see kernels.cu): wait for the predecessor
+// before touching memory, then let dependents be scheduled
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+template <class K, class... Args>
+cudaError_t launch_pdl(K kernel, unsigned grid, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThr);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // y = alpha * M x + beta * y   (CSR, one thread per row, ascending columns)
 __global__ void __launch_bounds__(kThr) k_csr_spmv(int64_t nrows, const int64_t *__restrict__ rp,
                                                    const int32_t *__restrict__ ci, const double *__restrict__ va,
                                                    const double *__restrict__ x, double *__restrict__ y, double alpha,
                                                    double beta) {
+    pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * kThr + threadIdx.x;
     if (i >= nrows) return;
     double s = 0.0;
@@ -55,6 +76,7 @@ __global__ void __launch_bounds__(kThr) k_csr_spmv_wide(int64_t nrows, const int
                                                         const int32_t *__restrict__ ci,
                                                         const double *__restrict__ va, const double *__restrict__ x,
                                                         double *__restrict__ y, double alpha, double beta) {
+    pdl_enter();
     const int64_t i = ((int64_t)blockIdx.x * kThr + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= nrows) return;
@@ -74,6 +96,7 @@ __global__ void __launch_bounds__(kThr) k_csr_spmv_wide(int64_t nrows, const int
 // y = Minv x, dense row-major n x n (coarse-level solve): one warp per row
 __global__ void __launch_bounds__(kThr) k_dense_gemv(int n, const double *__restrict__ Minv,
                                                      const double *__restrict__ x, double *__restrict__ y) {
+    pdl_enter();
     const int row = (int)(((int64_t)blockIdx.x * kThr + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (row >= n) return;
     double s = 0.0;
@@ -269,9 +292,11 @@ nsm_status spmat_from_host(const nsm_csr *M, int device, nsm_spmat **out, std::s
 cudaError_t spmat_apply(const nsm_spmat *M, const double *x, double *y, double alpha, double beta, cudaStream_t s) {
     if (M->nrows == 0) return cudaSuccess;
     if (M->maxrow > 24 && M->nrows <= 4096)  // few, wide rows: warp per row
-        k_csr_spmv_wide<<<blocks(M->nrows * 32), kThr, 0, s>>>(M->nrows, M->rp, M->ci, M->va, x, y, alpha, beta);
+        launch_pdl(k_csr_spmv_wide, blocks(M->nrows * 32), s, M->nrows, (const int64_t *)M->rp, (const int32_t *)M->ci,
+                   (const double *)M->va, x, y, alpha, beta);
     else
-        k_csr_spmv<<<blocks(M->nrows), kThr, 0, s>>>(M->nrows, M->rp, M->ci, M->va, x, y, alpha, beta);
+        launch_pdl(k_csr_spmv, blocks(M->nrows), s, M->nrows, (const int64_t *)M->rp, (const int32_t *)M->ci,
+                   (const double *)M->va, x, y, alpha, beta);
     return cudaGetLastError();
 }
 
@@ -294,7 +319,7 @@ void transpose(const nsm_csr *P, std::vector<int64_t> &rp, std::vector<int64_t> 
 
 nsm_status amg_cycle(nsm_amg *M, int lev, const double *b, double *x, cudaStream_t s) {
     if (lev == M->nlevels) {
-        k_dense_gemv<<<(unsigned)((M->nc * 32 + kThr - 1) / kThr), kThr, 0, s>>>(M->nc, M->Minv, b, x);
+        launch_pdl(k_dense_gemv, (unsigned)((M->nc * 32 + kThr - 1) / kThr), s, M->nc, (const double *)M->Minv, b, x);
         cudaError_t e = cudaGetLastError();
         return e == cudaSuccess ? NSM_OK : fail(&M->err, cudaGetErrorString(e), NSM_ERR_CUDA);
     }
