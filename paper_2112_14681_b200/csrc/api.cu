@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -36,6 +37,7 @@ struct Peer {
 
 struct nsm_handle {
     int device = 0;
+    uint64_t uid = 0;  // unique per setup (caches keyed by handle must not confuse a reused address)
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
     // A = L + D + U (+ ghost couplings LG / UG)
@@ -388,6 +390,7 @@ static nsm_status fused_alloc(nsm_handle *h) {
 }
 
 bool nsm::nsm_is_distributed(const nsm_handle *h) { return h && h->nranks > 1; }
+uint64_t nsm::nsm_handle_uid(const nsm_handle *h) { return h ? h->uid : 0; }
 
 extern "C" {
 
@@ -477,6 +480,8 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     preload_halo_kernels();
     preload_fused_kernels();
     nsm_handle *h = new nsm_handle();
+    static std::atomic<uint64_t> next_uid{1};
+    h->uid = next_uid++;
     h->device = device;
     h->n = sa.n;
     h->row_begin = rb;

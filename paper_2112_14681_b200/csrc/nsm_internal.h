@@ -190,6 +190,8 @@ void preload_halo_kernels();
 // True for handles of a multi-rank partition (their launches carry halo
 // sequence numbers and must not be captured into a replayed CUDA graph).
 bool nsm_is_distributed(const nsm_handle *h);
+// Unique id of a handle (never reused, unlike its address).
+uint64_t nsm_handle_uid(const nsm_handle *h);
 
 // Host ILUT(droptol, lfil) and Ruiz scaling of the U factor (NEXT-3).
 nsm_status ilut_host(const nsm_csr *A, double droptol, int lfil, std::vector<int64_t> &rp_out,

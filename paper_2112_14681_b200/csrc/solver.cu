@@ -194,7 +194,7 @@ struct GmresWs {
     double *V = nullptr, *u = nullptr, *w = nullptr, *z = nullptr, *part = nullptr, *red = nullptr, *hd = nullptr;
     double *hred = nullptr, *hh = nullptr;  // pinned host mirrors
     cudaGraphExec_t gexec = nullptr;
-    const nsm_handle *gA = nullptr;    // what the graph was captured for
+    uint64_t gA = 0;                   // uid of the operator handle the graph was captured for
     cudaStream_t gs = nullptr;
     bool stale = true;
     void release() {
@@ -525,7 +525,7 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
     double *V = W.V, *u = W.u, *w = W.w, *z = W.z, *part = W.part, *red = W.red, *hd = W.hd;
     const int nblk = W.nblk;
     auto cleanup = [&]() { if (!M) local.release(); };
-    if (W.gexec && (W.stale || W.gA != A || W.gs != s)) {
+    if (W.gexec && (W.stale || W.gA != nsm_handle_uid(A) || W.gs != s)) {
         cudaGraphExecDestroy(W.gexec);
         W.gexec = nullptr;
     }
@@ -562,7 +562,7 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
                     if (st == NSM_OK) st = nsm_spmv(A, z, w, s);
                     ok = cudaStreamEndCapture(s, &graph) == cudaSuccess && st == NSM_OK &&
                          cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
-                    W.gA = A;
+                    W.gA = nsm_handle_uid(A);
                     W.gs = s;
                     W.stale = false;
                     if (graph) cudaGraphDestroy(graph);

@@ -172,3 +172,38 @@ def test_solve_timing_table():
     with open("gpurun_out/solve_timing.json", "w") as f:
         json.dump(out, f, indent=1)
     assert all(r["iterations"] < 200 for r in t6["rows"] + t7["rows"])
+
+
+def test_gmres_workspace_reuse():
+    """nsm_gmres keeps its workspace and captured V-cycle graph in the AMG
+    object: changing a smoother setting must re-capture, a new operator
+    handle (possibly at a reused address) must not replay the old graph, and
+    repeated solves are bit-for-bit repeatable."""
+    A = inputs.var27(16).to_scipy()
+    levels = amg.hierarchy(A, rand_fn, min_coarse=200)
+    nl = len(levels) - 1
+    S = [nsm.Smoother(inputs.CSR.from_scipy(levels[l][0])) for l in range(nl)]
+    M = nsm.Amg(S, [inputs.CSR.from_scipy(levels[l][1]) for l in range(nl)], inputs.CSR.from_scipy(levels[-1][0]))
+    b = dev(inputs.uniform(0, A.shape[0]))
+    try:
+        def solve(op, k):
+            for l in range(nl):
+                M.set_smoother(l, "pgs", 1, 1, k, k)
+            x, its, hist = nsm.gmres(op, b, M, tol=1e-8)
+            return x.cpu().numpy(), its
+        x1, i1 = solve(S[0], 1)
+        x2, i2 = solve(S[0], 3)
+        x3, i3 = solve(S[0], 1)
+        assert i1 == i3 and np.array_equal(x1, x3)
+        assert not np.array_equal(x1, x2)           # the k = 3 cycle really ran
+        for _ in range(3):                           # fresh operator handles, same matrix
+            op = nsm.Smoother(inputs.CSR.from_scipy(levels[0][0]))
+            try:
+                x4, i4 = solve(op, 1)
+            finally:
+                op.close()
+            assert i4 == i1 and np.array_equal(x4, x1)
+    finally:
+        M.close()
+        for s_ in S:
+            s_.close()
