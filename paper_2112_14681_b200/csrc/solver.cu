@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -197,10 +199,14 @@ struct GmresWs {
     uint64_t gA = 0;                   // uid of the operator handle the graph was captured for
     cudaStream_t gs = nullptr;
     bool stale = true;
+    cudaStream_t own = nullptr;        // private stream when the caller's cannot be captured (legacy default)
+    cudaEvent_t ev = nullptr;
     void release() {
         cudaFree(V); cudaFree(u); cudaFree(w); cudaFree(z); cudaFree(part); cudaFree(red); cudaFree(hd);
         cudaFreeHost(hred); cudaFreeHost(hh);
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (own) cudaStreamDestroy(own);
+        if (ev) cudaEventDestroy(ev);
         *this = GmresWs();
     }
 };
@@ -524,6 +530,24 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
     }
     double *V = W.V, *u = W.u, *w = W.w, *z = W.z, *part = W.part, *red = W.red, *hd = W.hd;
     const int nblk = W.nblk;
+    // The legacy default stream cannot be captured into a graph: run the solve
+    // on a private non-blocking stream ordered after the caller's prior work
+    // (the solve ends with a host synchronisation, so later work on the
+    // caller's stream sees its result).
+    {
+        cudaStreamCaptureStatus cst;
+        const bool capturable = s != nullptr && s != cudaStreamLegacy &&
+                                cudaStreamIsCapturing(s, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusNone;
+        if (!capturable && !nsm_is_distributed(A)) {
+            if (!W.own && (cudaStreamCreateWithFlags(&W.own, cudaStreamNonBlocking) != cudaSuccess ||
+                           cudaEventCreateWithFlags(&W.ev, cudaEventDisableTiming) != cudaSuccess)) {
+                cudaGetLastError();
+                W.own = nullptr;
+            }
+            if (W.own && cudaEventRecord(W.ev, s) == cudaSuccess && cudaStreamWaitEvent(W.own, W.ev, 0) == cudaSuccess)
+                s = W.own;
+        }
+    }
     auto cleanup = [&]() { if (!M) local.release(); };
     if (W.gexec && (W.stale || W.gA != nsm_handle_uid(A) || W.gs != s)) {
         cudaGraphExecDestroy(W.gexec);
@@ -658,6 +682,9 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
     }
     if (iters) *iters = m;
     if (hist) std::copy(hv.begin(), hv.end(), hist);
+    static const bool dbg = getenv("NSM_DEBUG_GMRES") != nullptr;
+    if (dbg) fprintf(stderr, "[nsm_gmres] iterations %d, graph %s, private stream %s\n", m, gexec ? "yes" : "no",
+                     s == W.own && W.own ? "yes" : "no");
     cleanup();
     if (st != NSM_OK && g_solver_err.empty()) g_solver_err = "nsm_gmres: failed";
     return st;
