@@ -41,19 +41,25 @@ WORKLOADS = {
 
 # ------------------------------------------------------------------ helpers --
 def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k_l: int, k_u: int,
-                      n_ghost: int = 0) -> dict:
+                      n_ghost: int = 0, layout: dict | None = None) -> dict:
     """Bytes each kernel of one application must move (DESIGN.md §6 byte
-    model): every stored matrix entry once (8 B value + 4 B int32 column),
-    every n-vector the kernel reads or writes once; gathered neighbour values
-    are counted once (they hit L1/L2 after first touch)."""
-    res = 12 * nnz_off + 32 * n + 8 * n_ghost           # A streams, d, x, b, write r
+    model): every stored matrix entry once (8 B value + 4 B int32 column; an
+    offset-aligned part, nsm_layout, reads 8 B per entry plus one 4 B offset
+    per 32 entries), every n-vector the kernel reads or writes once; gathered
+    neighbour values are counted once (they hit L1/L2 after first touch)."""
+    layout = layout or {}
+
+    def mb(count, part):  # bytes of `count` stored entries of a part
+        return 8 * count + (count + 31) // 32 * 4 if layout.get(part) else 12 * count
+
+    res = mb(nnz_l, "L") + mb(nnz_u, "U") + 12 * (nnz_off - nnz_l - nnz_u) + 32 * n + 8 * n_ghost
     out = {}
     if kind == "pgs":
         # with sweeps following, the residual pass also writes g0 = r / d
         out["residual"] = res + (8 * n if k_l > 0 else 0)
         sw = []
         for j in range(1, k_l + 1):
-            b = 12 * nnz_l + 24 * n                       # L streams, r, d, previous iterate (g0 first)
+            b = mb(nnz_l, "L") + 24 * n                   # L streams, r, d, previous iterate (g0 first)
             b += 16 * n if j == k_l else 8 * n            # last: x read+write; else write g
             sw.append(b)
         if k_l == 0:
@@ -63,7 +69,7 @@ def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k
         out["residual"] = res
         sl, su = [], []
         for j in range(1, k_l + 1):
-            b = 12 * nnz_l + 8 * n + (0 if j == 1 else 8 * n)   # Ls, r (the first iterate is r), prev iterate
+            b = mb(nnz_l, "Ls") + 8 * n + (0 if j == 1 else 8 * n)   # Ls, r (the first iterate is r), prev iterate
             if j == k_l and k_u == 0:
                 b += 24 * n                               # dU, x read+write
             elif j == k_l:
@@ -72,7 +78,7 @@ def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k
                 b += 8 * n                                # write y
             sl.append(b)
         for j in range(1, k_u + 1):
-            b = 12 * nnz_u + 24 * n                       # Us, y, dU, previous iterate (z0 first)
+            b = mb(nnz_u, "Us") + 24 * n                  # Us, y, dU, previous iterate (z0 first)
             b += 16 * n if j == k_u else 8 * n
             su.append(b)
         if k_l == 0 and k_u == 0:
@@ -189,6 +195,33 @@ def split_counts(A):
     return lower, upper, int(np.count_nonzero(A.col != rows))
 
 
+def aligned_parts(A) -> dict:
+    """Which strict triangles of A the library stores offset-aligned (the
+    builder's criterion: the per-slice unions of column offsets widen the
+    SELL-32 slices by at most 15 % with at most 3 % pads; nsm_layout reports
+    it for a handle) —
+    for the reference arm, which has no handle, to count the same bytes."""
+    n = A.nrows
+    rows = np.repeat(np.arange(n, dtype=np.int64) + A.row_begin, np.diff(A.rowptr))
+    col = A.col.astype(np.int64)
+    local = (col >= A.row_begin) & (col < A.row_begin + n)
+    out = {}
+    for part, m in (("L", (col < rows) & local), ("U", (col > rows) & local)):
+        r = rows[m] - A.row_begin
+        off = col[m] - rows[m]
+        sl = r // 32
+        ns = (n + 31) // 32
+        cnt = np.bincount(r, minlength=n)
+        c = np.zeros(ns * 32, dtype=np.int64)
+        c[:n] = cnt
+        compact = int(c.reshape(ns, 32).max(1).sum())
+        uni = len(np.unique(sl * (1 << 32) + (off - off.min() if off.size else off))) if off.size else 0
+        pads = uni * 32 - int(m.sum())
+        out[part] = compact > 0 and uni * 100 <= compact * 115 and pads * 100 <= uni * 32 * 3
+    out["Ls"], out["Us"] = out["L"], out["U"]   # ILU(0) factors share A's pattern
+    return out
+
+
 def flush_l2(buf):
     """Evict L2 (126 MB) between timed steps by streaming a 256 MB buffer
     through it.  A read (not a write) leaves only clean lines behind, so the
@@ -206,7 +239,7 @@ def run_reference(args, rank, nranks):
     import oracle
     A, offsets, kind, k_l, k_u, desc = build_workload(args.config, 0, 1)
     nl, nu_, noff = split_counts(A)
-    ab = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u)["total"]   # same bytes as the default nsm path
+    ab = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, 0, aligned_parts(A))["total"]  # as the nsm path
     b, x0 = inputs.uniform(inputs.SEED_B, A.nrows), inputs.uniform(inputs.SEED_X0, A.nrows)
     F = oracle.ilu0(A) if kind == "ilu" else None
 
@@ -254,7 +287,8 @@ def run_nsm(args, rank, nranks, local_rank):
     if nranks > 1:
         S.connect(dist)
     nl, nu_, noff = split_counts(A)
-    model = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost)   # one kernel per pass
+    layout = S.layout()
+    model = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost, layout)   # one kernel per pass
     fmodel = floor_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost)       # fused passes / floor
     b = torch.from_numpy(inputs.uniform(inputs.SEED_B, A.nrows, idx0=A.row_begin)).to(dev)
     x0 = torch.from_numpy(inputs.uniform(inputs.SEED_X0, A.nrows, idx0=A.row_begin)).to(dev)
@@ -398,6 +432,7 @@ def run_nsm(args, rank, nranks, local_rank):
                        "bytes": ("algorithmic bytes of the path that ran (DESIGN.md §6): "
                                  + ("fused passes = the floor" if fused else "one kernel per pass")),
                        "bytes_per_step_per_gpu": ab, "floor_bytes_per_step_per_gpu": fmodel["total"],
+                       "offset_aligned_parts": [k for k, v in layout.items() if v],
                        "floor_gbs": round(floor_gbs, 2),
                        "frac_of_hbm_peak": round(value / nranks / peak, 4)},
             "ms_per_apply": round(ms_step, 4),

@@ -282,6 +282,13 @@ nsm_status nsm_info(const nsm_handle *h, int64_t *n_local, int64_t *n_ghost, int
  * call) and halo exchanges it performed.  Host-side, no synchronisation. */
 nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *halo_exchanges);
 
+/* Storage layout of the strict triangles: bit 1 / 2 / 4 / 8
+ * set when A's L / A's U / the factor's L_s / U_s uses the offset-aligned
+ * SELL layout (stencil-like rows: one int32 column offset per slice entry
+ * position; the pipelined kernels then read 8 instead of 12 bytes per entry).
+ * Chosen automatically at setup when it widens the slices by <= 15 %. */
+nsm_status nsm_layout(const nsm_handle *h, int *offset_aligned);
+
 /* Fused-pass synchronisation statistics since setup: work items whose
  * consumer warps found the item not yet ready (its condition "all items <=
  * w - Dw done", unmet) and had to wait, and the total time

@@ -26,7 +26,7 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual
                   "nsm_halo_commit", "nsm_set_option", "nsm_spmat_setup", "nsm_spmat_apply",
                   "nsm_spmat_destroy", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle", "nsm_amg_destroy",
                   "nsm_solver_last_error", "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz",
-                  "nsm_fused_stats"])
+                  "nsm_fused_stats", "nsm_layout"])
 
 
 class NsmError(RuntimeError):
@@ -92,6 +92,7 @@ def load():
     L.nsm_gmres.argtypes = [vp, vp, vp, vp, ci, ctypes.c_double, ci, P(ci), vp, vp]
     L.nsm_profile.argtypes = [vp, vp, vp]
     L.nsm_fused_stats.argtypes = [vp, P(i64), P(i64)]
+    L.nsm_layout.argtypes = [vp, P(ci)]
     L.nsm_ilut.argtypes = [P(_Csr), ctypes.c_double, ci, vp, P(i64), vp, vp]
     L.nsm_ruiz.argtypes = [P(_Csr), ci, vp, vp, vp]
     L.nsm_set_ruiz.argtypes = [vp, vp, vp]
@@ -103,7 +104,7 @@ def load():
                  "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
                  "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
-                 "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats"]:
+                 "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats", "nsm_layout"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -418,6 +419,12 @@ class Smoother:
         self._call(load().nsm_profile(self._h, ms.ctypes.data, cnt.ctypes.data))
         return {"residual": (float(ms[0]), int(cnt[0])), "sweep": (float(ms[1]), int(cnt[1])),
                 "fused": (float(ms[2]), int(cnt[2]))}
+
+    def layout(self):
+        """{'L', 'U', 'Ls', 'Us'}: which strict parts use the offset-aligned layout."""
+        v = ctypes.c_int(0)
+        self._call(load().nsm_layout(self._h, ctypes.byref(v)))
+        return {k: bool(v.value & b) for k, b in (("L", 1), ("U", 2), ("Ls", 4), ("Us", 8))}
 
     def fused_stats(self):
         """(waits that had to spin, total spin ns) of the fused passes since setup."""

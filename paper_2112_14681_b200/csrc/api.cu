@@ -125,6 +125,8 @@ bool upload_sell(DevAlloc &a, const SellHost &hs, Sell *s) {
     if (!a.get(&s->ptr, (int64_t)hs.ptr.size())) return false;
     if (!upload(s->ptr, hs.ptr.data(), (int64_t)hs.ptr.size())) return false;
     if (!a.get(&s->col, s->padded) || !a.get(&s->val, s->padded)) return false;
+    if (!hs.off.empty() && (!a.get(&s->off, (int64_t)hs.off.size()) || !upload(s->off, hs.off.data(), (int64_t)hs.off.size())))
+        return false;
     return upload(s->col, hs.col.data(), s->padded) && upload(s->val, hs.val.data(), s->padded);
 }
 
@@ -132,6 +134,7 @@ void free_sell(Sell &s) {
     cudaFree(s.ptr);
     cudaFree(s.col);
     cudaFree(s.val);
+    cudaFree(s.off);
     s = Sell();
 }
 
@@ -755,6 +758,12 @@ nsm_status nsm_set_ruiz(nsm_handle *h, const double *s_r, const double *s_c) {
         return NSM_ERR_OOM;
     if (!upload(h->s_r, s_r, h->n) || !upload(h->s_c, s_c, h->n)) return cuda_fail(h, cudaGetLastError(), "nsm_set_ruiz");
     h->ruiz = true;
+    return NSM_OK;
+}
+
+nsm_status nsm_layout(const nsm_handle *h, int *offset_aligned) {
+    if (!h || !offset_aligned) return NSM_ERR_ARG;
+    *offset_aligned = (h->L.off ? 1 : 0) | (h->U.off ? 2 : 0) | (h->Ls.off ? 4 : 0) | (h->Us.off ? 8 : 0);
     return NSM_OK;
 }
 

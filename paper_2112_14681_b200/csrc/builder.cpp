@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "nsm_internal.h"
@@ -78,6 +79,77 @@ void pack(int64_t n, const std::vector<int32_t> &cnt, const std::vector<int64_t>
             }
         }
     }
+}
+
+// Offset-aligned packing of a LOCAL part (stencil-like matrices): slice s
+// stores, for every offset o in the sorted union U_s of (column - row) over its
+// rows, one entry per row — the row's a_{i,i+o} or a pad (val 0) — so a slice
+// needs one int32 offset per entry position instead of one column per entry.
+// Within each row the entries stay in ascending column order (pads add 0).
+// Used only if the union widens the slices by at most 15 % and pads are at
+// most 3 % of the stored entries.
+bool pack_aligned(int64_t n, int64_t rb, const std::vector<int32_t> &cnt, const std::vector<int64_t> &first,
+                  const int64_t *ci, const double *va, SellHost *out) {
+    const int64_t ns = (n + kSlice - 1) / kSlice;
+    std::vector<std::vector<int32_t>> uni(ns);
+    std::vector<int64_t> wc(ns, 0);
+    int64_t sum_u = 0, sum_c = 0;
+#pragma omp parallel for schedule(static) reduction(+ : sum_u, sum_c)
+    for (int64_t s = 0; s < ns; ++s) {
+        std::vector<int32_t> &u = uni[s];
+        int32_t m = 0;
+        for (int64_t i = s * kSlice; i < std::min(n, (s + 1) * kSlice); ++i) {
+            m = std::max(m, cnt[i]);
+            for (int32_t j = 0; j < cnt[i]; ++j) u.push_back((int32_t)(ci[first[i] + j] - rb - i));
+        }
+        std::sort(u.begin(), u.end());
+        u.erase(std::unique(u.begin(), u.end()), u.end());
+        wc[s] = m;
+        sum_u += (int64_t)u.size();
+        sum_c += m;
+    }
+    // profitable only with (almost) no pads: a pad gathers a column the row
+    // does not couple to (lexicographic stencils: grid-line ends only)
+    int64_t nnz_part = 0;
+    for (int64_t i = 0; i < n; ++i) nnz_part += cnt[i];
+    if (sum_c == 0 || sum_u * 100 > sum_c * 115 || (sum_u * kSlice - nnz_part) * 100 > sum_u * kSlice * 3) return false;
+    out->ptr.assign(ns + 1, 0);
+    int32_t maxw = 0;
+    int64_t nnz = 0;
+    for (int64_t s = 0; s < ns; ++s) {
+        out->ptr[s + 1] = out->ptr[s] + (int64_t)uni[s].size() * kSlice;
+        maxw = std::max(maxw, (int32_t)uni[s].size());
+    }
+    for (int64_t i = 0; i < n; ++i) nnz += cnt[i];
+    out->maxw = maxw;
+    out->nnz = nnz;
+    const int64_t tot = out->ptr[ns];
+    out->col.assign(tot, 0);
+    out->val.assign(tot, 0.0);
+    out->off.assign(tot / kSlice, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < ns; ++s) {
+        const std::vector<int32_t> &u = uni[s];
+        const int64_t base = out->ptr[s];
+        for (size_t j = 0; j < u.size(); ++j) out->off[base / kSlice + j] = u[j];
+        for (int l = 0; l < kSlice; ++l) {
+            const int64_t i = s * kSlice + l;
+            int32_t q = 0;  // next entry of the row
+            for (size_t j = 0; j < u.size(); ++j) {
+                const int64_t e = base + (int64_t)j * kSlice + l;
+                const int64_t c = i + u[j];
+                if (i < n && q < cnt[i] && ci[first[i] + q] - rb == c) {
+                    out->col[e] = (int32_t)c;
+                    out->val[e] = va[first[i] + q];
+                    ++q;
+                } else {  // pad: val 0 at row + offset (or the row itself when out of range)
+                    out->col[e] = (int32_t)((i < n && c >= 0 && c < n) ? c : (i < n ? i : 0));
+                    out->val[e] = 0.0;
+                }
+            }
+        }
+    }
+    return true;
 }
 
 struct LocalMap {
@@ -179,8 +251,11 @@ nsm_status build_split(const nsm_csr *A, int64_t rb, int64_t re, Split *out, std
     out->n_ghost = (int64_t)g.size();
     LocalMap lm{rb};
     GhostMap gm{&g};
-    pack(n, cnt[P_L], first[P_L], ci, va, lm, &out->L);
-    pack(n, cnt[P_U], first[P_U], ci, va, lm, &out->U);
+    static const bool no_align = getenv("NSM_NO_ALIGNED_LAYOUT") != nullptr;  // A/B experiments
+    if (no_align || !pack_aligned(n, rb, cnt[P_L], first[P_L], ci, va, &out->L))
+        pack(n, cnt[P_L], first[P_L], ci, va, lm, &out->L);
+    if (no_align || !pack_aligned(n, rb, cnt[P_U], first[P_U], ci, va, &out->U))
+        pack(n, cnt[P_U], first[P_U], ci, va, lm, &out->U);
     pack(n, cnt[P_LG], first[P_LG], ci, va, gm, &out->LG);
     pack(n, cnt[P_UG], first[P_UG], ci, va, gm, &out->UG);
     out->nnz_off = out->L.nnz + out->U.nnz + out->LG.nnz + out->UG.nnz;

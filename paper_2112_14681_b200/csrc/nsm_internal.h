@@ -23,6 +23,11 @@ struct Sell {
     int64_t *ptr = nullptr;   // device, nslices + 1
     int32_t *col = nullptr;   // device, padded entries
     double *val = nullptr;    // device, padded entries
+    // Offset-aligned layout (stencil-like parts, builder.cpp pack_aligned):
+    // entry j of every row of slice s has column row + off[ptr[s]/32 + j]
+    // (a pad where the row lacks that offset: val 0, col = row + off if in
+    // range, else the row).  nullptr: compact layout, columns only in `col`.
+    int32_t *off = nullptr;
     int64_t padded = 0;       // stored entries incl. padding
     int64_t nnz = 0;          // real entries
     int32_t maxw = 0;         // widest slice
@@ -34,6 +39,7 @@ struct SellHost {
     std::vector<int64_t> ptr;
     std::vector<int32_t> col;
     std::vector<double> val;
+    std::vector<int32_t> off;   // offset-aligned layout (empty: compact)
     int64_t nnz = 0;
     int32_t maxw = 0;
 };
@@ -43,9 +49,10 @@ struct SellView {
     const int64_t *ptr;
     const int32_t *col;
     const double *val;
+    const int32_t *off;
 };
 
-inline SellView view(const Sell &s) { return SellView{s.ptr, s.col, s.val}; }
+inline SellView view(const Sell &s) { return SellView{s.ptr, s.col, s.val, s.off}; }
 
 // Result of splitting a CSR row block (builder.cpp).
 struct Split {

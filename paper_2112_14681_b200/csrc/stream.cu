@@ -88,16 +88,22 @@ struct GatherScaledT {
 
 // Shared-memory layout: full[NST], empty[NST] mbarriers, then NST stages of
 // NP parts of {val[cap], col[cap]} with cap = kTS * 32 * maxw entries.
+// With the offset-aligned layout (ofs) only the values are staged (8 B per
+// entry); columns are row + offset.
 struct Layout {
     int nst, np;
     int64_t cap;  // entries per part per stage
+    int eb;       // staged bytes per entry: 12 (values + columns) or 8 (values; + the slices' offsets)
+    __host__ __device__ static int64_t part_bytes(int64_t cap, int eb) {
+        return eb == 12 ? cap * 12 : cap * 8 + (cap / kSlice * 4 + 15) / 16 * 16;
+    }
     __device__ __forceinline__ uint64_t *full(char *s) const { return (uint64_t *)s; }
     __device__ __forceinline__ uint64_t *empty(char *s) const { return (uint64_t *)s + nst; }
     __device__ __forceinline__ double *val(char *s, int st, int p) const {
-        return (double *)(s + 128 + ((int64_t)st * np + p) * cap * 12);
+        return (double *)(s + 128 + ((int64_t)st * np + p) * part_bytes(cap, eb));
     }
-    __device__ __forceinline__ int32_t *col(char *s, int st, int p) const {
-        return (int32_t *)(s + 128 + ((int64_t)st * np + p) * cap * 12 + cap * 8);
+    __device__ __forceinline__ int32_t *col(char *s, int st, int p) const {   // eb 12: columns; eb 8: offsets
+        return (int32_t *)(s + 128 + ((int64_t)st * np + p) * part_bytes(cap, eb) + cap * 8);
     }
 };
 
@@ -113,9 +119,49 @@ __device__ __forceinline__ void init_barriers(const Layout &Ly, char *sm) {
 }
 
 // Producer: stream the parts' segments of each of this CTA's tiles.
+// Producer warp: stream the parts' segments of each of this CTA's tiles.  Lane
+// 0 issues the bulk copies; with the offset-aligned layout (eb 8) the whole
+// warp also copies the tile's slice offsets into the stage (plain loads; a
+// 4-byte-aligned segment the bulk engine cannot take), ordered before the
+// stage's arrival by __syncwarp.  Software-pipelined: the slice pointers and
+// offsets of the CTA's next tile are loaded while the current one is staged,
+// so neither round trip sits on the producer's per-tile path.
+constexpr int kOfsPerLane = 4;  // staged offsets per lane and part (8 slices x 16 entries)
+
 template <int NP>
-__device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellView (&P)[NP], int64_t s_begin,
-                                         int64_t s_end, int64_t ntiles) {
+struct TileRefs {
+    int64_t b[NP], e[NP];
+    int32_t o[NP][kOfsPerLane];
+};
+
+template <int NP>
+__device__ __forceinline__ void tile_refs(const Layout &Ly, const SellView (&P)[NP], int64_t s_begin, int64_t s_end,
+                                          int64_t t, int lane, TileRefs<NP> &r) {
+    const int64_t s0 = s_begin + t * kTS, s1 = min(s0 + kTS, s_end);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        r.b[p] = __ldg(P[p].ptr + s0);
+        r.e[p] = __ldg(P[p].ptr + s1);
+    }
+    if (Ly.eb == 8) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int64_t no = (r.e[p] - r.b[p]) / kSlice;
+            const int32_t *go = P[p].off + r.b[p] / kSlice;
+#pragma unroll
+            for (int q = 0; q < kOfsPerLane; ++q) {
+                const int64_t k = lane + 32 * q;
+                r.o[p][q] = k < no ? __ldg(go + k) : 0;
+            }
+        }
+    }
+}
+
+// Compact layout (values + columns, 12 B per entry): one lane, no prefetch
+// (the software-pipelined warp version below measured ~1.5 % slower here).
+template <int NP>
+__device__ __forceinline__ void producer_compact(const Layout &Ly, char *sm, const SellView (&P)[NP], int64_t s_begin,
+                                                 int64_t s_end, int64_t ntiles) {
     const uint64_t pol = policy_evict_first_t();
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -143,26 +189,111 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
     pdl_trigger();  // all of this CTA's copies are issued: dependents may be scheduled
 }
 
+template <int NP>
+__device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellView (&P)[NP], int64_t s_begin,
+                                         int64_t s_end, int64_t ntiles, int lane) {
+    const uint64_t pol = policy_evict_first_t();
+    int it = 0;
+    TileRefs<NP> cur, nxt;
+    if ((int64_t)blockIdx.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, blockIdx.x, lane, cur);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % Ly.nst;
+        const uint32_t use = (uint32_t)(it / Ly.nst);
+        if (t + gridDim.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, t + gridDim.x, lane, nxt);  // prefetch
+        if (it >= Ly.nst) mbar_wait(Ly.empty(sm) + st, (use - 1) & 1);
+        uint32_t bytes = 0;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) bytes += (uint32_t)((cur.e[p] - cur.b[p]) * Ly.eb);
+        if (Ly.eb == 8) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                int32_t *so = Ly.col(sm, st, p);
+                const int64_t no = (cur.e[p] - cur.b[p]) / kSlice;
+#pragma unroll
+                for (int q = 0; q < kOfsPerLane; ++q) {
+                    const int64_t k = lane + 32 * q;
+                    if (k < no) so[k] = cur.o[p][q];
+                }
+                const int32_t *go = P[p].off + cur.b[p] / kSlice;  // wider tiles (not staged above)
+                for (int64_t k = lane + 32 * kOfsPerLane; k < no; k += 32) so[k] = __ldg(go + k);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            mbar_expect_tx(Ly.full(sm) + st, bytes);  // bulk-copied bytes (values, and columns with eb 12)
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const int64_t b = cur.b[p], e = cur.e[p];
+                if (e > b) {
+                    bulk_g2s(Ly.val(sm, st, p), P[p].val + b, (uint32_t)((e - b) * 8), Ly.full(sm) + st, pol);
+                    if (Ly.eb == 12)
+                        bulk_g2s(Ly.col(sm, st, p), P[p].col + b, (uint32_t)((e - b) * 4), Ly.full(sm) + st, pol);
+                }
+            }
+        }
+        __syncwarp();
+        cur = nxt;
+    }
+    if (lane == 0) pdl_trigger();  // all of this CTA's copies are issued: dependents may be scheduled
+}
+
 // Register chunk of one row taken from the staged copy: the first CH entries
 // (predicated on the slice width w) are read from shared memory, all their
 // gathers issued together, and multiplied; add() sums them in stored order
 // and continues with any entries beyond CH one by one.
+// Slice offsets of the offset-aligned layout, loaded (warp-uniform) before
+// the stage wait: column of entry j = row + o[j], or the row itself when out
+// of range (a pad) — the builder's column for that pad, so the products are
+// those of the column-array path.
+// Slice offsets of the offset-aligned layout, staged by the producer: column of
+// entry j = row + o[j], or the row itself when out of range (a pad) — the
+// builder's column for that pad, so the products are those of the
+// column-array path.
+template <int CH>
+struct Offsets {
+    const int32_t *so;    // this slice's offsets in the stage
+    __device__ __forceinline__ void at(const int32_t *stage_offs, int64_t lo) { so = stage_offs + lo / kSlice; }
+    // 32-bit unsigned arithmetic (rows and columns < 2^31): one compare on
+    // the gather's dependent path (the 64-bit form cost ~10 % on C3)
+    __device__ __forceinline__ static int32_t col(int64_t i, int32_t off, int64_t n) {
+        const uint32_t c = (uint32_t)((int32_t)i + off);
+        return c < (uint32_t)n ? (int32_t)c : (int32_t)i;
+    }
+};
+
 template <int CH>
 struct StagedChunk {
     double v[CH];
     int32_t c[CH];
     const double *sv;
     const int32_t *sc;
+    const int32_t *otail;  // offset-aligned layout: offsets of the entries beyond CH
+    int64_t row, n;
     int w;
     __device__ __forceinline__ void load(const double *sv_, const int32_t *sc_, int64_t off, int w_, int lane) {
         sv = sv_ + off + lane;
         sc = sc_ + off + lane;
+        otail = nullptr;
         w = w_;
 #pragma unroll
         for (int j = 0; j < CH; ++j)
             if (j < w) {
                 v[j] = sv[j * kSlice];
                 c[j] = sc[j * kSlice];
+            }
+    }
+    __device__ __forceinline__ void load_ofs(const double *sv_, const Offsets<CH> &of, int64_t off, int w_, int lane,
+                                             int64_t row_, int64_t n_) {
+        sv = sv_ + off + lane;
+        otail = of.so;
+        row = row_;
+        n = n_;
+        w = w_;
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) {
+                v[j] = sv[j * kSlice];
+                c[j] = Offsets<CH>::col(row, of.so[j], n);
             }
     }
     template <class G>
@@ -176,28 +307,31 @@ struct StagedChunk {
 #pragma unroll
         for (int j = 0; j < CH; ++j)
             if (j < w) acc = __dadd_rn(acc, v[j]);
-        for (int j = CH; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn(sv[j * kSlice], g(sc[j * kSlice])));
+        for (int j = CH; j < w; ++j) {
+            const int32_t cj = otail ? Offsets<CH>::col(row, otail[j], n) : sc[j * kSlice];
+            acc = __dadd_rn(acc, __dmul_rn(sv[j * kSlice], g(cj)));
+        }
         return acc;
     }
 };
 
 
-template <int OUT, int CH>
+template <int OUT, int CH, bool OFS>
 __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView L,
                                                             SellView U, const double *__restrict__ d,
                                                             const double *__restrict__ b,
                                                             const double *__restrict__ x, double *__restrict__ out,
                                                             double *__restrict__ out2, int nst, int64_t cap) {
     extern __shared__ __align__(128) char sm[];
-    const Layout Ly{nst, 2, cap};
+    constexpr bool ofs = OFS;
+    const Layout Ly{nst, 2, cap, ofs ? 8 : 12};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     init_barriers(Ly, sm);
     if (warp == kTS) {
-        if (lane == 0) {
-            const SellView P[2] = {L, U};
-            producer<2>(Ly, sm, P, s_begin, s_end, ntiles);
-        }
+        const SellView P[2] = {L, U};
+        if constexpr (OFS) producer<2>(Ly, sm, P, s_begin, s_end, ntiles, lane);
+        else if (lane == 0) producer_compact<2>(Ly, sm, P, s_begin, s_end, ntiles);
         return;
     }
     const GatherPlainT gx{x};
@@ -215,6 +349,7 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
         const double bi = (OUT != OUT_AX && row) ? __ldg(b + i) : 0.0;
         int64_t lo = 0, uo = 0;
         int lw = 0, uw = 0;
+        Offsets<CH> ol, ou;
         if (has) {
             const int64_t l0 = __ldg(L.ptr + s0), ls = __ldg(L.ptr + s), ls1 = __ldg(L.ptr + s + 1);
             const int64_t u0 = __ldg(U.ptr + s0), us = __ldg(U.ptr + s), us1 = __ldg(U.ptr + s + 1);
@@ -224,12 +359,21 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
             uw = (int)((us1 - us) / kSlice);
         }
         mbar_wait(Ly.full(sm) + st, use & 1);
+        if constexpr (OFS) {
+            ol.at(Ly.col(sm, st, 0), lo);
+            ou.at(Ly.col(sm, st, 1), uo);
+        }
         double acc = 0.0;
         if (has) {
             if constexpr (CH <= 8) {  // both triangles' gathers in flight together
                 StagedChunk<CH> cl, cu;
-                cl.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), lo, lw, lane);
-                cu.load(Ly.val(sm, st, 1), Ly.col(sm, st, 1), uo, uw, lane);
+                if constexpr (OFS) {
+                    cl.load_ofs(Ly.val(sm, st, 0), ol, lo, lw, lane, i, n);
+                    cu.load_ofs(Ly.val(sm, st, 1), ou, uo, uw, lane, i, n);
+                } else {
+                    cl.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), lo, lw, lane);
+                    cu.load(Ly.val(sm, st, 1), Ly.col(sm, st, 1), uo, uw, lane);
+                }
                 cl.gather_mul(gx);
                 cu.gather_mul(gx);
                 acc = cl.add(acc, gx);
@@ -237,11 +381,13 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
                 acc = cu.add(acc, gx);
             } else {                  // wide rows: one triangle at a time (registers)
                 StagedChunk<CH> c;
-                c.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), lo, lw, lane);
+                if constexpr (OFS) c.load_ofs(Ly.val(sm, st, 0), ol, lo, lw, lane, i, n);
+                else c.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), lo, lw, lane);
                 c.gather_mul(gx);
                 acc = c.add(acc, gx);
                 acc = __dadd_rn(acc, __dmul_rn(di, xi));
-                c.load(Ly.val(sm, st, 1), Ly.col(sm, st, 1), uo, uw, lane);
+                if constexpr (OFS) c.load_ofs(Ly.val(sm, st, 1), ou, uo, uw, lane, i, n);
+                else c.load(Ly.val(sm, st, 1), Ly.col(sm, st, 1), uo, uw, lane);
                 c.gather_mul(gx);
                 acc = c.add(acc, gx);
             }
@@ -260,7 +406,7 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
     }
 }
 
-template <bool UNIT, int EPI, class G, int CH>
+template <bool UNIT, int EPI, class G, int CH, bool OFS>
 __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView T,
                                                          const double *__restrict__ dT,
                                                          const double *__restrict__ rhs, G gin,
@@ -269,15 +415,15 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
                                                          unsigned long long *flag, int64_t sweep_id, int nst,
                                                          int64_t cap) {
     extern __shared__ __align__(128) char sm[];
-    const Layout Ly{nst, 1, cap};
+    constexpr bool ofs = OFS;
+    const Layout Ly{nst, 1, cap, ofs ? 8 : 12};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     init_barriers(Ly, sm);
     if (warp == kTS) {
-        if (lane == 0) {
-            const SellView P[1] = {T};
-            producer<1>(Ly, sm, P, s_begin, s_end, ntiles);
-        }
+        const SellView P[1] = {T};
+        if constexpr (OFS) producer<1>(Ly, sm, P, s_begin, s_end, ntiles, lane);
+        else if (lane == 0) producer_compact<1>(Ly, sm, P, s_begin, s_end, ntiles);
         return;
     }
     pdl_wait();  // rhs, iterates, x of the previous kernels
@@ -295,16 +441,19 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
         const double dn = ((EPI == EPI_XADD_SCALE || EPI == EPI_STORE2) && row) ? __ldg(dnext + i) : 1.0;
         int64_t to = 0;
         int tw = 0;
+        Offsets<CH> ot;
         if (has) {
             const int64_t t0 = __ldg(T.ptr + s0), ts = __ldg(T.ptr + s), ts1 = __ldg(T.ptr + s + 1);
             to = ts - t0;
             tw = (int)((ts1 - ts) / kSlice);
         }
         mbar_wait(Ly.full(sm) + st, use & 1);
+        if constexpr (OFS) ot.at(Ly.col(sm, st, 0), to);
         double acc = 0.0;
         if (has) {
             StagedChunk<CH> ct;
-            ct.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), to, tw, lane);
+            if constexpr (OFS) ct.load_ofs(Ly.val(sm, st, 0), ot, to, tw, lane, i, n);
+            else ct.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), to, tw, lane);
             ct.gather_mul(gin);
             acc = ct.add(acc, gin);
         }
@@ -348,12 +497,12 @@ struct Geo {
 // Stages per CTA: maximise resident consumer warps (capped at 32 per SM),
 // then the pipeline depth.  Cached per kernel and stage size.
 template <class K>
-Geo geometry(K kernel, int np, int maxw) {
+Geo geometry(K kernel, int np, int maxw, int eb = 12) {
     static std::mutex mu;
     static std::map<std::pair<const void *, int64_t>, Geo> cache;
     Geo g;
     g.cap = (int64_t)kTS * kSlice * std::max(maxw, 1);
-    const int64_t stage = np * g.cap * 12;
+    const int64_t stage = np * Layout::part_bytes(g.cap, eb);
     std::lock_guard<std::mutex> lk(mu);
     auto key = std::make_pair((const void *)kernel, stage);
     auto itc = cache.find(key);
@@ -399,26 +548,42 @@ cudaError_t launch_pdl(bool pdl, K kernel, int grid, size_t smem, cudaStream_t s
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
-template <int OUT, int CH>
-cudaError_t residual_tma_ch(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
-                            const double *d, const double *b, const double *x, double *out, double *out2,
-                            bool pdl, cudaStream_t st) {
-    auto k = k_residual_tma<OUT, CH>;
-    const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw));
+template <int OUT, int CH, bool OFS>
+cudaError_t residual_tma_ofs(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
+                             const double *d, const double *b, const double *x, double *out, double *out2,
+                             bool pdl, cudaStream_t st) {
+    auto k = k_residual_tma<OUT, CH, OFS>;
+    const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw), OFS ? 8 : 12);
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     return launch_pdl(pdl, k, grid_of<decltype(k)>(g, ntiles), g.smem, st, n, s_begin, s_end, view(L), view(U), d, b, x,
                       out, out2, g.nst, g.cap);
 }
 
-template <bool UNIT, int EPI, class G, int CH>
-cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end, G gin, cudaStream_t st) {
-    auto k = k_sweep_tma<UNIT, EPI, G, CH>;
-    const Geo g = geometry(k, 1, a.T->maxw);
+template <int OUT, int CH>
+cudaError_t residual_tma_ch(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
+                            const double *d, const double *b, const double *x, double *out, double *out2,
+                            bool pdl, cudaStream_t st) {
+    // offset-aligned layout (both triangles): stage values only, columns = row + offset
+    if (L.off && U.off) return residual_tma_ofs<OUT, CH, true>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
+    return residual_tma_ofs<OUT, CH, false>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
+}
+
+template <bool UNIT, int EPI, class G, int CH, bool OFS>
+cudaError_t sweep_tma_ofs(const SweepArgs &a, int64_t s_begin, int64_t s_end, G gin, cudaStream_t st) {
+    auto k = k_sweep_tma<UNIT, EPI, G, CH, OFS>;
+    const Geo g = geometry(k, 1, a.T->maxw, OFS ? 8 : 12);
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     return launch_pdl(a.pdl, k, grid_of<decltype(k)>(g, ntiles), g.smem, st, a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs,
                       gin, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id, g.nst, g.cap);
+}
+
+template <bool UNIT, int EPI, class G, int CH>
+cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end, G gin, cudaStream_t st) {
+    // offset-aligned layout: stage values only, columns = row + offset
+    if (a.T->off) return sweep_tma_ofs<UNIT, EPI, G, CH, true>(a, s_begin, s_end, gin, st);
+    return sweep_tma_ofs<UNIT, EPI, G, CH, false>(a, s_begin, s_end, gin, st);
 }
 
 template <bool UNIT, int EPI, int CH>
@@ -486,30 +651,33 @@ void touch_t(K k) {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, k);
 }
-template <int CH>
+template <int CH, bool OFS>
 void touch_tma_ch() {
-    touch_t(k_residual_tma<OUT_R, CH>);
-    touch_t(k_residual_tma<OUT_AX, CH>);
-    touch_t(k_residual_tma<OUT_RG, CH>);
-    touch_t(k_sweep_tma<true, EPI_STORE2, GatherPlainT, CH>);
-    touch_t(k_sweep_tma<false, EPI_STORE2, GatherPlainT, CH>);
-    touch_t(k_sweep_tma<false, EPI_STORE2, GatherScaledT, CH>);
-    touch_t(k_sweep_tma<true, EPI_STORE, GatherPlainT, CH>);
-    touch_t(k_sweep_tma<true, EPI_XADD, GatherPlainT, CH>);
-    touch_t(k_sweep_tma<true, EPI_XADD_SCALE, GatherPlainT, CH>);
-    touch_t(k_sweep_tma<false, EPI_STORE, GatherPlainT, CH>);
-    touch_t(k_sweep_tma<false, EPI_XADD, GatherPlainT, CH>);
-    touch_t(k_sweep_tma<false, EPI_XADD_SCALE, GatherPlainT, CH>);
-    touch_t(k_sweep_tma<false, EPI_STORE, GatherScaledT, CH>);
-    touch_t(k_sweep_tma<false, EPI_XADD, GatherScaledT, CH>);
-    touch_t(k_sweep_tma<false, EPI_XADD_SCALE, GatherScaledT, CH>);
+    touch_t(k_residual_tma<OUT_R, CH, OFS>);
+    touch_t(k_residual_tma<OUT_AX, CH, OFS>);
+    touch_t(k_residual_tma<OUT_RG, CH, OFS>);
+    touch_t(k_sweep_tma<true, EPI_STORE2, GatherPlainT, CH, OFS>);
+    touch_t(k_sweep_tma<false, EPI_STORE2, GatherPlainT, CH, OFS>);
+    touch_t(k_sweep_tma<false, EPI_STORE2, GatherScaledT, CH, OFS>);
+    touch_t(k_sweep_tma<true, EPI_STORE, GatherPlainT, CH, OFS>);
+    touch_t(k_sweep_tma<true, EPI_XADD, GatherPlainT, CH, OFS>);
+    touch_t(k_sweep_tma<true, EPI_XADD_SCALE, GatherPlainT, CH, OFS>);
+    touch_t(k_sweep_tma<false, EPI_STORE, GatherPlainT, CH, OFS>);
+    touch_t(k_sweep_tma<false, EPI_XADD, GatherPlainT, CH, OFS>);
+    touch_t(k_sweep_tma<false, EPI_XADD_SCALE, GatherPlainT, CH, OFS>);
+    touch_t(k_sweep_tma<false, EPI_STORE, GatherScaledT, CH, OFS>);
+    touch_t(k_sweep_tma<false, EPI_XADD, GatherScaledT, CH, OFS>);
+    touch_t(k_sweep_tma<false, EPI_XADD_SCALE, GatherScaledT, CH, OFS>);
 }
 }  // namespace
 
 void preload_tma_kernels() {
-    touch_tma_ch<4>();
-    touch_tma_ch<8>();
-    touch_tma_ch<16>();
+    touch_tma_ch<4, false>();
+    touch_tma_ch<8, false>();
+    touch_tma_ch<16, false>();
+    touch_tma_ch<4, true>();
+    touch_tma_ch<8, true>();
+    touch_tma_ch<16, true>();
 }
 
 }  // namespace nsm

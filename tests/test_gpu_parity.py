@@ -67,6 +67,9 @@ SMALL = {
     "var27_9": lambda: inputs.var27(9),
     "cd_rcm_10": lambda: inputs.convdiff(10),
     "random_irregular": lambda: random_sparse(997, 5),
+    # offset-aligned layout (nsm_layout): stencil rows, ragged tail / 27-point
+    "lap_aligned_ragged": lambda: inputs.laplace(100, 9, 3),
+    "var27_aligned_40": lambda: inputs.var27(40),
 }
 
 
@@ -253,3 +256,12 @@ def test_other_smoothers(case, kind, k, nu, xz):
     x = start(x0, xz)
     S.smooth(dev(b), x, kind, nu=nu, k_l=k, x_is_zero=xz)
     agree(host(x), ORACLE_APPLY[kind](A, b, x0, k, nu, xz), f"{name} {kind} k={k} nu={nu} xz={xz}")
+
+
+def test_layout_choice_matches_host_mirror(case):
+    """The builder's offset-aligned layout choice (nsm_layout) is the one
+    bench.py's reference arm assumes when it counts bytes."""
+    import bench
+    name, A, F, S = case
+    lay, want = S.layout(), bench.aligned_parts(A)
+    assert lay["L"] == want["L"] and lay["U"] == want["U"], (name, lay, want)
