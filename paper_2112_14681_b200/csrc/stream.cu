@@ -89,13 +89,22 @@ struct GatherScaledT {
 // Shared-memory layout: full[NST], empty[NST] mbarriers, then NST stages of
 // NP parts of {val[cap], col[cap]} with cap = kTS * 32 * maxw entries.
 // With the offset-aligned layout (ofs) only the values are staged (8 B per
-// entry); columns are row + offset.
+// entry); columns are row + offset.  That layout's parts also carry a header
+// written by the producer warp: per slice of the tile, {first entry relative
+// to the tile, width}, so consumers take the slice geometry from shared memory
+// after the stage wait instead of a global round trip of their own per tile.
+constexpr int kHdrBytes = kTS * 2 * 4;
+
 struct Layout {
     int nst, np;
     int64_t cap;  // entries per part per stage
-    int eb;       // staged bytes per entry: 12 (values + columns) or 8 (values; + the slices' offsets)
+    int eb;       // staged bytes per entry: 12 (values + columns) or 8 (values; + the slices' offsets + header)
+    __host__ __device__ static int64_t ofs_bytes(int64_t cap) { return (cap / kSlice * 4 + 15) / 16 * 16; }
     __host__ __device__ static int64_t part_bytes(int64_t cap, int eb) {
-        return eb == 12 ? cap * 12 : cap * 8 + (cap / kSlice * 4 + 15) / 16 * 16;
+        return eb == 12 ? cap * 12 : cap * 8 + ofs_bytes(cap) + kHdrBytes;
+    }
+    __device__ __forceinline__ int32_t *hdr(char *s, int st, int p) const {  // eb 8 only
+        return (int32_t *)(s + 128 + ((int64_t)st * np + p) * part_bytes(cap, eb) + cap * 8 + ofs_bytes(cap));
     }
     __device__ __forceinline__ uint64_t *full(char *s) const { return (uint64_t *)s; }
     __device__ __forceinline__ uint64_t *empty(char *s) const { return (uint64_t *)s + nst; }
@@ -131,6 +140,7 @@ constexpr int kOfsPerLane = 4;  // staged offsets per lane and part (8 slices x 
 template <int NP>
 struct TileRefs {
     int64_t b[NP], e[NP];
+    int64_t sp[NP];  // lanes 0..kTS: slice pointer of slice s0 + lane (clamped to the tile end)
     int32_t o[NP][kOfsPerLane];
 };
 
@@ -144,6 +154,8 @@ __device__ __forceinline__ void tile_refs(const Layout &Ly, const SellView (&P)[
         r.e[p] = __ldg(P[p].ptr + s1);
     }
     if (Ly.eb == 8) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) r.sp[p] = lane <= kTS ? __ldg(P[p].ptr + min(s0 + lane, s1)) : 0;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const int64_t no = (r.e[p] - r.b[p]) / kSlice;
@@ -193,14 +205,13 @@ template <int NP>
 __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellView (&P)[NP], int64_t s_begin,
                                          int64_t s_end, int64_t ntiles, int lane) {
     const uint64_t pol = policy_evict_first_t();
-    int it = 0;
+    int it = 0, st = 0;
+    uint32_t ph = 0;  // (it / nst) & 1
     TileRefs<NP> cur, nxt;
     if ((int64_t)blockIdx.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, blockIdx.x, lane, cur);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int st = it % Ly.nst;
-        const uint32_t use = (uint32_t)(it / Ly.nst);
         if (t + gridDim.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, t + gridDim.x, lane, nxt);  // prefetch
-        if (it >= Ly.nst) mbar_wait(Ly.empty(sm) + st, (use - 1) & 1);
+        if (it >= Ly.nst) mbar_wait(Ly.empty(sm) + st, ph ^ 1);
         uint32_t bytes = 0;
 #pragma unroll
         for (int p = 0; p < NP; ++p) bytes += (uint32_t)((cur.e[p] - cur.b[p]) * Ly.eb);
@@ -216,6 +227,12 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
                 }
                 const int32_t *go = P[p].off + cur.b[p] / kSlice;  // wider tiles (not staged above)
                 for (int64_t k = lane + 32 * kOfsPerLane; k < no; k += 32) so[k] = __ldg(go + k);
+                const int64_t nsp = __shfl_down_sync(0xffffffffu, cur.sp[p], 1);
+                if (lane < kTS) {
+                    int32_t *h = Ly.hdr(sm, st, p);
+                    h[2 * lane] = (int32_t)(cur.sp[p] - cur.b[p]);
+                    h[2 * lane + 1] = (int32_t)((nsp - cur.sp[p]) / kSlice);
+                }
             }
             __syncwarp();
         }
@@ -233,6 +250,7 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
         }
         __syncwarp();
         cur = nxt;
+        if (++st == Ly.nst) { st = 0; ph ^= 1; }
     }
     if (lane == 0) pdl_trigger();  // all of this CTA's copies are issued: dependents may be scheduled
 }
@@ -336,10 +354,10 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
     }
     const GatherPlainT gx{x};
     pdl_wait();  // x, b of the previous kernel
-    int it = 0;
+    int it = 0;  // stage = it % nst (running stage/phase counters here measured 5-14 % slower on C3/C4)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int st = it % nst;
-        const uint32_t use = (uint32_t)(it / nst);
+        const uint32_t ph = (uint32_t)(it / nst) & 1;
         const int64_t s0 = s_begin + t * kTS, s = s0 + warp;
         const bool has = s < s_end;
         const int64_t i = s * kSlice + lane;
@@ -350,7 +368,7 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
         int64_t lo = 0, uo = 0;
         int lw = 0, uw = 0;
         Offsets<CH> ol, ou;
-        if (has) {
+        if (!OFS && has) {
             const int64_t l0 = __ldg(L.ptr + s0), ls = __ldg(L.ptr + s), ls1 = __ldg(L.ptr + s + 1);
             const int64_t u0 = __ldg(U.ptr + s0), us = __ldg(U.ptr + s), us1 = __ldg(U.ptr + s + 1);
             lo = ls - l0;
@@ -358,8 +376,12 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
             uo = us - u0;
             uw = (int)((us1 - us) / kSlice);
         }
-        mbar_wait(Ly.full(sm) + st, use & 1);
-        if constexpr (OFS) {
+        mbar_wait(Ly.full(sm) + st, ph);
+        if constexpr (OFS) {  // slice geometry from the producer's header
+            const int2 hl = *(const int2 *)(Ly.hdr(sm, st, 0) + 2 * warp);
+            const int2 hu = *(const int2 *)(Ly.hdr(sm, st, 1) + 2 * warp);
+            lo = hl.x; lw = hl.y;
+            uo = hu.x; uw = hu.y;
             ol.at(Ly.col(sm, st, 0), lo);
             ou.at(Ly.col(sm, st, 1), uo);
         }
@@ -427,10 +449,10 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
         return;
     }
     pdl_wait();  // rhs, iterates, x of the previous kernels
-    int it = 0;
+    int it = 0;  // stage = it % nst (running stage/phase counters here measured 5-14 % slower on C3/C4)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int st = it % nst;
-        const uint32_t use = (uint32_t)(it / nst);
+        const uint32_t ph = (uint32_t)(it / nst) & 1;
         const int64_t s0 = s_begin + t * kTS, s = s0 + warp;
         const bool has = s < s_end;
         const int64_t i = s * kSlice + lane;
@@ -442,13 +464,17 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
         int64_t to = 0;
         int tw = 0;
         Offsets<CH> ot;
-        if (has) {
+        if (!OFS && has) {
             const int64_t t0 = __ldg(T.ptr + s0), ts = __ldg(T.ptr + s), ts1 = __ldg(T.ptr + s + 1);
             to = ts - t0;
             tw = (int)((ts1 - ts) / kSlice);
         }
-        mbar_wait(Ly.full(sm) + st, use & 1);
-        if constexpr (OFS) ot.at(Ly.col(sm, st, 0), to);
+        mbar_wait(Ly.full(sm) + st, ph);
+        if constexpr (OFS) {  // slice geometry from the producer's header
+            const int2 h = *(const int2 *)(Ly.hdr(sm, st, 0) + 2 * warp);
+            to = h.x; tw = h.y;
+            ot.at(Ly.col(sm, st, 0), to);
+        }
         double acc = 0.0;
         if (has) {
             StagedChunk<CH> ct;

@@ -1,12 +1,13 @@
 #!/bin/bash
-# A/B of bench variants: CONFIGS, VARIANTS ("label:flags;label:flags")
+# A/B of library variants (build.py --variant) on one box: bench C2..C5, two reps, with clocks.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-for c in ${CONFIGS:-C2}; do
-  IFS=';' read -ra VS <<< "${VARIANTS:-base:}"
-  for rep in 1 2; do
-    for v in "${VS[@]}"; do
-      lab="${v%%:*}"; fl="${v#*:}"
-      python bench.py --steps 30 --warmup 5 --config $c --no-cpu $fl 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', '$lab', d['ms_per_step'], round(d['config']['frac_of_hbm_peak'],4), d['roofline']['frac'])"
-    done
+mkdir -p gpurun_out
+for rep in 1 2; do
+for v in "$@"; do
+  [ "$v" = default ] && v=""
+  for c in C2 C3 C4 C5; do
+    printf "v=%-8s %s rep=%s  " "$v" $c $rep >> gpurun_out/ab.log
+    NSM_LIB_VARIANT=$v timeout 300 python bench.py --config $c --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); r=d['roofline']; print(d['ms_per_step'], r['frac'], r.get('sweeps_frac'), d['clocks']['sm_mhz'])" >> gpurun_out/ab.log
   done
+done
 done
