@@ -272,7 +272,8 @@ struct Offsets {
     const int32_t *so;    // this slice's offsets in the stage
     __device__ __forceinline__ void at(const int32_t *stage_offs, int64_t lo) { so = stage_offs + lo / kSlice; }
     // 32-bit unsigned arithmetic (rows and columns < 2^31): one compare on
-    // the gather's dependent path (the 64-bit form cost ~10 % on C3)
+    // the gather's dependent path (the 64-bit form cost ~10 % on C3).  Only
+    // called for rows i < n (load_ofs gives the lanes past n width 0).
     __device__ __forceinline__ static int32_t col(int64_t i, int32_t off, int64_t n) {
         const uint32_t c = (uint32_t)((int32_t)i + off);
         return c < (uint32_t)n ? (int32_t)c : (int32_t)i;
@@ -306,7 +307,7 @@ struct StagedChunk {
         otail = of.so;
         row = row_;
         n = n_;
-        w = w_;
+        w = row_ < n_ ? w_ : 0;  // lanes past n in the last slice: nothing (a pad's column i would be out of bounds)
 #pragma unroll
         for (int j = 0; j < CH; ++j)
             if (j < w) {
