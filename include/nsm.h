@@ -264,6 +264,23 @@ nsm_status nsm_usolve(nsm_handle *h, const double *r, double *x, int k_sweeps, v
 nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, int nu, int k_l,
                       int k_u, int x_is_zero, void *stream);
 
+/*
+ * nsm_smooth_host — nsm_smooth on HOST vectors (the end-to-end call): copies
+ * b_host and x_in_host (not read when x_is_zero; may then be NULL) to two
+ * handle-owned device vectors on `stream`, runs nsm_smooth there, copies the
+ * result to x_out_host and synchronises the stream before returning.
+ * All three are n doubles in host memory; x_out_host may equal x_in_host
+ * (in place) but must not partially overlap it, and b_host aliases neither.
+ * Pinned (cudaHostAlloc / cudaHostRegister) memory gets full PCIe/C2C
+ * bandwidth; pageable memory works through the driver's staging.  The first
+ * call allocates the two staging vectors (2 n doubles, freed by nsm_destroy;
+ * NSM_ERR_OOM if that fails); later calls do not allocate.  Errors as
+ * nsm_smooth; a failed copy -> NSM_ERR_CUDA.  On error x_out_host is
+ * unspecified.
+ */
+nsm_status nsm_smooth_host(nsm_handle *h, nsm_kind kind, const double *b_host, const double *x_in_host,
+                           double *x_out_host, int nu, int k_l, int k_u, int x_is_zero, void *stream);
+
 /* y = A x  (plain SpMV with the stored split; used by the GMRES/V-cycle
  * driver).  With nranks > 1 the x halo is exchanged first. */
 nsm_status nsm_spmv(nsm_handle *h, const double *x, double *y, void *stream);

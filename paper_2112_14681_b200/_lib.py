@@ -20,7 +20,7 @@ _STATUS = {0: "NSM_OK", 1: "NSM_ERR_ARG", 2: "NSM_ERR_PATTERN", 3: "NSM_ERR_ZERO
            5: "NSM_ERR_CUDA", 6: "NSM_ERR_OOM", 7: "NSM_ERR_STATE", 8: "NSM_ERR_DIST"}
 
 # every symbol include/nsm.h declares (tests check the .so exports them)
-SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_spmv",
+SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_lsolve", "nsm_usolve", "nsm_smooth", "nsm_smooth_host", "nsm_spmv",
                   "nsm_check", "nsm_info", "nsm_stats", "nsm_last_error", "nsm_destroy", "nsm_halo_plan",
                   "nsm_halo_set_send", "nsm_halo_mailbox", "nsm_halo_connect_ipc", "nsm_halo_connect",
                   "nsm_halo_commit", "nsm_set_option", "nsm_spmat_setup", "nsm_spmat_apply",
@@ -68,6 +68,7 @@ def load():
     L.nsm_lsolve.argtypes = [vp, vp, vp, ci, vp]
     L.nsm_usolve.argtypes = [vp, vp, vp, ci, vp]
     L.nsm_smooth.argtypes = [vp, ci, vp, vp, ci, ci, ci, ci, vp]
+    L.nsm_smooth_host.argtypes = [vp, ci, vp, vp, vp, ci, ci, ci, ci, vp]
     L.nsm_check.argtypes = [vp, P(i64), vp]
     L.nsm_info.argtypes = [vp, P(i64), P(i64), P(i64), P(i64)]
     L.nsm_stats.argtypes = [vp, P(i64), P(i64)]
@@ -101,7 +102,7 @@ def load():
     L.nsm_destroy.argtypes = [vp]
     L.nsm_destroy.restype = None
     for name in ["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
-                 "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
+                 "nsm_smooth_host", "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
                  "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
                  "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats", "nsm_layout"]:
@@ -318,6 +319,30 @@ class Smoother:
         self._call(load().nsm_smooth(self._h, kd, self._vec(b, "b"), self._vec(x, "x"), int(nu), int(k_l), int(k_u),
                                      int(bool(x_is_zero)), self._stream(stream)))
         return x
+
+    def smooth_host(self, b, x, kind="pgs", nu=1, k_l=2, k_u=None, x_is_zero=False, stream=None, out=None):
+        """nsm_smooth_host: b, x (and out) are host vectors (float64, contiguous,
+        length n: numpy arrays or CPU tensors, pinned for full bandwidth).  The
+        result goes to `out`, or to x in place when out is None.  Synchronous."""
+        kd = KINDS[kind] if isinstance(kind, str) else int(kind)
+        k_u = k_l if k_u is None else k_u
+        dst = x if out is None else out
+        self._call(load().nsm_smooth_host(self._h, kd, self._hvec(b, "b"), self._hvec(x, "x"), self._hvec(dst, "out"),
+                                          int(nu), int(k_l), int(k_u), int(bool(x_is_zero)), self._stream(stream)))
+        return dst
+
+    def _hvec(self, t, name):
+        torch = self._torch
+        if isinstance(t, torch.Tensor):
+            ok = not t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() == self.n
+            ptr = t.data_ptr()
+        else:
+            import numpy as np
+            ok = isinstance(t, np.ndarray) and t.dtype == np.float64 and t.flags.c_contiguous and t.size == self.n
+            ptr = t.ctypes.data if ok else 0
+        if not ok:
+            raise TypeError(f"{name}: expected a contiguous float64 host vector (numpy or CPU tensor) of length {self.n}")
+        return ptr
 
     def check(self, stream=None):
         """Synchronises; returns None, or raises NsmError(NSM_ERR_NONFINITE)."""

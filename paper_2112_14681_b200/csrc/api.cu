@@ -46,6 +46,8 @@ struct nsm_handle {
     // ILU(0) factors: unit-lower L = I + Ls, U = D_U (I + D_U^{-1} Us)
     bool has_ilu = false;
     double *dU = nullptr;
+    // nsm_smooth_host staging vectors (allocated by its first call)
+    double *hb_dev = nullptr, *hx_dev = nullptr;
     // Ruiz-scaled U factor (Alg. 2 / NEXT-3): U~ = diag(1/s_r) U diag(1/s_c), unit diagonal
     bool ruiz = false;
     double *s_r = nullptr, *s_c = nullptr;
@@ -167,6 +169,8 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->ring_g);
     cudaFree(h->skew_sync);
     cudaFree(h->skew_prog);
+    cudaFree(h->hb_dev);
+    cudaFree(h->hx_dev);
     delete h;
 }
 
@@ -1083,6 +1087,50 @@ nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, 
         }
         if (st != NSM_OK) return st;
     }
+    return NSM_OK;
+}
+
+nsm_status nsm_smooth_host(nsm_handle *h, nsm_kind kind, const double *b_host, const double *x_in_host,
+                           double *x_out_host, int nu, int k_l, int k_u, int x_is_zero, void *stream) {
+    if (!h) return NSM_ERR_ARG;
+    if (h->n > 0 && (!b_host || !x_out_host || (!x_is_zero && !x_in_host))) {
+        h->err = "nsm_smooth_host: NULL host vector";
+        return NSM_ERR_ARG;
+    }
+    if (overlap(b_host, x_out_host, h->n) || (!x_is_zero && overlap(b_host, x_in_host, h->n))) {
+        h->err = "nsm_smooth_host: b aliases x";
+        return NSM_ERR_ARG;
+    }
+    if (!x_is_zero && x_in_host != x_out_host && overlap(x_in_host, x_out_host, h->n)) {
+        h->err = "nsm_smooth_host: x_in and x_out partially overlap";
+        return NSM_ERR_ARG;
+    }
+    cudaSetDevice(h->device);
+    const size_t bytes = (size_t)std::max<int64_t>(h->n, 1) * sizeof(double);
+    if (!h->hb_dev) {
+        cudaError_t e = cudaMalloc(&h->hb_dev, bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&h->hx_dev, bytes);
+        if (e != cudaSuccess) {
+            cudaFree(h->hb_dev);
+            h->hb_dev = h->hx_dev = nullptr;
+            cudaGetLastError();
+            h->err = "nsm_smooth_host: staging allocation failed";
+            return NSM_ERR_OOM;
+        }
+    }
+    cudaStream_t s = S(stream);
+    const size_t nb = (size_t)h->n * sizeof(double);
+    cudaError_t e = cudaSuccess;
+    if (nb) {
+        e = cudaMemcpyAsync(h->hb_dev, b_host, nb, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && !x_is_zero) e = cudaMemcpyAsync(h->hx_dev, x_in_host, nb, cudaMemcpyHostToDevice, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(h, e, "nsm_smooth_host (host to device)");
+    const nsm_status st = nsm_smooth(h, kind, h->hb_dev, h->hx_dev, nu, k_l, k_u, x_is_zero, stream);
+    if (st != NSM_OK) return st;
+    if (nb) e = cudaMemcpyAsync(x_out_host, h->hx_dev, nb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "nsm_smooth_host (device to host)");
     return NSM_OK;
 }
 

@@ -1,0 +1,70 @@
+"""nsm_smooth_host (the end-to-end C-ABI call on host vectors): bit-identical
+to nsm_smooth on device vectors, for pageable numpy and pinned CPU tensors,
+with and without x_is_zero; argument errors."""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _smoother(A, F=None):
+    import paper_2112_14681_b200 as nsm
+    return nsm.Smoother(A, F, device=0)
+
+
+@pytest.mark.parametrize("kind", ["pgs", "ilu", "pgs_symmetric"])
+@pytest.mark.parametrize("host", ["numpy", "pinned"])
+@pytest.mark.parametrize("x_is_zero", [False, True])
+def test_smooth_host_matches_device(kind, host, x_is_zero):
+    A = inputs.laplace(20, 13, 7)  # 1820 rows: a ragged last slice
+    F = oracle.ilu0(A)[2] if kind == "ilu" else None
+    b, x0 = inputs.uniform(3, A.nrows), inputs.uniform(4, A.nrows)
+    with _smoother(A, F) as S:
+        xd = torch.from_numpy(x0.copy()).cuda()
+        S.smooth(torch.from_numpy(b).cuda(), xd, kind, nu=2, k_l=2, k_u=3, x_is_zero=x_is_zero)
+        want = xd.cpu().numpy()
+        if host == "numpy":
+            bh, xh = b.copy(), x0.copy()
+        else:
+            bh = torch.from_numpy(b).pin_memory()
+            xh = torch.from_numpy(x0.copy()).pin_memory()
+        for _ in range(2):  # the second call reuses the staging vectors
+            xs = xh.copy() if host == "numpy" else xh.clone().pin_memory()
+            S.smooth_host(bh, xs, kind, nu=2, k_l=2, k_u=3, x_is_zero=x_is_zero)
+            got = xs if host == "numpy" else xs.numpy()
+            assert np.array_equal(got, want)
+        # out-of-place: x_in untouched, the result in out
+        xin = xh.copy() if host == "numpy" else xh.clone().pin_memory()
+        out = np.empty_like(x0) if host == "numpy" else torch.empty(A.nrows, dtype=torch.float64).pin_memory()
+        S.smooth_host(bh, xin, kind, nu=2, k_l=2, k_u=3, x_is_zero=x_is_zero, out=out)
+        assert np.array_equal(out if host == "numpy" else out.numpy(), want)
+        assert np.array_equal(xin if host == "numpy" else xin.numpy(), x0)
+        # b is untouched
+        assert np.array_equal(bh if host == "numpy" else bh.numpy(), b)
+        # and against the oracle (one more, independent check of the path)
+        if kind == "pgs" and not x_is_zero:
+            ref = oracle.pgs_apply(A, b, oracle.pgs_apply(A, b, x0, 2), 2)
+            np.testing.assert_allclose(got, ref, rtol=1e-13, atol=0)
+
+
+def test_smooth_host_errors():
+    import paper_2112_14681_b200 as nsm
+    A = inputs.laplace(8, 8, 2)
+    b = inputs.uniform(0, A.nrows)
+    with _smoother(A) as S:
+        with pytest.raises(TypeError):
+            S.smooth_host(b.astype(np.float32), b.copy())
+        with pytest.raises(TypeError):
+            S.smooth_host(b, torch.zeros(A.nrows, dtype=torch.float64, device="cuda"))
+        with pytest.raises(nsm.NsmError):
+            S.smooth_host(b, b)  # aliased
+        with pytest.raises(nsm.NsmError):
+            y = np.zeros(A.nrows + 1)
+            S.smooth_host(b, y[:-1], out=y[1:])  # partial overlap of x_in and out
+        with pytest.raises(nsm.NsmError):
+            S.smooth_host(b, b.copy(), "ilu")  # no factors on this handle
