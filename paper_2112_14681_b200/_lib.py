@@ -421,8 +421,8 @@ class Smoother:
         self._call(load().nsm_set_option(self._h, 0, int(bool(enable))))
 
     def set_fused(self, mode):
-        """Phase-skewed fused passes: False/0 off, True/1 whenever possible,
-        2 = automatic (the default: large problems)."""
+        """Phase-skewed fused passes: False/0 off (the default), True/1 whenever
+        possible, 2 = automatic (large problems)."""
         self._call(load().nsm_set_option(self._h, 2, int(mode)))
 
     def set_fused_window(self, items: int):
