@@ -95,6 +95,10 @@ struct GatherScaledT {
 // after the stage wait instead of a global round trip of their own per tile.
 constexpr int kHdrBytes = kTS * 2 * 4;
 
+#ifndef NSM_RES_PREFETCH_U
+#define NSM_RES_PREFETCH_U 1  // wide-row residual: prefetch U's gathers to L1 (C3 -1.2 %; tools/experiments/README.md)
+#endif
+
 struct Layout {
     int nst, np;
     int64_t cap;  // entries per part per stage
@@ -407,6 +411,16 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
                 if constexpr (OFS) c.load_ofs(Ly.val(sm, st, 0), ol, lo, lw, lane, i, n);
                 else c.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), lo, lw, lane);
                 c.gather_mul(gx);
+#if NSM_RES_PREFETCH_U
+                if constexpr (OFS) {  // U's gathers to L1 while L's are in flight (no registers held)
+                    if (i < n) {
+#pragma unroll
+                        for (int j = 0; j < CH; ++j)
+                            if (j < uw)
+                                asm volatile("prefetch.global.L1 [%0];" ::"l"(x + Offsets<CH>::col(i, ou.so[j], n)));
+                    }
+                }
+#endif
                 acc = c.add(acc, gx);
                 acc = __dadd_rn(acc, __dmul_rn(di, xi));
                 if constexpr (OFS) c.load_ofs(Ly.val(sm, st, 1), ou, uo, uw, lane, i, n);
