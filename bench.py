@@ -8,12 +8,16 @@ rows a2-a6; a7 halo exchange when N > 1).  value = algorithmic bytes of all
 steps of all ranks / max-over-ranks device time, in GB/s (BASELINE.json
 metric "smoother sweep GB/s (frac of HBM peak) and ms per pGS/ILU apply").
 
-Workload (default): BASELINE.json configs[1] = C2, 3-D 7-point Laplacian
-128^3, ILU(0) with k_l = k_u = 2 Jacobi sweeps; with N GPUs the grid is
-128 x 128 x 128N split into z-slabs (weak scaling, HYBRID halo exchange).
---config C3/C4/C5 select the other BASELINE workloads.
+Workload (default): BASELINE.json configs[2] = C3, the 27-point
+variable-coefficient pressure matrix on 256^3 (Nalu-Wind shaped, 449 M
+nonzeros), pGS with k = 2 Jacobi sweeps: the largest single-GPU
+configuration (SURVEY.md:715 -- C2 is about L2-sized and is a parity case).
+With N GPUs the grid is 256 x 256 x 256N split into z-slabs (weak scaling,
+one coefficient field over the global grid, HYBRID halo exchange), so the
+N = 1 line of a scaling run is this line.  --config C2/C4/C5 select the other
+BASELINE workloads (C4 is single-GPU: its RCM order is global).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl nsm|reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config C3] [--impl nsm|reference]
 """
 from __future__ import annotations
 
@@ -33,7 +37,7 @@ METRIC = "smoother sweep GB/s (frac of HBM peak) and ms per pGS/ILU apply at 1/2
 WORKLOADS = {
     # name: (generator edge N, kind, k_l, k_u, description)
     "C2": (128, "ilu", 2, 2, "C2: 3D 7-point Laplacian 128^3 per GPU, ILU(0) factors, Jacobi-iterated L/U solves k_l=k_u=2, nu=1"),
-    "C3": (256, "pgs", 2, 0, "C3: 3D 27-point variable-coefficient pressure matrix 256^3 (Nalu-Wind shaped), pGS k=2, nu=1"),
+    "C3": (256, "pgs", 2, 0, "C3: 3D 27-point variable-coefficient pressure matrix 256^3 per GPU (Nalu-Wind shaped), pGS k=2, nu=1"),
     "C4": (256, "ilu", 2, 2, "C4: convection-diffusion 256^3 + RCM (PeleLM shaped), ILU(0) k_l=k_u=2, nu=1"),
     "C5": (256, "pgs", 2, 0, "C5: 7-point Laplacian 256^3 rows per GPU, z-slab partition, pGS k=2, nu=1"),
 }
@@ -172,13 +176,16 @@ def build_workload(cfg: str, rank: int, nranks: int):
     """Matrix rows of this rank (global column ids), partition offsets, kind."""
     import inputs
     N, kind, k_l, k_u, desc = WORKLOADS[cfg]
-    if cfg in ("C2", "C5"):
+    if cfg in ("C2", "C3", "C5"):
         n_loc = N ** 3
-        A = inputs.laplace(N, N, N * nranks, rank * n_loc, (rank + 1) * n_loc)
+        if cfg == "C3":
+            A = inputs.var27_slab(N, nranks, rank)
+        else:
+            A = inputs.laplace(N, N, N * nranks, rank * n_loc, (rank + 1) * n_loc)
         offsets = np.arange(nranks + 1, dtype=np.int64) * n_loc
     else:
         if nranks > 1:
-            raise SystemExit(f"--config {cfg} is a single-GPU workload; use C2 or C5 for N > 1")
+            raise SystemExit(f"--config {cfg} is a single-GPU workload; use C2, C3 or C5 for N > 1")
         A = inputs.config_matrix(cfg)
         offsets = np.array([0, A.nrows], dtype=np.int64)
     return A, offsets, kind, k_l, k_u, desc
@@ -229,40 +236,66 @@ def flush_l2(buf):
     buf.sum()
 
 
+def workload_config(cfg: str, A, kind: str, k_l: int, k_u: int, nranks: int) -> dict:
+    """The `config` object of the JSON line: the workload only, identical for
+    the nsm arm and the reference arm (implementation details go elsewhere)."""
+    desc = WORKLOADS[cfg][4]
+    return {"workload": desc, "name": cfg, "n_per_gpu": int(A.nrows), "nnz_per_gpu": int(A.nnz), "kind": kind,
+            "k_l": k_l, "k_u": k_u, "nu": 1, "partition": "z-slab rows, HYBRID" if nranks > 1 else "none",
+            "l2": "flushed before every timed step (256 MB read through L2); the matrix alone is "
+                  f"{(12 * A.nnz) / 1e9:.1f} GB, far larger than the 126 MB L2"}
+
+
+def cpu_oracle(A, kind: str, k_l: int, k_u: int, b, x0, ab: int, seconds: float, all_cores: bool,
+               min_apps: int = 1) -> dict:
+    """Time the oracle (oracle/, as it stands) on whole applications of the
+    workload: at least `min_apps`, then more until `seconds` have passed.
+    all_cores: the same oracle.c built with -fopenmp (its row loops on every
+    host core, per-row arithmetic unchanged; bitwise equal to the 1-thread
+    build, tests/test_oracle_pins.py)."""
+    import oracle
+    cores = oracle.use_all_cores(all_cores)
+    try:
+        F = oracle.ilu0(A) if kind == "ilu" else None
+        x = x0.copy()
+        cnt, t0 = 0, time.perf_counter()
+        while cnt < min_apps or (time.perf_counter() - t0 < seconds and cnt < 200):
+            x = oracle.ilu_apply(A, F, b, x, k_l, k_u) if kind == "ilu" else oracle.pgs_apply(A, b, x, k_l)
+            cnt += 1
+        dt = time.perf_counter() - t0
+    finally:
+        oracle.use_all_cores(False)
+    return {"value": round(ab * cnt / dt / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "ms_per_apply": round(dt / cnt * 1e3, 2),
+            "sample": f"{cnt} full application(s) of the same workload, C oracle "
+                      f"({'-fopenmp row loops, ' + str(cores) + ' threads' if all_cores else 'single thread'}; "
+                      f"{dt:.1f} s)"}
+
+
 # ---------------------------------------------------------------- reference --
 def run_reference(args, rank, nranks):
     """The oracle (oracle/) timed as it stands on the host cores: the base
-    contract's reference arm for this tier (no runnable reference code)."""
+    contract's reference arm for this tier (no runnable reference code).
+    Each step is one whole application of the workload by the all-cores build
+    of the oracle (row loops on every host core, arithmetic unchanged); a
+    bounded single-thread sample is reported beside it."""
     if rank != 0:
         return
     import inputs
-    import oracle
     A, offsets, kind, k_l, k_u, desc = build_workload(args.config, 0, 1)
     nl, nu_, noff = split_counts(A)
     ab = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, 0, aligned_parts(A))["total"]  # as the nsm path
     b, x0 = inputs.uniform(inputs.SEED_B, A.nrows), inputs.uniform(inputs.SEED_X0, A.nrows)
-    F = oracle.ilu0(A) if kind == "ilu" else None
-
-    def step(x):
-        if kind == "ilu":
-            return oracle.ilu_apply(A, F, b, x, k_l, k_u)
-        return oracle.pgs_apply(A, b, x, k_l)
-
-    x = x0
-    for _ in range(args.warmup):
-        x = step(x)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        x = step(x)
-    dt = time.perf_counter() - t0
-    v = ab * args.steps / dt / 1e9
-    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+    cpu = cpu_oracle(A, kind, k_l, k_u, b, x0, ab, 0.0, True, min_apps=args.warmup)          # warm-up
+    cpu = cpu_oracle(A, kind, k_l, k_u, b, x0, ab, 0.0, True, min_apps=args.steps)
+    one = cpu_oracle(A, kind, k_l, k_u, b, x0, ab, 0.0, False, min_apps=1) if not args.no_cpu else None
+    v, ms = cpu["value"], cpu["ms_per_apply"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "n": A.nrows, "nnz": A.nnz},
-            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} full applications of the workload (single-threaded C oracle)"},
-            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": workload_config(args.config, A, kind, k_l, k_u, 1),
+            "cpu_baseline": {**cpu, "single_core": one},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -403,32 +436,24 @@ def run_nsm(args, rank, nranks, local_rank):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = ab * nranks * args.steps / (float(te.item()) * 1e-3) / 1e9
 
-    # ---- CPU oracle baseline (rank 0, N = 1, bounded sample)
+    # ---- CPU oracle baseline (rank 0, N = 1, bounded samples): the
+    # single-thread parity oracle and its all-cores build
     cpu = None
     if rank == 0 and nranks == 1 and not args.no_cpu:
-        import oracle
-        An = A
-        Fo = oracle.ilu0(An) if kind == "ilu" else None
         bn, xn = b.cpu().numpy(), x0.cpu().numpy()
-        cnt, t0 = 0, time.perf_counter()
-        while cnt < 200 and (time.perf_counter() - t0 < args.cpu_seconds or cnt == 0):
-            xn = oracle.ilu_apply(An, Fo, bn, xn, k_l, k_u) if kind == "ilu" else oracle.pgs_apply(An, bn, xn, k_l)
-            cnt += 1
-        dt = time.perf_counter() - t0
-        cpu = {"value": round(ab * cnt / dt / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"{cnt} full applications of the same workload, single-threaded C oracle ({dt:.1f} s)"}
+        one = cpu_oracle(A, kind, k_l, k_u, bn, xn, ab, args.cpu_seconds, False)
+        cpu = cpu_oracle(A, kind, k_l, k_u, bn, xn, ab, args.cpu_seconds, True)
+        cpu["single_core"] = one
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": nranks, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "n_per_gpu": A.nrows, "nnz_per_gpu": A.nnz, "kind": kind, "k_l": k_l,
-                       "k_u": k_u, "nu": 1, "partition": "z-slab rows" if nranks > 1 else "none",
-                       "kernels": ("plain register-blocked, one kernel per pass" if args.plain else
+            "config": workload_config(args.config, A, kind, k_l, k_u, nranks),
+            "detail": {"kernels": ("plain register-blocked, one kernel per pass" if args.plain else
                                    ("phase-skewed fused passes (k_skew, cp.async.bulk pipelined, persistent)" if fused
                                     else "cp.async.bulk pipelined (persistent), one kernel per pass")),
-                       "l2": "flushed before every timed step (256 MB read through L2)",
                        "bytes": ("algorithmic bytes of the path that ran (DESIGN.md §6): "
                                  + ("fused passes = the floor" if fused else "one kernel per pass")),
                        "bytes_per_step_per_gpu": ab, "floor_bytes_per_step_per_gpu": fmodel["total"],
@@ -455,10 +480,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=list(WORKLOADS))
+    ap.add_argument("--config", default="C3", choices=list(WORKLOADS))
     ap.add_argument("--impl", default="nsm", choices=["nsm", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--plain", action="store_true", help="plain register-blocked kernels instead of the bulk-copy pipelined ones")
     ap.add_argument("--pdl", default="auto", choices=["auto", "on", "off"],
                     help="programmatic dependent launch (auto: the library's size-based default)")

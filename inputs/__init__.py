@@ -149,6 +149,27 @@ def var27(N: int, seed: int = SEED_FIELD, contrast: float = 1e4, r0: int = 0, r1
                  r1 - r0, n, r0)
 
 
+def var27_grid(nx: int, ny: int, nz: int, r0: int = 0, r1: int | None = None, seed: int = SEED_FIELD,
+               contrast: float = 1e4) -> CSR:
+    """Rows [r0, r1) of the 27-point pressure matrix on an nx x ny x nz grid
+    (the C3 recipe; var27(N) is var27_grid(N, N, N))."""
+    n = nx * ny * nz
+    r1 = n if r1 is None else r1
+    kap = kappa_field(nx, ny, nz, seed, contrast)
+    L = _L()
+    return _fill(lambda: L.gen_var27_nnz(nx, ny, nz, r0, r1),
+                 lambda rp, ci, va: L.gen_var27_fill(nx, ny, nz, _p(kap), r0, r1, _p(rp), _p(ci), _p(va)),
+                 r1 - r0, n, r0)
+
+
+def var27_slab(N: int, nranks: int, rank: int) -> CSR:
+    """Weak-scaled C3: the 27-point pressure matrix on the global
+    N x N x (N * nranks) grid (one coefficient field over the whole grid);
+    rank p owns the z-slab of rows [p N^3, (p+1) N^3).  nranks == 1 is C3."""
+    n_loc = N ** 3
+    return var27_grid(N, N, N * nranks, rank * n_loc, (rank + 1) * n_loc)
+
+
 def rcm_order(A: CSR) -> np.ndarray:
     order = np.empty(A.nrows, dtype=np.int64)
     rc = _L().gen_rcm(A.nrows, _p(A.rowptr), _p(A.col), _p(order))
@@ -227,7 +248,7 @@ def config_matrix(name: str, scale: int | None = None, nranks: int = 1, rank: in
         N = scale or 128
         return laplace(N, N, N)
     if name == "C3":
-        return var27(scale or 256)
+        return var27_slab(scale or 256, nranks, rank)
     if name == "C4":
         return convdiff(scale or 256)
     if name == "C5":

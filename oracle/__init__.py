@@ -19,39 +19,66 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
-_lib = None
 
 
 class OracleError(RuntimeError):
     pass
 
 
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+_libs = {}
+_variant = "serial"
+_CFLAGS = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall", "-Wno-unknown-pragmas"]
+
+
+def _build_one(path: str, extra: list, force: bool) -> str:
+    if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_SRC):
+        tmp = path + f".tmp{os.getpid()}"
+        subprocess.check_call(_CFLAGS + extra + ["-o", tmp, _SRC])
+        os.replace(tmp, path)
+    return path
+
+
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-                               "-Wall", "-o", tmp, _SRC])
-        os.replace(tmp, _LIB)
-    return _LIB
+    """liboracle.so (single thread: the parity oracle) and liboracle_omp.so
+    (the same source with -fopenmp: its row loops run on all cores with
+    per-row arithmetic unchanged; used only for bench.py's all-cores CPU
+    baseline)."""
+    _build_one(_LIB_OMP, ["-fopenmp"], force)
+    return _build_one(_LIB, [], force)
+
+
+def use_all_cores(on: bool = True) -> int:
+    """Switch every function of this module to the -fopenmp build (on) or
+    back to the single-thread parity build (off).  Returns the number of
+    threads the row loops use (1 when off)."""
+    global _variant
+    _variant = "omp" if on else "serial"
+    if not on:
+        return 1
+    _L()
+    return len(os.sched_getaffinity(0)) if not os.environ.get("OMP_NUM_THREADS") else int(os.environ["OMP_NUM_THREADS"])
 
 
 def _L():
-    global _lib
-    if _lib is None:
-        _lib = ctypes.CDLL(build())
+    lib = _libs.get(_variant)
+    if lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_OMP if _variant == "omp" else _LIB)
         i64, vp, ci = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
-        _lib.orc_residual.argtypes = [i64, vp, vp, vp, vp, vp, vp]
-        _lib.orc_spmv.argtypes = [i64, vp, vp, vp, vp, vp]
-        _lib.orc_tri_jacobi.argtypes = [i64, vp, vp, vp, ci, ci, vp, ci, ci, vp, vp]
-        _lib.orc_tri_direct.argtypes = [i64, vp, vp, vp, ci, ci, vp, ci, vp, vp]
-        _lib.orc_pgs_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, ci, ci, vp]
-        _lib.orc_gs_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, vp]
-        _lib.orc_pgs_backward_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, ci, ci, vp]
-        _lib.orc_l1_jacobi_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci]
-        _lib.orc_ilu0.argtypes = [i64, vp, vp, vp, vp]
-        _lib.orc_ilu0_fixed_point.argtypes = [i64, vp, vp, vp, ci, vp]
-        _lib.orc_ilu_apply.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci, ci, ci, ci, ci, vp]
-    return _lib
+        lib.orc_residual.argtypes = [i64, vp, vp, vp, vp, vp, vp]
+        lib.orc_spmv.argtypes = [i64, vp, vp, vp, vp, vp]
+        lib.orc_tri_jacobi.argtypes = [i64, vp, vp, vp, ci, ci, vp, ci, ci, vp, vp]
+        lib.orc_tri_direct.argtypes = [i64, vp, vp, vp, ci, ci, vp, ci, vp, vp]
+        lib.orc_pgs_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, ci, ci, vp]
+        lib.orc_gs_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, vp]
+        lib.orc_pgs_backward_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci, ci, ci, vp]
+        lib.orc_l1_jacobi_apply.argtypes = [i64, vp, vp, vp, vp, vp, ci, ci]
+        lib.orc_ilu0.argtypes = [i64, vp, vp, vp, vp]
+        lib.orc_ilu0_fixed_point.argtypes = [i64, vp, vp, vp, ci, vp]
+        lib.orc_ilu_apply.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci, ci, ci, ci, ci, vp]
+        _libs[_variant] = lib
+    return lib
 
 
 def _p(a):

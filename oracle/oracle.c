@@ -35,6 +35,18 @@
 
 typedef int64_t i64;
 
+/* Row-parallel loops (each row's arithmetic is independent of the others and
+ * keeps its own ascending order, so results do not depend on the thread
+ * count).  The parity oracle is built WITHOUT -fopenmp (pragma ignored,
+ * single thread); bench.py's all-cores CPU baseline loads the same source
+ * built with -fopenmp (liboracle_omp.so).  tests/test_oracle_pins.py checks
+ * the two builds agree bit for bit. */
+#ifdef _OPENMP
+#define ORC_ROWS _Pragma("omp parallel for schedule(static)")
+#else
+#define ORC_ROWS
+#endif
+
 /* owner block of row/column j under the partition (bounds ascending) */
 static i64 owner(i64 j, int nblocks, const i64 *bounds) {
     if (nblocks <= 1) return 0;
@@ -49,12 +61,14 @@ static i64 owner(i64 j, int nblocks, const i64 *bounds) {
 /* d_i = a_ii (A = L + D + U).  Missing or zero diagonal is an
  * error (reading R9). */
 static int diagonal(i64 n, const i64 *rp, const i64 *ci, const double *va, double *d) {
+    ORC_ROWS
     for (i64 i = 0; i < n; ++i) {
         d[i] = 0.0;
         for (i64 p = rp[i]; p < rp[i + 1]; ++p)
             if (ci[p] == i) d[i] = va[p];
-        if (d[i] == 0.0) return (int)(-(2 + i));
     }
+    for (i64 i = 0; i < n; ++i)
+        if (d[i] == 0.0) return (int)(-(2 + i));
     return 0;
 }
 
@@ -62,6 +76,7 @@ static int diagonal(i64 n, const i64 *rp, const i64 *ci, const double *va, doubl
  * ("r^(k) = b - A x^(k)"). */
 int orc_residual(i64 n, const i64 *rp, const i64 *ci, const double *va,
                  const double *b, const double *x, double *r) {
+    ORC_ROWS
     for (i64 i = 0; i < n; ++i) {
         double s = 0.0;
         for (i64 p = rp[i]; p < rp[i + 1]; ++p) s = s + va[p] * x[ci[p]];
@@ -72,6 +87,7 @@ int orc_residual(i64 n, const i64 *rp, const i64 *ci, const double *va,
 
 /* y = A x  (plain SpMV, ascending columns; used by the driver tests) */
 int orc_spmv(i64 n, const i64 *rp, const i64 *ci, const double *va, const double *x, double *y) {
+    ORC_ROWS
     for (i64 i = 0; i < n; ++i) {
         double s = 0.0;
         for (i64 p = rp[i]; p < rp[i + 1]; ++p) s = s + va[p] * x[ci[p]];
@@ -103,8 +119,10 @@ int orc_tri_jacobi(i64 n, const i64 *rp, const i64 *ci, const double *va, int lo
     int rc = 0;
     if (unit) { for (i64 i = 0; i < n; ++i) d[i] = 1.0; }
     else if ((rc = diagonal(n, rp, ci, va, d)) != 0) { free(d); free(gn); return rc; }
+    ORC_ROWS
     for (i64 i = 0; i < n; ++i) g[i] = r[i] / d[i];
     for (int s = 0; s < k; ++s) {
+        ORC_ROWS
         for (i64 i = 0; i < n; ++i) {
             i64 oi = owner(i, nblocks, bounds);
             double acc = 0.0;
@@ -163,6 +181,7 @@ int orc_pgs_apply(i64 n, const i64 *rp, const i64 *ci, const double *va, const d
         else orc_residual(n, rp, ci, va, b, x, r);
         rc = orc_tri_jacobi(n, rp, ci, va, 1, 0, r, k, nblocks, bounds, g);
         if (rc) break;
+        ORC_ROWS
         for (i64 i = 0; i < n; ++i) x[i] = x[i] + g[i];
     }
     free(r); free(g);
@@ -183,6 +202,7 @@ int orc_pgs_backward_apply(i64 n, const i64 *rp, const i64 *ci, const double *va
         else orc_residual(n, rp, ci, va, b, x, r);
         rc = orc_tri_jacobi(n, rp, ci, va, 0, 0, r, k, nblocks, bounds, g);
         if (rc) break;
+        ORC_ROWS
         for (i64 i = 0; i < n; ++i) x[i] = x[i] + g[i];
     }
     free(r); free(g);
@@ -373,6 +393,7 @@ int orc_ilu_apply(i64 n, const i64 *rp, const i64 *ci, const double *va,
             if (!rc) rc = orc_tri_jacobi(n, frp, fci, fva, 0, 0, y, kU, nblocks, bounds, z);
         }
         if (rc) break;
+        ORC_ROWS
         for (i64 i = 0; i < n; ++i) x[i] = x[i] + z[i];
     }
     free(r); free(y); free(z);

@@ -19,8 +19,15 @@ def test_reference_arm_json_line():
         assert k in line, k
     assert line["value"] > 0 and line["unit"] == "GB/s"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
-    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
-    assert "C2" in line["config"]["workload"]
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] == len(os.sched_getaffinity(0))
+    assert cb["single_core"]["cores"] == 1 and cb["single_core"]["value"] > 0
+    # default workload = C3 (the largest single-GPU config); the config object
+    # carries the workload only, the same keys as the nsm arm's
+    assert line["config"]["name"] == "C3" and "27-point" in line["config"]["workload"]
+    assert set(line["config"]) == {"workload", "name", "n_per_gpu", "nnz_per_gpu", "kind", "k_l", "k_u", "nu",
+                                   "partition", "l2"}
+    assert line["config"]["n_per_gpu"] == 256 ** 3 and line["config"]["nnz_per_gpu"] == 449455096
 
 
 def test_byte_models():

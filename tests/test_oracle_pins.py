@@ -458,3 +458,26 @@ def test_l1_jacobi_properties():
     # unconditionally convergent for SPD A (Baker et al. 2011): rho(I - D_l1^-1 A) < 1
     rho = max(abs(np.linalg.eigvals(np.eye(A.nrows) - M / dl1[:, None])))
     assert rho < 1.0
+
+
+# ------------------------------------------------ all-cores oracle build ---
+# bench.py's all-cores CPU baseline (SURVEY.md §8(d) "Oracle timing") loads the
+# same oracle.c built with -fopenmp.  Its row loops keep each row's ascending
+# order, so it must agree with the single-thread parity build bit for bit.
+def test_all_cores_build_is_bitwise_serial():
+    A = inputs.var27(20)
+    F = oracle.ilu0(A)
+    b, x = inputs.uniform(0, A.nrows), inputs.uniform(1, A.nrows)
+    bounds = np.array([0, 3000, 5100, A.nrows], dtype=np.int64)
+    want = [oracle.residual(A, b, x), oracle.pgs_apply(A, b, x, 3, nu=2),
+            oracle.pgs_backward_apply(A, b, x, 2), oracle.ilu_apply(A, F, b, x, 2, 3),
+            oracle.pgs_apply(A, b, x, 2, bounds=bounds), oracle.l1_jacobi_apply(A, b, x, nu=2)]
+    try:
+        assert oracle.use_all_cores(True) >= 1
+        got = [oracle.residual(A, b, x), oracle.pgs_apply(A, b, x, 3, nu=2),
+               oracle.pgs_backward_apply(A, b, x, 2), oracle.ilu_apply(A, F, b, x, 2, 3),
+               oracle.pgs_apply(A, b, x, 2, bounds=bounds), oracle.l1_jacobi_apply(A, b, x, nu=2)]
+    finally:
+        oracle.use_all_cores(False)
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
