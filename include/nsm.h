@@ -399,9 +399,58 @@ const char *nsm_solver_last_error(const nsm_amg *M);
  * blocks of columns as the iteration needs them, pinned host buffers, the
  * captured V-cycle graph) is kept in M across calls and freed by
  * nsm_amg_destroy; with M = NULL it is allocated and freed per call.  One M
- * must not be used by concurrent nsm_gmres calls. */
+ * must not be used by concurrent nsm_gmres calls.  The graph is re-captured
+ * when a handle's options or Ruiz scaling changed (nsm_set_option,
+ * nsm_set_ruiz, nsm_set_comm).
+ * Distributed A (a row block per rank): every rank calls nsm_gmres with its
+ * rows of b and x; the reduction runs through the comm attached with
+ * nsm_set_comm (NSM_ERR_STATE without one; NSM_ERR_DIST if a rank timed
+ * out), so every rank takes the same iteration count. */
 nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int maxit, double tol, int t_mode,
                      int *iters, double *hist, void *stream);
+
+/* ---- cross-rank reduction of the distributed solver (NEXT-1) ------------
+ * Algorithm 1 step 6 is "Global synchronization": ONE all-reduce of the
+ * 2(k+1) partial dot products per iteration ("one MPI_AllReduce per
+ * iteration").  nsm_comm is that all-reduce on the device, over
+ * NVLink / NVSwitch peer memory: every rank stores its m values into slot
+ * `rank` of every rank's mailbox (CUDA IPC mappings across processes, plain
+ * device pointers for ranks sharing a process) and each rank adds the slots
+ * in ascending rank order, so all ranks hold bit-identical sums.
+ *
+ * nsm_comm_create: rank / nranks of the partition, capacity = largest m
+ * (GMRES needs 2 (maxit + 2); the distributed V-cycle the first coarse
+ * level's size), device ordinal.  nsm_comm_mailbox: the device base of this
+ * rank's mailbox and (ipc_handle != NULL) its 64-byte CUDA IPC handle.
+ * nsm_comm_connect[_ipc]: peer q's mailbox (base pointer in this process, or
+ * its IPC handle); once every rank is connected the comm is usable.
+ * nsm_comm_allreduce: out[j] = sum over ranks of in[j] (j < m), in and out
+ * device arrays of this rank (may alias), stream-ordered, no host sync; every
+ * rank must call it the same number of times in the same order.  A rank that
+ * waits longer than the timeout (default 20 s, nsm_comm_set_timeout) flags
+ * the comm; nsm_comm_check (synchronises `stream`) then returns
+ * NSM_ERR_DIST.  NSM_ERR_STATE before every rank is connected, NSM_ERR_ARG
+ * for m > capacity.
+ *
+ * nsm_set_comm attaches a comm (BORROWED, same rank / nranks / device) to a
+ * distributed handle: nsm_gmres on a distributed operator reduces its dot
+ * products through it (NSM_ERR_STATE without one), and an nsm_amg whose
+ * finest smoother is distributed restricts onto the replicated coarse levels
+ * through it: level 0 holds the rank's rows (P[0] = the rank's rows of the
+ * prolongation, n_local x n_1, global coarse columns), levels >= 1 are
+ * identical single-rank handles on every rank. */
+typedef struct nsm_comm nsm_comm;
+nsm_status nsm_comm_create(nsm_comm **out, int rank, int nranks, int64_t capacity, int device);
+nsm_status nsm_comm_mailbox(nsm_comm *c, void **base, void *ipc_handle);
+nsm_status nsm_comm_connect(nsm_comm *c, int q, void *peer_base);
+nsm_status nsm_comm_connect_ipc(nsm_comm *c, int q, const void *ipc_handle);
+nsm_status nsm_comm_allreduce(nsm_comm *c, const double *in, double *out, int64_t m, void *stream);
+nsm_status nsm_comm_check(nsm_comm *c, void *stream);
+nsm_status nsm_comm_set_timeout(nsm_comm *c, int64_t ms);
+nsm_status nsm_comm_stats(const nsm_comm *c, int64_t *allreduces);
+const char *nsm_comm_last_error(const nsm_comm *c);
+void nsm_comm_destroy(nsm_comm *c);
+nsm_status nsm_set_comm(nsm_handle *h, nsm_comm *c);
 
 /* Frees all device memory of the handle (synchronises its device).  NULL ok. */
 void nsm_destroy(nsm_handle *h);

@@ -8,8 +8,6 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIBPATH = os.path.join(_HERE, "libnsm.so")
-if os.environ.get("NSM_LIB_VARIANT"):   # build experiments (build.py --variant): an alternative in-tree build
-    _LIBPATH = os.path.join(_HERE, f"libnsm_{os.environ['NSM_LIB_VARIANT']}.so")
 _lib = None
 
 NSM_PGS, NSM_ILU0, NSM_PGS_BACKWARD, NSM_PGS_SYMMETRIC, NSM_L1_JACOBI = 0, 1, 2, 3, 4
@@ -26,7 +24,9 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual
                   "nsm_halo_commit", "nsm_set_option", "nsm_spmat_setup", "nsm_spmat_apply",
                   "nsm_spmat_destroy", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle", "nsm_amg_destroy",
                   "nsm_solver_last_error", "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz",
-                  "nsm_fused_stats", "nsm_layout"])
+                  "nsm_fused_stats", "nsm_layout", "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect",
+                  "nsm_comm_connect_ipc", "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout",
+                  "nsm_comm_stats", "nsm_comm_last_error", "nsm_comm_destroy", "nsm_set_comm"])
 
 
 class NsmError(RuntimeError):
@@ -50,11 +50,18 @@ def lib_path() -> str:
     return _LIBPATH
 
 
-def load():
-    """Load libnsm.so; raises if it has not been built (no fallback)."""
-    global _lib
+def load(variant: str = ""):
+    """Load libnsm.so; raises if it has not been built (no fallback).
+    variant: an alternative in-tree build for A/B experiments
+    (build.py --variant NAME -> libnsm_NAME.so), chosen explicitly before the
+    first handle is created."""
+    global _lib, _LIBPATH
     if _lib is not None:
+        if variant and not _LIBPATH.endswith(f"libnsm_{variant}.so"):
+            raise RuntimeError("load(variant) after the library was loaded")
         return _lib
+    if variant:
+        _LIBPATH = os.path.join(_HERE, f"libnsm_{variant}.so")
     if not os.path.exists(_LIBPATH):
         raise ImportError(f"{_LIBPATH} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
     L = ctypes.CDLL(_LIBPATH)
@@ -101,11 +108,26 @@ def load():
     L.nsm_last_error.restype = ctypes.c_char_p
     L.nsm_destroy.argtypes = [vp]
     L.nsm_destroy.restype = None
+    L.nsm_comm_create.argtypes = [P(vp), ci, ci, i64, ci]
+    L.nsm_comm_mailbox.argtypes = [vp, P(vp), vp]
+    L.nsm_comm_connect.argtypes = [vp, ci, vp]
+    L.nsm_comm_connect_ipc.argtypes = [vp, ci, vp]
+    L.nsm_comm_allreduce.argtypes = [vp, vp, vp, i64, vp]
+    L.nsm_comm_check.argtypes = [vp, vp]
+    L.nsm_comm_set_timeout.argtypes = [vp, i64]
+    L.nsm_comm_stats.argtypes = [vp, P(i64)]
+    L.nsm_comm_last_error.argtypes = [vp]
+    L.nsm_comm_last_error.restype = ctypes.c_char_p
+    L.nsm_comm_destroy.argtypes = [vp]
+    L.nsm_comm_destroy.restype = None
+    L.nsm_set_comm.argtypes = [vp, vp]
     for name in ["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
                  "nsm_smooth_host", "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
                  "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
-                 "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats", "nsm_layout"]:
+                 "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats", "nsm_layout",
+                 "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect", "nsm_comm_connect_ipc",
+                 "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout", "nsm_comm_stats", "nsm_set_comm"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -407,6 +429,12 @@ class Smoother:
         for S in ranks:
             S._call(L.nsm_halo_commit(S._h))
 
+    def set_comm(self, comm: "Comm | None"):
+        """Attach the cross-rank reduction used by gmres / Amg on this
+        distributed handle (nsm_set_comm; the comm is borrowed: keep it alive)."""
+        self._comm = comm
+        self._call(load().nsm_set_comm(self._h, comm._h if comm is not None else None))
+
     def set_ruiz(self, s_r, s_c):
         """Ruiz form of the ILU U solve (the factor must hold U~); None, None = off."""
         if s_r is None:
@@ -489,6 +517,87 @@ class Smoother:
 def _solver_err(h=None) -> str:
     m = load().nsm_solver_last_error(h)
     return m.decode() if m else ""
+
+
+class Comm:
+    """Device-side all-reduce across the ranks of a row-block partition
+    (nsm_comm: Algorithm 1's one global reduction per iteration, over
+    NVLink / NVSwitch peer memory; sums in ascending rank order)."""
+
+    def __init__(self, rank: int, nranks: int, capacity: int, device: int | None = None):
+        import torch
+        self._torch = torch
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.rank, self.nranks, self.capacity = int(rank), int(nranks), int(capacity)
+        h = ctypes.c_void_p()
+        st = load().nsm_comm_create(ctypes.byref(h), self.rank, self.nranks, self.capacity, self.device)
+        if st != 0:
+            raise NsmError(st, load().nsm_comm_last_error(None).decode())
+        self._h = h
+
+    def _call(self, st):
+        if st != 0:
+            raise NsmError(st, load().nsm_comm_last_error(self._h).decode())
+
+    def _mailbox(self):
+        base = ctypes.c_void_p()
+        ipc = ctypes.create_string_buffer(64)
+        self._call(load().nsm_comm_mailbox(self._h, ctypes.byref(base), ipc))
+        return base.value, ipc.raw
+
+    def connect(self, dist=None, group=None):
+        """Across processes (one rank per GPU): the IPC handles travel over
+        torch.distributed (plumbing)."""
+        if self.nranks == 1:
+            return
+        if dist is None:
+            import torch.distributed as dist
+        _, ipc = self._mailbox()
+        info = [None] * self.nranks
+        dist.all_gather_object(info, ipc, group=group)
+        for q in range(self.nranks):
+            if q != self.rank:
+                self._call(load().nsm_comm_connect_ipc(self._h, q, ctypes.create_string_buffer(info[q], 64)))
+
+    @staticmethod
+    def connect_local(comms):
+        """Ranks of ONE process (virtual ranks): plain device pointers."""
+        boxes = [c._mailbox()[0] for c in comms]
+        for c in comms:
+            for q, b in enumerate(boxes):
+                if q != c.rank:
+                    c._call(load().nsm_comm_connect(c._h, q, b))
+
+    def allreduce(self, x, out=None, stream=None):
+        torch = self._torch
+        out = torch.empty_like(x) if out is None else out
+        s = torch.cuda.current_stream(self.device).cuda_stream if stream is None else getattr(stream, "cuda_stream", stream)
+        self._call(load().nsm_comm_allreduce(self._h, x.data_ptr(), out.data_ptr(), x.numel(), s))
+        return out
+
+    def check(self, stream=None):
+        torch = self._torch
+        s = torch.cuda.current_stream(self.device).cuda_stream if stream is None else getattr(stream, "cuda_stream", stream)
+        self._call(load().nsm_comm_check(self._h, s))
+
+    def set_timeout(self, ms: int):
+        self._call(load().nsm_comm_set_timeout(self._h, int(ms)))
+
+    def stats(self) -> int:
+        v = ctypes.c_int64()
+        self._call(load().nsm_comm_stats(self._h, ctypes.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().nsm_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class SpMat:

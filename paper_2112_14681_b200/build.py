@@ -37,19 +37,39 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False, variant: str = "", extra: list[str] | None = None) -> str:
     """variant / extra: an alternative build (libnsm_<variant>.so, extra nvcc
-    flags) for A/B experiments, loaded with NSM_LIB_VARIANT=<variant>."""
+    flags, e.g. -DNSM_EXPERIMENTS for the environment knobs) for A/B
+    experiments, loaded with paper_2112_14681_b200.load(variant=<variant>).
+    Each source is compiled to an object in parallel, then linked."""
     lib = LIB if not variant else os.path.join(HERE, f"libnsm_{variant}.so")
     if not variant and not force and not stale():
         return LIB
+    import concurrent.futures as cf
+    import tempfile
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra or []) + ["-I", os.path.join(ROOT, "include")]
+    tmpd = tempfile.mkdtemp(prefix="nsm_build_")
+    objs = [os.path.join(tmpd, os.path.basename(src) + ".o") for src in sources()]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
+        return subprocess.run([nvcc, *flags, "-c", "-o", obj, src], capture_output=True, text=True)
+
+    with cf.ThreadPoolExecutor(max_workers=min(len(objs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, zip(sources(), objs)))
+    log = "".join(r.stdout + r.stderr for r in results)
+    if any(r.returncode != 0 for r in results):
+        raise RuntimeError("nvcc failed:\n" + log)
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [nvcc, *NVCC_FLAGS, *(extra or []), "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources(), "-lgomp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    res = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
+                          "-Xcompiler", "-fopenmp", "-lgomp"], capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     if verbose:
-        print(res.stderr)
+        print(log)
     os.replace(tmp, lib)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(tmpd)
     return lib
 
 

@@ -38,6 +38,8 @@ struct Peer {
 struct nsm_handle {
     int device = 0;
     uint64_t uid = 0;  // unique per setup (caches keyed by handle must not confuse a reused address)
+    uint64_t cfg_gen = 0;  // bumped by nsm_set_option / nsm_set_ruiz (captured graphs compare it)
+    nsm_comm *comm = nullptr;  // borrowed cross-rank reduction (nsm_set_comm), distributed solver layer
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
     // A = L + D + U (+ ghost couplings LG / UG)
@@ -373,7 +375,7 @@ static nsm_status fused_alloc(nsm_handle *h) {
         need(skew_shape(SKEW_NONE, false, 0, 0, mwf, K, h->n, std::max(h->DLs, h->DUs), 0, 0));
     }
     if (!all) return NSM_OK;  // shapes that do not fit shared memory: per-pass kernels
-    if (getenv("NSM_DEBUG_FULL_RINGS")) {  // window experiments (tools/skew_exp.py) only
+    if (knob("NSM_DEBUG_FULL_RINGS")) {  // window experiments (tools/skew_exp.py) only
         int64_t t = 1;
         while (t * tr < h->n) t <<= 1;
         mr = mg = t;
@@ -398,6 +400,9 @@ static nsm_status fused_alloc(nsm_handle *h) {
 
 bool nsm::nsm_is_distributed(const nsm_handle *h) { return h && h->nranks > 1; }
 uint64_t nsm::nsm_handle_uid(const nsm_handle *h) { return h ? h->uid : 0; }
+uint64_t nsm::nsm_handle_cfg_gen(const nsm_handle *h) { return h ? h->cfg_gen : 0; }
+int nsm::nsm_handle_device(const nsm_handle *h) { return h ? h->device : 0; }
+nsm_comm *nsm::nsm_handle_comm(const nsm_handle *h) { return h ? h->comm : nullptr; }
 
 extern "C" {
 
@@ -677,6 +682,8 @@ void nsm_destroy(nsm_handle *h) { free_handle(h); }
 
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
     if (!h) return NSM_ERR_ARG;
+    DeviceScope dev(h->device);
+    ++h->cfg_gen;
     switch (opt) {
         case NSM_OPT_PIPELINE: h->pipeline = value != 0; return NSM_OK;
         case NSM_OPT_FUSED:
@@ -691,7 +698,6 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
         case NSM_OPT_PROFILE:
             h->profile = value != 0;
             if (h->profile && h->ev.empty()) {
-                cudaSetDevice(h->device);
                 h->ev.resize(2 * 4096);
                 for (cudaEvent_t &e : h->ev) cudaEventCreate(&e);
                 h->ev_kind.assign(4096, 0);
@@ -704,6 +710,17 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
             return NSM_OK;
     }
     return NSM_ERR_ARG;
+}
+
+nsm_status nsm_set_comm(nsm_handle *h, nsm_comm *c) {
+    if (!h) return NSM_ERR_ARG;
+    if (c && (comm_rank(c) != h->rank || comm_nranks(c) != h->nranks || comm_device(c) != h->device)) {
+        h->err = "nsm_set_comm: the communicator's rank, rank count or device differs from the handle's";
+        return NSM_ERR_ARG;
+    }
+    h->comm = c;
+    ++h->cfg_gen;
+    return NSM_OK;
 }
 
 nsm_status nsm_info(const nsm_handle *h, int64_t *n_local, int64_t *n_ghost, int64_t *nnz_offdiag,
@@ -752,7 +769,8 @@ nsm_status nsm_ruiz(const nsm_csr *F, int max_iters, double *val, double *s_r, d
 
 nsm_status nsm_set_ruiz(nsm_handle *h, const double *s_r, const double *s_c) {
     if (!h || !h->has_ilu) return NSM_ERR_STATE;
-    cudaSetDevice(h->device);
+    DeviceScope dev(h->device);
+    ++h->cfg_gen;
     if (!s_r || !s_c) {
         h->ruiz = false;
         return NSM_OK;
@@ -798,12 +816,14 @@ nsm_status nsm_residual(nsm_handle *h, const double *b, const double *x, double 
         h->err = "nsm_residual: NULL or aliased vector";
         return NSM_ERR_ARG;
     }
+    DeviceScope dev(h->device);
     return residual_into(h, b, x, r, OUT_R, S(stream));
 }
 
 nsm_status nsm_spmv(nsm_handle *h, const double *x, double *y, void *stream) {
     if (!h) return NSM_ERR_ARG;
     if ((h->n > 0 && (!x || !y)) || overlap(x, y, h->n)) { h->err = "nsm_spmv: NULL or aliased vector"; return NSM_ERR_ARG; }
+    DeviceScope dev(h->device);
     return residual_into(h, nullptr, x, y, OUT_AX, S(stream));
 }
 
@@ -814,6 +834,7 @@ static nsm_status tri_solve(nsm_handle *h, bool lower, const double *r, double *
                        : "nsm_usolve: bad argument (k < 0, NULL or aliased vector)";
         return NSM_ERR_ARG;
     }
+    DeviceScope dev(h->device);
     cudaStream_t s = S(stream);
     Stage stg;
     if (h->has_ilu) stg = lower ? Stage{&h->Ls, &h->LsG, nullptr, r, k} : Stage{&h->Us, &h->UsG, h->dU, r, k};
@@ -855,15 +876,20 @@ static nsm_status skew_run(nsm_handle *h, SkewLaunch &L, bool unit, int DT, int 
     L.sync = h->skew_sync;
     L.prog = h->skew_prog;
     ProfScope prof(h, 2, s);
+#ifdef NSM_EXPERIMENTS
     // debug: per-unit timestamps of two CTAs, summarised on stderr
     static unsigned long long *trace = nullptr;
-    static const bool want_trace = getenv("NSM_DEBUG_SKEW_TRACE") != nullptr;
+    static const bool want_trace = knob("NSM_DEBUG_SKEW_TRACE") != nullptr;
     if (want_trace && !trace) {
         cudaMalloc(&trace, 2 * 3 * 2048 * 4 * sizeof(unsigned long long));
     }
     if (want_trace) cudaMemsetAsync(trace, 0, 2 * 3 * 2048 * 4 * sizeof(unsigned long long), s);
     L.trace = want_trace ? trace : nullptr;
+#else
+    L.trace = nullptr;
+#endif
     cudaError_t e = launch_skew(L, s);
+#ifdef NSM_EXPERIMENTS
     if (want_trace && e == cudaSuccess) {
         std::vector<unsigned long long> tb(2 * 3 * 2048 * 4);
         cudaStreamSynchronize(s);
@@ -893,6 +919,7 @@ static nsm_status skew_run(nsm_handle *h, SkewLaunch &L, bool unit, int DT, int 
             }
         }
     }
+#endif
     ++h->launches;
     if (e != cudaSuccess) return cuda_fail(h, e, "fused pass launch");
     *ran = true;
@@ -1075,6 +1102,7 @@ nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, 
     }
     if (kind < NSM_PGS || kind > NSM_L1_JACOBI) { h->err = "nsm_smooth: unknown kind"; return NSM_ERR_ARG; }
     if (kind == NSM_ILU0 && !h->has_ilu) { h->err = "nsm_smooth: ILU0 requested on a handle without factors"; return NSM_ERR_STATE; }
+    DeviceScope dev(h->device);
     cudaStream_t s = S(stream);
     for (int it = 0; it < nu; ++it) {
         const bool fresh = it == 0 && x_is_zero;
@@ -1105,7 +1133,14 @@ nsm_status nsm_smooth_host(nsm_handle *h, nsm_kind kind, const double *b_host, c
         h->err = "nsm_smooth_host: x_in and x_out partially overlap";
         return NSM_ERR_ARG;
     }
-    cudaSetDevice(h->device);
+    if (nu == 0) {  // no application: the result is the start vector
+        if (h->n > 0) {
+            if (x_is_zero) std::memset(x_out_host, 0, (size_t)h->n * sizeof(double));
+            else if (x_out_host != x_in_host) std::memcpy(x_out_host, x_in_host, (size_t)h->n * sizeof(double));
+        }
+        return NSM_OK;
+    }
+    DeviceScope dev(h->device);
     const size_t bytes = (size_t)std::max<int64_t>(h->n, 1) * sizeof(double);
     if (!h->hb_dev) {
         cudaError_t e = cudaMalloc(&h->hb_dev, bytes);
@@ -1136,7 +1171,7 @@ nsm_status nsm_smooth_host(nsm_handle *h, nsm_kind kind, const double *b_host, c
 
 nsm_status nsm_check(nsm_handle *h, int64_t *first_bad_sweep, void *stream) {
     if (!h) return NSM_ERR_ARG;
-    cudaSetDevice(h->device);
+    DeviceScope dev(h->device);
     cudaError_t e = cudaStreamSynchronize(S(stream));
     if (e != cudaSuccess) return cuda_fail(h, e, "nsm_check");
     unsigned long long v = 0, init = ULLONG_MAX;

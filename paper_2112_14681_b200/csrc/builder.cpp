@@ -251,7 +251,7 @@ nsm_status build_split(const nsm_csr *A, int64_t rb, int64_t re, Split *out, std
     out->n_ghost = (int64_t)g.size();
     LocalMap lm{rb};
     GhostMap gm{&g};
-    static const bool no_align = getenv("NSM_NO_ALIGNED_LAYOUT") != nullptr;  // A/B experiments
+    static const bool no_align = knob("NSM_NO_ALIGNED_LAYOUT") != nullptr;  // A/B experiments
     if (no_align || !pack_aligned(n, rb, cnt[P_L], first[P_L], ci, va, &out->L))
         pack(n, cnt[P_L], first[P_L], ci, va, lm, &out->L);
     if (no_align || !pack_aligned(n, rb, cnt[P_U], first[P_U], ci, va, &out->U))

@@ -65,6 +65,7 @@
 #include <climits>
 #include <cstdlib>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <utility>
 
@@ -790,15 +791,17 @@ const void *pick(int ph0, bool unit, int ch) {
 #undef NSM_PK
 }
 
-int sm_count_f() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+int sm_count_f() {  // of the current device (launches happen with the handle's device current)
+    static int n[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!n[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[dev] = v > 0 ? v : 148;
     }
-    return n;
+    return n[dev];
 }
 
 struct GeoF {
@@ -809,16 +812,18 @@ struct GeoF {
 // stages: maximise resident consumer warps (<= 32 per SM, <= 4 CTAs), then depth
 GeoF geometry_f(const void *k, int64_t stage_bytes) {
     static std::mutex mu;
-    static std::map<std::pair<const void *, int64_t>, GeoF> cache;
+    static std::map<std::tuple<int, const void *, int64_t>, GeoF> cache;  // per device (opt-in attribute)
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair(k, stage_bytes);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto key = std::make_tuple(dev, k, stage_bytes);
     auto itc = cache.find(key);
     if (itc != cache.end()) return itc->second;
     GeoF g;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxF);
     // experiment knobs (tools/skew_exp.py): cap stages / CTAs per SM
-    static const int max_nst = getenv("NSM_DEBUG_SKEW_NST") ? atoi(getenv("NSM_DEBUG_SKEW_NST")) : kMaxStages;
-    static const int max_per = getenv("NSM_DEBUG_SKEW_PERSM") ? atoi(getenv("NSM_DEBUG_SKEW_PERSM")) : 4;
+    static const int max_nst = knob("NSM_DEBUG_SKEW_NST") ? atoi(knob("NSM_DEBUG_SKEW_NST")) : kMaxStages;
+    static const int max_per = knob("NSM_DEBUG_SKEW_PERSM") ? atoi(knob("NSM_DEBUG_SKEW_PERSM")) : 4;
     int best = -1;
     for (int nst = 2; nst <= std::min(kMaxStages, max_nst); ++nst) {
         const int64_t smem = kHeader + nst * stage_bytes;
@@ -874,7 +879,7 @@ SkewShape skew_shape(int ph0, bool unit, int maxw0, int maxw1, int maxwT, int k,
     sh.ntiles = (n + kRowsF - 1) / kRowsF;
     // B consecutive 256-row tiles per scheduling tile: the per-item
     // synchronisation is paid once per B tiles of every phase
-    static const int env_b = getenv("NSM_DEBUG_SKEW_B") ? atoi(getenv("NSM_DEBUG_SKEW_B")) : 0;
+    static const int env_b = knob("NSM_DEBUG_SKEW_B") ? atoi(knob("NSM_DEBUG_SKEW_B")) : 0;
     int B = env_b > 0 ? env_b : 8;
     while (B > 1 && (B & (B - 1))) --B;  // power of two (ring masks)
     sh.B = B;
@@ -946,7 +951,7 @@ cudaError_t launch_skew(const SkewLaunch &L, cudaStream_t st) {
     auto al = [](const void *q) { return q == nullptr || ((uintptr_t)q & 15) == 0; };
     p.trace = L.trace;
     p.vec_bulk = al(p.dA) && al(p.b) && al(p.xin) && al(p.dT) && al(p.rhs) && al(p.x) && al(p.dn);
-    static const bool novec = getenv("NSM_DEBUG_SKEW_NOVEC") != nullptr;  // experiment knob
+    static const bool novec = knob("NSM_DEBUG_SKEW_NOVEC") != nullptr;  // experiment knob
     if (novec) p.vec_bulk = 0;
     void *args[] = {&p};
     // cooperative: all CTAs co-resident (the item schedule relies on it)

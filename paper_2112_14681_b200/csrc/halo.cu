@@ -27,6 +27,7 @@
 #include <algorithm>
 
 #include "nsm_internal.h"
+#include "ptx.cuh"
 
 namespace nsm {
 
@@ -35,19 +36,9 @@ namespace {
 constexpr int kPutThreads = 256;
 constexpr int kPutItems = 4;  // entries per thread per block
 
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
+using ptx::globaltimer_ns;
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) { ptx::st_release_sys_u64(p, v); }
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) { return ptx::ld_acquire_sys_u64(p); }
 
 __global__ void __launch_bounds__(kPutThreads) k_halo_put(const PutDesc *__restrict__ desc, int npeers,
                                                           const double *__restrict__ src,

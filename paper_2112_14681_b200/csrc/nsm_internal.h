@@ -9,6 +9,16 @@
 
 #include "../../include/nsm.h"
 
+// Experiment knobs (the A/B scripts under tools/experiments) exist only in a
+// build with -DNSM_EXPERIMENTS; the product build reads no environment
+// variable (knob() is a constant nullptr and the branches fold away).
+#ifdef NSM_EXPERIMENTS
+#include <cstdlib>
+inline const char *knob(const char *name) { return std::getenv(name); }
+#else
+inline const char *knob(const char *) { return nullptr; }
+#endif
+
 namespace nsm {
 
 constexpr int kSlice = 32;  // SELL-C slice height = warp width: one thread per row
@@ -193,12 +203,45 @@ void preload_fused_kernels();
 void preload_plain_kernels();
 void preload_tma_kernels();
 void preload_halo_kernels();
+void preload_solver_kernels();
 
 // True for handles of a multi-rank partition (their launches carry halo
 // sequence numbers and must not be captured into a replayed CUDA graph).
 bool nsm_is_distributed(const nsm_handle *h);
 // Unique id of a handle (never reused, unlike its address).
 uint64_t nsm_handle_uid(const nsm_handle *h);
+// Device ordinal of a handle; the cross-rank reduction attached to it
+// (nsm_set_comm), or nullptr.
+int nsm_handle_device(const nsm_handle *h);
+nsm_comm *nsm_handle_comm(const nsm_handle *h);
+// comm.cu: device-side all-reduce (sum, ascending rank order) of m doubles;
+// comm_failed reads the mapped error word (after a stream synchronisation).
+nsm_status comm_allreduce(nsm_comm *c, const double *in, double *out, int64_t m, cudaStream_t s);
+bool comm_failed(const nsm_comm *c);
+int comm_rank(const nsm_comm *c);
+int comm_nranks(const nsm_comm *c);
+int64_t comm_capacity(const nsm_comm *c);
+int comm_device(const nsm_comm *c);
+
+// Configuration generation of a handle: bumped by every nsm_set_option /
+// nsm_set_ruiz, so a replayed graph can tell that its launch sequence is stale.
+uint64_t nsm_handle_cfg_gen(const nsm_handle *h);
+
+// The C-ABI calls run on their object's device: make it current for the
+// call and give the caller back its own current device afterwards
+// (cudaGetDevice is a thread-local read).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        int cur = 0;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceScope(const DeviceScope &) = delete;
+    DeviceScope &operator=(const DeviceScope &) = delete;
+};
 
 // Host ILUT(droptol, lfil) and Ruiz scaling of the U factor (NEXT-3).
 nsm_status ilut_host(const nsm_csr *A, double droptol, int lfil, std::vector<int64_t> &rp_out,

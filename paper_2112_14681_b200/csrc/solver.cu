@@ -174,6 +174,20 @@ inline unsigned blocks(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + k
 
 }  // namespace
 
+// Load every solver kernel now (lazy module loading synchronises the context:
+// a first launch while a peer rank's halo / reduction wait spins on this
+// device would stall until the timeout).
+void nsm::preload_solver_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, k_csr_spmv);
+    cudaFuncGetAttributes(&a, k_csr_spmv_wide);
+    cudaFuncGetAttributes(&a, k_dense_gemv);
+    cudaFuncGetAttributes(&a, k_multidot);
+    cudaFuncGetAttributes(&a, k_sum_parts);
+    cudaFuncGetAttributes(&a, k_multiaxpy);
+    cudaFuncGetAttributes(&a, k_scal);
+}
+
 // ------------------------------------------------------------ sparse matrix --
 struct nsm_spmat {
     int device = 0;
@@ -196,7 +210,8 @@ struct GmresWs {
     double *V = nullptr, *u = nullptr, *w = nullptr, *z = nullptr, *part = nullptr, *red = nullptr, *hd = nullptr;
     double *hred = nullptr, *hh = nullptr;  // pinned host mirrors
     cudaGraphExec_t gexec = nullptr;
-    uint64_t gA = 0;                   // uid of the operator handle the graph was captured for
+    std::vector<uint64_t> gsig;        // (uid, configuration generation) of the operator and every
+                                       // smoother handle the graph was captured with
     cudaStream_t gs = nullptr;
     bool stale = true;
     cudaStream_t own = nullptr;        // private stream when the caller's cannot be captured (legacy default)
@@ -221,6 +236,7 @@ struct nsm_amg {
     std::vector<Cfg> cfg;
     std::vector<double *> b, x, r;        // level work vectors (levels 1 .. nlevels; r on 0 .. nlevels-1)
     double *Minv = nullptr;               // dense inverse of the coarsest matrix
+    double *rpart = nullptr;              // distributed finest level: this rank's share of R r (n_1)
     int nc = 0;
     std::string err;
 };
@@ -336,8 +352,24 @@ nsm_status amg_cycle(nsm_amg *M, int lev, const double *b, double *x, cudaStream
     nsm_status st = nsm_smooth(S, c.kind, b, x, c.nu_pre, c.k_l, c.k_u, 1, s);
     if (st == NSM_OK) st = nsm_residual(S, b, x, M->r[lev], s);
     if (st != NSM_OK) return fail(&M->err, std::string("level ") + std::to_string(lev) + ": " + nsm_last_error(S), st);
-    cudaError_t e = spmat_apply(M->R[lev], M->r[lev], M->b[lev + 1], 1.0, 0.0, s);
-    if (e != cudaSuccess) return fail(&M->err, cudaGetErrorString(e), NSM_ERR_CUDA);
+    cudaError_t e;
+    if (nsm_is_distributed(S)) {
+        // the rank's rows of the fine level restrict to a share of the
+        // (replicated) coarse right-hand side: b_{l+1} = sum over ranks of
+        // P_p^T r_p, summed on the device over peer memory (nsm_comm)
+        if (lev != 0) return fail(&M->err, "only the finest level may be distributed (coarse levels are replicated)", NSM_ERR_STATE);
+        nsm_comm *c = nsm_handle_comm(S);
+        if (!c) return fail(&M->err, "distributed finest level without a comm (nsm_set_comm)", NSM_ERR_STATE);
+        if (comm_capacity(c) < M->n[1]) return fail(&M->err, "comm capacity below the first coarse level's size", NSM_ERR_ARG);
+        if (!M->rpart) return fail(&M->err, "distributed level 0 set up after nsm_amg_setup", NSM_ERR_STATE);
+        e = spmat_apply(M->R[lev], M->r[lev], M->rpart, 1.0, 0.0, s);
+        if (e != cudaSuccess) return fail(&M->err, cudaGetErrorString(e), NSM_ERR_CUDA);
+        st = comm_allreduce(c, M->rpart, M->b[lev + 1], M->n[1], s);
+        if (st != NSM_OK) return fail(&M->err, "coarse restriction all-reduce failed", st);
+    } else {
+        e = spmat_apply(M->R[lev], M->r[lev], M->b[lev + 1], 1.0, 0.0, s);
+        if (e != cudaSuccess) return fail(&M->err, cudaGetErrorString(e), NSM_ERR_CUDA);
+    }
     st = amg_cycle(M, lev + 1, M->b[lev + 1], M->x[lev + 1], s);
     if (st != NSM_OK) return st;
     e = spmat_apply(M->P[lev], M->x[lev + 1], x, 1.0, 1.0, s);
@@ -382,6 +414,7 @@ void nsm_amg_destroy(nsm_amg *M) {
     for (double *p : M->x) cudaFree(p);
     for (double *p : M->r) cudaFree(p);
     cudaFree(M->Minv);
+    cudaFree(M->rpart);
     M->ws.release();
     delete M;
 }
@@ -395,9 +428,10 @@ nsm_status nsm_amg_setup(nsm_amg **out, int nlevels, nsm_handle *const *smoother
         return fail(&g_solver_err, "nsm_amg_setup: the coarse matrix must be square with 1..8192 rows", NSM_ERR_ARG);
     nsm_amg *M = new nsm_amg();
     M->device = device;
+    DeviceScope devscope(device);
+    preload_solver_kernels();
     M->nlevels = nlevels;
     M->cfg.resize(nlevels);
-    cudaSetDevice(device);
     nsm_status st = NSM_OK;
     for (int l = 0; l < nlevels && st == NSM_OK; ++l) {
         int64_t nl = 0;
@@ -442,6 +476,13 @@ nsm_status nsm_amg_setup(nsm_amg **out, int nlevels, nsm_handle *const *smoother
     M->b.assign(nlevels + 1, nullptr);
     M->x.assign(nlevels + 1, nullptr);
     M->r.assign(nlevels, nullptr);
+    // distributed finest level: this rank's share of the restriction (allocated
+    // here, not in the cycle: no allocation inside a distributed solve)
+    if (st == NSM_OK && nlevels > 0 && nsm_is_distributed(M->S[0]) &&
+        cudaMalloc(&M->rpart, std::max<int64_t>(M->n[1], 1) * sizeof(double)) != cudaSuccess) {
+        st = NSM_ERR_OOM;
+        g_solver_err = "nsm_amg_setup: device allocation failed";
+    }
     for (int l = 0; l <= nlevels && st == NSM_OK; ++l) {
         const size_t bytes = std::max<int64_t>(M->n[l], 1) * sizeof(double);
         if (l < nlevels && cudaMalloc(&M->r[l], bytes) != cudaSuccess) st = NSM_ERR_OOM;
@@ -466,7 +507,7 @@ nsm_status nsm_amg_set_smoother(nsm_amg *M, int level, nsm_kind kind, int nu_pre
 
 nsm_status nsm_amg_vcycle(nsm_amg *M, const double *b, double *x, void *stream) {
     if (!M || !b || !x || b == x) return NSM_ERR_ARG;
-    cudaSetDevice(M->device);
+    DeviceScope dev(M->device);
     return amg_cycle(M, 0, b, x, (cudaStream_t)stream);
 }
 
@@ -479,22 +520,44 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
         g_solver_err = "nsm_gmres: bad argument";
         return NSM_ERR_ARG;
     }
+    DeviceScope devscope(nsm_handle_device(A));
     cudaStream_t s = (cudaStream_t)stream;
     int64_t n = 0;
     nsm_info(A, &n, nullptr, nullptr, nullptr);
     const int m1 = maxit + 1;
+    // a distributed operator reduces its dot products across ranks (step 6's
+    // "Global synchronization") through its comm; without one each rank
+    // would build its own Krylov coefficients
+    nsm_comm *comm = nsm_is_distributed(A) ? nsm_handle_comm(A) : nullptr;
+    if (nsm_is_distributed(A) && !comm) {
+        g_solver_err = "nsm_gmres: a distributed operator needs a comm for the global reduction (nsm_set_comm)";
+        return NSM_ERR_STATE;
+    }
+    if (comm && comm_capacity(comm) < 2 * (int64_t)(maxit + 2)) {
+        g_solver_err = "nsm_gmres: comm capacity below 2 (maxit + 2)";
+        return NSM_ERR_ARG;
+    }
+    if (M && nsm_is_distributed(A) != (M->nlevels > 0 && nsm_is_distributed(M->S[0]))) {
+        g_solver_err = "nsm_gmres: operator and finest smoother differ in distribution";
+        return NSM_ERR_ARG;
+    }
     GmresWs local;
     GmresWs &W = M ? M->ws : local;   // persistent with a preconditioner object
-    auto grow = [&](int cols) -> bool {  // basis capacity >= cols (keeps columns 0 .. cap-1)
+    // Basis capacity >= cols (keeps columns 0 .. cap-1).  Stream-ordered
+    // allocation: no device-wide synchronisation in the middle of a solve
+    // (cudaFree would wait for every stream of the device — with ranks sharing
+    // a device, for a peer's halo / reduction wait on a put this rank has not
+    // launched yet).
+    auto grow = [&](int cols) -> bool {
         if (cols <= W.cap) return true;
         const int nc = std::min(m1, std::max(cols, std::max(32, 2 * W.cap)));
         double *nv = nullptr;
-        if (cudaMalloc(&nv, (size_t)nc * std::max<int64_t>(n, 1) * sizeof(double)) != cudaSuccess) return false;
+        if (cudaMallocAsync((void **)&nv, (size_t)nc * std::max<int64_t>(n, 1) * sizeof(double), s) != cudaSuccess)
+            return false;
         if (W.V && W.cap > 0 &&
             cudaMemcpyAsync(nv, W.V, (size_t)W.cap * n * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
             return false;
-        cudaStreamSynchronize(s);
-        cudaFree(W.V);
+        if (W.V) cudaFreeAsync(W.V, s);
         W.V = nv;
         W.cap = nc;
         return true;
@@ -549,7 +612,13 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
         }
     }
     auto cleanup = [&]() { if (!M) local.release(); };
-    if (W.gexec && (W.stale || W.gA != nsm_handle_uid(A) || W.gs != s)) {
+    // signature of everything baked into the captured launch sequence: the
+    // operator and smoother handles (by unique id, not address) and their
+    // option / Ruiz generations (a changed option changes the launches)
+    std::vector<uint64_t> sig{nsm_handle_uid(A), nsm_handle_cfg_gen(A)};
+    if (M)
+        for (nsm_handle *S : M->S) { sig.push_back(nsm_handle_uid(S)); sig.push_back(nsm_handle_cfg_gen(S)); }
+    if (W.gexec && (W.stale || W.gsig != sig || W.gs != s)) {
         cudaGraphExecDestroy(W.gexec);
         W.gexec = nullptr;
     }
@@ -586,7 +655,7 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
                     if (st == NSM_OK) st = nsm_spmv(A, z, w, s);
                     ok = cudaStreamEndCapture(s, &graph) == cudaSuccess && st == NSM_OK &&
                          cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
-                    W.gA = nsm_handle_uid(A);
+                    W.gsig = sig;
                     W.gs = s;
                     W.stale = false;
                     if (graph) cudaGraphDestroy(graph);
@@ -610,8 +679,14 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
         // step 6: the single reduction [V_k, u]^T [u, w]
         k_multidot<<<nblk, kThr, 0, s>>>(n, k, V, u, k < maxit ? w : u, part);
         k_sum_parts<<<(2 * (k + 1) + 127) / 128, 128, 0, s>>>(nblk, 2 * (k + 1), part, red);
+        if (comm && (st = comm_allreduce(comm, red, red, 2 * (k + 1), s)) != NSM_OK) break;
         cudaMemcpyAsync(hred, red, 2 * (k + 1) * sizeof(double), cudaMemcpyDeviceToHost, s);
         if (cudaStreamSynchronize(s) != cudaSuccess) { st = NSM_ERR_CUDA; break; }
+        if (comm && comm_failed(comm)) {
+            g_solver_err = "nsm_gmres: the global reduction timed out waiting for a rank";
+            st = NSM_ERR_DIST;
+            break;
+        }
         const double nu = hred[2 * k], mu = hred[2 * k + 1];
         const double rho = std::sqrt(nu);                     // step 7 (lagged norm)
         if (k == 0) { beta = rho; g[0] = beta; }
@@ -682,9 +757,6 @@ nsm_status nsm_gmres(nsm_handle *A, nsm_amg *M, const double *b, double *x, int 
     }
     if (iters) *iters = m;
     if (hist) std::copy(hv.begin(), hv.end(), hist);
-    static const bool dbg = getenv("NSM_DEBUG_GMRES") != nullptr;
-    if (dbg) fprintf(stderr, "[nsm_gmres] iterations %d, graph %s, private stream %s\n", m, gexec ? "yes" : "no",
-                     s == W.own && W.own ? "yes" : "no");
     cleanup();
     if (st != NSM_OK && g_solver_err.empty()) g_solver_err = "nsm_gmres: failed";
     return st;

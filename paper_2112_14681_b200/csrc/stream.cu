@@ -24,9 +24,11 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 
 #include "nsm_internal.h"
+#include "ptx.cuh"
 
 namespace nsm {
 
@@ -35,38 +37,12 @@ namespace {
 constexpr int kTS = 8;                    // slices (consumer warps) per tile
 constexpr int kThreadsT = (kTS + 1) * 32; // + 1 producer warp
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first_t() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
+using ptx::mbar_arrive;
+using ptx::mbar_expect_tx;
+using ptx::mbar_init;
+using ptx::mbar_wait;
+using ptx::bulk_g2s;
+__device__ __forceinline__ uint64_t policy_evict_first_t() { return ptx::policy_evict_first(); }
 
 // Programmatic dependent launch: the kernels are launched with
 // programmatic stream serialisation, so a kernel's CTAs may start while the
@@ -515,15 +491,17 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
 // ---- launch geometry ---------------------------------------------------------
 constexpr int64_t kSmemMax = 220 * 1024;  // per CTA (opt-in max 227 KB)
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+int sm_count() {  // of the current device (launches happen with the handle's device current)
+    static int n[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!n[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[dev] = v > 0 ? v : 148;
     }
-    return n;
+    return n[dev];
 }
 
 inline int chunk_for_t(int maxw) { return maxw <= 4 ? 4 : (maxw <= 8 ? 8 : 16); }
@@ -540,17 +518,20 @@ struct Geo {
 template <class K>
 Geo geometry(K kernel, int np, int maxw, int eb = 12) {
     static std::mutex mu;
-    static std::map<std::pair<const void *, int64_t>, Geo> cache;
+    // keyed by device too: the shared-memory opt-in attribute is per device
+    static std::map<std::tuple<int, const void *, int64_t>, Geo> cache;
     Geo g;
     g.cap = (int64_t)kTS * kSlice * std::max(maxw, 1);
     const int64_t stage = np * Layout::part_bytes(g.cap, eb);
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair((const void *)kernel, stage);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto key = std::make_tuple(dev, (const void *)kernel, stage);
     auto itc = cache.find(key);
     if (itc != cache.end()) return itc->second;
     int best_warps = -1;
-    // the attribute is per kernel (shared by all handles): allow the maximum
-    // once; each launch passes its own dynamic size
+    // the attribute is per kernel and device (shared by all handles): allow
+    // the maximum once per device; each launch passes its own dynamic size
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
     for (int nst = 1; nst <= 6; ++nst) {  // nst = 1: overlap comes from co-resident CTAs
         const int64_t smem = 128 + nst * stage;

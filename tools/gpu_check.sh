@@ -1,7 +1,8 @@
 #!/bin/bash
-# Final check: full GPU suite, smoke(), the default bench line.
+# Quick GPU check: selected tests (args: pytest -k expression or file list via TESTS), then the default bench.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2 > gpurun_out/check_pytest.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/check_smoke.log 2>&1
-timeout 600 python bench.py > gpurun_out/check_bench.json 2> gpurun_out/check_bench.err
+timeout 900 python -m pytest ${TESTS:-tests} -m gpu -x -q ${K:+-k "$K"} 2>&1 | tail -30 > gpurun_out/pytest_gpu.log
+if [ -z "$NOBENCH" ]; then
+  timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
+fi
