@@ -171,6 +171,37 @@ nsm_status nsm_ilut(const nsm_csr *A, double droptol, int lfil, int64_t *rowptr,
 nsm_status nsm_ruiz(const nsm_csr *F, int max_iters, double *val, double *s_r, double *s_c);
 
 /*
+ * nsm_ruiz_dep — nsm_ruiz with the early termination the paper proposes
+ * (P:L1216-1228): after each round the departure from normality of the
+ * current scaled U is computed, dep_hist[k] (NULL or max_iters + 1 entries;
+ * k = 0 is the input) receives it, and the rounds stop once it is below
+ * dep_tol (> 0; 0 = never, i.e. nsm_ruiz).  *iters (NULL ok) = rounds done.
+ * For a triangular matrix dep = ||U_s||_F (its eigenvalues are its diagonal).
+ */
+nsm_status nsm_ruiz_dep(const nsm_csr *F, int max_iters, double dep_tol, double *val, double *s_r, double *s_c,
+                        int *iters, double *dep_hist);
+
+/*
+ * nsm_dep — departure-from-normality diagnostics of a factor CSR's
+ * triangle (host only): upper = 1 the U part (upper incl. diagonal), 0 the
+ * unit-lower L (strict lower part + implicit unit diagonal).  val: values on
+ * F's pattern (NULL = F->val; e.g. the nsm_ruiz output).
+ *   dep          Henrici: sqrt(||T||_F^2 - ||eig(T)||^2) = ||T_s||_F
+ *   fro, fro_strict   ||T||_F, ||T_s||_F
+ *   delta        Definition 2: max_i max(0, sum_{j!=i}|t_ij| - |t_ii|)
+ *   bound_thm3   Theorem 3: sqrt((2 sqrt(n) + nu) nu), nu = ||T_s||_F
+ *   bound_table5 the same with nu = ||T||_F — how Table 5
+ *                evaluates it (reading R20)
+ *   bound_thm4   Theorem 4: sqrt(n) (1 + delta)
+ * Theorems 3 and 4 assume a unit diagonal (a Ruiz-scaled U, or L).
+ */
+typedef struct {
+    int64_t n;
+    double dep, fro, fro_strict, delta, bound_thm3, bound_table5, bound_thm4;
+} nsm_dep_info;
+nsm_status nsm_dep(const nsm_csr *F, const double *val, int upper, nsm_dep_info *out);
+
+/*
  * nsm_set_ruiz — make NSM_ILU0 smoothing use the Ruiz form of Alg. 2: the
  * handle's factor F must then hold U~ (nsm_ruiz output); after the L solve
  * y~ = y / s_r, the U~ solve runs on the unit-diagonal U~, and x += v / s_c

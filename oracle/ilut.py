@@ -82,13 +82,26 @@ def ruiz_upper(rp, col, val, max_iters: int = 5):
     Returns (val_scaled, s_r, s_c): on the upper entries u~_ij = u_ij / s_r_i /
     s_c_j, then rows divided by their diagonal (s_r_i *= u~_ii) so u~_ii = 1;
     strictly-lower entries (L_s) are returned unchanged."""
+    v, s_r, s_c, _, _ = ruiz_upper_dep(rp, col, val, max_iters, 0.0)
+    return v, s_r, s_c
+
+
+def ruiz_upper_dep(rp, col, val, max_iters: int = 5, dep_tol: float = 0.0):
+    """ruiz_upper with the early termination of P:L1216-1228 ("if at step k of
+    the Ruiz algorithm, dep(U_s) < tol ... the algorithm can be terminated
+    early"): after each round the departure from normality of the current
+    scaled U (dep_upper) is recorded and the rounds stop once it is below
+    dep_tol (> 0).  Returns (val, s_r, s_c, rounds done, dep history
+    [input, after round 1, ...])."""
     n = len(rp) - 1
     rows = np.repeat(np.arange(n), np.diff(rp))
     up = col >= rows
     v = val.copy()
     s_r = np.ones(n)
     s_c = np.ones(n)
-    for _ in range(max_iters):
+    hist = [dep_upper(rp, col, v)]
+    it = 0
+    while it < max_iters:
         rmax = np.zeros(n)
         cmax = np.zeros(n)
         for p in np.nonzero(up)[0]:
@@ -102,6 +115,10 @@ def ruiz_upper(rp, col, val, max_iters: int = 5):
             v[p] = v[p] / dr[rows[p]] / dc[col[p]]
         s_r = s_r * dr
         s_c = s_c * dc
+        it += 1
+        hist.append(dep_upper(rp, col, v))
+        if dep_tol > 0.0 and hist[-1] < dep_tol:
+            break
     # exact unit diagonal: divide each row by its diagonal
     diag = np.ones(n)
     for p in np.nonzero(up & (col == rows))[0]:
@@ -109,7 +126,68 @@ def ruiz_upper(rp, col, val, max_iters: int = 5):
     for p in np.nonzero(up)[0]:
         v[p] = v[p] / diag[rows[p]]
     s_r = s_r * diag
-    return v, s_r, s_c
+    return v, s_r, s_c, it, hist
+
+
+# ---------------------------------------------- departure from normality ---
+def dep_dense(M) -> float:
+    """Henrici's departure from normality, the definition as
+    written: sqrt(||M||_F^2 - ||D||_F^2), D = diag(eigenvalues of M)."""
+    M = np.asarray(M, dtype=np.complex128)
+    lam = np.linalg.eigvals(M)
+    d2 = float(np.sum(np.abs(M) ** 2) - np.sum(np.abs(lam) ** 2))
+    return math.sqrt(max(d2, 0.0))
+
+
+def dep_upper(rp, col, val) -> float:
+    """dep of the upper triangle (incl. diagonal) of a factor CSR: the
+    eigenvalues of a triangular matrix are its diagonal entries, so the
+    definition gives sqrt(||U||_F^2 - sum u_ii^2) = ||U_s||_F.  Per row the
+    squares of the strictly-upper entries in stored order, rows summed in
+    order (pinned against dep_dense on small matrices)."""
+    s = 0.0
+    for i in range(len(rp) - 1):
+        r = 0.0
+        for p in range(rp[i], rp[i + 1]):
+            if col[p] > i:
+                r = r + val[p] * val[p]
+        s = s + r
+    return math.sqrt(s)
+
+
+def dep_info(rp, col, val, upper: bool = True) -> dict:
+    """The diagnostics of P:L1171-1265 for the U part (upper = True) or the
+    unit-lower L part (strict lower + implicit unit diagonal):
+      dep         = ||T_s||_F (dep of a triangular matrix)
+      fro         = ||T||_F,  fro_strict = ||T_s||_F
+      delta       Definition 2: max_i max(0, sum_{j != i} |t_ij| - |t_ii|)
+      bound_thm3  Theorem 3: sqrt((2 sqrt(n) + nu) nu), nu = ||T_s||_F
+      bound_table5   the same with nu = ||T||_F (Table 5's evaluation, R20)
+      bound_thm4  Theorem 4: sqrt(n) (1 + delta)"""
+    n = len(rp) - 1
+    strict = 0.0
+    diag = 0.0
+    delta = 0.0
+    for i in range(n):
+        r2 = 0.0
+        rabs = 0.0
+        dii = 0.0 if upper else 1.0
+        for p in range(rp[i], rp[i + 1]):
+            j = col[p]
+            if (j > i) if upper else (j < i):
+                r2 = r2 + val[p] * val[p]
+                rabs = rabs + abs(val[p])
+            elif upper and j == i:
+                dii = val[p]
+        strict = strict + r2
+        diag = diag + dii * dii
+        delta = max(delta, rabs - abs(dii))
+    fs = math.sqrt(strict)
+    fr = math.sqrt(strict + diag)
+    sq = math.sqrt(n)
+    return {"n": n, "dep": fs, "fro": fr, "fro_strict": fs, "delta": delta,
+            "bound_thm3": math.sqrt((2.0 * sq + fs) * fs), "bound_table5": math.sqrt((2.0 * sq + fr) * fr),
+            "bound_thm4": sq * (1.0 + delta)}
 
 
 def ilu_ruiz_apply(A, F, s_r, s_c, b, x, kL, kU, nu=1, x_is_zero=False):

@@ -9,8 +9,8 @@ is missing or no CUDA device is present the calls raise.
 from __future__ import annotations
 
 from ._lib import (NSM_DIST_GLOBAL, NSM_DIST_HYBRID, NSM_ILU0, NSM_PGS, Amg, Comm, FactorCSR, NsmError, Smoother, SpMat,
-                   exchange_plan, exported_symbols, gmres, halo_plan, ilu0, ilu0_fixed_point, ilut, lib_path, load,
+                   dep, exchange_plan, exported_symbols, gmres, halo_plan, ilu0, ilu0_fixed_point, ilut, lib_path, load,
                    ruiz)
 
-__all__ = ["Smoother", "SpMat", "Amg", "Comm", "gmres", "ilut", "ruiz", "FactorCSR", "NsmError", "ilu0", "ilu0_fixed_point", "halo_plan", "exchange_plan", "load", "lib_path", "exported_symbols", "NSM_PGS", "NSM_ILU0",
+__all__ = ["Smoother", "SpMat", "Amg", "Comm", "gmres", "ilut", "ruiz", "dep", "FactorCSR", "NsmError", "ilu0", "ilu0_fixed_point", "halo_plan", "exchange_plan", "load", "lib_path", "exported_symbols", "NSM_PGS", "NSM_ILU0",
            "NSM_DIST_HYBRID", "NSM_DIST_GLOBAL"]

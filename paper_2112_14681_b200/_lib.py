@@ -26,7 +26,8 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual
                   "nsm_solver_last_error", "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz",
                   "nsm_fused_stats", "nsm_layout", "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect",
                   "nsm_comm_connect_ipc", "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout",
-                  "nsm_comm_stats", "nsm_comm_last_error", "nsm_comm_destroy", "nsm_set_comm"])
+                  "nsm_comm_stats", "nsm_comm_last_error", "nsm_comm_destroy", "nsm_set_comm", "nsm_ruiz_dep",
+                  "nsm_dep"])
 
 
 class NsmError(RuntimeError):
@@ -121,13 +122,16 @@ def load(variant: str = ""):
     L.nsm_comm_destroy.argtypes = [vp]
     L.nsm_comm_destroy.restype = None
     L.nsm_set_comm.argtypes = [vp, vp]
+    L.nsm_ruiz_dep.argtypes = [P(_Csr), ci, ctypes.c_double, vp, vp, vp, P(ci), vp]
+    L.nsm_dep.argtypes = [P(_Csr), vp, ci, vp]
     for name in ["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
                  "nsm_smooth_host", "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
                  "nsm_spmat_setup", "nsm_spmat_apply", "nsm_amg_setup", "nsm_amg_set_smoother", "nsm_amg_vcycle",
                  "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats", "nsm_layout",
                  "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect", "nsm_comm_connect_ipc",
-                 "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout", "nsm_comm_stats", "nsm_set_comm"]:
+                 "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout", "nsm_comm_stats", "nsm_set_comm",
+                 "nsm_ruiz_dep", "nsm_dep"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -243,19 +247,50 @@ def ilut(A, droptol: float, lfil: int) -> FactorCSR:
     return FactorCSR(n, rp, col, val)
 
 
-def ruiz(F, max_iters: int = 5):
-    """Ruiz scaling of the U part of a factor CSR (nsm_ruiz): returns
-    (FactorCSR with U~, s_r, s_c)."""
+def ruiz(F, max_iters: int = 5, dep_tol: float = 0.0, history: bool = False):
+    """Ruiz scaling of the U part of a factor CSR (nsm_ruiz; with dep_tol > 0
+    or history, nsm_ruiz_dep: early termination on dep(U)).
+    Returns (FactorCSR with U~, s_r, s_c) [+ (rounds done, dep history)]."""
     L = load()
     keep: list = []
     cs = _csr_struct(F, keep)
     n = int(F.nrows)
     val = np.zeros(int(F.rowptr[-1]), dtype=np.float64)
     sr, sc = np.zeros(n), np.zeros(n)
-    st = L.nsm_ruiz(ctypes.byref(cs), int(max_iters), val.ctypes.data, sr.ctypes.data, sc.ctypes.data)
+    if dep_tol > 0.0 or history:
+        its = ctypes.c_int()
+        hist = np.zeros(max_iters + 1)
+        st = L.nsm_ruiz_dep(ctypes.byref(cs), int(max_iters), float(dep_tol), val.ctypes.data, sr.ctypes.data,
+                            sc.ctypes.data, ctypes.byref(its), hist.ctypes.data)
+    else:
+        st = L.nsm_ruiz(ctypes.byref(cs), int(max_iters), val.ctypes.data, sr.ctypes.data, sc.ctypes.data)
     if st != 0:
         raise NsmError(st, _err(None))
-    return FactorCSR(n, np.asarray(F.rowptr, np.int64), np.asarray(F.col, np.int64), val), sr, sc
+    out = (FactorCSR(n, np.asarray(F.rowptr, np.int64), np.asarray(F.col, np.int64), val), sr, sc)
+    if dep_tol > 0.0 or history:
+        return out + ((its.value, hist[:its.value + 1]),)
+    return out
+
+
+class _DepInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("dep", ctypes.c_double), ("fro", ctypes.c_double),
+                ("fro_strict", ctypes.c_double), ("delta", ctypes.c_double), ("bound_thm3", ctypes.c_double),
+                ("bound_table5", ctypes.c_double), ("bound_thm4", ctypes.c_double)]
+
+
+def dep(F, val=None, upper: bool = True) -> dict:
+    """nsm_dep: departure-from-normality diagnostics (Henrici dep, Theorem 3
+    and 4 bounds, near diagonal dominance delta) of the U (upper) or unit-L
+    part of a factor CSR; val = values on F's pattern (default F.val)."""
+    keep: list = []
+    cs = _csr_struct(F, keep)
+    v = None if val is None else np.ascontiguousarray(val, dtype=np.float64)
+    out = _DepInfo()
+    st = load().nsm_dep(ctypes.byref(cs), v.ctypes.data if v is not None else None, int(bool(upper)),
+                        ctypes.byref(out))
+    if st != 0:
+        raise NsmError(st, _err(None))
+    return {k: getattr(out, k) for k, _ in _DepInfo._fields_}
 
 
 class Smoother:

@@ -767,6 +767,16 @@ nsm_status nsm_ruiz(const nsm_csr *F, int max_iters, double *val, double *s_r, d
     return ruiz_host(F, max_iters, val, s_r, s_c, &g_setup_err);
 }
 
+nsm_status nsm_ruiz_dep(const nsm_csr *F, int max_iters, double dep_tol, double *val, double *s_r, double *s_c,
+                        int *iters, double *dep_hist) {
+    if (!F || !val || !s_r || !s_c || dep_tol < 0.0) { g_setup_err = "nsm_ruiz_dep: bad argument"; return NSM_ERR_ARG; }
+    return ruiz_host(F, max_iters, val, s_r, s_c, &g_setup_err, dep_tol, iters, dep_hist);
+}
+
+nsm_status nsm_dep(const nsm_csr *F, const double *val, int upper, nsm_dep_info *out) {
+    return dep_host(F, val, upper, out, &g_setup_err);
+}
+
 nsm_status nsm_set_ruiz(nsm_handle *h, const double *s_r, const double *s_c) {
     if (!h || !h->has_ilu) return NSM_ERR_STATE;
     DeviceScope dev(h->device);

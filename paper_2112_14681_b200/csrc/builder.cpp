@@ -431,14 +431,32 @@ nsm_status ilut_host(const nsm_csr *A, double droptol, int lfil, std::vector<int
 
 // Ruiz equilibration of the upper part (incl. diagonal) of a factor CSR, then
 // an exact unit diagonal; the scaling is returned as divisors s_r, s_c.
-nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, double *s_c, std::string *err) {
+// Departure from normality of the U part (upper incl. diagonal) of a factor
+// CSR with values v: Henrici's dep(A) = sqrt(||A||_F^2 - ||Lambda||_F^2)
+// (P:L847-855); a triangular matrix's eigenvalues are its diagonal entries,
+// so dep(U) = ||U_s||_F.  Row-wise sums in stored order, then over rows.
+static double dep_upper(const nsm_csr *F, const double *v) {
+    double s = 0.0;
+    for (int64_t i = 0; i < F->nrows; ++i) {
+        double r = 0.0;
+        for (int64_t p = F->rowptr[i]; p < F->rowptr[i + 1]; ++p)
+            if (F->colind[p] > i) r = r + v[p] * v[p];
+        s = s + r;
+    }
+    return std::sqrt(s);
+}
+
+nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, double *s_c, std::string *err,
+                     double dep_tol, int *iters_done, double *dep_hist) {
     const int64_t n = F->nrows;
     if (!F->rowptr || n < 0 || max_iters < 0) { *err = "nsm_ruiz: bad argument"; return NSM_ERR_ARG; }
     const int64_t nnz = F->rowptr[n];
     std::copy(F->val, F->val + nnz, v);
     for (int64_t i = 0; i < n; ++i) { s_r[i] = 1.0; s_c[i] = 1.0; }
     std::vector<double> rmax(n), cmax(n);
-    for (int it = 0; it < max_iters; ++it) {
+    int it = 0;
+    if (dep_hist) dep_hist[0] = dep_upper(F, v);
+    while (it < max_iters) {
         std::fill(rmax.begin(), rmax.end(), 0.0);
         std::fill(cmax.begin(), cmax.end(), 0.0);
         for (int64_t i = 0; i < n; ++i)
@@ -458,7 +476,16 @@ nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, do
                 if (j >= i) v[p] = v[p] / rmax[i] / cmax[j];
             }
         for (int64_t i = 0; i < n; ++i) { s_r[i] = s_r[i] * rmax[i]; s_c[i] = s_c[i] * cmax[i]; }
+        ++it;
+        // early termination on the departure from normality:
+        // dep(U) after this round below the caller's tolerance
+        if (dep_hist || dep_tol > 0.0) {
+            const double dk = dep_upper(F, v);
+            if (dep_hist) dep_hist[it] = dk;
+            if (dep_tol > 0.0 && dk < dep_tol) break;
+        }
     }
+    if (iters_done) *iters_done = it;
     for (int64_t i = 0; i < n; ++i) {
         double dg = 1.0;
         bool has = false;
@@ -469,6 +496,43 @@ nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, do
             if (F->colind[p] >= i) v[p] = v[p] / dg;
         s_r[i] = s_r[i] * dg;
     }
+    return NSM_OK;
+}
+
+// Departure-from-normality diagnostics of a triangular factor (P:L847-855,
+// Theorem 3, Definition 2 / Theorem 4).
+nsm_status dep_host(const nsm_csr *F, const double *val, int upper, nsm_dep_info *out, std::string *err) {
+    if (!F || !F->rowptr || !out || F->nrows < 0 || (F->rowptr[F->nrows] > 0 && (!F->colind || !(val ? val : F->val)))) {
+        *err = "nsm_dep: bad argument";
+        return NSM_ERR_ARG;
+    }
+    const double *v = val ? val : F->val;
+    const int64_t n = F->nrows;
+    double strict = 0.0, diag = 0.0, delta = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double r2 = 0.0, rabs = 0.0, dii = upper ? 0.0 : 1.0;  // unit-lower L: implicit diagonal 1
+        for (int64_t p = F->rowptr[i]; p < F->rowptr[i + 1]; ++p) {
+            const int64_t j = F->colind[p];
+            if (upper ? j > i : j < i) {
+                r2 = r2 + v[p] * v[p];
+                rabs = rabs + std::fabs(v[p]);
+            } else if (upper && j == i) {
+                dii = v[p];
+            }
+        }
+        strict = strict + r2;
+        diag = diag + dii * dii;
+        delta = std::max(delta, rabs - std::fabs(dii));   // delta_i of Definition 2 (>= 0)
+    }
+    out->n = n;
+    out->dep = std::sqrt(strict);                 // eigenvalues = diagonal: dep = ||T_s||_F
+    out->fro_strict = std::sqrt(strict);
+    out->fro = std::sqrt(strict + diag);
+    out->delta = delta;
+    const double sq = std::sqrt((double)n);
+    out->bound_thm3 = std::sqrt((2.0 * sq + out->fro_strict) * out->fro_strict);
+    out->bound_table5 = std::sqrt((2.0 * sq + out->fro) * out->fro);
+    out->bound_thm4 = sq * (1.0 + delta);
     return NSM_OK;
 }
 

@@ -246,7 +246,9 @@ struct DeviceScope {
 // Host ILUT(droptol, lfil) and Ruiz scaling of the U factor (NEXT-3).
 nsm_status ilut_host(const nsm_csr *A, double droptol, int lfil, std::vector<int64_t> &rp_out,
                      std::vector<int64_t> &ci_out, std::vector<double> &va_out, std::string *err);
-nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, double *s_c, std::string *err);
+nsm_status ruiz_host(const nsm_csr *F, int max_iters, double *v, double *s_r, double *s_c, std::string *err,
+                     double dep_tol = 0.0, int *iters_done = nullptr, double *dep_hist = nullptr);
+nsm_status dep_host(const nsm_csr *F, const double *val, int upper, nsm_dep_info *out, std::string *err);
 
 // ILU(0) by Chow-Patel fixed-point sweeps on the GPU (nsm_ilu0_fixed_point).
 nsm_status ilu0_fixed_point_device(const nsm_csr *A, int64_t row_begin, int sweeps, double *fval, int device,

@@ -68,3 +68,20 @@ def test_smooth_host_errors():
             S.smooth_host(b, y[:-1], out=y[1:])  # partial overlap of x_in and out
         with pytest.raises(nsm.NsmError):
             S.smooth_host(b, b.copy(), "ilu")  # no factors on this handle
+
+
+def test_smooth_host_nu_zero():
+    """nu = 0: no application, the result is the start vector (x_in, or zeros
+    with x_is_zero) — never the staging buffer's stale contents."""
+    A = inputs.laplace(8, 8, 2)
+    b = inputs.uniform(0, A.nrows)
+    x0 = inputs.uniform(1, A.nrows)
+    with _smoother(A) as S:
+        out = np.full(A.nrows, 7.0)
+        S.smooth_host(b, x0.copy(), nu=1, out=out)              # fills the staging vectors
+        out2 = np.full(A.nrows, 7.0)
+        S.smooth_host(b, x0, nu=0, x_is_zero=True, out=out2)
+        assert np.array_equal(out2, np.zeros(A.nrows))
+        out3 = np.full(A.nrows, 7.0)
+        S.smooth_host(b, x0, nu=0, out=out3)
+        assert np.array_equal(out3, x0)

@@ -207,3 +207,43 @@ def test_gmres_workspace_reuse():
         M.close()
         for s_ in S:
             s_.close()
+
+
+def test_gmres_recaptures_after_ruiz_change():
+    """A replayed V-cycle graph must notice nsm_set_ruiz / nsm_set_option on a
+    borrowed smoother (the handle's configuration generation): Ruiz on the
+    finest ILU level changes the preconditioner, so the history must equal
+    that of a fresh AMG object set up with the same scaling."""
+    A = inputs.convdiff(12).to_scipy()
+    levels = amg.hierarchy(A, rand_fn, min_coarse=200)
+    nl = len(levels) - 1
+    F0 = oracle.ilu0(levels[0][0])[2]
+    b = dev(inputs.uniform(0, A.shape[0]))
+    n0 = levels[0][0].shape[0]
+    s_r, s_c = np.full(n0, 2.0), np.full(n0, 0.5)
+
+    def build():
+        S = [nsm.Smoother(inputs.CSR.from_scipy(levels[0][0]), F0)] + \
+            [nsm.Smoother(inputs.CSR.from_scipy(levels[l][0])) for l in range(1, nl)]
+        M = nsm.Amg(S, [inputs.CSR.from_scipy(levels[l][1]) for l in range(nl)], inputs.CSR.from_scipy(levels[-1][0]))
+        M.set_smoother(0, "ilu", 1, 1, 2, 2)
+        return S, M
+
+    S, M = build()
+    S2, M2 = build()
+    try:
+        _, i0, h0 = nsm.gmres(S[0], b, M, tol=1e-8)            # captures the graph
+        S[0].set_ruiz(s_r, s_c)                                  # changes the U solve
+        _, i1, h1 = nsm.gmres(S[0], b, M, tol=1e-8)
+        S2[0].set_ruiz(s_r, s_c)
+        _, i2, h2 = nsm.gmres(S2[0], b, M2, tol=1e-8)           # fresh object, scaling set first
+        assert not np.array_equal(h0, h1)
+        assert i1 == i2 and np.array_equal(h1, h2)
+        S[0].set_ruiz(None, None)                                # back: the original history
+        _, i3, h3 = nsm.gmres(S[0], b, M, tol=1e-8)
+        assert i3 == i0 and np.array_equal(h3, h0)
+    finally:
+        M.close()
+        M2.close()
+        for s_ in S + S2:
+            s_.close()
