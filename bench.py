@@ -317,6 +317,8 @@ def run_nsm(args, rank, nranks, local_rank):
         S.set_fused({"auto": 2, "on": 1, "off": 0}[args.fused])
     if args.pdl != "auto":
         S.set_pdl(args.pdl == "on")
+    if args.window == "off":
+        S.set_window(False)
     if nranks > 1:
         S.connect(dist)
     nl, nu_, noff = split_counts(A)
@@ -487,6 +489,8 @@ def main():
     ap.add_argument("--plain", action="store_true", help="plain register-blocked kernels instead of the bulk-copy pipelined ones")
     ap.add_argument("--pdl", default="auto", choices=["auto", "on", "off"],
                     help="programmatic dependent launch (auto: the library's size-based default)")
+    ap.add_argument("--window", default="on", choices=["on", "off"],
+                    help="shared-memory gather windows in the pipelined kernels (offset-aligned parts)")
     ap.add_argument("--fused", default="default", choices=["default", "auto", "on", "off"],
                     help="phase-skewed fused passes (default: the library's default, per-pass kernels; "
                          "auto: fused on large problems)")

@@ -388,7 +388,11 @@ typedef enum {
     NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2, NSM_OPT_PDL = 3,
     NSM_OPT_PROFILE = 4 /* 1: record a CUDA event pair around every residual / sweep / fused pass
                            (up to 4096 passes) for nsm_profile(); 0: off (default) */,
-    NSM_OPT_FUSED_WINDOW = 5
+    NSM_OPT_FUSED_WINDOW = 5,
+    NSM_OPT_WINDOW = 6 /* 1 (default): pipelined kernels over an offset-aligned part stage the gathered
+                        * vector's window (the tile's columns, merged into a few segments) into shared
+                        * memory with the tile and gather from there (single rank); 0: gathers from
+                        * global memory through L1/L2.  Results are identical. */
 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 

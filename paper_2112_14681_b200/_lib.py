@@ -492,6 +492,10 @@ class Smoother:
         """Wait distance of the fused passes in work items (0 = automatic)."""
         self._call(load().nsm_set_option(self._h, 5, int(items)))
 
+    def set_window(self, enable: bool):
+        """NSM_OPT_WINDOW: shared-memory gather windows in the pipelined kernels."""
+        self._call(load().nsm_set_option(self._h, 6, int(bool(enable))))
+
     def set_pdl(self, enable: bool):
         """Programmatic dependent launch between consecutive pipelined kernels."""
         self._call(load().nsm_set_option(self._h, 3, int(bool(enable))))

@@ -40,6 +40,8 @@ struct nsm_handle {
     uint64_t uid = 0;  // unique per setup (caches keyed by handle must not confuse a reused address)
     uint64_t cfg_gen = 0;  // bumped by nsm_set_option / nsm_set_ruiz (captured graphs compare it)
     nsm_comm *comm = nullptr;  // borrowed cross-rank reduction (nsm_set_comm), distributed solver layer
+    Window res_win;            // gather window of the residual (L and U together), single rank
+    bool window = true;        // NSM_OPT_WINDOW: windowed pipelined kernels where a window exists
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
     // A = L + D + U (+ ghost couplings LG / UG)
@@ -134,12 +136,44 @@ bool upload_sell(DevAlloc &a, const SellHost &hs, Sell *s) {
     return upload(s->col, hs.col.data(), s->padded) && upload(s->val, hs.val.data(), s->padded);
 }
 
+void free_window(Window &w) {
+    cudaFree(w.tseg);
+    cudaFree(w.glo);
+    cudaFree(w.len);
+    cudaFree(w.sbase);
+    cudaFree(w.wpos[0]);
+    cudaFree(w.wpos[1]);
+    w = Window();
+}
+
 void free_sell(Sell &s) {
     cudaFree(s.ptr);
     cudaFree(s.col);
     cudaFree(s.val);
     cudaFree(s.off);
+    free_window(s.win);
     s = Sell();
+}
+
+// Gather window of a group of offset-aligned parts (stream.cu windowed
+// kernels).  Not built (wmax = 0) when a part is compact or a tile's window
+// would exceed kWinCap doubles; failure to allocate is an error.
+constexpr int32_t kWinCap = 8192;
+bool make_window(DevAlloc &a, int64_t n, const std::vector<const SellHost *> &parts, Window *w) {
+    WindowHost wh;
+    if (n <= 0 || !build_window(n, parts, kWinCap, &wh)) return true;
+    if (!a.get(&w->tseg, (int64_t)wh.tseg.size()) || !upload(w->tseg, wh.tseg.data(), (int64_t)wh.tseg.size()) ||
+        !a.get(&w->glo, (int64_t)wh.glo.size()) || !upload(w->glo, wh.glo.data(), (int64_t)wh.glo.size()) ||
+        !a.get(&w->len, (int64_t)wh.len.size()) || !upload(w->len, wh.len.data(), (int64_t)wh.len.size()) ||
+        !a.get(&w->sbase, (int64_t)wh.sbase.size()) || !upload(w->sbase, wh.sbase.data(), (int64_t)wh.sbase.size()))
+        return false;
+    for (size_t p = 0; p < parts.size(); ++p)
+        if (!a.get(&w->wpos[p], (int64_t)wh.wpos[p].size()) ||
+            !upload(w->wpos[p], wh.wpos[p].data(), (int64_t)wh.wpos[p].size()))
+            return false;
+    w->wmax = wh.wmax;
+    w->maxseg = wh.maxseg;
+    return true;
 }
 
 void free_handle(nsm_handle *h) {
@@ -147,6 +181,7 @@ void free_handle(nsm_handle *h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     for (Sell *s : {&h->L, &h->U, &h->LG, &h->UG, &h->Ls, &h->Us, &h->LsG, &h->UsG}) free_sell(*s);
+    free_window(h->res_win);
     cudaFree(h->d);
     cudaFree(h->dl1);
     cudaFree(h->dU);
@@ -318,6 +353,8 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 a.flag = h->flag;
                                 a.sweep_id = sid;
                                 a.pdl = h->pdl;
+                                a.win = (h->window && st.T->win.wmax && !scaled && sl.begin == 0 &&
+                                         sl.end == h->nslices) ? &st.T->win : nullptr;
                                 if (use_pipelined(h, sl, with_ghost, 1, st.T->maxw))
                                     return launch_sweep_tma(a, sl.begin, sl.end, s);
                                 return launch_sweep(a, s);
@@ -334,7 +371,9 @@ nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double
                          double *out2 = nullptr) {
     return pass(h, true, x, nullptr, s, [&](const Slices &sl, bool with_ghost, const double *ghost) {
         if (use_pipelined(h, sl, with_ghost, 2, std::max(h->L.maxw, h->U.maxw)))
-            return launch_residual_tma(mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
+            return launch_residual_tma((h->window && h->res_win.wmax && sl.begin == 0 && sl.end == h->nslices)
+                                           ? &h->res_win : nullptr,
+                                       mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
         return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
                                out, out2, h->pdl, s);
     }, 0);
@@ -516,6 +555,11 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         ok = a.get(&h->dU, h->n) && upload(h->dU, sf.d.data(), h->n) && upload_sell(a, sf.L, &h->Ls) &&
              upload_sell(a, sf.U, &h->Us) && upload_sell(a, sf.LG, &h->LsG) && upload_sell(a, sf.UG, &h->UsG);
     }
+    if (ok && nranks == 1) {  // gather windows (stream.cu), full-range launches of one rank
+        ok = make_window(a, h->n, {&sa.L, &sa.U}, &h->res_win) && make_window(a, h->n, {&sa.L}, &h->L.win) &&
+             make_window(a, h->n, {&sa.U}, &h->U.win);
+        if (ok && F) ok = make_window(a, h->n, {&sf.L}, &h->Ls.win) && make_window(a, h->n, {&sf.U}, &h->Us.win);
+    }
     for (int i = 0; ok && i < 4; ++i) ok = a.get(&h->w[i], std::max<int64_t>(h->n, 1));
     ok = ok && a.get(&h->flag, 1) && a.get(&h->ghost_null, 1) && a.get(&h->d_dist_err, 1) &&
          cudaMemset(h->d_dist_err, 0, sizeof(unsigned int)) == cudaSuccess;
@@ -695,6 +739,7 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
             h->skew_dw = (int)value;
             return NSM_OK;
         case NSM_OPT_PDL: h->pdl = value != 0; return NSM_OK;
+        case NSM_OPT_WINDOW: h->window = value != 0; return NSM_OK;
         case NSM_OPT_PROFILE:
             h->profile = value != 0;
             if (h->profile && h->ev.empty()) {

@@ -22,6 +22,39 @@ inline const char *knob(const char *) { return nullptr; }
 namespace nsm {
 
 constexpr int kSlice = 32;  // SELL-C slice height = warp width: one thread per row
+constexpr int kTileSlices = 8;  // slices per tile of the pipelined kernels (stream.cu)
+
+// Gather window of the pipelined kernels for offset-aligned parts (stream.cu
+// "windowed" variants): for every tile of kTileSlices slices, the columns its
+// rows gather (row + offset over the group's parts) merged into a few
+// contiguous segments of the gathered vector, bulk-copied into shared memory
+// with the tile, so the gathers become shared-memory loads.  Segment k of
+// tile t: global first index glo[k] (even; may reach below 0 / past n at the
+// ends of the matrix: the producer zero-fills those positions), length len[k]
+// (even), start sbase[k] in the tile's window.  wpos[p][ptr[s]/32 + j] = the
+// window index of lane 0's gather of entry j of slice s of part p (lane l
+// adds l).  wmax = 0: no window (compact layout, or a window too large).
+struct Window {
+    int32_t *tseg = nullptr;   // ntiles + 1: first segment of tile t
+    int64_t *glo = nullptr;
+    int32_t *len = nullptr, *sbase = nullptr;
+    int32_t *wpos[2] = {nullptr, nullptr};
+    int32_t wmax = 0;          // largest window of a tile, in doubles
+    int32_t maxseg = 0;        // most segments of a tile
+};
+struct WindowHost {
+    std::vector<int32_t> tseg, len, sbase;
+    std::vector<int64_t> glo;
+    std::vector<int32_t> wpos[2];
+    int32_t wmax = 0, maxseg = 0;
+};
+struct WinView {
+    const int32_t *tseg;
+    const int64_t *glo;
+    const int32_t *len, *sbase;
+    const int32_t *wpos[2];
+    int32_t wcap;              // window capacity per stage (doubles, >= wmax)
+};
 
 // One strictly-triangular (or ghost) part in SELL-32 form (σ = 1: rows keep
 // their order).  Slice s holds rows [32 s, 32 s + 32); its entries occupy
@@ -41,6 +74,7 @@ struct Sell {
     int64_t padded = 0;       // stored entries incl. padding
     int64_t nnz = 0;          // real entries
     int32_t maxw = 0;         // widest slice
+    Window win;               // gather window of sweeps over this part alone (offset-aligned only)
     bool empty() const { return padded == 0; }
 };
 
@@ -63,6 +97,10 @@ struct SellView {
 };
 
 inline SellView view(const Sell &s) { return SellView{s.ptr, s.col, s.val, s.off}; }
+
+// Gather-window plan of offset-aligned parts (builder.cpp): false if a
+// tile's window would exceed wcap doubles or 32 segments.
+bool build_window(int64_t n, const std::vector<const SellHost *> &parts, int32_t wcap, WindowHost *out);
 
 // Result of splitting a CSR row block (builder.cpp).
 struct Split {
@@ -102,6 +140,7 @@ struct SweepArgs {
     unsigned long long *flag;
     int64_t sweep_id;
     bool pdl;                // programmatic dependent launch (pipelined kernels)
+    const Window *win;       // gather window of T over the full slice range (or nullptr)
 };
 
 // Residual kernel output modes.
@@ -141,7 +180,8 @@ cudaError_t launch_halo_wait(const unsigned long long *flags, const int *peers, 
 
 // ---- bulk-copy pipelined kernels (stream.cu), contiguous slice ranges --------
 bool tma_ok(int np, int maxw);
-cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
+// win: gather window of (L, U) for the full slice range (or nullptr).
+cudaError_t launch_residual_tma(const Window *win, int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
                                 const Sell &U, const double *d, const double *b, const double *x, double *out,
                                 double *out2, bool pdl, cudaStream_t st);
 cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st);

@@ -25,6 +25,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <utility>
 
 #include "nsm_internal.h"
@@ -34,7 +35,7 @@ namespace nsm {
 
 namespace {
 
-constexpr int kTS = 8;                    // slices (consumer warps) per tile
+constexpr int kTS = kTileSlices;          // slices (consumer warps) per tile
 constexpr int kThreadsT = (kTS + 1) * 32; // + 1 producer warp
 
 using ptx::mbar_arrive;
@@ -79,6 +80,7 @@ struct Layout {
     int nst, np;
     int64_t cap;  // entries per part per stage
     int eb;       // staged bytes per entry: 12 (values + columns) or 8 (values; + the slices' offsets + header)
+    int64_t wcap = 0;  // gather-window doubles per stage (windowed kernels), after all stages' parts
     __host__ __device__ static int64_t ofs_bytes(int64_t cap) { return (cap / kSlice * 4 + 15) / 16 * 16; }
     __host__ __device__ static int64_t part_bytes(int64_t cap, int eb) {
         return eb == 12 ? cap * 12 : cap * 8 + ofs_bytes(cap) + kHdrBytes;
@@ -93,6 +95,9 @@ struct Layout {
     }
     __device__ __forceinline__ int32_t *col(char *s, int st, int p) const {   // eb 12: columns; eb 8: offsets
         return (int32_t *)(s + 128 + ((int64_t)st * np + p) * part_bytes(cap, eb) + cap * 8);
+    }
+    __device__ __forceinline__ double *win(char *s, int st) const {
+        return (double *)(s + 128 + (int64_t)nst * np * part_bytes(cap, eb)) + (int64_t)st * wcap;
     }
 };
 
@@ -122,11 +127,21 @@ struct TileRefs {
     int64_t b[NP], e[NP];
     int64_t sp[NP];  // lanes 0..kTS: slice pointer of slice s0 + lane (clamped to the tile end)
     int32_t o[NP][kOfsPerLane];
+    // windowed kernels: this tile's gather-window segments, lane k holds segment k
+    int32_t nseg, sg_len, sg_base;
+    int64_t sg_lo;
 };
+
+// Entry-position arrays staged into the "offsets" slot: the column offsets,
+// or (windowed kernels) the gather-window positions.
+template <int NP>
+__device__ __forceinline__ const int32_t *staged_pos(const SellView (&P)[NP], const WinView &W, bool win, int p) {
+    return win ? W.wpos[p] : P[p].off;
+}
 
 template <int NP>
 __device__ __forceinline__ void tile_refs(const Layout &Ly, const SellView (&P)[NP], int64_t s_begin, int64_t s_end,
-                                          int64_t t, int lane, TileRefs<NP> &r) {
+                                          int64_t t, int lane, TileRefs<NP> &r, const WinView &W, bool win) {
     const int64_t s0 = s_begin + t * kTS, s1 = min(s0 + kTS, s_end);
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -139,12 +154,21 @@ __device__ __forceinline__ void tile_refs(const Layout &Ly, const SellView (&P)[
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const int64_t no = (r.e[p] - r.b[p]) / kSlice;
-            const int32_t *go = P[p].off + r.b[p] / kSlice;
+            const int32_t *go = staged_pos<NP>(P, W, win, p) + r.b[p] / kSlice;
 #pragma unroll
             for (int q = 0; q < kOfsPerLane; ++q) {
                 const int64_t k = lane + 32 * q;
                 r.o[p][q] = k < no ? __ldg(go + k) : 0;
             }
+        }
+    }
+    if (win) {  // tile t of the window plan (s_begin == 0)
+        const int32_t g0 = __ldg(W.tseg + t), g1 = __ldg(W.tseg + t + 1);
+        r.nseg = g1 - g0;
+        if (lane < r.nseg) {
+            r.sg_lo = __ldg(W.glo + g0 + lane);
+            r.sg_len = __ldg(W.len + g0 + lane);
+            r.sg_base = __ldg(W.sbase + g0 + lane);
         }
     }
 }
@@ -181,20 +205,50 @@ __device__ __forceinline__ void producer_compact(const Layout &Ly, char *sm, con
     pdl_trigger();  // all of this CTA's copies are issued: dependents may be scheduled
 }
 
-template <int NP>
+// WIN: also stage the tile's gather window of `vec` (the vector the
+// consumers gather: x for the residual, the previous iterate for a sweep):
+// each lane owns one segment, bulk-copies its in-range, 16-byte-aligned part
+// and writes the rest itself (zeros outside [0, n), an odd last element).
+// `vec` is written by the previous kernel, so with programmatic dependent
+// launch the producer waits for it before the first window copy.
+template <int NP, bool WIN = false>
 __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellView (&P)[NP], int64_t s_begin,
-                                         int64_t s_end, int64_t ntiles, int lane) {
+                                         int64_t s_end, int64_t ntiles, int lane, const WinView &W = WinView{},
+                                         const double *vec = nullptr, int64_t n = 0) {
     const uint64_t pol = policy_evict_first_t();
+    const uint64_t pol_win = ptx::policy_evict_normal();  // neighbouring tiles (other CTAs) gather it too
     int it = 0, st = 0;
     uint32_t ph = 0;  // (it / nst) & 1
     TileRefs<NP> cur, nxt;
-    if ((int64_t)blockIdx.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, blockIdx.x, lane, cur);
+    if (WIN) pdl_wait();
+    if ((int64_t)blockIdx.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, blockIdx.x, lane, cur, W, WIN);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        if (t + gridDim.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, t + gridDim.x, lane, nxt);  // prefetch
+        if (t + gridDim.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, t + gridDim.x, lane, nxt, W, WIN);  // prefetch
         if (it >= Ly.nst) mbar_wait(Ly.empty(sm) + st, ph ^ 1);
         uint32_t bytes = 0;
 #pragma unroll
         for (int p = 0; p < NP; ++p) bytes += (uint32_t)((cur.e[p] - cur.b[p]) * Ly.eb);
+        int64_t wa = 0;         // this lane's window segment: bulk part [wa, wa + wbytes / 8)
+        uint32_t wbytes = 0;
+        if (WIN && lane < cur.nseg) {
+            double *ws = Ly.win(sm, st) + cur.sg_base - cur.sg_lo;  // ws[q] = window slot of vec[q]
+            const int64_t lo = cur.sg_lo, hi = lo + cur.sg_len;
+            const int64_t a = max(lo, (int64_t)0), e = min(hi, n);
+            for (int64_t q = lo; q < min(a, hi); ++q) ws[q] = 0.0;           // below row 0
+            for (int64_t q = max(e, lo); q < hi; ++q) ws[q] = 0.0;           // past row n - 1
+            if (e > a) {
+                const int64_t be = e & ~(int64_t)1;
+                if (be < e) ws[e - 1] = __ldcg(vec + e - 1);                  // odd n: last element
+                wa = a;
+                wbytes = be > a ? (uint32_t)((be - a) * 8) : 0u;
+            }
+        }
+        if (WIN) {
+            uint32_t wsum = wbytes;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+            bytes += wsum;
+        }
         if (Ly.eb == 8) {
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
@@ -205,7 +259,7 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
                     const int64_t k = lane + 32 * q;
                     if (k < no) so[k] = cur.o[p][q];
                 }
-                const int32_t *go = P[p].off + cur.b[p] / kSlice;  // wider tiles (not staged above)
+                const int32_t *go = staged_pos<NP>(P, W, WIN, p) + cur.b[p] / kSlice;  // wider tiles (not staged above)
                 for (int64_t k = lane + 32 * kOfsPerLane; k < no; k += 32) so[k] = __ldg(go + k);
                 const int64_t nsp = __shfl_down_sync(0xffffffffu, cur.sp[p], 1);
                 if (lane < kTS) {
@@ -216,6 +270,7 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
             }
             __syncwarp();
         }
+        if (WIN) __syncwarp();  // the window's plain stores precede the arrival (release)
         if (lane == 0) {
             mbar_expect_tx(Ly.full(sm) + st, bytes);  // bulk-copied bytes (values, and columns with eb 12)
 #pragma unroll
@@ -227,6 +282,11 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
                         bulk_g2s(Ly.col(sm, st, p), P[p].col + b, (uint32_t)((e - b) * 4), Ly.full(sm) + st, pol);
                 }
             }
+        }
+        if (WIN) {
+            __syncwarp();  // the expected byte count is registered before any window copy completes
+            if (wbytes)
+                bulk_g2s(Ly.win(sm, st) + cur.sg_base + (wa - cur.sg_lo), vec + wa, wbytes, Ly.full(sm) + st, pol_win);
         }
         __syncwarp();
         cur = nxt;
@@ -315,21 +375,51 @@ struct StagedChunk {
 };
 
 
-template <int OUT, int CH, bool OFS>
-__global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView L,
-                                                            SellView U, const double *__restrict__ d,
-                                                            const double *__restrict__ b,
-                                                            const double *__restrict__ x, double *__restrict__ out,
-                                                            double *__restrict__ out2, int nst, int64_t cap) {
+// Windowed gathers (WIN kernels): entry j of this lane's row multiplies the
+// gathered vector's value at window slot wp[j] + lane (staged by the
+// producer with the tile), so a row's products need shared-memory loads only.
+// Same products and the same stored-order additions as StagedChunk.
+template <int CH>
+struct WinChunk {
+    double v[CH];
+    const double *sv;   // this lane's values of the slice
+    const int32_t *wp;  // the slice's window positions (warp-uniform)
+    const double *ws;   // window + lane
+    int w;
+    __device__ __forceinline__ void load(const double *sv_, const int32_t *stage_pos, const double *win, int64_t off,
+                                         int w_, int lane, bool row) {
+        sv = sv_ + off + lane;
+        wp = stage_pos + off / kSlice;
+        ws = win + lane;
+        w = row ? w_ : 0;
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) v[j] = __dmul_rn(sv[j * kSlice], ws[wp[j]]);
+    }
+    __device__ __forceinline__ double add(double acc) const {
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) acc = __dadd_rn(acc, v[j]);
+        for (int j = CH; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn(sv[j * kSlice], ws[wp[j]]));
+        return acc;
+    }
+};
+
+template <int OUT, int CH, bool OFS, bool WIN>
+__device__ __forceinline__ void residual_tma_body(int64_t n, int64_t s_begin, int64_t s_end, SellView L, SellView U,
+                                                  const double *__restrict__ d, const double *__restrict__ b,
+                                                  const double *__restrict__ x, double *__restrict__ out,
+                                                  double *__restrict__ out2, int nst, int64_t cap, WinView W) {
     extern __shared__ __align__(128) char sm[];
     constexpr bool ofs = OFS;
-    const Layout Ly{nst, 2, cap, ofs ? 8 : 12};
+    static_assert(!WIN || OFS, "windowed kernels need the offset-aligned layout");
+    const Layout Ly{nst, 2, cap, ofs ? 8 : 12, WIN ? (int64_t)W.wcap : 0};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     init_barriers(Ly, sm);
     if (warp == kTS) {
         const SellView P[2] = {L, U};
-        if constexpr (OFS) producer<2>(Ly, sm, P, s_begin, s_end, ntiles, lane);
+        if constexpr (OFS) producer<2, WIN>(Ly, sm, P, s_begin, s_end, ntiles, lane, W, x, n);
         else if (lane == 0) producer_compact<2>(Ly, sm, P, s_begin, s_end, ntiles);
         return;
     }
@@ -367,7 +457,26 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
             ou.at(Ly.col(sm, st, 1), uo);
         }
         double acc = 0.0;
-        if (has) {
+        if constexpr (WIN) {
+            if (has) {
+                const double *ws = Ly.win(sm, st);
+                if constexpr (CH <= 8) {
+                    WinChunk<CH> cl, cu;
+                    cl.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), ws, lo, lw, lane, row);
+                    cu.load(Ly.val(sm, st, 1), Ly.col(sm, st, 1), ws, uo, uw, lane, row);
+                    acc = cl.add(acc);
+                    acc = __dadd_rn(acc, __dmul_rn(di, xi));
+                    acc = cu.add(acc);
+                } else {
+                    WinChunk<CH> c;
+                    c.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), ws, lo, lw, lane, row);
+                    acc = c.add(acc);
+                    acc = __dadd_rn(acc, __dmul_rn(di, xi));
+                    c.load(Ly.val(sm, st, 1), Ly.col(sm, st, 1), ws, uo, uw, lane, row);
+                    acc = c.add(acc);
+                }
+            }
+        } else if (has) {
             if constexpr (CH <= 8) {  // both triangles' gathers in flight together
                 StagedChunk<CH> cl, cu;
                 if constexpr (OFS) {
@@ -419,23 +528,47 @@ __global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s
     }
 }
 
-template <bool UNIT, int EPI, class G, int CH, bool OFS>
-__global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView T,
-                                                         const double *__restrict__ dT,
-                                                         const double *__restrict__ rhs, G gin,
-                                                         double *__restrict__ gout, double *__restrict__ x,
-                                                         const double *__restrict__ dnext, double *__restrict__ gout2,
-                                                         unsigned long long *flag, int64_t sweep_id, int nst,
-                                                         int64_t cap) {
+template <int OUT, int CH, bool OFS>
+__global__ void __launch_bounds__(kThreadsT) k_residual_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView L,
+                                                            SellView U, const double *__restrict__ d,
+                                                            const double *__restrict__ b,
+                                                            const double *__restrict__ x, double *__restrict__ out,
+                                                            double *__restrict__ out2, int nst, int64_t cap,
+                                                            WinView W) {
+    residual_tma_body<OUT, CH, OFS, false>(n, s_begin, s_end, L, U, d, b, x, out, out2, nst, cap, W);
+}
+
+// Windowed variant: the producer's window bookkeeping must not cost the
+// short-row kernels their third co-resident CTA (72 registers; without the
+// bound ptxas takes 96 and the C2 / C5 residual lost a third of its warps).
+template <int OUT, int CH>
+__global__ void __launch_bounds__(kThreadsT, CH <= 8 ? 3 : 2)
+    k_residual_tma_w(int64_t n, int64_t s_begin, int64_t s_end, SellView L, SellView U, const double *__restrict__ d,
+                     const double *__restrict__ b, const double *__restrict__ x, double *__restrict__ out,
+                     double *__restrict__ out2, int nst, int64_t cap, WinView W) {
+    residual_tma_body<OUT, CH, true, true>(n, s_begin, s_end, L, U, d, b, x, out, out2, nst, cap, W);
+}
+
+__device__ __forceinline__ const double *gathered(const GatherPlainT &g) { return g.g; }
+__device__ __forceinline__ const double *gathered(const GatherScaledT &) { return nullptr; }
+
+template <bool UNIT, int EPI, class G, int CH, bool OFS, bool WIN>
+__device__ __forceinline__ void sweep_tma_body(int64_t n, int64_t s_begin, int64_t s_end, SellView T,
+                                               const double *__restrict__ dT, const double *__restrict__ rhs, G gin,
+                                               double *__restrict__ gout, double *__restrict__ x,
+                                               const double *__restrict__ dnext, double *__restrict__ gout2,
+                                               unsigned long long *flag, int64_t sweep_id, int nst, int64_t cap,
+                                               WinView W) {
     extern __shared__ __align__(128) char sm[];
     constexpr bool ofs = OFS;
-    const Layout Ly{nst, 1, cap, ofs ? 8 : 12};
+    static_assert(!WIN || OFS, "windowed kernels need the offset-aligned layout");
+    const Layout Ly{nst, 1, cap, ofs ? 8 : 12, WIN ? (int64_t)W.wcap : 0};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     init_barriers(Ly, sm);
     if (warp == kTS) {
         const SellView P[1] = {T};
-        if constexpr (OFS) producer<1>(Ly, sm, P, s_begin, s_end, ntiles, lane);
+        if constexpr (OFS) producer<1, WIN>(Ly, sm, P, s_begin, s_end, ntiles, lane, W, gathered(gin), n);
         else if (lane == 0) producer_compact<1>(Ly, sm, P, s_begin, s_end, ntiles);
         return;
     }
@@ -467,7 +600,13 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
             ot.at(Ly.col(sm, st, 0), to);
         }
         double acc = 0.0;
-        if (has) {
+        if constexpr (WIN) {
+            if (has) {
+                WinChunk<CH> ct;
+                ct.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), Ly.win(sm, st), to, tw, lane, row);
+                acc = ct.add(acc);
+            }
+        } else if (has) {
             StagedChunk<CH> ct;
             if constexpr (OFS) ct.load_ofs(Ly.val(sm, st, 0), ot, to, tw, lane, i, n);
             else ct.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), to, tw, lane);
@@ -486,6 +625,28 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
             if (EPI == EPI_XADD_SCALE) x[i] = __dadd_rn(xi, __ddiv_rn(v, dn));
         }
     }
+}
+
+template <bool UNIT, int EPI, class G, int CH, bool OFS>
+__global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_begin, int64_t s_end, SellView T,
+                                                         const double *__restrict__ dT,
+                                                         const double *__restrict__ rhs, G gin,
+                                                         double *__restrict__ gout, double *__restrict__ x,
+                                                         const double *__restrict__ dnext, double *__restrict__ gout2,
+                                                         unsigned long long *flag, int64_t sweep_id, int nst,
+                                                         int64_t cap, WinView W) {
+    sweep_tma_body<UNIT, EPI, G, CH, OFS, false>(n, s_begin, s_end, T, dT, rhs, gin, gout, x, dnext, gout2, flag,
+                                                 sweep_id, nst, cap, W);
+}
+
+template <bool UNIT, int EPI, int CH>
+__global__ void __launch_bounds__(kThreadsT, 3)
+    k_sweep_tma_w(int64_t n, int64_t s_begin, int64_t s_end, SellView T, const double *__restrict__ dT,
+                  const double *__restrict__ rhs, GatherPlainT gin, double *__restrict__ gout, double *__restrict__ x,
+                  const double *__restrict__ dnext, double *__restrict__ gout2, unsigned long long *flag,
+                  int64_t sweep_id, int nst, int64_t cap, WinView W) {
+    sweep_tma_body<UNIT, EPI, GatherPlainT, CH, true, true>(n, s_begin, s_end, T, dT, rhs, gin, gout, x, dnext, gout2,
+                                                           flag, sweep_id, nst, cap, W);
 }
 
 // ---- launch geometry ---------------------------------------------------------
@@ -516,13 +677,13 @@ struct Geo {
 // Stages per CTA: maximise resident consumer warps (capped at 32 per SM),
 // then the pipeline depth.  Cached per kernel and stage size.
 template <class K>
-Geo geometry(K kernel, int np, int maxw, int eb = 12) {
+Geo geometry(K kernel, int np, int maxw, int eb = 12, int64_t win_bytes = 0) {
     static std::mutex mu;
     // keyed by device too: the shared-memory opt-in attribute is per device
     static std::map<std::tuple<int, const void *, int64_t>, Geo> cache;
     Geo g;
     g.cap = (int64_t)kTS * kSlice * std::max(maxw, 1);
-    const int64_t stage = np * Layout::part_bytes(g.cap, eb);
+    const int64_t stage = np * Layout::part_bytes(g.cap, eb) + win_bytes;
     std::lock_guard<std::mutex> lk(mu);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -570,42 +731,61 @@ cudaError_t launch_pdl(bool pdl, K kernel, int grid, size_t smem, cudaStream_t s
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
-template <int OUT, int CH, bool OFS>
-cudaError_t residual_tma_ofs(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
+// Kernel view of a gather window; capacity = its largest tile window rounded
+// up to 32 doubles (256 bytes).
+WinView win_view(const Window *w) {
+    if (!w) return WinView{};
+    return WinView{w->tseg, w->glo, w->len, w->sbase, {w->wpos[0], w->wpos[1]}, (w->wmax + 31) / 32 * 32};
+}
+
+template <int OUT, int CH, bool OFS, bool WIN>
+cudaError_t residual_tma_ofs(const Window *w, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
                              const double *d, const double *b, const double *x, double *out, double *out2,
                              bool pdl, cudaStream_t st) {
-    auto k = k_residual_tma<OUT, CH, OFS>;
-    const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw), OFS ? 8 : 12);
+    auto k = WIN ? k_residual_tma_w<OUT, CH> : k_residual_tma<OUT, CH, OFS>;
+    const WinView W = win_view(WIN ? w : nullptr);
+    const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw), OFS ? 8 : 12, (int64_t)W.wcap * 8);
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     return launch_pdl(pdl, k, grid_of<decltype(k)>(g, ntiles), g.smem, st, n, s_begin, s_end, view(L), view(U), d, b, x,
-                      out, out2, g.nst, g.cap);
+                      out, out2, g.nst, g.cap, W);
 }
 
 template <int OUT, int CH>
-cudaError_t residual_tma_ch(int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
+cudaError_t residual_tma_ch(const Window *w, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
                             const double *d, const double *b, const double *x, double *out, double *out2,
                             bool pdl, cudaStream_t st) {
-    // offset-aligned layout (both triangles): stage values only, columns = row + offset
-    if (L.off && U.off) return residual_tma_ofs<OUT, CH, true>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
-    return residual_tma_ofs<OUT, CH, false>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
+    // offset-aligned layout (both triangles): stage values only, columns = row + offset;
+    // with a gather window over the whole range: gathers from shared memory
+    if (L.off && U.off && w && s_begin == 0)
+        return residual_tma_ofs<OUT, CH, true, true>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
+    if (L.off && U.off)
+        return residual_tma_ofs<OUT, CH, true, false>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
+    return residual_tma_ofs<OUT, CH, false, false>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
 }
 
-template <bool UNIT, int EPI, class G, int CH, bool OFS>
+template <bool UNIT, int EPI, class G, int CH, bool OFS, bool WIN>
 cudaError_t sweep_tma_ofs(const SweepArgs &a, int64_t s_begin, int64_t s_end, G gin, cudaStream_t st) {
+    const WinView W = win_view(WIN ? a.win : nullptr);
     auto k = k_sweep_tma<UNIT, EPI, G, CH, OFS>;
-    const Geo g = geometry(k, 1, a.T->maxw, OFS ? 8 : 12);
+    if constexpr (WIN) k = k_sweep_tma_w<UNIT, EPI, CH>;
+    const Geo g = geometry(k, 1, a.T->maxw, OFS ? 8 : 12, (int64_t)W.wcap * 8);
     if (!g.nst) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     return launch_pdl(a.pdl, k, grid_of<decltype(k)>(g, ntiles), g.smem, st, a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs,
-                      gin, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id, g.nst, g.cap);
+                      gin, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id, g.nst, g.cap, W);
 }
 
 template <bool UNIT, int EPI, class G, int CH>
 cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end, G gin, cudaStream_t st) {
-    // offset-aligned layout: stage values only, columns = row + offset
-    if (a.T->off) return sweep_tma_ofs<UNIT, EPI, G, CH, true>(a, s_begin, s_end, gin, st);
-    return sweep_tma_ofs<UNIT, EPI, G, CH, false>(a, s_begin, s_end, gin, st);
+    // offset-aligned layout: stage values only, columns = row + offset; with a
+    // gather window of the plain iterate over the whole range: gathers from
+    // shared memory
+    if constexpr (std::is_same<G, GatherPlainT>::value) {
+        if (a.T->off && a.win && s_begin == 0) return sweep_tma_ofs<UNIT, EPI, G, CH, true, true>(a, s_begin, s_end, gin, st);
+    }
+    if (a.T->off) return sweep_tma_ofs<UNIT, EPI, G, CH, true, false>(a, s_begin, s_end, gin, st);
+    return sweep_tma_ofs<UNIT, EPI, G, CH, false, false>(a, s_begin, s_end, gin, st);
 }
 
 template <bool UNIT, int EPI, int CH>
@@ -635,15 +815,15 @@ bool tma_ok(int np, int maxw) {
     return 128 + stage <= kSmemMax;
 }
 
-cudaError_t launch_residual_tma(int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
+cudaError_t launch_residual_tma(const Window *w, int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
                                 const Sell &U, const double *d, const double *b, const double *x, double *out,
                                 double *out2, bool pdl, cudaStream_t st) {
     if (s_end <= s_begin) return cudaSuccess;
     const int ch = chunk_for_t(std::max(L.maxw, U.maxw));
 #define NSM_RT(OUT)                                                                                  \
-    (ch == 4 ? residual_tma_ch<OUT, 4>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st)              \
-             : ch == 8 ? residual_tma_ch<OUT, 8>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st)    \
-                       : residual_tma_ch<OUT, 16>(n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st))
+    (ch == 4 ? residual_tma_ch<OUT, 4>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st)           \
+             : ch == 8 ? residual_tma_ch<OUT, 8>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st) \
+                       : residual_tma_ch<OUT, 16>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st))
     return out_mode == OUT_AX ? NSM_RT(OUT_AX) : (out_mode == OUT_RG ? NSM_RT(OUT_RG) : NSM_RT(OUT_R));
 #undef NSM_RT
 }
@@ -673,6 +853,20 @@ void touch_t(K k) {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, k);
 }
+template <int CH>
+void touch_tma_win() {
+    touch_t(k_residual_tma_w<OUT_R, CH>);
+    touch_t(k_residual_tma_w<OUT_AX, CH>);
+    touch_t(k_residual_tma_w<OUT_RG, CH>);
+    touch_t(k_sweep_tma_w<true, EPI_STORE2, CH>);
+    touch_t(k_sweep_tma_w<false, EPI_STORE2, CH>);
+    touch_t(k_sweep_tma_w<true, EPI_STORE, CH>);
+    touch_t(k_sweep_tma_w<true, EPI_XADD, CH>);
+    touch_t(k_sweep_tma_w<true, EPI_XADD_SCALE, CH>);
+    touch_t(k_sweep_tma_w<false, EPI_STORE, CH>);
+    touch_t(k_sweep_tma_w<false, EPI_XADD, CH>);
+    touch_t(k_sweep_tma_w<false, EPI_XADD_SCALE, CH>);
+}
 template <int CH, bool OFS>
 void touch_tma_ch() {
     touch_t(k_residual_tma<OUT_R, CH, OFS>);
@@ -700,6 +894,9 @@ void preload_tma_kernels() {
     touch_tma_ch<4, true>();
     touch_tma_ch<8, true>();
     touch_tma_ch<16, true>();
+    touch_tma_win<4>();
+    touch_tma_win<8>();
+    touch_tma_win<16>();
 }
 
 }  // namespace nsm

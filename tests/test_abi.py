@@ -94,3 +94,14 @@ def test_product_path_does_not_touch_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h")):
                 src = open(os.path.join(dp, f)).read()
                 assert not re.search(r"import\s+oracle|from\s+oracle|liboracle|oracle\.c|\borc_", src), f
+
+
+def test_library_resolves_every_symbol_at_load():
+    """dlopen with RTLD_NOW: an undefined internal symbol (a host function
+    declared but defined in the wrong namespace) fails here, on the CPU, not
+    on the GPU box."""
+    import ctypes
+    import os as _os
+    from paper_2112_14681_b200 import build, lib_path
+    build.build()
+    ctypes.CDLL(lib_path(), mode=_os.RTLD_NOW)

@@ -73,16 +73,19 @@ SMALL = {
 }
 
 
-KERNELS = ("fused", "fusedw1", "pipelined", "plain")
+KERNELS = ("fused", "fusedw1", "pipelined", "nowindow", "plain")
 
 
 def set_kernels(S, mode):
     """fused: phase-skewed fused passes wherever possible (pGS one pass, ILU
     two) + pipelined kernels; fusedw1: the same with wait distance 1 (every
     item waits for its predecessor, rings wrap after a few tiles: stresses the
-    synchronisation); pipelined: one cp.async.bulk pipelined kernel per pass;
-    plain: register-blocked."""
+    synchronisation); pipelined: one cp.async.bulk pipelined kernel per pass,
+    gathering from shared-memory windows where the layout allows (the
+    default); nowindow: the same gathering through L1/L2; plain:
+    register-blocked."""
     S.set_pipeline(mode != "plain")
+    S.set_window(mode != "nowindow")
     S.set_fused(1 if mode.startswith("fused") else 0)
     S.set_fused_window(1 if mode == "fusedw1" else 0)
 

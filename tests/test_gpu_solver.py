@@ -220,7 +220,7 @@ def test_gmres_recaptures_after_ruiz_change():
     F0 = oracle.ilu0(levels[0][0])[2]
     b = dev(inputs.uniform(0, A.shape[0]))
     n0 = levels[0][0].shape[0]
-    s_r, s_c = np.full(n0, 2.0), np.full(n0, 0.5)
+    s_r, s_c = inputs.uniform(7, n0, 1.0, 2.0), np.ones(n0)   # non-uniform: a real change of M
 
     def build():
         S = [nsm.Smoother(inputs.CSR.from_scipy(levels[0][0]), F0)] + \
