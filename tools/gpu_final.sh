@@ -1,16 +1,22 @@
 #!/bin/bash
-# Round measurement: tests, smoke, bench lines for every config, reference arm,
-# ncu launch list of the default bench command, full capture of the top kernel.
+# Round measurement: tests, smoke, bench lines for every config (default = C3),
+# the reference arm, ncu launch lists of the default bench command (C3) and of
+# C4, and full captures of the C3 / C4 residual kernels (DRAM traffic).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 600 python bench.py > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
-for c in C3 C4 C5; do
+if [ -z "$NOTESTS" ]; then
+  timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+fi
+timeout 900 python bench.py > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3.err
+for c in C2 C4 C5; do
   timeout 600 python bench.py --config $c --no-cpu > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
-timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_C2.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:'k_' -c 60 --csv --log-file gpurun_out/launches_C5.csv python bench.py --config C5 --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch5.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_residual' -s 10 -c 1 -o gpurun_out/prof_residual_C2 python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
+timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+timeout 900 ncu --metrics $M --clock-control none -c 400 --csv --log-file gpurun_out/launches_C3.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --metrics $M --clock-control none -k regex:'k_' -c 60 --csv --log-file gpurun_out/launches_C4.csv python bench.py --config C4 --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_residual' -s 6 -c 1 -o gpurun_out/prof_residual_C3 python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep' -s 10 -c 1 -o gpurun_out/prof_sweep_C3 python bench.py --steps 2 --warmup 3 --no-cpu >> gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_residual' -s 6 -c 1 -o gpurun_out/prof_residual_C4 python bench.py --config C4 --steps 2 --warmup 3 --no-cpu >> gpurun_out/ncu_full.log 2>&1

@@ -1,9 +1,10 @@
 #!/usr/bin/env python
 """Write profiles/<name>.md from a tools/gpu_final.sh run brought back in gpurun_out/
-(bench lines C2..C5, the reference arm, ncu launch lists and the full capture of the C2
-residual) and refresh profiles/ncu_traffic.json and the committed launch lists.
+(bench lines C2..C5 with C3 the default workload, the reference arm, ncu launch lists of
+C3 and C4 and the full captures of their residual kernels and the C3 sweep) and refresh
+profiles/ncu_traffic.json and the committed launch lists.
 
-  python tools/round_md.py r01_v9_round "title" "intro paragraph"
+  python tools/round_md.py r02_round "title" "intro paragraph"
 """
 import json
 import os
@@ -20,33 +21,40 @@ def sh(*a):
                           capture_output=True, text=True, check=True).stdout
 
 
-def main(name, title, intro):
-    b = {c: json.load(open(os.path.join(G, f"bench_{c}.json"))) for c in ["C2", "C3", "C4", "C5"]}
-    ref = json.loads(open(os.path.join(G, "bench_ref.json")).readline())
-    l2 = sh("launches", os.path.join(G, "launches_C2.csv"), "--bench", os.path.join(G, "bench_C2.json"))
-    l5 = sh("launches", os.path.join(G, "launches_C5.csv"))
-    full = sh("full", os.path.join(G, "prof_residual_C2.ncu-rep"))
+def dram_of(full: str):
     rd = wr = None
     for line in full.splitlines():
         if line.startswith("| dram__bytes_read.sum (Mbyte)"):
             rd = float(line.split("|")[2])
         if line.startswith("| dram__bytes_write.sum (Mbyte)"):
             wr = float(line.split("|")[2])
-    traffic = int(round((rd + wr) * 1e6)) if rd is not None and wr is not None else None
-    if traffic:
-        json.dump({"_source": "ncu --set full (cold cache, serialised): dram__bytes_read.sum + dram__bytes_write.sum "
-                              f"of one launch; profiles/{name}.md", "C2": {"residual": traffic}},
-                  open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
-    for c in ["C2", "C5"]:
-        shutil.copy(os.path.join(G, f"launches_{c}.csv"), os.path.join(ROOT, "profiles", f"r01_launches_{c}.csv"))
+    return int(round((rd + wr) * 1e6)) if rd is not None and wr is not None else None
+
+
+def main(name, title, intro):
+    b = {c: json.load(open(os.path.join(G, f"bench_{c}.json"))) for c in ["C3", "C2", "C4", "C5"]}
+    ref = json.loads(open(os.path.join(G, "bench_ref.json")).readline())
+    l3 = sh("launches", os.path.join(G, "launches_C3.csv"))
+    l4 = sh("launches", os.path.join(G, "launches_C4.csv"))
+    fulls = {k: sh("full", os.path.join(G, f"prof_{k}.ncu-rep")) for k in ("residual_C3", "sweep_C3", "residual_C4")}
+    traffic = {k: dram_of(v) for k, v in fulls.items()}
+    json.dump({"_source": "ncu --set full (cold cache, serialised): dram__bytes_read.sum + dram__bytes_write.sum "
+                          f"of one launch; profiles/{name}.md",
+               "C3": {"residual": traffic["residual_C3"], "sweep": traffic["sweep_C3"]},
+               "C4": {"residual": traffic["residual_C4"]}},
+              open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+    for c in ["C3", "C4"]:
+        shutil.copy(os.path.join(G, f"launches_{c}.csv"), os.path.join(ROOT, "profiles", f"{name}_launches_{c}.csv"))
     rows = []
     for c, d in b.items():
         r = d["roofline"]
-        parts = ", ".join(d["config"].get("offset_aligned_parts") or []) or "-"
-        rows.append(f"| {c} | {d['ms_per_step']} | {d['value']} | {d['config']['frac_of_hbm_peak']} | "
-                    f"{d['config']['floor_gbs']} | {r['frac']} | {r['alone_frac']} | {r['sweeps_frac']} | {parts} | "
+        det = d.get("detail", {})
+        parts = ", ".join(det.get("offset_aligned_parts") or []) or "-"
+        rows.append(f"| {c} | {d['ms_per_step']} | {d['value']} | {det.get('frac_of_hbm_peak')} | "
+                    f"{det.get('floor_gbs')} | {r['frac']} | {r.get('alone_frac')} | {r.get('sweeps_frac')} | {parts} | "
                     f"{d['e2e']['value']} |")
-    clk = b["C2"]["clocks"]
+    clk = b["C3"]["clocks"]
+    cpu = b["C3"].get("cpu_baseline") or {}
     md = f"""# {title}
 
 `bash tools/gpu_final.sh` on one B200 (SM clock {clk['sm_mhz']} MHz under load, throttle reasons {clk['reasons']}).
@@ -60,28 +68,38 @@ def main(name, title, intro):
 implementation-independent floor (each stored entry at 12 B, each n-vector once) / the same time; `e2e` = the same
 bytes / the time of `nsm_smooth_host` on pinned host vectors (PCIe copies included).
 
-Reference arm (`bench.py --impl reference`: the single-threaded C oracle, C2): {ref['ms_per_step']} ms per
-application, {ref['value']} GB/s.
+CPU oracle on the box's host (C3, the default line's `cpu_baseline`): all cores {cpu.get('cores')} threads
+{cpu.get('ms_per_apply')} ms per application ({cpu.get('value')} GB/s); one thread
+{(cpu.get('single_core') or {}).get('ms_per_apply')} ms ({(cpu.get('single_core') or {}).get('value')} GB/s).
+Reference arm (`bench.py --impl reference`, the all-cores oracle, C3): {ref.get('ms_per_step')} ms per
+application, {ref.get('value')} GB/s.
 
-Full bench line (C2, the default workload):
+Full bench line (C3, the default workload):
 
 ```json
-{json.dumps(b['C2'])}
+{json.dumps(b['C3'])}
 ```
 
-## ncu launch list, C2 default command (cold cache, serialised; `profiles/r01_launches_C2.csv`)
+## ncu launch list, default command (C3; cold cache, serialised; `profiles/{name}_launches_C3.csv`)
 
-{l2}
-(The `at::` kernels are the bench's own L2-flush fill/read, outside the timed smoother calls.)
+{l3}
+(The `at::` kernels are the bench's own L2-flush reads, outside the timed smoother calls.)
 
-## ncu launch list, C5 (`profiles/r01_launches_C5.csv`)
+## ncu launch list, C4 (`profiles/{name}_launches_C4.csv`)
 
-{l5}
-## ncu --set full, C2 residual kernel
+{l4}
+## ncu --set full, C3 residual kernel
 
-{full}
-DRAM traffic per launch {traffic / 1e6 if traffic else float('nan'):.1f} MB vs the algorithmic
-{b['C2']['roofline']['bytes_per_launch'] / 1e6:.1f} MB (the r write stays in L2 at kernel end).
+{fulls['residual_C3']}
+## ncu --set full, C3 sweep kernel
+
+{fulls['sweep_C3']}
+## ncu --set full, C4 residual kernel
+
+{fulls['residual_C4']}
+DRAM traffic per launch (ncu, cold): C3 residual {(traffic['residual_C3'] or 0) / 1e6:.1f} MB vs the algorithmic
+{b['C3']['roofline']['bytes_per_launch'] / 1e6:.1f} MB; C4 residual {(traffic['residual_C4'] or 0) / 1e6:.1f} MB vs
+{b['C4']['roofline']['bytes_per_launch'] / 1e6:.1f} MB.
 """
     open(os.path.join(ROOT, "profiles", f"{name}.md"), "w").write(md)
     print(f"profiles/{name}.md written; traffic {traffic}")
