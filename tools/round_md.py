@@ -22,13 +22,18 @@ def sh(*a):
 
 
 def dram_of(full: str):
-    rd = wr = None
+    """dram__bytes_read.sum + dram__bytes_write.sum of a full-capture summary
+    (ncu prints them in byte / Kbyte / Mbyte / Gbyte)."""
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    got = {}
     for line in full.splitlines():
-        if line.startswith("| dram__bytes_read.sum (Mbyte)"):
-            rd = float(line.split("|")[2])
-        if line.startswith("| dram__bytes_write.sum (Mbyte)"):
-            wr = float(line.split("|")[2])
-    return int(round((rd + wr) * 1e6)) if rd is not None and wr is not None else None
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if line.startswith(f"| {k} ("):
+                unit = line.split("(")[1].split(")")[0]
+                got[k] = float(line.split("|")[2]) * scale.get(unit, float("nan"))
+    if len(got) != 2:
+        return None
+    return int(round(got["dram__bytes_read.sum"] + got["dram__bytes_write.sum"]))
 
 
 def main(name, title, intro):
