@@ -487,6 +487,24 @@ const char *nsm_comm_last_error(const nsm_comm *c);
 void nsm_comm_destroy(nsm_comm *c);
 nsm_status nsm_set_comm(nsm_handle *h, nsm_comm *c);
 
+/* ---- device-side set-up -----------
+ * nsm_setup_device: single-rank nsm_setup from a DEVICE CSR — A's (and F's)
+ * rowptr / colind / val are device pointers of `device` (int64 / int64 /
+ * fp64, the nsm_csr layout), borrowed for the call.  The split, the SELL-32
+ * packing (compact or offset-aligned, the same decision) and the diagonals
+ * are built by GPU kernels and are identical to nsm_setup's host build;
+ * errors as nsm_setup (pattern, zero diagonal with the first offending row).
+ *
+ * nsm_part_info / nsm_part_copy / nsm_diag_copy: host copies of a handle's
+ * device arrays (diagnostics, builder parity).  part 0..7 = L, U, LG, UG,
+ * Ls, Us, LsG, UsG (slice pointers nslices + 1, columns / values `padded`
+ * entries, offsets padded / 32 when aligned; NULL buffers are skipped);
+ * which 0 = d, 1 = l1 diagonal, 2 = d_U (NSM_ERR_STATE without factors). */
+nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, int device);
+nsm_status nsm_part_info(const nsm_handle *h, int part, int64_t *padded, int64_t *nnz, int *maxw, int *aligned);
+nsm_status nsm_part_copy(const nsm_handle *h, int part, int64_t *ptr, int32_t *col, double *val, int32_t *off);
+nsm_status nsm_diag_copy(const nsm_handle *h, int which, double *out);
+
 /* Frees all device memory of the handle (synchronises its device).  NULL ok. */
 void nsm_destroy(nsm_handle *h);
 

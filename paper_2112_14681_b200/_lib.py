@@ -27,7 +27,7 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual
                   "nsm_fused_stats", "nsm_layout", "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect",
                   "nsm_comm_connect_ipc", "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout",
                   "nsm_comm_stats", "nsm_comm_last_error", "nsm_comm_destroy", "nsm_set_comm", "nsm_ruiz_dep",
-                  "nsm_dep"])
+                  "nsm_dep", "nsm_setup_device", "nsm_part_info", "nsm_part_copy", "nsm_diag_copy"])
 
 
 class NsmError(RuntimeError):
@@ -124,6 +124,10 @@ def load(variant: str = ""):
     L.nsm_set_comm.argtypes = [vp, vp]
     L.nsm_ruiz_dep.argtypes = [P(_Csr), ci, ctypes.c_double, vp, vp, vp, P(ci), vp]
     L.nsm_dep.argtypes = [P(_Csr), vp, ci, vp]
+    L.nsm_setup_device.argtypes = [P(vp), P(_Csr), P(_Csr), ci]
+    L.nsm_part_info.argtypes = [vp, ci, P(i64), P(i64), P(ci), P(ci)]
+    L.nsm_part_copy.argtypes = [vp, ci, vp, vp, vp, vp]
+    L.nsm_diag_copy.argtypes = [vp, ci, vp]
     for name in ["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
                  "nsm_smooth_host", "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
@@ -131,7 +135,7 @@ def load(variant: str = ""):
                  "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats", "nsm_layout",
                  "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect", "nsm_comm_connect_ipc",
                  "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout", "nsm_comm_stats", "nsm_set_comm",
-                 "nsm_ruiz_dep", "nsm_dep"]:
+                 "nsm_ruiz_dep", "nsm_dep", "nsm_setup_device", "nsm_part_info", "nsm_part_copy", "nsm_diag_copy"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -327,6 +331,59 @@ class Smoother:
         n, ng, nnz, db = (ctypes.c_int64() for _ in range(4))
         L.nsm_info(h, ctypes.byref(n), ctypes.byref(ng), ctypes.byref(nnz), ctypes.byref(db))
         self.n, self.n_ghost, self.nnz_offdiag, self.device_bytes = n.value, ng.value, nnz.value, db.value
+
+    @classmethod
+    def from_device_csr(cls, rowptr, col, val, fval=None, device: int | None = None):
+        """nsm_setup_device: a single-rank handle built ON THE GPU from a device
+        CSR (torch CUDA tensors: int64 rowptr, int64 col, float64 val; fval =
+        the ILU factor values on the same pattern, or None)."""
+        import torch
+        self = cls.__new__(cls)
+        self._torch = torch
+        L = load()
+        self.device = rowptr.device.index if device is None else int(device)
+        for t, dt in ((rowptr, torch.int64), (col, torch.int64), (val, torch.float64)):
+            if not (t.is_cuda and t.dtype == dt and t.is_contiguous() and t.device.index == self.device):
+                raise TypeError("from_device_csr: contiguous CUDA tensors (int64 rowptr, int64 col, float64 val)")
+        n = rowptr.numel() - 1
+        ca = _Csr(n, n, rowptr.data_ptr(), col.data_ptr(), val.data_ptr())
+        cf = _Csr(n, n, rowptr.data_ptr(), col.data_ptr(), fval.data_ptr()) if fval is not None else None
+        h = ctypes.c_void_p()
+        st = L.nsm_setup_device(ctypes.byref(h), ctypes.byref(ca), ctypes.byref(cf) if cf is not None else None,
+                                self.device)
+        if st != 0:
+            raise NsmError(st, _err(None))
+        self._h = h
+        self.has_ilu = fval is not None
+        self.rank, self.nranks = 0, 1
+        self.requests = {}
+        nn, ng, nnz, db = (ctypes.c_int64() for _ in range(4))
+        L.nsm_info(h, ctypes.byref(nn), ctypes.byref(ng), ctypes.byref(nnz), ctypes.byref(db))
+        self.n, self.n_ghost, self.nnz_offdiag, self.device_bytes = nn.value, ng.value, nnz.value, db.value
+        return self
+
+    def part(self, p: int) -> dict:
+        """Host copy of device part p (0..7 = L, U, LG, UG, Ls, Us, LsG, UsG)."""
+        L = load()
+        padded, nnz = ctypes.c_int64(), ctypes.c_int64()
+        maxw, al = ctypes.c_int(), ctypes.c_int()
+        self._call(L.nsm_part_info(self._h, int(p), ctypes.byref(padded), ctypes.byref(nnz), ctypes.byref(maxw),
+                                   ctypes.byref(al)))
+        ns = (self.n + 31) // 32
+        ptr = np.zeros(ns + 1, dtype=np.int64)
+        col = np.zeros(padded.value, dtype=np.int32)
+        val = np.zeros(padded.value, dtype=np.float64)
+        off = np.zeros(padded.value // 32 if al.value else 0, dtype=np.int32)
+        self._call(L.nsm_part_copy(self._h, int(p), ptr.ctypes.data, col.ctypes.data if len(col) else None,
+                                   val.ctypes.data if len(val) else None, off.ctypes.data if len(off) else None))
+        return {"ptr": ptr, "col": col, "val": val, "off": off, "nnz": nnz.value, "maxw": maxw.value,
+                "aligned": bool(al.value)}
+
+    def diag(self, which: int = 0) -> np.ndarray:
+        """Host copy of d (0), the l1 diagonal (1) or d_U (2)."""
+        out = np.zeros(self.n, dtype=np.float64)
+        self._call(load().nsm_diag_copy(self._h, int(which), out.ctypes.data if self.n else None))
+        return out
 
     # -- marshalling helpers ------------------------------------------------
     def _stream(self, stream):

@@ -385,6 +385,11 @@ nsm_status scale_into(nsm_handle *h, bool xadd, const double *rhs, const double 
     return e == cudaSuccess ? NSM_OK : cuda_fail(h, e, "scale launch");
 }
 
+uint64_t next_handle_uid() {
+    static std::atomic<uint64_t> next_uid{1};
+    return next_uid++;
+}
+
 size_t flags_bytes_for(int nranks) { return (((size_t)nranks * 8 + 255) / 256) * 256; }
 
 }  // namespace
@@ -531,8 +536,7 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     preload_halo_kernels();
     preload_fused_kernels();
     nsm_handle *h = new nsm_handle();
-    static std::atomic<uint64_t> next_uid{1};
-    h->uid = next_uid++;
+    h->uid = next_handle_uid();
     h->device = device;
     h->n = sa.n;
     h->row_begin = rb;
@@ -624,6 +628,124 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     }
     *out = h;
     return NSM_OK;
+}
+
+// Single-rank set-up from a DEVICE CSR: the split / SELL-32 packing runs on
+// the GPU (builder_gpu.cu) and yields the same arrays as nsm_setup's host
+// builder; the rest of the handle is assembled as in nsm_setup.
+nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, int device) {
+    if (!out || !A) { g_setup_err = "nsm_setup_device: NULL argument"; return NSM_ERR_ARG; }
+    *out = nullptr;
+    if (A->ncols != A->nrows) { g_setup_err = "nsm_setup_device: A must be square"; return NSM_ERR_ARG; }
+    if (F && (F->nrows != A->nrows || F->ncols != A->ncols)) {
+        g_setup_err = "nsm_setup: F shape differs from A";
+        return NSM_ERR_ARG;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) { g_setup_err = "nsm_setup_device: cudaSetDevice failed"; return NSM_ERR_CUDA; }
+    preload_plain_kernels();
+    preload_tma_kernels();
+    preload_halo_kernels();
+    preload_fused_kernels();
+    nsm_handle *h = new nsm_handle();
+    h->uid = next_handle_uid();
+    h->device = device;
+    DevSplit sa, sf;
+    nsm_status st = build_split_device(A, &sa, &h->device_bytes, &g_setup_err);
+    h->d = sa.d;
+    h->dl1 = sa.dl1;
+    h->L = sa.L;
+    h->U = sa.U;
+    if (st == NSM_OK && F) {
+        st = build_split_device(F, &sf, &h->device_bytes, &g_setup_err);
+        h->dU = sf.d;
+        cudaFree(sf.dl1);
+        h->Ls = sf.L;
+        h->Us = sf.U;
+        if (st != NSM_OK) g_setup_err = "factor: " + g_setup_err;
+        h->has_ilu = st == NSM_OK;
+    }
+    if (st != NSM_OK) {
+        free_handle(h);
+        return st;
+    }
+    h->n = sa.n;
+    h->nnz_off = sa.nnz_off;
+    h->nslices = (int)((sa.n + kSlice - 1) / kSlice);
+    h->pdl = sa.n <= (int64_t)8 * 1024 * 1024;  // as nsm_setup
+    DevAlloc a{h};
+    const int64_t ns = h->nslices;
+    auto empty_part = [&](Sell *s) {  // no ghost couplings on one rank: zero slice pointers
+        return a.get(&s->ptr, ns + 1) && cudaMemset(s->ptr, 0, (ns + 1) * sizeof(int64_t)) == cudaSuccess;
+    };
+    bool ok = empty_part(&h->LG) && empty_part(&h->UG) && (!F || (empty_part(&h->LsG) && empty_part(&h->UsG)));
+    ok = ok && make_window(a, h->n, {&sa.Lh, &sa.Uh}, &h->res_win) && make_window(a, h->n, {&sa.Lh}, &h->L.win) &&
+         make_window(a, h->n, {&sa.Uh}, &h->U.win);
+    if (ok && F) ok = make_window(a, h->n, {&sf.Lh}, &h->Ls.win) && make_window(a, h->n, {&sf.Uh}, &h->Us.win);
+    for (int i = 0; ok && i < 4; ++i) ok = a.get(&h->w[i], std::max<int64_t>(h->n, 1));
+    ok = ok && a.get(&h->flag, 1) && a.get(&h->ghost_null, 1) && a.get(&h->d_dist_err, 1) &&
+         cudaMemset(h->d_dist_err, 0, sizeof(unsigned int)) == cudaSuccess;
+    if (ok) {
+        unsigned long long init = ULLONG_MAX;
+        ok = cudaMemcpy(h->flag, &init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+    if (ok && h->n > 0) {
+        const int64_t tr = skew_tile_rows();
+        auto tiles = [tr](int64_t bw) { return (int)((bw + tr - 1) / tr); };
+        h->DLA = tiles(sa.bw_lower);
+        h->DUA = tiles(sa.bw_upper);
+        h->DLs = F ? tiles(sf.bw_lower) : 0;
+        h->DUs = F ? tiles(sf.bw_upper) : 0;
+        h->fused_possible = true;
+    }
+    if (!ok) {
+        cudaGetLastError();
+        g_setup_err = "nsm_setup_device: device allocation failed";
+        free_handle(h);
+        return NSM_ERR_OOM;
+    }
+    *out = h;
+    return NSM_OK;
+}
+
+// Copies of a handle's device arrays (diagnostics and the builder parity
+// tests): part 0..7 = L, U, LG, UG, Ls, Us, LsG, UsG.
+static const Sell *part_of(const nsm_handle *h, int part) {
+    const Sell *p[8] = {&h->L, &h->U, &h->LG, &h->UG, &h->Ls, &h->Us, &h->LsG, &h->UsG};
+    return part >= 0 && part < 8 ? p[part] : nullptr;
+}
+
+nsm_status nsm_part_info(const nsm_handle *h, int part, int64_t *padded, int64_t *nnz, int *maxw, int *aligned) {
+    const Sell *s = h ? part_of(h, part) : nullptr;
+    if (!s) return NSM_ERR_ARG;
+    if (padded) *padded = s->padded;
+    if (nnz) *nnz = s->nnz;
+    if (maxw) *maxw = s->maxw;
+    if (aligned) *aligned = s->off != nullptr;
+    return NSM_OK;
+}
+
+nsm_status nsm_part_copy(const nsm_handle *h, int part, int64_t *ptr, int32_t *col, double *val, int32_t *off) {
+    const Sell *s = h ? part_of(h, part) : nullptr;
+    if (!s) return NSM_ERR_ARG;
+    DeviceScope dev(h->device);
+    const int64_t ns = h->nslices;
+    bool ok = true;
+    if (ptr && s->ptr) ok = cudaMemcpy(ptr, s->ptr, (ns + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (ok && col && s->padded) ok = cudaMemcpy(col, s->col, s->padded * sizeof(int32_t), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (ok && val && s->padded) ok = cudaMemcpy(val, s->val, s->padded * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (ok && off && s->off)
+        ok = cudaMemcpy(off, s->off, s->padded / kSlice * sizeof(int32_t), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (ok && ptr && !s->ptr) std::fill(ptr, ptr + ns + 1, (int64_t)0);
+    return ok ? NSM_OK : NSM_ERR_CUDA;
+}
+
+nsm_status nsm_diag_copy(const nsm_handle *h, int which, double *out) {
+    if (!h || !out || which < 0 || which > 2) return NSM_ERR_ARG;
+    const double *src = which == 0 ? h->d : (which == 1 ? h->dl1 : h->dU);
+    if (!src) return NSM_ERR_STATE;
+    DeviceScope dev(h->device);
+    return h->n == 0 || cudaMemcpy(out, src, h->n * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess ? NSM_OK
+                                                                                                         : NSM_ERR_CUDA;
 }
 
 nsm_status nsm_halo_set_send(nsm_handle *h, int q, const int64_t *rows, int64_t count) {

@@ -86,15 +86,17 @@ void pack(int64_t n, const std::vector<int32_t> &cnt, const std::vector<int64_t>
 // rows, one entry per row — the row's a_{i,i+o} or a pad (val 0) — so a slice
 // needs one int32 offset per entry position instead of one column per entry.
 // Within each row the entries stay in ascending column order (pads add 0).
-// Used only if the union widens the slices by at most 15 % and pads are at
-// most 3 % of the stored entries.
+// Used only if the union widens the slices by at most 15 %, pads are at
+// most 3 % of the stored entries and no slice's union exceeds 2 w + 8 (the
+// device builder, builder_gpu.cu, takes the same decision).
 bool pack_aligned(int64_t n, int64_t rb, const std::vector<int32_t> &cnt, const std::vector<int64_t> &first,
                   const int64_t *ci, const double *va, SellHost *out) {
     const int64_t ns = (n + kSlice - 1) / kSlice;
     std::vector<std::vector<int32_t>> uni(ns);
     std::vector<int64_t> wc(ns, 0);
     int64_t sum_u = 0, sum_c = 0;
-#pragma omp parallel for schedule(static) reduction(+ : sum_u, sum_c)
+    int over = 0;
+#pragma omp parallel for schedule(static) reduction(+ : sum_u, sum_c) reduction(max : over)
     for (int64_t s = 0; s < ns; ++s) {
         std::vector<int32_t> &u = uni[s];
         int32_t m = 0;
@@ -104,6 +106,7 @@ bool pack_aligned(int64_t n, int64_t rb, const std::vector<int32_t> &cnt, const 
         }
         std::sort(u.begin(), u.end());
         u.erase(std::unique(u.begin(), u.end()), u.end());
+        if ((int64_t)u.size() > 2 * (int64_t)m + 8) over = 1;  // a scattered slice: keep it compact
         wc[s] = m;
         sum_u += (int64_t)u.size();
         sum_c += m;
@@ -112,7 +115,8 @@ bool pack_aligned(int64_t n, int64_t rb, const std::vector<int32_t> &cnt, const 
     // does not couple to (lexicographic stencils: grid-line ends only)
     int64_t nnz_part = 0;
     for (int64_t i = 0; i < n; ++i) nnz_part += cnt[i];
-    if (sum_c == 0 || sum_u * 100 > sum_c * 115 || (sum_u * kSlice - nnz_part) * 100 > sum_u * kSlice * 3) return false;
+    if (over || sum_c == 0 || sum_u * 100 > sum_c * 115 || (sum_u * kSlice - nnz_part) * 100 > sum_u * kSlice * 3)
+        return false;
     out->ptr.assign(ns + 1, 0);
     int32_t maxw = 0;
     int64_t nnz = 0;

@@ -114,6 +114,18 @@ struct Split {
     int64_t bw_lower = 0, bw_upper = 0;  // max (i - j) over L entries, max (j - i) over U entries
 };
 
+// The same split built on the device from a DEVICE CSR (builder_gpu.cu;
+// single rank: no ghost parts).  d, dl1 and the parts are device memory owned
+// by the caller afterwards; Lh / Uh hold host copies of the slice pointers and
+// offsets (the gather-window plans are built from them).
+struct DevSplit {
+    int64_t n = 0, nnz_off = 0, bw_lower = 0, bw_upper = 0;
+    double *d = nullptr, *dl1 = nullptr;
+    Sell L, U;
+    SellHost Lh, Uh;
+};
+nsm_status build_split_device(const nsm_csr *A, DevSplit *out, int64_t *device_bytes, std::string *err);
+
 // Builds the SELL split of rows [row_begin, row_begin + n) of A.
 //   unit_lower: the strictly-lower part belongs to a unit-lower factor (the
 //               stored diagonal is the U factor's; used for ILU factors).
