@@ -96,6 +96,8 @@ struct nsm_handle {
     int put_grid = 0;
     bool committed = false;
     unsigned long long exch_seq = 0;
+    cudaStream_t side = nullptr;           // the halo put runs here, concurrently with the interior kernel
+    cudaEvent_t ev_fork = nullptr, ev_put = nullptr;
     unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
     double *ghost_null = nullptr;      // 1-element dummy ghost buffer (single rank)
     std::string err;
@@ -195,6 +197,9 @@ void free_handle(nsm_handle *h) {
         cudaFree(p.d_send_rows);
         if (p.ipc_base) cudaIpcCloseMemHandle(p.ipc_base);
     }
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_put) cudaEventDestroy(h->ev_put);
     cudaFree(h->mailbox);
     cudaFree(h->d_put);
     cudaFree(h->d_peer_ids);
@@ -274,14 +279,29 @@ nsm_status pass(nsm_handle *h, bool exchange, const double *src, const double *s
     const unsigned long long seq = ++h->exch_seq;
     const int parity = (int)(seq & 1);
     const double *ghost = h->mb_data + (int64_t)parity * h->n_ghost;
-    cudaError_t e = launch_halo_put(h->d_put, (int)h->peers.size(), h->put_grid, src, scale, parity, seq,
-                                    h->d_counters, s);
+    // the put (gather of the boundary entries + peer stores over NVLink) runs
+    // on the side stream, concurrently with the interior slices on `s`; the
+    // wait kernel is ordered after both
+    const bool fork = h->side && h->n_interior > 0;
+    cudaError_t e = cudaSuccess;
+    if (fork) {
+        e = cudaEventRecord(h->ev_fork, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+        if (e != cudaSuccess) return cuda_fail(h, e, "halo fork");
+    }
+    e = launch_halo_put(h->d_put, (int)h->peers.size(), h->put_grid, src, scale, parity, seq, h->d_counters,
+                        fork ? h->side : s);
     if (e != cudaSuccess) return cuda_fail(h, e, "halo put");
+    if (fork) {
+        e = cudaEventRecord(h->ev_put, h->side);
+        if (e != cudaSuccess) return cuda_fail(h, e, "halo put event");
+    }
     if (h->n_interior > 0) {
         e = launch(Slices{h->interior, h->n_interior, h->interior_begin, h->interior_end}, false, ghost);
         ++h->launches;
         if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch (interior)");
     }
+    if (fork && (e = cudaStreamWaitEvent(s, h->ev_put, 0)) != cudaSuccess) return cuda_fail(h, e, "halo join");
     e = launch_halo_wait(h->mb_flags, h->d_peer_ids, (int)h->peers.size(), seq, h->timeout_ns, h->d_dist_err, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "halo wait");
     if (h->n_boundary > 0) {
@@ -839,6 +859,16 @@ nsm_status nsm_halo_commit(nsm_handle *h) {
             !upload(h->d_peer_ids, ids.data(), np) || !a.get(&h->d_counters, np) ||
             cudaMemset(h->d_counters, 0, np * sizeof(unsigned int)) != cudaSuccess)
             return NSM_ERR_OOM;
+    }
+    // side stream for the put (overlaps the interior kernel, see pass())
+    DeviceScope dev(h->device);
+    if (np > 0 && !h->side &&
+        (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&h->ev_put, cudaEventDisableTiming) != cudaSuccess)) {
+        cudaGetLastError();
+        h->err = "nsm_halo_commit: stream / event creation failed";
+        return NSM_ERR_CUDA;
     }
     h->committed = true;
     return NSM_OK;

@@ -3,6 +3,13 @@ import sys
 
 import pytest
 
+# Virtual ranks (several row-block "ranks" on one device) run up to 8 ranks x
+# 2 streams (halo puts overlap the interior kernels on a side stream) plus
+# their spinning halo waits: give every stream its own hardware queue, so a
+# spinning wait never sits in front of a peer's put in a shared queue.
+# (Must be set before CUDA initialises; one process per GPU needs only 2.)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -259,3 +259,80 @@ def test_eight_rank_slabs(mode):
               f"8 ranks {mode} ilu")
     finally:
         V.close()
+
+
+def _xdev_worker(rank, world, port, q, same_device):
+    """One rank per process (CUDA IPC mailboxes, gloo plumbing): HYBRID and
+    GLOBAL pGS, the device all-reduce and Algorithm 1 across the ranks."""
+    import torch.distributed as dist
+    from oracle import krylov
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dev = 0 if same_device else rank
+        torch.cuda.set_device(dev)
+        N = 8
+        n_loc = N ** 3
+        offsets = np.arange(world + 1) * n_loc
+        A = inputs.weak_slab(N, world, rank)
+        rb = rank * n_loc
+        Ag = inputs.laplace(N, N, N * world)
+        bg, xg = inputs.uniform(0, Ag.nrows), inputs.uniform(1, Ag.nrows)
+        ok = True
+        for mode, bounds in ((nsm.NSM_DIST_HYBRID, offsets), (nsm.NSM_DIST_GLOBAL, None)):
+            S = nsm.Smoother(A, device=dev, rank=rank, nranks=world, row_offsets=offsets, mode=mode)
+            S.connect(dist)
+            b = torch.from_numpy(bg[rb:rb + n_loc].copy()).cuda(dev)
+            x = torch.from_numpy(xg[rb:rb + n_loc].copy()).cuda(dev)
+            S.smooth(b, x, "pgs", nu=2, k_l=2)
+            S.check()
+            out = [torch.empty(n_loc, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(out, x.cpu())
+            want = oracle.pgs_apply(Ag, bg, xg, 2, nu=2, bounds=bounds)
+            ok = ok and bool(np.array_equal(torch.cat(out).numpy(), want))
+            if mode == nsm.NSM_DIST_GLOBAL:
+                C = nsm.Comm(rank, world, 1024, device=dev)
+                C.connect(dist)
+                v = torch.full((37,), float(rank + 1), dtype=torch.float64, device=f"cuda:{dev}")
+                s = C.allreduce(v)
+                C.check()
+                ok = ok and bool(torch.all(s.cpu() == world * (world + 1) / 2))
+                S.set_comm(C)
+                xs, its, hist = nsm.gmres(S, b, None, tol=1e-8, maxit=200)
+                _, its_o, _ = krylov.gmres_lowsync(Ag.to_scipy(), bg, lambda v_: v_, tol=1e-8)
+                ok = ok and its == its_o
+                C.check()
+                dist.barrier()
+                S.set_comm(None)
+                C.close()
+            dist.barrier()
+            S.close()
+        res = [None] * world
+        dist.all_gather_object(res, ok)
+        if rank == 0:
+            q.put(all(res))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put(repr(e))
+        raise
+
+
+@pytest.mark.parametrize("same_device", [True, False])
+def test_two_process_halo_comm_gmres(same_device):
+    """Two processes exchange halos and reduce through CUDA IPC mappings: on
+    one device (always runnable) and on two distinct devices over NVLink
+    (skipped unless two GPUs are visible)."""
+    if not same_device and torch.cuda.device_count() < 2:
+        pytest.skip("needs two visible GPUs (peer stores over NVLink)")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_xdev_worker, args=(r, 2, port, q, same_device)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    assert res is True, res
