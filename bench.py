@@ -314,7 +314,7 @@ def run_nsm(args, rank, nranks, local_rank):
     S = nsm.Smoother(A, F, device=local_rank, rank=rank, nranks=nranks, row_offsets=offsets)
     S.set_pipeline(not args.plain)
     if args.fused != "default":
-        S.set_fused({"auto": 2, "on": 1, "off": 0}[args.fused])
+        S.set_fused({"auto": 2, "on": 1, "off": 0, "onepass": 3}[args.fused])
     if args.pdl != "auto":
         S.set_pdl(args.pdl == "on")
     if args.window == "off":
@@ -491,7 +491,7 @@ def main():
                     help="programmatic dependent launch (auto: the library's size-based default)")
     ap.add_argument("--window", default="on", choices=["on", "off"],
                     help="shared-memory gather windows in the pipelined kernels (offset-aligned parts)")
-    ap.add_argument("--fused", default="default", choices=["default", "auto", "on", "off"],
+    ap.add_argument("--fused", default="default", choices=["default", "auto", "on", "off", "onepass"],
                     help="phase-skewed fused passes (default: the library's default, per-pass kernels; "
                          "auto: fused on large problems)")
     ap.add_argument("--same-device", action="store_true",

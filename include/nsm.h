@@ -376,6 +376,12 @@ const char *nsm_last_error(const nsm_handle *h);
  *                           per-pass kernels.  Switching it
  *                           on allocates the passes' L2 ring buffers (up to
  *                           ~9 n-vectors; NSM_ERR_OOM if that fails).
+ *                           3 = as 1, and a forward pGS application on a
+ *                           stencil-like matrix (offset-aligned L and U with
+ *                           gather windows) runs as ONE windowed pass with
+ *                           per-phase readiness (fused_w.cu; experimental:
+ *                           reads the matrix from HBM once but is slower,
+ *                           DESIGN.md §6).
  *   NSM_OPT_FUSED_WINDOW    wait distance Dw of the fused passes in work
  *                           items (0 = automatic, about the items in flight);
  *                           a small value forces frequent waits and ring
@@ -504,6 +510,13 @@ nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F
 nsm_status nsm_part_info(const nsm_handle *h, int part, int64_t *padded, int64_t *nnz, int *maxw, int *aligned);
 nsm_status nsm_part_copy(const nsm_handle *h, int part, int64_t *ptr, int32_t *col, double *val, int32_t *off);
 nsm_status nsm_diag_copy(const nsm_handle *h, int which, double *out);
+
+/* nsm_fused_counters: cumulative counters of the one-pass windowed pGS
+ * (NSM_OPT_FUSED on stencil-like matrices), summed over its CTAs' producer
+ * warps: out[0] synchronous frontier polls, [1] their ns, [2] ns waiting for a
+ * free stage, [3] ns in readiness checks, [4] ns per unit in total, [5]
+ * acquire fences.  Diagnostics; out has 6 entries. */
+nsm_status nsm_fused_counters(const nsm_handle *h, int64_t *out);
 
 /* Frees all device memory of the handle (synchronises its device).  NULL ok. */
 void nsm_destroy(nsm_handle *h);

@@ -27,7 +27,8 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual
                   "nsm_fused_stats", "nsm_layout", "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect",
                   "nsm_comm_connect_ipc", "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout",
                   "nsm_comm_stats", "nsm_comm_last_error", "nsm_comm_destroy", "nsm_set_comm", "nsm_ruiz_dep",
-                  "nsm_dep", "nsm_setup_device", "nsm_part_info", "nsm_part_copy", "nsm_diag_copy"])
+                  "nsm_dep", "nsm_setup_device", "nsm_part_info", "nsm_part_copy", "nsm_diag_copy",
+                  "nsm_fused_counters"])
 
 
 class NsmError(RuntimeError):
@@ -128,6 +129,7 @@ def load(variant: str = ""):
     L.nsm_part_info.argtypes = [vp, ci, P(i64), P(i64), P(ci), P(ci)]
     L.nsm_part_copy.argtypes = [vp, ci, vp, vp, vp, vp]
     L.nsm_diag_copy.argtypes = [vp, ci, vp]
+    L.nsm_fused_counters.argtypes = [vp, vp]
     for name in ["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
                  "nsm_smooth_host", "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
@@ -135,7 +137,8 @@ def load(variant: str = ""):
                  "nsm_gmres", "nsm_profile", "nsm_ilut", "nsm_ruiz", "nsm_set_ruiz", "nsm_fused_stats", "nsm_layout",
                  "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect", "nsm_comm_connect_ipc",
                  "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout", "nsm_comm_stats", "nsm_set_comm",
-                 "nsm_ruiz_dep", "nsm_dep", "nsm_setup_device", "nsm_part_info", "nsm_part_copy", "nsm_diag_copy"]:
+                 "nsm_ruiz_dep", "nsm_dep", "nsm_setup_device", "nsm_part_info", "nsm_part_copy", "nsm_diag_copy",
+                 "nsm_fused_counters"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -542,7 +545,8 @@ class Smoother:
 
     def set_fused(self, mode):
         """Phase-skewed fused passes: False/0 off (the default), True/1 whenever
-        possible, 2 = automatic (large problems)."""
+        possible, 2 = automatic (large problems), 3 = as 1 plus the one-pass
+        windowed pGS on stencil-like matrices (experimental)."""
         self._call(load().nsm_set_option(self._h, 2, int(mode)))
 
     def set_fused_window(self, items: int):
@@ -580,6 +584,12 @@ class Smoother:
         w, t = ctypes.c_int64(0), ctypes.c_int64(0)
         self._call(load().nsm_fused_stats(self._h, ctypes.byref(w), ctypes.byref(t)))
         return int(w.value), int(t.value)
+
+    def fused_counters(self) -> np.ndarray:
+        """nsm_fused_counters: polls, poll ns, stage-wait ns, readiness ns, unit ns, fences."""
+        out = np.zeros(6, dtype=np.int64)
+        self._call(load().nsm_fused_counters(self._h, out.ctypes.data))
+        return out
 
     def set_halo_timeout(self, ms: int):
         """How long a halo wait spins before reporting NSM_ERR_DIST."""

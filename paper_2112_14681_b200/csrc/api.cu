@@ -41,6 +41,12 @@ struct nsm_handle {
     uint64_t cfg_gen = 0;  // bumped by nsm_set_option / nsm_set_ruiz (captured graphs compare it)
     nsm_comm *comm = nullptr;  // borrowed cross-rank reduction (nsm_set_comm), distributed solver layer
     Window res_win;            // gather window of the residual (L and U together), single rank
+    // one-pass windowed pGS (fused_w.cu): rings, per-phase progress, launch state
+    bool fw_ready = false;
+    double *fw_ring_r = nullptr, *fw_ring_g = nullptr;
+    int64_t fw_Mr = 0, fw_Mg = 0;
+    unsigned long long *fw_prog = nullptr;
+    unsigned int *fw_sync = nullptr;
     bool window = true;        // NSM_OPT_WINDOW: windowed pipelined kernels where a window exists
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
@@ -209,6 +215,10 @@ void free_handle(nsm_handle *h) {
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
     cudaFree(h->ring_r);
     cudaFree(h->ring_g);
+    cudaFree(h->fw_ring_r);
+    cudaFree(h->fw_ring_g);
+    cudaFree(h->fw_prog);
+    cudaFree(h->fw_sync);
     cudaFree(h->skew_sync);
     cudaFree(h->skew_prog);
     cudaFree(h->hb_dev);
@@ -416,7 +426,40 @@ size_t flags_bytes_for(int nranks) { return (((size_t)nranks * 8 + 255) / 256) *
 
 // Rings, progress counters and launch state of the fused passes, sized for
 // the largest shape any k <= kFusedKmax can need (single rank; once).
+// Rings and counters of the one-pass windowed pGS (fused_w.cu), sized for
+// k <= kMaxPhW - 1: single rank, offset-aligned L and U with gather windows.
+constexpr int64_t kFwProgStride = 1024;
+static bool fw_possible(const nsm_handle *h) {
+    return h->fused_possible && h->L.off && h->U.off && h->res_win.wmax && h->L.win.wmax;
+}
+static FusedWShape fw_shape(const nsm_handle *h, int k) {
+    return fused_w_shape(std::max(h->L.maxw, h->U.maxw), std::max(h->res_win.wmax, h->L.win.wmax), k, h->n, h->DLA,
+                         std::max(h->DLA, h->DUA), h->skew_dw);
+}
+static nsm_status fw_alloc(nsm_handle *h) {
+    if (h->fw_ready || !fw_possible(h)) return NSM_OK;
+    const FusedWShape sh = fw_shape(h, kMaxPhW - 1);
+    if (!sh.ok || sh.grid > kFwProgStride) return NSM_OK;
+    DevAlloc a{h};
+    const unsigned int init[16] = {1u};
+    const bool ok = a.get(&h->fw_ring_r, sh.Mr * 256) && a.get(&h->fw_ring_g, (int64_t)(kMaxPhW - 1) * sh.Mg * 256) &&
+                    a.get(&h->fw_prog, kMaxPhW * kFwProgStride) && a.get(&h->fw_sync, 16) &&
+                    cudaMemset(h->fw_prog, 0, kMaxPhW * kFwProgStride * sizeof(unsigned long long)) == cudaSuccess &&
+                    cudaMemcpy(h->fw_sync, init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        h->err = "NSM_OPT_FUSED: device allocation of the one-pass rings failed";
+        return NSM_ERR_OOM;
+    }
+    h->fw_Mr = sh.Mr;
+    h->fw_Mg = sh.Mg;
+    h->fw_ready = true;
+    return NSM_OK;
+}
+
 static nsm_status fused_alloc(nsm_handle *h) {
+    const nsm_status fst = fw_alloc(h);
+    if (fst != NSM_OK) return fst;
     if (h->fused_ready || !h->fused_possible) return NSM_OK;
     cudaSetDevice(h->device);
     const int64_t tr = skew_tile_rows();
@@ -555,6 +598,7 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     preload_tma_kernels();
     preload_halo_kernels();
     preload_fused_kernels();
+    preload_fused_w_kernels();
     nsm_handle *h = new nsm_handle();
     h->uid = next_handle_uid();
     h->device = device;
@@ -666,6 +710,7 @@ nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F
     preload_tma_kernels();
     preload_halo_kernels();
     preload_fused_kernels();
+    preload_fused_w_kernels();
     nsm_handle *h = new nsm_handle();
     h->uid = next_handle_uid();
     h->device = device;
@@ -883,7 +928,7 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
     switch (opt) {
         case NSM_OPT_PIPELINE: h->pipeline = value != 0; return NSM_OK;
         case NSM_OPT_FUSED:
-            if (value < 0 || value > 2) return NSM_ERR_ARG;
+            if (value < 0 || value > 3) return NSM_ERR_ARG;
             h->fused_mode = (int)value;
             return value ? fused_alloc(h) : NSM_OK;
         case NSM_OPT_FUSED_WINDOW:
@@ -1000,13 +1045,33 @@ nsm_status nsm_fused_stats(nsm_handle *h, int64_t *waits, int64_t *wait_ns) {
     if (!h || !waits || !wait_ns) return NSM_ERR_ARG;
     *waits = 0;
     *wait_ns = 0;
-    if (!h->skew_sync) return NSM_OK;
-    cudaSetDevice(h->device);
-    SkewSync v{};
-    cudaError_t e = cudaMemcpy(&v, h->skew_sync, sizeof(v), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_fail(h, e, "nsm_fused_stats");
-    *waits = (int64_t)v.waits;
-    *wait_ns = (int64_t)v.wait_ns;
+    DeviceScope dev(h->device);
+    if (h->skew_sync) {
+        SkewSync v{};
+        cudaError_t e = cudaMemcpy(&v, h->skew_sync, sizeof(v), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(h, e, "nsm_fused_stats");
+        *waits += (int64_t)v.waits;
+        *wait_ns += (int64_t)v.wait_ns;
+    }
+    if (h->fw_sync) {  // one-pass windowed kernel: the producer's frontier polls
+        unsigned long long v[4] = {0, 0, 0, 0};
+        cudaError_t e = cudaMemcpy(v, h->fw_sync, sizeof(v), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(h, e, "nsm_fused_stats");
+        *waits += (int64_t)v[2];
+        *wait_ns += (int64_t)v[3];
+    }
+    return NSM_OK;
+}
+
+nsm_status nsm_fused_counters(const nsm_handle *h, int64_t *out) {
+    if (!h || !out) return NSM_ERR_ARG;
+    for (int i = 0; i < 6; ++i) out[i] = 0;
+    if (!h->fw_sync) return NSM_OK;
+    DeviceScope dev(h->device);
+    unsigned long long v[8] = {};
+    if (cudaMemcpy(v, h->fw_sync, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return NSM_ERR_CUDA;
+    for (int i = 0; i < 6; ++i) out[i] = (int64_t)v[2 + i];
     return NSM_OK;
 }
 
@@ -1136,6 +1201,46 @@ static nsm_status skew_run(nsm_handle *h, SkewLaunch &L, bool unit, int DT, int 
 // One smoother application of the given kind (rows a2-a5).  fresh: x is
 // taken as 0 (its contents are ignored), so the residual is b (reading R3)
 // and the last kernel STORES x instead of adding to it.
+// One pGS application as ONE windowed pass (fused_w.cu), when the handle has
+// the rings (NSM_OPT_FUSED) and the matrix is stencil-like.
+static nsm_status fused_w_run(nsm_handle *h, const double *b, double *x, int k, bool fresh, cudaStream_t s, bool *ran) {
+    *ran = false;
+    if (!h->fw_ready || h->fused_mode != 3 || !h->pipeline || !h->window || k < 1 || k > kMaxPhW - 1 || h->n == 0)
+        return NSM_OK;
+    FusedWLaunch L{};
+    L.shape = fw_shape(h, k);
+    const FusedWShape &sh = L.shape;
+    if (!sh.ok || sh.Mr > h->fw_Mr || sh.Mg > h->fw_Mg || sh.grid > kFwProgStride) return NSM_OK;
+    L.n = h->n;
+    L.k = k;
+    L.DT = h->DLA;
+    L.DA = std::max(h->DLA, h->DUA);
+    L.fresh = fresh ? 1 : 0;
+    L.Lp = &h->L;
+    L.Up = &h->U;
+    L.wres = &h->res_win;
+    L.wl = &h->L.win;
+    L.d = h->d;
+    L.b = b;
+    L.x = x;
+    L.ring_r = h->fw_ring_r;
+    L.ring_g = h->fw_ring_g;
+    L.prog = h->fw_prog;
+    L.pstride = kFwProgStride;
+    L.flag = h->flag;
+    L.sweep_id0 = h->sweep_counter + 1;
+    h->sweep_counter += k;
+    L.err = h->d_dist_err;
+    L.timeout_ns = h->timeout_ns;
+    L.sync = h->fw_sync;
+    ProfScope prof(h, 2, s);
+    const cudaError_t e = launch_fused_w(L, s);
+    ++h->launches;
+    if (e != cudaSuccess) return cuda_fail(h, e, "one-pass fused launch");
+    *ran = true;
+    return NSM_OK;
+}
+
 static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, double *x, int k_l, int k_u, bool fresh,
                              cudaStream_t s) {
     double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
@@ -1149,6 +1254,10 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
     }
     if (kind == NSM_PGS || kind == NSM_PGS_BACKWARD) {
         const bool fwd = kind == NSM_PGS;
+        if (fwd && k_l >= 1) {  // stencil-like matrices: the one-pass windowed kernel
+            st = fused_w_run(h, b, x, k_l, fresh, s, &ran);
+            if (st != NSM_OK || ran) return st;
+        }
         if (k_l >= 1) {
             // rows a2-a4 in ONE pass over the matrix: residual, k sweeps, x update
             SkewLaunch L{};

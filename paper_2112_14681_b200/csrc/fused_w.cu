@@ -1,0 +1,675 @@
+// fused_w.cu — one-pass pGS application for offset-aligned (stencil-like)
+// matrices with gather windows: the residual, the k Jacobi sweeps and the x
+// update in ONE launch that reads each matrix entry from HBM about once
+// (SURVEY.md §7.3, §8(d) "fused floor"; the pGS application of P:L743-785):
+//
+//   phase 0 (tile u):  r = b - A x,  g(0) = r / d        (eq:jr-initial-guess)
+//   phase j (tile u):  g(j) = (r - L g(j-1)) / d         (eq:jacobi), j = 1..k
+//                      the last one x += g(k)
+//
+// Dependencies.  Phase j of 256-row tile u needs phase j-1 of the tiles
+// within L's bandwidth below it, [u - DT, u].  Work item w bundles phase j of
+// tile w - jD, j = 0..k (D > DT); items are dealt round-robin to a
+// cooperative grid (item w to CTA w mod G) and every CTA runs its items'
+// units in (item, phase) order.
+//
+// Readiness is tracked PER PHASE: prog[j][c] counts the items of CTA c whose
+// phase-j unit is complete, so "phase j done for all items < F_j" with
+// F_j = min_c (c + count_j(c) G).  Before staging unit (j, u) of item w the
+// producer warp requires
+//   F_{j-1} > w - D                        (its gathered iterate g(j-1) and r)
+//   F_0 > u + DA            (j = k)        (x of tile u: every residual reading it is done)
+//   F_{j+1} > u - Mg + DT + (j+1) D (j < k) (the ring slot it writes is no longer read)
+//   F_k > u - Mr + kD       (j = 0)        (the r slot it writes is no longer read)
+// each a statement about strictly earlier (item, phase) pairs, so the lowest
+// unfinished unit can always proceed (deadlock-free with all CTAs resident).
+// With per-phase frontiers D need only exceed DT by a small margin: the
+// matrix rows a later phase re-reads were streamed about k D tiles earlier
+// (C3: ~2 planes, ~30 MB) and are still in L2, and the iterates live in
+// L2-resident rings of a few MB.
+//
+// Data movement (all through shared memory, no gathers from global memory):
+// the producer warp stages, per unit, the tile's values of L (and U for
+// phase 0), the window positions and slice geometry, and the gather window —
+// of x for phase 0 (builder.cpp's residual window), of the ring g(j-1) for a
+// sweep (the L window mapped into the ring) — with cp.async.bulk, after the
+// readiness wait (acquire + proxy fence: the ring was written by other CTAs
+// through the generic proxy).  Consumers (one row per thread) read own-row
+// vectors directly, multiply values by window entries and add in stored
+// order: the same arithmetic as the per-pass kernels and the oracle, so
+// results are bit-identical.  Each unit is published by the last consumer
+// warp to finish it (CTA-scope acq_rel count, then red.release.gpu).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <climits>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "nsm_internal.h"
+#include "ptx.cuh"
+
+namespace nsm {
+
+namespace {
+
+constexpr int kWC = 8;                    // consumer warps = slices per tile
+constexpr int kRowsW = kWC * kSlice;      // 256 rows per tile (the window plans' tiles)
+constexpr int kThreadsW = (kWC + 1) * 32;
+constexpr int kMaxStW = 4;
+constexpr int kHdrW = 256;                // barriers, counters, unit descriptors
+constexpr int64_t kSmemMaxW = 220 * 1024;
+
+struct FwParams {
+    int64_t n, nslices, ntiles, nitems;
+    int k, D, DT, DA, fresh, maxph;
+    int64_t Mr, Mg;                // ring lengths in tiles (powers of two)
+    SellView L, U;
+    WinView WR, WL;                // residual window (L, U), L-sweep window
+    const double *d, *b;
+    double *x;
+    double *ring_r, *ring_g;       // ring_g: k rings of Mg tiles each
+    unsigned long long *prog;      // [kMaxPhW][pstride] per-CTA progress per phase
+    int64_t pstride;
+    unsigned long long *flag;
+    int64_t sweep_id0;
+    unsigned int *err;
+    unsigned long long timeout_ns;
+    unsigned int *sync;            // [0] epoch, [1] CTAs finished, [4..5] polls, [6..7] poll ns (u64)
+    int nst;
+    int64_t cap;                   // entries per part per stage
+    int64_t wcap;                  // window doubles per stage
+    int64_t stage_bytes;
+};
+
+struct UDescW {
+    int u;        // tile, -1: empty unit
+    int j;
+};
+
+__device__ __forceinline__ uint64_t *fullb(char *s) { return (uint64_t *)s; }
+__device__ __forceinline__ uint64_t *emptyb(char *s) { return (uint64_t *)s + kMaxStW; }
+__device__ __forceinline__ unsigned int *pubc(char *s) { return (unsigned int *)(s + 2 * kMaxStW * 8); }
+__device__ __forceinline__ UDescW *udw(char *s) { return (UDescW *)(s + 2 * kMaxStW * 8 + kMaxStW * 4); }
+
+struct StageW {
+    char *base;
+    int64_t cap;
+    __device__ __forceinline__ double *val(int p) const { return (double *)base + (int64_t)p * cap; }
+    __device__ __forceinline__ int32_t *pos(int p) const {
+        return (int32_t *)(base + 2 * cap * 8) + (int64_t)p * (cap / kSlice);
+    }
+    __device__ __forceinline__ int2 *hdr(int p) const {
+        return (int2 *)(base + 2 * cap * 8 + ((2 * (cap / kSlice) * 4 + 15) / 16) * 16) + p * kWC;
+    }
+    __device__ __forceinline__ double *win() const {
+        return (double *)(base + 2 * cap * 8 + ((2 * (cap / kSlice) * 4 + 15) / 16) * 16 + 2 * kWC * 8);
+    }
+};
+__host__ __device__ inline int64_t stage_bytes_w(int64_t cap, int64_t wcap) {
+    return ((2 * cap * 8 + ((2 * (cap / kSlice) * 4 + 15) / 16) * 16 + 2 * kWC * 8 + wcap * 8) + 127) / 128 * 128;
+}
+__device__ __forceinline__ StageW stage_w(char *sm, const FwParams &p, int st) {
+    return StageW{sm + kHdrW + (int64_t)st * p.stage_bytes, p.cap};
+}
+
+// all items < F have their phase-ph unit complete (acquire reads)
+__device__ __forceinline__ int64_t frontier(const FwParams &p, int ph, unsigned int epoch, int lane) {
+    const int64_t G = gridDim.x;
+    int64_t f = INT64_MAX;
+    const unsigned long long *pr = p.prog + (int64_t)ph * p.pstride;
+    for (int64_t c = lane; c < G; c += 32) {
+        const unsigned long long v = ptx::ld_acquire_gpu_u64(pr + c);
+        const int64_t cnt = (unsigned int)(v >> 32) == epoch ? (int64_t)(v & 0xffffffffull) : 0;
+        f = min(f, c + cnt * G);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) f = min(f, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)f, o));
+    return f;
+}
+
+// Bulk copy of the 16-byte-aligned part [a, e & ~1) of a window piece (a
+// even; the odd last element, if any, is written by the caller before the
+// stage's arrival).  Ring sources map row q to ring[q & mask]; a piece never
+// crosses the ring end (split by the caller).
+__device__ __forceinline__ uint32_t copy_piece(double *wslot, const double *src, int64_t a, int64_t e, uint64_t *bar,
+                                               uint64_t pol) {
+    if (e <= a) return 0;
+    const int64_t be = e & ~(int64_t)1;
+    if (be > a) {
+        ptx::bulk_g2s(wslot, src, (uint32_t)((be - a) * 8), bar, pol);
+        return (uint32_t)((be - a) * 8);
+    }
+    return 0;
+}
+
+template <int CH>
+struct WinSum {
+    // sum_j val[j] * win[pos[j] + lane] over the slice's entries, in stored
+    // order (products of the first CH issued together)
+    __device__ __forceinline__ static double run(const double *sv, const int32_t *wp, const double *ws, int w,
+                                                 double acc) {
+        double v[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) v[j] = __dmul_rn(sv[j * kSlice], ws[wp[j]]);
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j < w) acc = __dadd_rn(acc, v[j]);
+        for (int j = CH; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn(sv[j * kSlice], ws[wp[j]]));
+        return acc;
+    }
+};
+
+template <int CH>
+__global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_constant__ FwParams p) {
+    extern __shared__ __align__(128) char sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    const unsigned int epoch = *(volatile unsigned int *)&p.sync[0];
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < p.nst; ++st) {
+            ptx::mbar_init(fullb(sm) + st, 1);
+            ptx::mbar_init(emptyb(sm) + st, kWC);
+            pubc(sm)[st] = 0;
+        }
+        ptx::mbar_init_fence();
+    }
+    __syncthreads();
+    const int K = p.k;
+    const int64_t NT = p.ntiles;
+    const int64_t rmask = p.Mr * kRowsW - 1, gmask = p.Mg * kRowsW - 1;
+
+    if (warp == kWC) {
+        // ------------------------------------------------------------ producer
+        // Unit metadata is software-pipelined: the slice pointers and window
+        // segment range of unit N+2 and the dependent loads (window
+        // positions, segments) of unit N+1 are in flight while unit N is
+        // staged, so no global round trip sits on the per-unit path.
+        const uint64_t pol_first = ptx::policy_evict_first(), pol_keep = ptx::policy_evict_normal();
+        // F[q]: phase q is done for all items < F[q].  The progress counters
+        // are read with ld.acquire (no fence draining the producer's prefetch
+        // loads; the reads order everything this warp does afterwards — across
+        // lanes through __syncwarp); a proxy fence orders the following bulk
+        // copies (async proxy) after them.  Every unit refreshes one phase's
+        // view asynchronously (counter loads issued at the end of one unit,
+        // reduced at the end of the next), so the producer rarely waits.
+        int64_t F[kMaxPhW];
+#pragma unroll
+        for (int q = 0; q < kMaxPhW; ++q) F[q] = 0;
+        bool proxy_dirty = false;
+        int st = 0;
+        uint32_t round = 0;
+        unsigned long long polls = 0, poll_ns = 0, t_empty = 0, t_need = 0, t_all = 0, n_acq = 0;
+        auto need = [&](int ph, int64_t t) {  // phase ph done for every item <= t
+            if (t < F[ph]) return;
+            const uint64_t t0 = ptx::globaltimer_ns();
+            ++polls;
+            while (true) {
+                F[ph] = max(F[ph], frontier(p, ph, epoch, lane));
+                if (t < F[ph]) break;
+                if (ptx::globaltimer_ns() - t0 > p.timeout_ns) {
+                    if (lane == 0) atomicOr(p.err, 2u);
+                    F[ph] = INT64_MAX;
+                    break;
+                }
+                __nanosleep(64);
+            }
+            proxy_dirty = true;
+            poll_ns += ptx::globaltimer_ns() - t0;
+        };
+        // asynchronous refresh: counters of phase rph loaded (acquire) at the
+        // end of one unit, reduced into F[rph] at the end of the next
+        constexpr int kPR = 8;   // counters per lane (grids <= 256 CTAs)
+        unsigned long long rv[kPR];
+        int rph = -1;
+        auto refresh_issue = [&](int ph) {
+            rph = ph;
+            const unsigned long long *pr = p.prog + (int64_t)ph * p.pstride;
+#pragma unroll
+            for (int r = 0; r < kPR; ++r) {
+                const int64_t cc = lane + 32 * r;
+                rv[r] = cc < G ? ptx::ld_acquire_gpu_u64(pr + cc) : 0ull;
+            }
+        };
+        auto refresh_reduce = [&]() {
+            if (rph < 0) return;
+            int64_t f = INT64_MAX;
+#pragma unroll
+            for (int r = 0; r < kPR; ++r) {
+                const int64_t cc = lane + 32 * r;
+                if (cc < G) {
+                    const int64_t cnt = (unsigned int)(rv[r] >> 32) == epoch ? (int64_t)(rv[r] & 0xffffffffull) : 0;
+                    f = min(f, cc + cnt * G);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) f = min(f, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)f, o));
+            if (f > F[rph]) {
+                F[rph] = f;
+                proxy_dirty = true;
+            }
+            rph = -1;
+        };
+        // unit sequence of this CTA: (w, j), w = c + m G, j = 0..K
+        struct Meta {
+            int64_t w, u;
+            int j;
+            bool live, valid;
+            int64_t pv;                 // lanes 0..8: part-0 slice pointers, 16..24: part 1
+            int32_t g0, g1;             // window segment range
+            int32_t pos[2][4];          // window positions (first 128 entry positions of each part)
+            int64_t sg_lo;
+            int32_t sg_len, sg_base;
+        };
+        auto advance = [&](int64_t &w, int &j) {
+            if (++j > K) { j = 0; w += G; }
+        };
+        auto load1 = [&](Meta &M, int64_t w, int j) {  // independent loads
+            M.w = w;
+            M.j = j;
+            M.live = w < p.nitems;
+            M.u = w - (int64_t)j * p.D;
+            M.valid = M.live && M.u >= 0 && M.u < NT;
+            M.pv = 0;
+            M.g0 = M.g1 = 0;
+            if (!M.valid) return;
+            const int np = j == 0 ? 2 : 1;
+            const int part = lane >> 4, sl = lane & 15;
+            const int64_t s0 = M.u * kWC, s1 = min(s0 + kWC, p.nslices);
+            if (sl <= kWC && part < np) M.pv = __ldg((part == 0 ? p.L.ptr : p.U.ptr) + min(s0 + sl, s1));
+            const WinView &W = j == 0 ? p.WR : p.WL;
+            M.g0 = __ldg(W.tseg + M.u);
+            M.g1 = __ldg(W.tseg + M.u + 1);
+        };
+        auto load2 = [&](Meta &M) {  // loads that depend on load1's
+            if (!M.valid) return;
+            const int np = M.j == 0 ? 2 : 1;
+            const WinView &W = M.j == 0 ? p.WR : p.WL;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int64_t bq = __shfl_sync(0xffffffffu, M.pv, 16 * q), eq = __shfl_sync(0xffffffffu, M.pv, 16 * q + kWC);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int64_t e = lane + 32 * r;
+                    M.pos[q][r] = (q < np && e < (eq - bq) / kSlice) ? __ldg(W.wpos[q] + bq / kSlice + e) : 0;
+                }
+            }
+            if (lane < M.g1 - M.g0) {
+                M.sg_lo = __ldg(W.glo + M.g0 + lane);
+                M.sg_len = __ldg(W.len + M.g0 + lane);
+                M.sg_base = __ldg(W.sbase + M.g0 + lane);
+            }
+        };
+        Meta m1, m2, m3;
+        int64_t wn = c;
+        int jn = 0;
+        load1(m1, wn, jn);
+        advance(wn, jn);
+        load1(m2, wn, jn);
+        advance(wn, jn);
+        load2(m1);
+        // one unit: loads for the units two and one ahead are issued first;
+        // the three Meta records rotate roles (no register copies, so the
+        // loads' latency overlaps a whole unit)
+        auto step = [&](Meta &cur, Meta &nx1, Meta &nx2) -> bool {
+            if (!cur.live) return false;
+            load1(nx2, wn, jn);  // unit N+2
+            advance(wn, jn);
+            load2(nx1);          // unit N+1 (its slice pointers arrived during unit N-1)
+            const int j = cur.j;
+            const int64_t w = cur.w, u = cur.u;
+            const uint64_t tA = ptx::globaltimer_ns();
+            if (round > 0) ptx::mbar_wait(emptyb(sm) + st, (round - 1) & 1);
+            const uint64_t tB = ptx::globaltimer_ns();
+            t_empty += tB - tA;
+            if (!cur.valid) {
+                if (lane == 0) {
+                    udw(sm)[st] = UDescW{-1, j};
+                    ptx::mbar_arrive(fullb(sm) + st);
+                }
+                __syncwarp();
+            } else {
+                if (j >= 1) need(j - 1, w - p.D);
+                if (j == K) need(0, u + p.DA);
+                if (j < K && u >= p.Mg) need(j + 1, u - p.Mg + p.DT + (int64_t)(j + 1) * p.D);
+                if (j == 0 && u >= p.Mr) need(K, u - p.Mr + (int64_t)K * p.D);
+                if (proxy_dirty) {  // the bulk copies below read what the new frontiers published
+                    __syncwarp();
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    proxy_dirty = false;
+                    ++n_acq;
+                }
+                const uint64_t tC = ptx::globaltimer_ns();
+                t_need += tC - tB;
+                const StageW S = stage_w(sm, p, st);
+                const int np = j == 0 ? 2 : 1;
+                const WinView &W = j == 0 ? p.WR : p.WL;
+                const int part = lane >> 4, sl = lane & 15;
+                const int64_t pnext = __shfl_down_sync(0xffffffffu, cur.pv, 1);
+                const int64_t b0 = __shfl_sync(0xffffffffu, cur.pv, 0), e0 = __shfl_sync(0xffffffffu, cur.pv, kWC);
+                const int64_t b1 = __shfl_sync(0xffffffffu, cur.pv, 16), e1 = __shfl_sync(0xffffffffu, cur.pv, 16 + kWC);
+                if (sl < kWC && part < np)
+                    S.hdr(part)[sl] = make_int2((int)(cur.pv - (part == 0 ? b0 : b1)), (int)((pnext - cur.pv) / kSlice));
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    if (q >= np) break;
+                    const int64_t bq = q == 0 ? b0 : b1, ne = ((q == 0 ? e0 : e1) - bq) / kSlice;
+                    int32_t *sp = S.pos(q);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (lane + 32 * r < ne) sp[lane + 32 * r] = cur.pos[q][r];
+                    for (int64_t e = lane + 128; e < ne; e += 32) sp[e] = __ldg(W.wpos[q] + bq / kSlice + e);  // wide tiles
+                }
+                // window segments: lane k owns segment k
+                double *ws = S.win();
+                uint64_t *bar = fullb(sm) + st;
+                int64_t wa = 0, we = 0, wl0 = 0;
+                double *wdst = nullptr;
+                if (lane < cur.g1 - cur.g0 && !(j == 0 && p.fresh)) {  // (x = 0: no residual, no window)
+                    const int64_t lo = cur.sg_lo, hi = lo + cur.sg_len;
+                    wdst = ws + cur.sg_base;
+                    wl0 = lo;
+                    const int64_t a = max(lo, (int64_t)0), e = min(hi, p.n);
+                    for (int64_t q = lo; q < min(a, hi); ++q) wdst[q - lo] = 0.0;   // below row 0
+                    for (int64_t q = max(e, lo); q < hi; ++q) wdst[q - lo] = 0.0;  // past row n - 1
+                    wa = a;
+                    we = e;
+                    if (e > a && (e & 1)) {  // odd n: the last element by a plain load (the only odd end)
+                        const double *src = j == 0 ? p.x + (e - 1)
+                                                   : p.ring_g + (int64_t)(j - 1) * p.Mg * kRowsW + ((e - 1) & gmask);
+                        wdst[e - 1 - lo] = __ldcg(src);
+                    }
+                }
+                // bytes of the bulk copies (matrix values, window pieces)
+                const int64_t rl = p.Mg * kRowsW;
+                int64_t cut = we;
+                uint32_t wbytes = 0;
+                if (we > wa) {
+                    if (j == 0) {
+                        const int64_t be = we & ~(int64_t)1;
+                        wbytes = be > wa ? (uint32_t)((be - wa) * 8) : 0;
+                    } else {  // ring pieces: split where the ring wraps
+                        cut = min(we, (wa / rl + 1) * rl);
+                        const int64_t be1 = cut & ~(int64_t)1, be2 = we & ~(int64_t)1;
+                        wbytes = (be1 > wa ? (uint32_t)((be1 - wa) * 8) : 0) + (be2 > cut ? (uint32_t)((be2 - cut) * 8) : 0);
+                    }
+                }
+                uint32_t wsum = wbytes;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+                __syncwarp();
+                if (lane == 0) {
+                    udw(sm)[st] = UDescW{(int)u, j};
+                    const uint32_t mbytes = (uint32_t)((e0 - b0) * 8 + (np == 2 ? (e1 - b1) * 8 : 0));
+                    ptx::mbar_expect_tx(bar, mbytes + wsum);
+                    // L's values are re-read by the later phases: keep them in L2
+                    if (e0 > b0)
+                        ptx::bulk_g2s(S.val(0), p.L.val + b0, (uint32_t)((e0 - b0) * 8), bar, j < K ? pol_keep : pol_first);
+                    if (np == 2 && e1 > b1)
+                        ptx::bulk_g2s(S.val(1), p.U.val + b1, (uint32_t)((e1 - b1) * 8), bar, pol_first);
+                }
+                __syncwarp();
+                if (we > wa) {
+                    if (j == 0) {
+                        copy_piece(wdst + (wa - wl0), p.x + wa, wa, we, bar, pol_keep);
+                    } else {
+                        const double *ring = p.ring_g + (int64_t)(j - 1) * rl;
+                        copy_piece(wdst + (wa - wl0), ring + (wa & gmask), wa, cut, bar, pol_keep);
+                        if (we > cut) copy_piece(wdst + (cut - wl0), ring + (cut & gmask), cut, we, bar, pol_keep);
+                    }
+                }
+                __syncwarp();
+            }
+            refresh_reduce();    // the counters loaded during this unit
+            refresh_issue(j);
+            t_all += ptx::globaltimer_ns() - tA;
+            if (++st == p.nst) { st = 0; ++round; }
+            return true;
+        };
+        while (step(m1, m2, m3) && step(m2, m3, m1) && step(m3, m1, m2)) {
+        }
+        // end of the sequence
+        if (round > 0 || st > 0) {
+            if (round > 0) ptx::mbar_wait(emptyb(sm) + st, (round - 1) & 1);
+        }
+        if (lane == 0) {
+            udw(sm)[st] = UDescW{-2, 0};
+            ptx::mbar_arrive(fullb(sm) + st);
+            // statistics (nsm_fused_stats): frontier polls of the producer and their time
+            atomicAdd((unsigned long long *)(p.sync + 4), polls);
+            atomicAdd((unsigned long long *)(p.sync + 6), poll_ns);
+            atomicAdd((unsigned long long *)(p.sync + 8), t_empty);
+            atomicAdd((unsigned long long *)(p.sync + 10), t_need);
+            atomicAdd((unsigned long long *)(p.sync + 12), t_all);
+            atomicAdd((unsigned long long *)(p.sync + 14), n_acq);
+        }
+    } else {
+        // ----------------------------------------------------------- consumers
+        int st = 0;
+        uint32_t par = 0;
+        for (int64_t w = c, m = 0;; w += G, ++m) {
+            bool end = false;
+            for (int j = 0; j <= K; ++j) {
+                const int64_t u = w - (int64_t)j * p.D;
+                const bool valid = w < p.nitems && u >= 0 && u < NT;
+                const int64_t i = u * kRowsW + warp * kSlice + lane;
+                const bool row = valid && i < p.n;
+                // own-row vectors: immutable (d, b), or written only by this unit (x of tile u, j = K)
+                double di = 1.0, bi = 0.0, xi = 0.0;
+                if (row) {
+                    di = __ldg(p.d + i);
+                    if (j == 0) {
+                        bi = __ldg(p.b + i);
+                        if (!p.fresh) xi = __ldg(p.x + i);
+                    } else if (j == K && !p.fresh) {
+                        xi = p.x[i];
+                    }
+                }
+                ptx::mbar_wait(fullb(sm) + st, par);
+                const UDescW un = udw(sm)[st];
+                if (un.u == -2) { end = true; break; }
+                double res = 0.0;
+                if (un.u >= 0) {
+                    const StageW S = stage_w(sm, p, st);
+                    const double *ws = S.win() + lane;
+                    const int2 hl = S.hdr(0)[warp];
+                    if (j == 0) {
+                        if (p.fresh) {
+                            res = bi;  // x = 0: r = b (reading R3)
+                        } else {
+                            const int2 hu = S.hdr(1)[warp];
+                            double acc = 0.0;
+                            if (row) {
+                                acc = WinSum<CH>::run(S.val(0) + hl.x + lane, S.pos(0) + hl.x / kSlice, ws, hl.y, acc);
+                                acc = __dadd_rn(acc, __dmul_rn(di, xi));
+                                acc = WinSum<CH>::run(S.val(1) + hu.x + lane, S.pos(1) + hu.x / kSlice, ws, hu.y, acc);
+                            }
+                            res = __dsub_rn(bi, acc);
+                        }
+                    } else if (row) {
+                        res = WinSum<CH>::run(S.val(0) + hl.x + lane, S.pos(0) + hl.x / kSlice, ws, hl.y, 0.0);
+                    }
+                }
+                if (row) {
+                    if (j == 0) {
+                        p.ring_r[i & rmask] = res;
+                        p.ring_g[i & gmask] = __ddiv_rn(res, di);   // g(0) = D^{-1} r
+                    } else {
+                        const double ri = __ldcg(p.ring_r + (i & rmask));
+                        const double v = __ddiv_rn(__dsub_rn(ri, res), di);
+                        if (!isfinite(v)) atomicMin(p.flag, (unsigned long long)(p.sweep_id0 + j - 1));
+                        if (j < K) p.ring_g[(int64_t)j * p.Mg * kRowsW + (i & gmask)] = v;
+                        else p.x[i] = p.fresh ? v : __dadd_rn(xi, v);
+                    }
+                }
+                // publish "phase j of this CTA's items <= m is complete": the last
+                // warp to finish the unit (CTA-scope acq_rel count makes the
+                // other warps' stores visible to its gpu-scope release)
+                // (the stage is released after the count: a warp cannot reach the
+                // stage's next unit before every warp has counted this one)
+                __syncwarp();
+                if (lane == 0) {
+                    const unsigned int prev = ptx::atom_add_acqrel_cta_shared(pubc(sm) + st, 1u);
+                    if ((prev + 1) % kWC == 0)
+                        ptx::red_max_release_gpu_u64(p.prog + (int64_t)j * p.pstride + c,
+                                                     ((unsigned long long)epoch << 32) | (unsigned long long)(m + 1));
+                    ptx::mbar_arrive(emptyb(sm) + st);
+                }
+                if (++st == p.nst) { st = 0; par ^= 1; }
+            }
+            if (end) break;
+        }
+    }
+    // ---- the last CTA out advances the epoch for the next launch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(&p.sync[1], 1u);
+        if (prev == gridDim.x - 1) {
+            p.sync[1] = 0;
+            p.sync[0] = epoch + 1 == 0 ? 1 : epoch + 1;
+            __threadfence();
+        }
+    }
+}
+
+const void *pick_w(int ch) {
+    return ch <= 4 ? (const void *)k_fused_pgs_w<4> : (ch <= 8 ? (const void *)k_fused_pgs_w<8> : (const void *)k_fused_pgs_w<16>);
+}
+
+int sm_count_w() {
+    static int nsm[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!nsm[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        nsm[dev] = v > 0 ? v : 148;
+    }
+    return nsm[dev];
+}
+
+struct GeoW {
+    int nst = 0, per_sm = 0;
+    size_t smem = 0;
+};
+
+// stages: maximise co-resident CTAs (<= 2 by the launch bounds), then depth
+GeoW geometry_w(const void *k, int64_t stage_bytes) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void *, int64_t>, GeoW> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto key = std::make_tuple(dev, k, stage_bytes);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxW);
+    GeoW g;
+    int best = -1;
+    for (int nst = 2; nst <= kMaxStW; ++nst) {
+        const int64_t smem = kHdrW + nst * stage_bytes;
+        if (smem > kSmemMaxW) break;
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreadsW, (size_t)smem);
+        per = std::min(per, 1);  // one CTA per SM: its stages take most of the shared memory
+        if (per > 0 && per >= best) {
+            best = per;
+            g.nst = nst;
+            g.per_sm = per;
+            g.smem = (size_t)smem;
+        }
+    }
+    cache[key] = g;
+    return g;
+}
+
+int64_t pow2_ge(int64_t v) {
+    int64_t q = 1;
+    while (q < v) q <<= 1;
+    return q;
+}
+
+}  // namespace
+
+FusedWShape fused_w_shape(int maxw, int64_t wmax, int k, int64_t n, int DT, int DA, int d_extra) {
+    FusedWShape sh;
+    if (k < 1 || k > kMaxPhW - 1 || n <= 0) return sh;
+    const int ch = maxw <= 4 ? 4 : (maxw <= 8 ? 8 : 16);
+    const void *kern = pick_w(ch);
+    const int64_t cap = (int64_t)kRowsW * std::max(maxw, 1);
+    const int64_t wcap = (wmax + 31) / 32 * 32;
+    const int64_t sbytes = stage_bytes_w(cap, wcap);
+    const GeoW g = geometry_w(kern, sbytes);
+    if (!g.nst) return sh;
+    sh.ok = true;
+    sh.kernel = kern;
+    sh.nst = g.nst;
+    sh.smem = g.smem;
+    sh.cap = cap;
+    sh.wcap = wcap;
+    sh.stage_bytes = sbytes;
+    sh.ntiles = (n + kRowsW - 1) / kRowsW;
+    sh.grid = (int)std::min<int64_t>((int64_t)sm_count_w() * g.per_sm, std::max<int64_t>(sh.ntiles, 1));
+    sh.D = std::max(DT, DA) + (d_extra > 0 ? d_extra : 16);
+    sh.nitems = sh.ntiles + (int64_t)k * sh.D;
+    const int64_t tp2 = pow2_ge(sh.ntiles);
+    // rings (tiles): every slot's previous occupant is at least two grids of
+    // items older than the reuse conditions require
+    sh.Mr = std::min(pow2_ge((int64_t)k * sh.D + 2 * sh.grid + 1), tp2);
+    sh.Mg = std::min(pow2_ge((int64_t)sh.D + DT + 2 * sh.grid + 1), tp2);
+    return sh;
+}
+
+cudaError_t launch_fused_w(const FusedWLaunch &L, cudaStream_t st) {
+    const FusedWShape &sh = L.shape;
+    if (!sh.ok) return cudaErrorInvalidConfiguration;
+    FwParams p{};
+    p.n = L.n;
+    p.nslices = (L.n + kSlice - 1) / kSlice;
+    p.ntiles = sh.ntiles;
+    p.nitems = sh.nitems;
+    p.k = L.k;
+    p.D = sh.D;
+    p.DT = L.DT;
+    p.DA = L.DA;
+    p.fresh = L.fresh;
+    p.Mr = sh.Mr;
+    p.Mg = sh.Mg;
+    p.L = view(*L.Lp);
+    p.U = view(*L.Up);
+    auto wv = [&](const Window *w) {
+        return WinView{w->tseg, w->glo, w->len, w->sbase, {w->wpos[0], w->wpos[1]}, (int32_t)sh.wcap};
+    };
+    p.WR = wv(L.wres);
+    p.WL = wv(L.wl);
+    p.d = L.d;
+    p.b = L.b;
+    p.x = L.x;
+    p.ring_r = L.ring_r;
+    p.ring_g = L.ring_g;
+    p.prog = L.prog;
+    p.pstride = L.pstride;
+    p.flag = L.flag;
+    p.sweep_id0 = L.sweep_id0;
+    p.err = L.err;
+    p.timeout_ns = L.timeout_ns;
+    p.sync = L.sync;
+    p.nst = sh.nst;
+    p.cap = sh.cap;
+    p.wcap = sh.wcap;
+    p.stage_bytes = sh.stage_bytes;
+    void *args[] = {&p};
+    return cudaLaunchCooperativeKernel(sh.kernel, dim3((unsigned)sh.grid), dim3(kThreadsW), args, sh.smem, st);
+}
+
+void preload_fused_w_kernels() {
+    cudaFuncAttributes a;
+    for (int ch : {4, 8, 16}) cudaFuncGetAttributes(&a, pick_w(ch));
+}
+
+}  // namespace nsm

@@ -251,6 +251,40 @@ struct SkewLaunch {
 cudaError_t launch_skew(const SkewLaunch &L, cudaStream_t st);
 void preload_fused_kernels();
 
+// ---- one-pass windowed pGS (fused_w.cu) ---------------------------------------
+constexpr int kMaxPhW = 5;   // phases 0..k, k <= 4
+struct FusedWShape {
+    bool ok = false;
+    const void *kernel = nullptr;
+    int nst = 0, grid = 0, D = 0;
+    size_t smem = 0;
+    int64_t cap = 0, wcap = 0, stage_bytes = 0, ntiles = 0, nitems = 0;
+    int64_t Mr = 0, Mg = 0;   // ring lengths in 256-row tiles (powers of two)
+};
+// maxw: widest slice of L and U; wmax: largest window (residual or L);
+// DT, DA: bandwidths of L and A in 256-row tiles; d_extra: D - max(DT, DA)
+// (0 = automatic).
+FusedWShape fused_w_shape(int maxw, int64_t wmax, int k, int64_t n, int DT, int DA, int d_extra);
+struct FusedWLaunch {
+    FusedWShape shape;
+    int64_t n;
+    int k, DT, DA, fresh;
+    const Sell *Lp, *Up;
+    const Window *wres, *wl;
+    const double *d, *b;
+    double *x;
+    double *ring_r, *ring_g;
+    unsigned long long *prog;
+    int64_t pstride;
+    unsigned long long *flag;
+    int64_t sweep_id0;
+    unsigned int *err;
+    unsigned long long timeout_ns;
+    unsigned int *sync;
+};
+cudaError_t launch_fused_w(const FusedWLaunch &L, cudaStream_t st);
+void preload_fused_w_kernels();
+
 // Force-load every kernel of the library (see kernels.cu "eager loading").
 void preload_plain_kernels();
 void preload_tma_kernels();

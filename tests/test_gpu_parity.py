@@ -73,7 +73,7 @@ SMALL = {
 }
 
 
-KERNELS = ("fused", "fusedw1", "pipelined", "nowindow", "plain")
+KERNELS = ("fused", "fusedw1", "onepass", "onepassw1", "pipelined", "nowindow", "plain")
 
 
 def set_kernels(S, mode):
@@ -83,11 +83,12 @@ def set_kernels(S, mode):
     synchronisation); pipelined: one cp.async.bulk pipelined kernel per pass,
     gathering from shared-memory windows where the layout allows (the
     default); nowindow: the same gathering through L1/L2; plain:
-    register-blocked."""
+    register-blocked; onepass(w1): the one-pass windowed pGS (NSM_OPT_FUSED = 3)
+    where the matrix allows it, else as fused (w1: skew margin 1)."""
     S.set_pipeline(mode != "plain")
     S.set_window(mode != "nowindow")
-    S.set_fused(1 if mode.startswith("fused") else 0)
-    S.set_fused_window(1 if mode == "fusedw1" else 0)
+    S.set_fused(1 if mode.startswith("fused") else (3 if mode.startswith("onepass") else 0))
+    S.set_fused_window(1 if mode.endswith("w1") else 0)
 
 
 @pytest.fixture(scope="module", params=[(c, p) for c in SMALL for p in KERNELS], ids=lambda v: f"{v[0]}-{v[1]}")
@@ -268,3 +269,26 @@ def test_layout_choice_matches_host_mirror(case):
     name, A, F, S = case
     lay, want = S.layout(), bench.aligned_parts(A)
     assert lay["L"] == want["L"] and lay["U"] == want["U"], (name, lay, want)
+
+
+@pytest.mark.parametrize("name", ["var27_aligned_40", "var27_ragged"])
+@pytest.mark.parametrize("xz", [False, True])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_onepass_windowed_pgs(name, xz, k):
+    """The one-pass windowed pGS (fused_w.cu, NSM_OPT_FUSED = 3) really runs on
+    27-point matrices (its producer counters move) and is bit-identical to
+    the oracle for k = 1..4, from x = 0 and x != 0, nu = 2, at the default and
+    the tightest skew."""
+    A = SMALL[name]() if name in SMALL else inputs.var27_grid(130, 20, 6)   # 15,600 rows: a ragged last tile
+    b = inputs.uniform(0, A.nrows)
+    x0 = np.zeros(A.nrows) if xz else inputs.uniform(1, A.nrows)
+    want = oracle.pgs_apply(A, b, x0, k, nu=2, x_is_zero=xz)
+    with nsm.Smoother(A) as S:
+        for margin in (0, 1):
+            set_kernels(S, "onepass" if margin == 0 else "onepassw1")
+            c0 = S.fused_counters()
+            x = start(x0, xz)
+            S.smooth(dev(b), x, "pgs", nu=2, k_l=k, x_is_zero=xz)
+            agree(host(x), want, f"{name} onepass k={k} xz={xz} margin={margin}")
+            assert S.fused_counters()[4] > c0[4], "the one-pass kernel did not run"
+            S.check()
