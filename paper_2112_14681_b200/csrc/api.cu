@@ -47,6 +47,9 @@ struct nsm_handle {
     int64_t fw_Mr = 0, fw_Mg = 0;
     unsigned long long *fw_prog = nullptr;
     unsigned int *fw_sync = nullptr;
+    int32_t *fw_tpos[2] = {nullptr, nullptr}, *fw_nseg[2] = {nullptr, nullptr};
+    int4 *fw_tseg[2] = {nullptr, nullptr};
+    int fw_pst = 0;
     bool window = true;        // NSM_OPT_WINDOW: windowed pipelined kernels where a window exists
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
@@ -219,6 +222,11 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->fw_ring_g);
     cudaFree(h->fw_prog);
     cudaFree(h->fw_sync);
+    for (int q = 0; q < 2; ++q) {
+        cudaFree(h->fw_tpos[q]);
+        cudaFree(h->fw_nseg[q]);
+        cudaFree(h->fw_tseg[q]);
+    }
     cudaFree(h->skew_sync);
     cudaFree(h->skew_prog);
     cudaFree(h->hb_dev);
@@ -430,10 +438,10 @@ size_t flags_bytes_for(int nranks) { return (((size_t)nranks * 8 + 255) / 256) *
 // k <= kMaxPhW - 1: single rank, offset-aligned L and U with gather windows.
 constexpr int64_t kFwProgStride = 1024;
 static bool fw_possible(const nsm_handle *h) {
-    return h->fused_possible && h->L.off && h->U.off && h->res_win.wmax && h->L.win.wmax;
+    return h->fused_possible && h->L.off && h->U.off && h->U.win.wmax && h->L.win.wmax;
 }
 static FusedWShape fw_shape(const nsm_handle *h, int k) {
-    return fused_w_shape(std::max(h->L.maxw, h->U.maxw), std::max(h->res_win.wmax, h->L.win.wmax), k, h->n, h->DLA,
+    return fused_w_shape(std::max(h->L.maxw, h->U.maxw), std::max(h->U.win.wmax, h->L.win.wmax), k, h->n, h->DLA,
                          std::max(h->DLA, h->DUA), h->skew_dw);
 }
 static nsm_status fw_alloc(nsm_handle *h) {
@@ -446,11 +454,19 @@ static nsm_status fw_alloc(nsm_handle *h) {
                     a.get(&h->fw_prog, kMaxPhW * kFwProgStride) && a.get(&h->fw_sync, 16) &&
                     cudaMemset(h->fw_prog, 0, kMaxPhW * kFwProgStride * sizeof(unsigned long long)) == cudaSuccess &&
                     cudaMemcpy(h->fw_sync, init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
-    if (!ok) {
+    const int64_t nt = (h->n + 255) / 256;
+    const int pst = 8 * std::max(h->L.maxw, h->U.maxw);
+    bool tok = ok;
+    for (int q = 0; tok && q < 2; ++q)
+        tok = a.get(&h->fw_tpos[q], nt * pst) && a.get(&h->fw_nseg[q], nt) && a.get(&h->fw_tseg[q], nt * 32) &&
+              fused_w_tables(h->n, q == 0 ? h->L : h->U, q == 0 ? h->L.win : h->U.win, pst, h->fw_tpos[q],
+                             h->fw_nseg[q], h->fw_tseg[q]) == cudaSuccess;
+    if (!tok) {
         cudaGetLastError();
         h->err = "NSM_OPT_FUSED: device allocation of the one-pass rings failed";
         return NSM_ERR_OOM;
     }
+    h->fw_pst = pst;
     h->fw_Mr = sh.Mr;
     h->fw_Mg = sh.Mg;
     h->fw_ready = true;
@@ -1218,7 +1234,14 @@ static nsm_status fused_w_run(nsm_handle *h, const double *b, double *x, int k, 
     L.fresh = fresh ? 1 : 0;
     L.Lp = &h->L;
     L.Up = &h->U;
-    L.wres = &h->res_win;
+    L.wu = &h->U.win;
+    L.tposL = h->fw_tpos[0];
+    L.tposU = h->fw_tpos[1];
+    L.nsegL = h->fw_nseg[0];
+    L.nsegU = h->fw_nseg[1];
+    L.tsegL = h->fw_tseg[0];
+    L.tsegU = h->fw_tseg[1];
+    L.pst = h->fw_pst;
     L.wl = &h->L.win;
     L.d = h->d;
     L.b = b;

@@ -67,7 +67,13 @@ struct FwParams {
     int k, D, DT, DA, fresh, maxph;
     int64_t Mr, Mg;                // ring lengths in tiles (powers of two)
     SellView L, U;
-    WinView WR, WL;                // residual window (L, U), L-sweep window
+    WinView WR, WL;                // gather windows of U and of L
+    // per-tile padded copies of the windows (fw_tables): positions [t][pst],
+    // segment count [t], segments [t][32] = {glo lo, glo hi, len, sbase}, so a
+    // unit's metadata loads do not depend on each other
+    const int32_t *tposL, *tposU, *nsegL, *nsegU;
+    const int4 *tsegL, *tsegU;
+    int pst;
     const double *d, *b;
     double *x;
     double *ring_r, *ring_g;       // ring_g: k rings of Mg tiles each
@@ -97,19 +103,18 @@ __device__ __forceinline__ UDescW *udw(char *s) { return (UDescW *)(s + 2 * kMax
 struct StageW {
     char *base;
     int64_t cap;
-    __device__ __forceinline__ double *val(int p) const { return (double *)base + (int64_t)p * cap; }
-    __device__ __forceinline__ int32_t *pos(int p) const {
-        return (int32_t *)(base + 2 * cap * 8) + (int64_t)p * (cap / kSlice);
-    }
-    __device__ __forceinline__ int2 *hdr(int p) const {
-        return (int2 *)(base + 2 * cap * 8 + ((2 * (cap / kSlice) * 4 + 15) / 16) * 16) + p * kWC;
+    // one part per unit: values, window positions, slice geometry, window
+    __device__ __forceinline__ double *val(int) const { return (double *)base; }
+    __device__ __forceinline__ int32_t *pos(int) const { return (int32_t *)(base + cap * 8); }
+    __device__ __forceinline__ int2 *hdr(int) const {
+        return (int2 *)(base + cap * 8 + (((cap / kSlice) * 4 + 15) / 16) * 16);
     }
     __device__ __forceinline__ double *win() const {
-        return (double *)(base + 2 * cap * 8 + ((2 * (cap / kSlice) * 4 + 15) / 16) * 16 + 2 * kWC * 8);
+        return (double *)(base + cap * 8 + (((cap / kSlice) * 4 + 15) / 16) * 16 + kWC * 8);
     }
 };
 __host__ __device__ inline int64_t stage_bytes_w(int64_t cap, int64_t wcap) {
-    return ((2 * cap * 8 + ((2 * (cap / kSlice) * 4 + 15) / 16) * 16 + 2 * kWC * 8 + wcap * 8) + 127) / 128 * 128;
+    return ((cap * 8 + (((cap / kSlice) * 4 + 15) / 16) * 16 + kWC * 8 + wcap * 8) + 127) / 128 * 128;
 }
 __device__ __forceinline__ StageW stage_w(char *sm, const FwParams &p, int st) {
     return StageW{sm + kHdrW + (int64_t)st * p.stage_bytes, p.cap};
@@ -163,8 +168,14 @@ struct WinSum {
     }
 };
 
+// Units of an item (s = 0 .. K + 1): s = 0 / 1 = phase 0 over L / U (the
+// residual's two triangles, each with its own gather window of x; the row
+// sum continues in the consumer's registers from s = 0 to s = 1, so the
+// additions keep the stored order L, D, U), s >= 2 = sweep j = s - 1 over L
+// with the window of the ring g(j-1).  Every unit stages ONE part and one
+// window (~38 KB for C3), so two CTAs fit per SM.
 template <int CH>
-__global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_constant__ FwParams p) {
+__global__ void __launch_bounds__(kThreadsW, 2) k_fused_pgs_w(const __grid_constant__ FwParams p) {
     extern __shared__ __align__(128) char sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t G = gridDim.x, c = blockIdx.x;
@@ -179,23 +190,19 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
     }
     __syncthreads();
     const int K = p.k;
+    const int NS = K + 2;                 // units per item
     const int64_t NT = p.ntiles;
     const int64_t rmask = p.Mr * kRowsW - 1, gmask = p.Mg * kRowsW - 1;
+    auto phase_of = [](int sidx) { return sidx <= 1 ? 0 : sidx - 1; };
 
     if (warp == kWC) {
         // ------------------------------------------------------------ producer
-        // Unit metadata is software-pipelined: the slice pointers and window
-        // segment range of unit N+2 and the dependent loads (window
-        // positions, segments) of unit N+1 are in flight while unit N is
-        // staged, so no global round trip sits on the per-unit path.
         const uint64_t pol_first = ptx::policy_evict_first(), pol_keep = ptx::policy_evict_normal();
-        // F[q]: phase q is done for all items < F[q].  The progress counters
-        // are read with ld.acquire (no fence draining the producer's prefetch
-        // loads; the reads order everything this warp does afterwards — across
-        // lanes through __syncwarp); a proxy fence orders the following bulk
-        // copies (async proxy) after them.  Every unit refreshes one phase's
-        // view asynchronously (counter loads issued at the end of one unit,
-        // reduced at the end of the next), so the producer rarely waits.
+        // F[q]: phase q is done for all items < F[q] (acquire reads of the
+        // progress counters; a proxy fence orders the following bulk copies).
+        // Every phase-advancing unit refreshes one phase's view asynchronously
+        // (counter loads issued at the end of one unit, reduced at the end of
+        // the next), so the producer rarely waits.
         int64_t F[kMaxPhW];
 #pragma unroll
         for (int q = 0; q < kMaxPhW; ++q) F[q] = 0;
@@ -220,9 +227,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
             proxy_dirty = true;
             poll_ns += ptx::globaltimer_ns() - t0;
         };
-        // asynchronous refresh: counters of phase rph loaded (acquire) at the
-        // end of one unit, reduced into F[rph] at the end of the next
-        constexpr int kPR = 8;   // counters per lane (grids <= 256 CTAs)
+        constexpr int kPR = 10;   // counters per lane (grids <= 320 CTAs)
         unsigned long long rv[kPR];
         int rph = -1;
         auto refresh_issue = [&](int ph) {
@@ -253,73 +258,52 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
             }
             rph = -1;
         };
-        // unit sequence of this CTA: (w, j), w = c + m G, j = 0..K
+        // unit metadata, loaded one unit ahead (two dependent round trips:
+        // slice pointers / segment range, then positions / segments)
         struct Meta {
             int64_t w, u;
-            int j;
+            int sidx;
             bool live, valid;
-            int64_t pv;                 // lanes 0..8: part-0 slice pointers, 16..24: part 1
-            int32_t g0, g1;             // window segment range
-            int32_t pos[2][4];          // window positions (first 128 entry positions of each part)
-            int64_t sg_lo;
-            int32_t sg_len, sg_base;
+            int64_t pv;                 // lanes 0..8: slice pointers of the unit's part
+            int32_t nseg;               // window segments
+            int4 seg;                   // lane k: segment k
+            int32_t pos[4];             // window positions pos[lane + 32 r]
         };
-        auto advance = [&](int64_t &w, int &j) {
-            if (++j > K) { j = 0; w += G; }
-        };
-        auto load1 = [&](Meta &M, int64_t w, int j) {  // independent loads
+        auto unit_part = [&](int sidx) -> const SellView & { return sidx == 1 ? p.U : p.L; };
+        // all loads of a unit's metadata are independent (per-tile tables)
+        auto load1 = [&](Meta &M, int64_t w, int sidx) {
             M.w = w;
-            M.j = j;
+            M.sidx = sidx;
             M.live = w < p.nitems;
-            M.u = w - (int64_t)j * p.D;
-            M.valid = M.live && M.u >= 0 && M.u < NT;
+            M.u = w - (int64_t)phase_of(sidx) * p.D;
+            M.valid = M.live && M.u >= 0 && M.u < NT && !(sidx <= 1 && p.fresh);
             M.pv = 0;
-            M.g0 = M.g1 = 0;
+            M.nseg = 0;
             if (!M.valid) return;
-            const int np = j == 0 ? 2 : 1;
-            const int part = lane >> 4, sl = lane & 15;
             const int64_t s0 = M.u * kWC, s1 = min(s0 + kWC, p.nslices);
-            if (sl <= kWC && part < np) M.pv = __ldg((part == 0 ? p.L.ptr : p.U.ptr) + min(s0 + sl, s1));
-            const WinView &W = j == 0 ? p.WR : p.WL;
-            M.g0 = __ldg(W.tseg + M.u);
-            M.g1 = __ldg(W.tseg + M.u + 1);
-        };
-        auto load2 = [&](Meta &M) {  // loads that depend on load1's
-            if (!M.valid) return;
-            const int np = M.j == 0 ? 2 : 1;
-            const WinView &W = M.j == 0 ? p.WR : p.WL;
+            if (lane <= kWC) M.pv = __ldg(unit_part(sidx).ptr + min(s0 + lane, s1));
+            const bool up = sidx == 1;
+            M.nseg = __ldg((up ? p.nsegU : p.nsegL) + M.u);
+            M.seg = __ldg((up ? p.tsegU : p.tsegL) + M.u * 32 + lane);
+            const int32_t *tp = (up ? p.tposU : p.tposL) + M.u * p.pst;
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int64_t bq = __shfl_sync(0xffffffffu, M.pv, 16 * q), eq = __shfl_sync(0xffffffffu, M.pv, 16 * q + kWC);
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int64_t e = lane + 32 * r;
-                    M.pos[q][r] = (q < np && e < (eq - bq) / kSlice) ? __ldg(W.wpos[q] + bq / kSlice + e) : 0;
-                }
-            }
-            if (lane < M.g1 - M.g0) {
-                M.sg_lo = __ldg(W.glo + M.g0 + lane);
-                M.sg_len = __ldg(W.len + M.g0 + lane);
-                M.sg_base = __ldg(W.sbase + M.g0 + lane);
-            }
+            for (int r = 0; r < 4; ++r) M.pos[r] = lane + 32 * r < p.pst ? __ldg(tp + lane + 32 * r) : 0;
         };
-        Meta m1, m2, m3;
+        Meta ma, mb;
         int64_t wn = c;
-        int jn = 0;
-        load1(m1, wn, jn);
-        advance(wn, jn);
-        load1(m2, wn, jn);
-        advance(wn, jn);
-        load2(m1);
-        // one unit: loads for the units two and one ahead are issued first;
-        // the three Meta records rotate roles (no register copies, so the
-        // loads' latency overlaps a whole unit)
-        auto step = [&](Meta &cur, Meta &nx1, Meta &nx2) -> bool {
+        int sn = 0;
+        auto advance = [&]() {
+            if (++sn == NS) { sn = 0; wn += G; }
+        };
+        load1(ma, wn, sn);
+        advance();
+        // one unit; the two Meta records alternate roles (no register copy,
+        // so the next unit's loads overlap this unit's staging)
+        auto step = [&](Meta &cur, Meta &nxt) -> bool {
             if (!cur.live) return false;
-            load1(nx2, wn, jn);  // unit N+2
-            advance(wn, jn);
-            load2(nx1);          // unit N+1 (its slice pointers arrived during unit N-1)
-            const int j = cur.j;
+            load1(nxt, wn, sn);   // the next unit's metadata
+            advance();
+            const int sidx = cur.sidx, j = phase_of(sidx);
             const int64_t w = cur.w, u = cur.u;
             const uint64_t tA = ptx::globaltimer_ns();
             if (round > 0) ptx::mbar_wait(emptyb(sm) + st, (round - 1) & 1);
@@ -327,15 +311,15 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
             t_empty += tB - tA;
             if (!cur.valid) {
                 if (lane == 0) {
-                    udw(sm)[st] = UDescW{-1, j};
+                    udw(sm)[st] = UDescW{-1, sidx};
                     ptx::mbar_arrive(fullb(sm) + st);
                 }
                 __syncwarp();
             } else {
                 if (j >= 1) need(j - 1, w - p.D);
                 if (j == K) need(0, u + p.DA);
-                if (j < K && u >= p.Mg) need(j + 1, u - p.Mg + p.DT + (int64_t)(j + 1) * p.D);
-                if (j == 0 && u >= p.Mr) need(K, u - p.Mr + (int64_t)K * p.D);
+                if (sidx <= 1 && u >= p.Mr) need(K, u - p.Mr + (int64_t)K * p.D);
+                if (sidx != 1 && j < K && u >= p.Mg) need(j + 1, u - p.Mg + p.DT + (int64_t)(j + 1) * p.D);
                 if (proxy_dirty) {  // the bulk copies below read what the new frontiers published
                     __syncwarp();
                     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -345,50 +329,42 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
                 const uint64_t tC = ptx::globaltimer_ns();
                 t_need += tC - tB;
                 const StageW S = stage_w(sm, p, st);
-                const int np = j == 0 ? 2 : 1;
-                const WinView &W = j == 0 ? p.WR : p.WL;
-                const int part = lane >> 4, sl = lane & 15;
+                const SellView &P = unit_part(sidx);
                 const int64_t pnext = __shfl_down_sync(0xffffffffu, cur.pv, 1);
                 const int64_t b0 = __shfl_sync(0xffffffffu, cur.pv, 0), e0 = __shfl_sync(0xffffffffu, cur.pv, kWC);
-                const int64_t b1 = __shfl_sync(0xffffffffu, cur.pv, 16), e1 = __shfl_sync(0xffffffffu, cur.pv, 16 + kWC);
-                if (sl < kWC && part < np)
-                    S.hdr(part)[sl] = make_int2((int)(cur.pv - (part == 0 ? b0 : b1)), (int)((pnext - cur.pv) / kSlice));
+                if (lane < kWC) S.hdr(0)[lane] = make_int2((int)(cur.pv - b0), (int)((pnext - cur.pv) / kSlice));
+                const int64_t ne = (e0 - b0) / kSlice;
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    if (q >= np) break;
-                    const int64_t bq = q == 0 ? b0 : b1, ne = ((q == 0 ? e0 : e1) - bq) / kSlice;
-                    int32_t *sp = S.pos(q);
-#pragma unroll
-                    for (int r = 0; r < 4; ++r)
-                        if (lane + 32 * r < ne) sp[lane + 32 * r] = cur.pos[q][r];
-                    for (int64_t e = lane + 128; e < ne; e += 32) sp[e] = __ldg(W.wpos[q] + bq / kSlice + e);  // wide tiles
-                }
+                for (int r = 0; r < 4; ++r)
+                    if (lane + 32 * r < ne) S.pos(0)[lane + 32 * r] = cur.pos[r];
+                for (int64_t e = lane + 128; e < ne; e += 32)   // tiles wider than 128 entry positions
+                    S.pos(0)[e] = __ldg((sidx == 1 ? p.tposU : p.tposL) + u * p.pst + e);
                 // window segments: lane k owns segment k
                 double *ws = S.win();
                 uint64_t *bar = fullb(sm) + st;
                 int64_t wa = 0, we = 0, wl0 = 0;
                 double *wdst = nullptr;
-                if (lane < cur.g1 - cur.g0 && !(j == 0 && p.fresh)) {  // (x = 0: no residual, no window)
-                    const int64_t lo = cur.sg_lo, hi = lo + cur.sg_len;
-                    wdst = ws + cur.sg_base;
+                const double *vsrc = sidx <= 1 ? p.x : p.ring_g + (int64_t)(j - 1) * p.Mg * kRowsW;
+                const bool ring = sidx >= 2;
+                if (lane < cur.nseg) {
+                    const int64_t lo = (int64_t)(((uint64_t)(uint32_t)cur.seg.y << 32) | (uint32_t)cur.seg.x);
+                    const int64_t hi = lo + cur.seg.z;
+                    wdst = ws + cur.seg.w;
                     wl0 = lo;
                     const int64_t a = max(lo, (int64_t)0), e = min(hi, p.n);
                     for (int64_t q = lo; q < min(a, hi); ++q) wdst[q - lo] = 0.0;   // below row 0
                     for (int64_t q = max(e, lo); q < hi; ++q) wdst[q - lo] = 0.0;  // past row n - 1
                     wa = a;
                     we = e;
-                    if (e > a && (e & 1)) {  // odd n: the last element by a plain load (the only odd end)
-                        const double *src = j == 0 ? p.x + (e - 1)
-                                                   : p.ring_g + (int64_t)(j - 1) * p.Mg * kRowsW + ((e - 1) & gmask);
-                        wdst[e - 1 - lo] = __ldcg(src);
-                    }
+                    if (e > a && (e & 1))  // odd n: the last element by a plain load (the only odd end)
+                        wdst[e - 1 - lo] = __ldcg(vsrc + (ring ? ((e - 1) & gmask) : e - 1));
                 }
                 // bytes of the bulk copies (matrix values, window pieces)
                 const int64_t rl = p.Mg * kRowsW;
                 int64_t cut = we;
                 uint32_t wbytes = 0;
                 if (we > wa) {
-                    if (j == 0) {
+                    if (!ring) {
                         const int64_t be = we & ~(int64_t)1;
                         wbytes = be > wa ? (uint32_t)((be - wa) * 8) : 0;
                     } else {  // ring pieces: split where the ring wraps
@@ -402,43 +378,40 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
                 for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
                 __syncwarp();
                 if (lane == 0) {
-                    udw(sm)[st] = UDescW{(int)u, j};
-                    const uint32_t mbytes = (uint32_t)((e0 - b0) * 8 + (np == 2 ? (e1 - b1) * 8 : 0));
-                    ptx::mbar_expect_tx(bar, mbytes + wsum);
-                    // L's values are re-read by the later phases: keep them in L2
+                    udw(sm)[st] = UDescW{(int)u, sidx};
+                    ptx::mbar_expect_tx(bar, (uint32_t)((e0 - b0) * 8) + wsum);
+                    // L's values are re-read by the sweeps: keep them in L2
                     if (e0 > b0)
-                        ptx::bulk_g2s(S.val(0), p.L.val + b0, (uint32_t)((e0 - b0) * 8), bar, j < K ? pol_keep : pol_first);
-                    if (np == 2 && e1 > b1)
-                        ptx::bulk_g2s(S.val(1), p.U.val + b1, (uint32_t)((e1 - b1) * 8), bar, pol_first);
+                        ptx::bulk_g2s(S.val(0), P.val + b0, (uint32_t)((e0 - b0) * 8), bar,
+                                      (sidx == 1 || j == K) ? pol_first : pol_keep);
                 }
                 __syncwarp();
                 if (we > wa) {
-                    if (j == 0) {
-                        copy_piece(wdst + (wa - wl0), p.x + wa, wa, we, bar, pol_keep);
+                    if (!ring) {
+                        copy_piece(wdst + (wa - wl0), vsrc + wa, wa, we, bar, pol_keep);
                     } else {
-                        const double *ring = p.ring_g + (int64_t)(j - 1) * rl;
-                        copy_piece(wdst + (wa - wl0), ring + (wa & gmask), wa, cut, bar, pol_keep);
-                        if (we > cut) copy_piece(wdst + (cut - wl0), ring + (cut & gmask), cut, we, bar, pol_keep);
+                        copy_piece(wdst + (wa - wl0), vsrc + (wa & gmask), wa, cut, bar, pol_keep);
+                        if (we > cut) copy_piece(wdst + (cut - wl0), vsrc + (cut & gmask), cut, we, bar, pol_keep);
                     }
                 }
                 __syncwarp();
             }
-            refresh_reduce();    // the counters loaded during this unit
-            refresh_issue(j);
+            if (sidx != 0) {  // units that complete a phase refresh that phase's view
+                refresh_reduce();
+                refresh_issue(j);
+            }
             t_all += ptx::globaltimer_ns() - tA;
             if (++st == p.nst) { st = 0; ++round; }
             return true;
         };
-        while (step(m1, m2, m3) && step(m2, m3, m1) && step(m3, m1, m2)) {
+        while (step(ma, mb) && step(mb, ma)) {
         }
         // end of the sequence
-        if (round > 0 || st > 0) {
-            if (round > 0) ptx::mbar_wait(emptyb(sm) + st, (round - 1) & 1);
-        }
+        if (round > 0) ptx::mbar_wait(emptyb(sm) + st, (round - 1) & 1);
         if (lane == 0) {
             udw(sm)[st] = UDescW{-2, 0};
             ptx::mbar_arrive(fullb(sm) + st);
-            // statistics (nsm_fused_stats): frontier polls of the producer and their time
+            // statistics (nsm_fused_counters)
             atomicAdd((unsigned long long *)(p.sync + 4), polls);
             atomicAdd((unsigned long long *)(p.sync + 6), poll_ns);
             atomicAdd((unsigned long long *)(p.sync + 8), t_empty);
@@ -450,54 +423,53 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
         // ----------------------------------------------------------- consumers
         int st = 0;
         uint32_t par = 0;
+        double acc = 0.0, di = 1.0, bi = 0.0, xi = 0.0;   // carried from unit s = 0 to s = 1
         for (int64_t w = c, m = 0;; w += G, ++m) {
             bool end = false;
-            for (int j = 0; j <= K; ++j) {
+            for (int sidx = 0; sidx < NS; ++sidx) {
+                const int j = phase_of(sidx);
                 const int64_t u = w - (int64_t)j * p.D;
                 const bool valid = w < p.nitems && u >= 0 && u < NT;
                 const int64_t i = u * kRowsW + warp * kSlice + lane;
                 const bool row = valid && i < p.n;
                 // own-row vectors: immutable (d, b), or written only by this unit (x of tile u, j = K)
-                double di = 1.0, bi = 0.0, xi = 0.0;
-                if (row) {
-                    di = __ldg(p.d + i);
-                    if (j == 0) {
-                        bi = __ldg(p.b + i);
-                        if (!p.fresh) xi = __ldg(p.x + i);
-                    } else if (j == K && !p.fresh) {
-                        xi = p.x[i];
+                if (sidx != 1) {
+                    di = 1.0;
+                    bi = 0.0;
+                    xi = 0.0;
+                    if (row) {
+                        di = __ldg(p.d + i);
+                        if (j == 0) {
+                            bi = __ldg(p.b + i);
+                            if (!p.fresh) xi = __ldg(p.x + i);
+                        } else if (j == K && !p.fresh) {
+                            xi = p.x[i];
+                        }
                     }
                 }
                 ptx::mbar_wait(fullb(sm) + st, par);
                 const UDescW un = udw(sm)[st];
                 if (un.u == -2) { end = true; break; }
                 double res = 0.0;
-                if (un.u >= 0) {
+                if (un.u >= 0 && row) {
                     const StageW S = stage_w(sm, p, st);
+                    const int2 h = S.hdr(0)[warp];
                     const double *ws = S.win() + lane;
-                    const int2 hl = S.hdr(0)[warp];
-                    if (j == 0) {
-                        if (p.fresh) {
-                            res = bi;  // x = 0: r = b (reading R3)
-                        } else {
-                            const int2 hu = S.hdr(1)[warp];
-                            double acc = 0.0;
-                            if (row) {
-                                acc = WinSum<CH>::run(S.val(0) + hl.x + lane, S.pos(0) + hl.x / kSlice, ws, hl.y, acc);
-                                acc = __dadd_rn(acc, __dmul_rn(di, xi));
-                                acc = WinSum<CH>::run(S.val(1) + hu.x + lane, S.pos(1) + hu.x / kSlice, ws, hu.y, acc);
-                            }
-                            res = __dsub_rn(bi, acc);
-                        }
-                    } else if (row) {
-                        res = WinSum<CH>::run(S.val(0) + hl.x + lane, S.pos(0) + hl.x / kSlice, ws, hl.y, 0.0);
+                    if (sidx == 0) {
+                        acc = WinSum<CH>::run(S.val(0) + h.x + lane, S.pos(0) + h.x / kSlice, ws, h.y, 0.0);
+                    } else if (sidx == 1) {
+                        acc = __dadd_rn(acc, __dmul_rn(di, xi));
+                        acc = WinSum<CH>::run(S.val(0) + h.x + lane, S.pos(0) + h.x / kSlice, ws, h.y, acc);
+                    } else {
+                        res = WinSum<CH>::run(S.val(0) + h.x + lane, S.pos(0) + h.x / kSlice, ws, h.y, 0.0);
                     }
                 }
                 if (row) {
-                    if (j == 0) {
-                        p.ring_r[i & rmask] = res;
-                        p.ring_g[i & gmask] = __ddiv_rn(res, di);   // g(0) = D^{-1} r
-                    } else {
+                    if (sidx == 1) {
+                        const double r = p.fresh ? bi : __dsub_rn(bi, acc);   // x = 0: r = b (reading R3)
+                        p.ring_r[i & rmask] = r;
+                        p.ring_g[i & gmask] = __ddiv_rn(r, di);   // g(0) = D^{-1} r
+                    } else if (sidx >= 2) {
                         const double ri = __ldcg(p.ring_r + (i & rmask));
                         const double v = __ddiv_rn(__dsub_rn(ri, res), di);
                         if (!isfinite(v)) atomicMin(p.flag, (unsigned long long)(p.sweep_id0 + j - 1));
@@ -505,15 +477,15 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
                         else p.x[i] = p.fresh ? v : __dadd_rn(xi, v);
                     }
                 }
-                // publish "phase j of this CTA's items <= m is complete": the last
-                // warp to finish the unit (CTA-scope acq_rel count makes the
-                // other warps' stores visible to its gpu-scope release)
-                // (the stage is released after the count: a warp cannot reach the
-                // stage's next unit before every warp has counted this one)
+                // publish "phase j of this CTA's items <= m is complete" (units
+                // s >= 1): the last warp to finish the unit (CTA-scope acq_rel
+                // count, then a gpu-scope release); the stage is released
+                // after the count, so no warp reaches the stage's next unit
+                // before every warp has counted this one
                 __syncwarp();
                 if (lane == 0) {
                     const unsigned int prev = ptx::atom_add_acqrel_cta_shared(pubc(sm) + st, 1u);
-                    if ((prev + 1) % kWC == 0)
+                    if (sidx != 0 && (prev + 1) % kWC == 0)
                         ptx::red_max_release_gpu_u64(p.prog + (int64_t)j * p.pstride + c,
                                                      ((unsigned long long)epoch << 32) | (unsigned long long)(m + 1));
                     ptx::mbar_arrive(emptyb(sm) + st);
@@ -534,6 +506,26 @@ __global__ void __launch_bounds__(kThreadsW, 1) k_fused_pgs_w(const __grid_const
             __threadfence();
         }
     }
+}
+
+// Per-tile padded window tables (one warp per tile): positions, segment
+// count and segments of window W, for the one-pass kernel's independent loads.
+__global__ void k_fw_tables(int64_t ntiles, int64_t nslices, const int64_t *__restrict__ ptr, WinView W, int pst,
+                            int32_t *__restrict__ tpos, int32_t *__restrict__ nseg, int4 *__restrict__ tseg) {
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= ntiles) return;
+    const int64_t s0 = t * kWC, s1 = min(s0 + kWC, nslices);
+    const int64_t b = ptr[s0] / kSlice, e = ptr[s1] / kSlice;
+    for (int64_t k = lane; k < pst; k += 32) tpos[t * pst + k] = k < e - b ? W.wpos[0][b + k] : 0;
+    const int32_t g0 = W.tseg[t], g1 = W.tseg[t + 1];
+    if (lane == 0) nseg[t] = g1 - g0;
+    int4 v = make_int4(0, 0, 0, 0);
+    if (lane < g1 - g0) {
+        const int64_t lo = W.glo[g0 + lane];
+        v = make_int4((int)(uint32_t)(uint64_t)lo, (int)(uint32_t)((uint64_t)lo >> 32), W.len[g0 + lane], W.sbase[g0 + lane]);
+    }
+    tseg[t * 32 + lane] = v;
 }
 
 const void *pick_w(int ch) {
@@ -576,7 +568,7 @@ GeoW geometry_w(const void *k, int64_t stage_bytes) {
         if (smem > kSmemMaxW) break;
         int per = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreadsW, (size_t)smem);
-        per = std::min(per, 1);  // one CTA per SM: its stages take most of the shared memory
+        per = std::min(per, 2);
         if (per > 0 && per >= best) {
             best = per;
             g.nst = nst;
@@ -615,7 +607,9 @@ FusedWShape fused_w_shape(int maxw, int64_t wmax, int k, int64_t n, int DT, int 
     sh.stage_bytes = sbytes;
     sh.ntiles = (n + kRowsW - 1) / kRowsW;
     sh.grid = (int)std::min<int64_t>((int64_t)sm_count_w() * g.per_sm, std::max<int64_t>(sh.ntiles, 1));
-    sh.D = std::max(DT, DA) + (d_extra > 0 ? d_extra : 16);
+    // skew: above the bandwidth, and (automatic) above one grid of items, so a
+    // unit's dependencies were processed in an earlier round
+    sh.D = std::max(DT, DA) + (d_extra > 0 ? d_extra : std::max(16, sh.grid + 32 - std::max(DT, DA)));
     sh.nitems = sh.ntiles + (int64_t)k * sh.D;
     const int64_t tp2 = pow2_ge(sh.ntiles);
     // rings (tiles): every slot's previous occupant is at least two grids of
@@ -645,7 +639,14 @@ cudaError_t launch_fused_w(const FusedWLaunch &L, cudaStream_t st) {
     auto wv = [&](const Window *w) {
         return WinView{w->tseg, w->glo, w->len, w->sbase, {w->wpos[0], w->wpos[1]}, (int32_t)sh.wcap};
     };
-    p.WR = wv(L.wres);
+    p.WR = wv(L.wu);
+    p.tposL = L.tposL;
+    p.tposU = L.tposU;
+    p.nsegL = L.nsegL;
+    p.nsegU = L.nsegU;
+    p.tsegL = L.tsegL;
+    p.tsegU = L.tsegU;
+    p.pst = L.pst;
     p.WL = wv(L.wl);
     p.d = L.d;
     p.b = L.b;
@@ -667,9 +668,19 @@ cudaError_t launch_fused_w(const FusedWLaunch &L, cudaStream_t st) {
     return cudaLaunchCooperativeKernel(sh.kernel, dim3((unsigned)sh.grid), dim3(kThreadsW), args, sh.smem, st);
 }
 
+cudaError_t fused_w_tables(int64_t n, const Sell &T, const Window &w, int pst, int32_t *tpos, int32_t *nseg,
+                           int4 *tseg) {
+    const int64_t nt = (n + kRowsW - 1) / kRowsW, ns = (n + kSlice - 1) / kSlice;
+    const WinView W{w.tseg, w.glo, w.len, w.sbase, {w.wpos[0], w.wpos[1]}, 0};
+    k_fw_tables<<<(unsigned)((nt * 32 + 255) / 256), 256>>>(nt, ns, T.ptr, W, pst, tpos, nseg, tseg);
+    const cudaError_t e = cudaGetLastError();
+    return e != cudaSuccess ? e : cudaDeviceSynchronize();
+}
+
 void preload_fused_w_kernels() {
     cudaFuncAttributes a;
     for (int ch : {4, 8, 16}) cudaFuncGetAttributes(&a, pick_w(ch));
+    cudaFuncGetAttributes(&a, k_fw_tables);
 }
 
 }  // namespace nsm

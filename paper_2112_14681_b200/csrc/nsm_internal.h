@@ -270,7 +270,10 @@ struct FusedWLaunch {
     int64_t n;
     int k, DT, DA, fresh;
     const Sell *Lp, *Up;
-    const Window *wres, *wl;
+    const Window *wu, *wl;          // gather windows of U and L (each alone)
+    const int32_t *tposL, *tposU, *nsegL, *nsegU;   // per-tile tables (fused_w_tables)
+    const int4 *tsegL, *tsegU;
+    int pst;
     const double *d, *b;
     double *x;
     double *ring_r, *ring_g;
@@ -283,6 +286,9 @@ struct FusedWLaunch {
     unsigned int *sync;
 };
 cudaError_t launch_fused_w(const FusedWLaunch &L, cudaStream_t st);
+// per-tile padded tables of window w of part T (pst >= 8 * T.maxw positions per tile)
+cudaError_t fused_w_tables(int64_t n, const Sell &T, const Window &w, int pst, int32_t *tpos, int32_t *nseg,
+                           int4 *tseg);
 void preload_fused_w_kernels();
 
 // Force-load every kernel of the library (see kernels.cu "eager loading").

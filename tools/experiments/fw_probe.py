@@ -21,7 +21,7 @@ x = torch.from_numpy(inputs.uniform(1, A.nrows)).cuda()
 flush = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
 for mode in ("off", "on"):
     for mg in (margins if mode == "on" else [0]):
-        S.set_fused(1 if mode == "on" else 0)
+        S.set_fused(3 if mode == "on" else 0)
         S.set_fused_window(mg)
         for _ in range(3):
             S.smooth(b, x, "pgs", nu=1, k_l=k_l)
