@@ -391,8 +391,11 @@ nsm_status run_sweeps(nsm_handle *h, const Stage &st, double *bufA, double *bufB
                                 a.flag = h->flag;
                                 a.sweep_id = sid;
                                 a.pdl = h->pdl;
-                                a.win = (h->window && st.T->win.wmax && !scaled && sl.begin == 0 &&
-                                         sl.end == h->nslices) ? &st.T->win : nullptr;
+                                // windows of the local parts are planned on tiles of the full
+                                // local range: usable for any tile-aligned contiguous range (the
+                                // interior slices of a slab partition too)
+                                a.win = (h->window && st.T->win.wmax && !scaled && sl.begin >= 0 &&
+                                         sl.begin % kTileSlices == 0) ? &st.T->win : nullptr;
                                 if (use_pipelined(h, sl, with_ghost, 1, st.T->maxw))
                                     return launch_sweep_tma(a, sl.begin, sl.end, s);
                                 return launch_sweep(a, s);
@@ -409,7 +412,7 @@ nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double
                          double *out2 = nullptr) {
     return pass(h, true, x, nullptr, s, [&](const Slices &sl, bool with_ghost, const double *ghost) {
         if (use_pipelined(h, sl, with_ghost, 2, std::max(h->L.maxw, h->U.maxw)))
-            return launch_residual_tma((h->window && h->res_win.wmax && sl.begin == 0 && sl.end == h->nslices)
+            return launch_residual_tma((h->window && h->res_win.wmax && sl.begin >= 0 && sl.begin % kTileSlices == 0)
                                            ? &h->res_win : nullptr,
                                        mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
         return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
@@ -639,7 +642,7 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         ok = a.get(&h->dU, h->n) && upload(h->dU, sf.d.data(), h->n) && upload_sell(a, sf.L, &h->Ls) &&
              upload_sell(a, sf.U, &h->Us) && upload_sell(a, sf.LG, &h->LsG) && upload_sell(a, sf.UG, &h->UsG);
     }
-    if (ok && nranks == 1) {  // gather windows (stream.cu), full-range launches of one rank
+    if (ok) {  // gather windows (stream.cu): launches over tile-aligned slice ranges
         ok = make_window(a, h->n, {&sa.L, &sa.U}, &h->res_win) && make_window(a, h->n, {&sa.L}, &h->L.win) &&
              make_window(a, h->n, {&sa.U}, &h->U.win);
         if (ok && F) ok = make_window(a, h->n, {&sf.L}, &h->Ls.win) && make_window(a, h->n, {&sf.U}, &h->Us.win);

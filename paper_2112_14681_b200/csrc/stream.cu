@@ -162,8 +162,9 @@ __device__ __forceinline__ void tile_refs(const Layout &Ly, const SellView (&P)[
             }
         }
     }
-    if (win) {  // tile t of the window plan (s_begin == 0)
-        const int32_t g0 = __ldg(W.tseg + t), g1 = __ldg(W.tseg + t + 1);
+    if (win) {  // tile s0 / kTS of the window plan (s_begin is a multiple of kTS)
+        const int64_t wt = s0 / kTS;
+        const int32_t g0 = __ldg(W.tseg + wt), g1 = __ldg(W.tseg + wt + 1);
         r.nseg = g1 - g0;
         if (lane < r.nseg) {
             r.sg_lo = __ldg(W.glo + g0 + lane);
@@ -757,7 +758,7 @@ cudaError_t residual_tma_ch(const Window *w, int64_t n, int64_t s_begin, int64_t
                             bool pdl, cudaStream_t st) {
     // offset-aligned layout (both triangles): stage values only, columns = row + offset;
     // with a gather window over the whole range: gathers from shared memory
-    if (L.off && U.off && w && s_begin == 0)
+    if (L.off && U.off && w && s_begin % kTS == 0)
         return residual_tma_ofs<OUT, CH, true, true>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
     if (L.off && U.off)
         return residual_tma_ofs<OUT, CH, true, false>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
@@ -782,7 +783,8 @@ cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end,
     // gather window of the plain iterate over the whole range: gathers from
     // shared memory
     if constexpr (std::is_same<G, GatherPlainT>::value) {
-        if (a.T->off && a.win && s_begin == 0) return sweep_tma_ofs<UNIT, EPI, G, CH, true, true>(a, s_begin, s_end, gin, st);
+        if (a.T->off && a.win && s_begin % kTS == 0)
+            return sweep_tma_ofs<UNIT, EPI, G, CH, true, true>(a, s_begin, s_end, gin, st);
     }
     if (a.T->off) return sweep_tma_ofs<UNIT, EPI, G, CH, true, false>(a, s_begin, s_end, gin, st);
     return sweep_tma_ofs<UNIT, EPI, G, CH, false, false>(a, s_begin, s_end, gin, st);

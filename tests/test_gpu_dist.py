@@ -37,6 +37,10 @@ CASES = {
     "lap3d_3_uneven": (lambda: inputs.laplace(10, 9, 8), [0, 101, 450, 720]),
     "random_3": (lambda: random_sparse(900, 3), [0, 250, 610, 900]),   # couplings between all ranks
     "cd_rcm_4": (lambda: inputs.convdiff(8), [0, 128, 256, 384, 512]),
+    # 27-point z-slabs (offset-aligned, gather windows): the interior slices of
+    # each rank start on a tile boundary, so they run the windowed kernels
+    "var27_slab_3": (lambda: inputs.var27_grid(64, 40, 12), [0, 10240, 20480, 30720]),
+    "var27_slab_uneven": (lambda: inputs.var27_grid(64, 40, 12), [0, 7680, 20480, 30720]),
 }
 
 
