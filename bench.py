@@ -313,6 +313,11 @@ def run_nsm(args, rank, nranks, local_rank):
     F = nsm.ilu0(A, row_begin=A.row_begin) if kind == "ilu" else None
     S = nsm.Smoother(A, F, device=local_rank, rank=rank, nranks=nranks, row_offsets=offsets)
     S.set_pipeline(not args.plain)
+    if args.fused == "onepass" and args.config in ("C3",):
+        try:   # the plane wavefront (256 x 256 grid planes) where the structure check accepts it
+            S.set_plane_rows(256 * 256)
+        except nsm.NsmError:
+            pass
     if args.fused != "default":
         S.set_fused({"auto": 2, "on": 1, "off": 0, "onepass": 3}[args.fused])
     if args.pdl != "auto":

@@ -398,7 +398,13 @@ typedef enum {
     NSM_OPT_WINDOW = 6 /* 1 (default): pipelined kernels over an offset-aligned part stage the gathered
                         * vector's window (the tile's columns, merged into a few segments) into shared
                         * memory with the tile and gather from there (single rank); 0: gathers from
-                        * global memory through L1/L2.  Results are identical. */
+                        * global memory through L1/L2.  Results are identical. */,
+    NSM_OPT_PLANE_ROWS = 7 /* > 0 (a multiple of 256): the rows form planes of this many rows whose 256-row
+                            * tiles couple only to tiles within two lines (tile index mod plane) in the same
+                            * or a neighbouring plane (lexicographic 7- / 27-point grids with 256-point grid
+                            * lines; checked: NSM_ERR_PATTERN otherwise).  With NSM_OPT_FUSED = 3 a forward
+                            * pGS application with k >= 2 then runs as a plane wavefront: one CTA per line,
+                            * readiness from the neighbouring lines' step counters only (fused_w.cu). */
 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 

@@ -557,6 +557,12 @@ class Smoother:
         """NSM_OPT_WINDOW: shared-memory gather windows in the pipelined kernels."""
         self._call(load().nsm_set_option(self._h, 6, int(bool(enable))))
 
+    def set_plane_rows(self, rows: int):
+        """NSM_OPT_PLANE_ROWS: declare planes of `rows` rows (a multiple of 256)
+        for the plane-wavefront one-pass pGS (checked; NsmError if the matrix
+        lacks the structure)."""
+        self._call(load().nsm_set_option(self._h, 7, int(rows)))
+
     def set_pdl(self, enable: bool):
         """Programmatic dependent launch between consecutive pipelined kernels."""
         self._call(load().nsm_set_option(self._h, 3, int(bool(enable))))

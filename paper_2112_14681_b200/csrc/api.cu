@@ -50,6 +50,7 @@ struct nsm_handle {
     int32_t *fw_tpos[2] = {nullptr, nullptr}, *fw_nseg[2] = {nullptr, nullptr};
     int4 *fw_tseg[2] = {nullptr, nullptr};
     int fw_pst = 0;
+    int64_t plane_tiles = 0;   // NSM_OPT_PLANE_ROWS / 256 when the plane-wavefront check passed
     bool window = true;        // NSM_OPT_WINDOW: windowed pipelined kernels where a window exists
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
@@ -443,14 +444,29 @@ constexpr int64_t kFwProgStride = 1024;
 static bool fw_possible(const nsm_handle *h) {
     return h->fused_possible && h->L.off && h->U.off && h->U.win.wmax && h->L.win.wmax;
 }
-static FusedWShape fw_shape(const nsm_handle *h, int k) {
+static FusedWShape fw_shape(const nsm_handle *h, int k, bool planes) {
     return fused_w_shape(std::max(h->L.maxw, h->U.maxw), std::max(h->U.win.wmax, h->L.win.wmax), k, h->n, h->DLA,
-                         std::max(h->DLA, h->DUA), h->skew_dw);
+                         std::max(h->DLA, h->DUA), h->skew_dw, planes ? h->plane_tiles : 0);
+}
+
+// NSM_OPT_PLANE_ROWS: the plane-wavefront schedule (fused_w.cu
+// k_fused_pgs_planes) is valid when every coupling of a tile lies within two
+// lines (tile index mod tpp) in the same or a neighbouring plane (checked on
+// the device over the stored entries; pads are free: they multiply by 0).
+static bool planes_ok(nsm_handle *h, int64_t tpp) {
+    const int64_t nt = (h->n + 255) / 256;
+    if (tpp < 1 || nt < 2 * tpp) return false;
+    return fused_w_plane_check(h->n, tpp, h->L, h->U);
 }
 static nsm_status fw_alloc(nsm_handle *h) {
     if (h->fw_ready || !fw_possible(h)) return NSM_OK;
-    const FusedWShape sh = fw_shape(h, kMaxPhW - 1);
+    FusedWShape sh = fw_shape(h, kMaxPhW - 1, false);
     if (!sh.ok || sh.grid > kFwProgStride) return NSM_OK;
+    const FusedWShape shp = fw_shape(h, kMaxPhW - 1, true);   // rings large enough for both schedules
+    if (shp.ok) {
+        sh.Mr = std::max(sh.Mr, shp.Mr);
+        sh.Mg = std::max(sh.Mg, shp.Mg);
+    }
     DevAlloc a{h};
     const unsigned int init[16] = {1u};
     const bool ok = a.get(&h->fw_ring_r, sh.Mr * 256) && a.get(&h->fw_ring_g, (int64_t)(kMaxPhW - 1) * sh.Mg * 256) &&
@@ -460,6 +476,8 @@ static nsm_status fw_alloc(nsm_handle *h) {
     const int64_t nt = (h->n + 255) / 256;
     const int pst = 8 * std::max(h->L.maxw, h->U.maxw);
     bool tok = ok;
+    tok = tok && cudaMemset(h->fw_ring_r, 0, sh.Mr * 256 * sizeof(double)) == cudaSuccess &&
+          cudaMemset(h->fw_ring_g, 0, (int64_t)(kMaxPhW - 1) * sh.Mg * 256 * sizeof(double)) == cudaSuccess;
     for (int q = 0; tok && q < 2; ++q)
         tok = a.get(&h->fw_tpos[q], nt * pst) && a.get(&h->fw_nseg[q], nt) && a.get(&h->fw_tseg[q], nt * 32) &&
               fused_w_tables(h->n, q == 0 ? h->L : h->U, q == 0 ? h->L.win : h->U.win, pst, h->fw_tpos[q],
@@ -956,6 +974,19 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
             return NSM_OK;
         case NSM_OPT_PDL: h->pdl = value != 0; return NSM_OK;
         case NSM_OPT_WINDOW: h->window = value != 0; return NSM_OK;
+        case NSM_OPT_PLANE_ROWS:
+            if (value < 0 || value % 256) return NSM_ERR_ARG;
+            h->plane_tiles = 0;
+            if (value > 0 && fw_possible(h) && planes_ok(h, value / 256)) h->plane_tiles = value / 256;
+            if (value > 0 && !h->plane_tiles) {
+                h->err = "NSM_OPT_PLANE_ROWS: the matrix does not have the plane structure (or no gather windows)";
+                return NSM_ERR_PATTERN;
+            }
+            if (h->fw_ready) {  // the rings were sized without the plane schedule
+                const FusedWShape sp = fw_shape(h, kMaxPhW - 1, true);
+                if (!sp.ok || sp.Mr > h->fw_Mr || sp.Mg > h->fw_Mg) h->plane_tiles = 0;
+            }
+            return NSM_OK;
         case NSM_OPT_PROFILE:
             h->profile = value != 0;
             if (h->profile && h->ev.empty()) {
@@ -1227,7 +1258,8 @@ static nsm_status fused_w_run(nsm_handle *h, const double *b, double *x, int k, 
     if (!h->fw_ready || h->fused_mode != 3 || !h->pipeline || !h->window || k < 1 || k > kMaxPhW - 1 || h->n == 0)
         return NSM_OK;
     FusedWLaunch L{};
-    L.shape = fw_shape(h, k);
+    L.shape = fw_shape(h, k, h->plane_tiles > 0);
+    if (h->plane_tiles > 0 && !L.shape.ok) L.shape = fw_shape(h, k, false);  // (k = 1: the item schedule)
     const FusedWShape &sh = L.shape;
     if (!sh.ok || sh.Mr > h->fw_Mr || sh.Mg > h->fw_Mg || sh.grid > kFwProgStride) return NSM_OK;
     L.n = h->n;

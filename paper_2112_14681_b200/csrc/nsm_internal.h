@@ -260,11 +260,13 @@ struct FusedWShape {
     size_t smem = 0;
     int64_t cap = 0, wcap = 0, stage_bytes = 0, ntiles = 0, nitems = 0;
     int64_t Mr = 0, Mg = 0;   // ring lengths in 256-row tiles (powers of two)
+    int64_t tpp = 0, nplanes = 0;  // plane schedule (k_fused_pgs_planes): tiles per plane, planes
 };
 // maxw: widest slice of L and U; wmax: largest window (residual or L);
 // DT, DA: bandwidths of L and A in 256-row tiles; d_extra: D - max(DT, DA)
 // (0 = automatic).
-FusedWShape fused_w_shape(int maxw, int64_t wmax, int k, int64_t n, int DT, int DA, int d_extra);
+// tpp > 0: the plane-wavefront schedule with tpp tiles per plane (k >= 2).
+FusedWShape fused_w_shape(int maxw, int64_t wmax, int k, int64_t n, int DT, int DA, int d_extra, int64_t tpp = 0);
 struct FusedWLaunch {
     FusedWShape shape;
     int64_t n;
@@ -290,6 +292,8 @@ cudaError_t launch_fused_w(const FusedWLaunch &L, cudaStream_t st);
 cudaError_t fused_w_tables(int64_t n, const Sell &T, const Window &w, int pst, int32_t *tpos, int32_t *nseg,
                            int4 *tseg);
 void preload_fused_w_kernels();
+// plane structure of L and U for the plane wavefront (tpp tiles per plane)
+bool fused_w_plane_check(int64_t n, int64_t tpp, const Sell &L, const Sell &U);
 
 // Force-load every kernel of the library (see kernels.cu "eager loading").
 void preload_plain_kernels();

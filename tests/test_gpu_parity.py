@@ -292,3 +292,29 @@ def test_onepass_windowed_pgs(name, xz, k):
             agree(host(x), want, f"{name} onepass k={k} xz={xz} margin={margin}")
             assert S.fused_counters()[4] > c0[4], "the one-pass kernel did not run"
             S.check()
+
+
+@pytest.mark.parametrize("grid", [(128, 16, 12), (256, 4, 10)])
+@pytest.mark.parametrize("xz", [False, True])
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_onepass_plane_wavefront(grid, xz, k):
+    """The plane-wavefront one-pass pGS (NSM_OPT_PLANE_ROWS + NSM_OPT_FUSED =
+    3; one CTA per line, neighbour-only readiness) is bit-identical to the
+    oracle for k = 2..4, x = 0 and x != 0, nu = 2; the structure check rejects
+    a wrong plane size."""
+    nx, ny, nz = grid
+    A = inputs.var27_grid(nx, ny, nz)
+    b = inputs.uniform(0, A.nrows)
+    x0 = np.zeros(A.nrows) if xz else inputs.uniform(1, A.nrows)
+    want = oracle.pgs_apply(A, b, x0, k, nu=2, x_is_zero=xz)
+    with nsm.Smoother(A) as S:
+        S.set_plane_rows(nx * ny)
+        set_kernels(S, "onepass")
+        c0 = S.fused_counters()
+        x = start(x0, xz)
+        S.smooth(dev(b), x, "pgs", nu=2, k_l=k, x_is_zero=xz)
+        agree(host(x), want, f"plane wavefront {grid} k={k} xz={xz}")
+        assert S.fused_counters()[4] > c0[4], "the one-pass kernel did not run"
+        S.check()
+        with pytest.raises(nsm.NsmError):
+            S.set_plane_rows(nx * ny * 2 if (nx * ny) % 256 == 0 and nz % 2 == 1 else nx * ny // 2 * 3)
