@@ -404,7 +404,11 @@ typedef enum {
                             * or a neighbouring plane (lexicographic 7- / 27-point grids with 256-point grid
                             * lines; checked: NSM_ERR_PATTERN otherwise).  With NSM_OPT_FUSED = 3 a forward
                             * pGS application with k >= 2 then runs as a plane wavefront: one CTA per line,
-                            * readiness from the neighbouring lines' step counters only (fused_w.cu). */
+                            * readiness from the neighbouring lines' step counters only (fused_w.cu). */,
+    NSM_OPT_HOST_CHUNKS = 8 /* 1 (default): nsm_smooth_host runs a single-rank forward pGS application
+                             * (nu = 1, k <= 3, x_in != x_out) in row chunks longer than A's bandwidth, so
+                             * the host-to-device copies, the passes and the device-to-host copy overlap
+                             * (separate copy streams); 0: copy in, smooth, copy out.  Same results. */
 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 

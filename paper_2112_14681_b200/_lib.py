@@ -563,6 +563,10 @@ class Smoother:
         lacks the structure)."""
         self._call(load().nsm_set_option(self._h, 7, int(rows)))
 
+    def set_host_chunks(self, enable: bool):
+        """NSM_OPT_HOST_CHUNKS: nsm_smooth_host overlaps copies and passes in row chunks."""
+        self._call(load().nsm_set_option(self._h, 8, int(bool(enable))))
+
     def set_pdl(self, enable: bool):
         """Programmatic dependent launch between consecutive pipelined kernels."""
         self._call(load().nsm_set_option(self._h, 3, int(bool(enable))))

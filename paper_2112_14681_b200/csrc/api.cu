@@ -52,6 +52,7 @@ struct nsm_handle {
     int fw_pst = 0;
     int64_t plane_tiles = 0;   // NSM_OPT_PLANE_ROWS / 256 when the plane-wavefront check passed
     bool window = true;        // NSM_OPT_WINDOW: windowed pipelined kernels where a window exists
+    bool chunked_host = true;  // NSM_OPT_HOST_CHUNKS: nsm_smooth_host overlaps copies and passes
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
     // A = L + D + U (+ ghost couplings LG / UG)
@@ -62,6 +63,9 @@ struct nsm_handle {
     double *dU = nullptr;
     // nsm_smooth_host staging vectors (allocated by its first call)
     double *hb_dev = nullptr, *hx_dev = nullptr;
+    // chunked nsm_smooth_host (copies overlapped with the passes): streams, events
+    cudaStream_t hs_in = nullptr, hs_out = nullptr;
+    std::vector<cudaEvent_t> hev;          // 2 per chunk + 2
     // Ruiz-scaled U factor (Alg. 2 / NEXT-3): U~ = diag(1/s_r) U diag(1/s_c), unit diagonal
     bool ruiz = false;
     double *s_r = nullptr, *s_c = nullptr;
@@ -232,6 +236,9 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->skew_prog);
     cudaFree(h->hb_dev);
     cudaFree(h->hx_dev);
+    if (h->hs_in) cudaStreamDestroy(h->hs_in);
+    if (h->hs_out) cudaStreamDestroy(h->hs_out);
+    for (cudaEvent_t e : h->hev) cudaEventDestroy(e);
     delete h;
 }
 
@@ -974,6 +981,7 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
             return NSM_OK;
         case NSM_OPT_PDL: h->pdl = value != 0; return NSM_OK;
         case NSM_OPT_WINDOW: h->window = value != 0; return NSM_OK;
+        case NSM_OPT_HOST_CHUNKS: h->chunked_host = value != 0; return NSM_OK;
         case NSM_OPT_PLANE_ROWS:
             if (value < 0 || value % 256) return NSM_ERR_ARG;
             h->plane_tiles = 0;
@@ -1492,6 +1500,114 @@ nsm_status nsm_smooth(nsm_handle *h, nsm_kind kind, const double *b, double *x, 
     return NSM_OK;
 }
 
+// nsm_smooth_host for one forward pGS application on one rank, in row
+// chunks (tile-aligned, each longer than A's bandwidth) so that the
+// host-to-device copies of b and x, the passes and the device-to-host copy
+// of x overlap.  Chunk c's residual needs x of chunks c-1 .. c+1 (unmodified:
+// the x update of chunk c-1 is launched after it); sweep j of chunk c-1 needs
+// g(j-1) of chunks c-2 and c-1, each level in its own buffer (k <= 3).  Same
+// kernels and per-row arithmetic as nsm_smooth: bit-identical results.
+static nsm_status smooth_host_chunked(nsm_handle *h, const double *b_host, const double *x_in_host, double *x_out_host,
+                                      int k, cudaStream_t s, bool *done) {
+    *done = false;
+    const int mwr = std::max(h->L.maxw, h->U.maxw);
+    if (h->nranks != 1 || k < 1 || k > 3 || !h->pipeline || h->fused_mode != 0 || !tma_ok(2, mwr) ||
+        wide_rows(mwr, h->nslices) || !tma_ok(1, h->L.maxw) || wide_rows(h->L.maxw, h->nslices))
+        return NSM_OK;
+    const int64_t nt = (h->n + 255) / 256;
+    const int64_t ct = std::max<int64_t>(std::max(h->DLA, h->DUA) + 1, (nt + 15) / 16);  // tiles per chunk
+    const int64_t C = (nt + ct - 1) / ct;
+    if (C < 3 || C > 64) return NSM_OK;
+    if (!h->hs_in) {
+        if (cudaStreamCreateWithFlags(&h->hs_in, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&h->hs_out, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            return NSM_OK;
+        }
+        h->hev.resize(2 * 64 + 2);
+        for (cudaEvent_t &e : h->hev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+                cudaGetLastError();
+                return NSM_OK;
+            }
+    }
+    cudaEvent_t *hin = h->hev.data(), *fin = h->hev.data() + 64, ev0 = h->hev[128], ev1 = h->hev[129];
+    auto rows = [&](int64_t c, int64_t &r0, int64_t &r1) {
+        r0 = std::min(c * ct * 256, h->n);
+        r1 = std::min((c + 1) * ct * 256, h->n);
+    };
+    auto slices = [&](int64_t c, int64_t &s0, int64_t &s1) {
+        s0 = std::min<int64_t>(c * ct * kTileSlices, h->nslices);
+        s1 = std::min<int64_t>((c + 1) * ct * kTileSlices, h->nslices);
+    };
+    double *R = h->w[0], *G0 = h->w[3], *G1 = h->w[1], *G2 = h->w[2];
+    double *gbuf[3] = {G0, G1, G2};
+    double *xd = h->hx_dev, *bd = h->hb_dev;
+    cudaError_t e = cudaEventRecord(ev0, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->hs_in, ev0, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->hs_out, ev0, 0);
+    for (int64_t c = 0; c < C && e == cudaSuccess; ++c) {  // all host-to-device copies, in chunk order
+        int64_t r0, r1;
+        rows(c, r0, r1);
+        const size_t nb = (size_t)(r1 - r0) * sizeof(double);
+        e = cudaMemcpyAsync(bd + r0, b_host + r0, nb, cudaMemcpyHostToDevice, h->hs_in);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(xd + r0, x_in_host + r0, nb, cudaMemcpyHostToDevice, h->hs_in);
+        if (e == cudaSuccess) e = cudaEventRecord(hin[c], h->hs_in);
+    }
+    if (e != cudaSuccess) return cuda_fail(h, e, "nsm_smooth_host (chunked copies in)");
+    const int64_t sid0 = h->sweep_counter + 1;
+    h->sweep_counter += k;
+    for (int64_t c = 0; c <= C; ++c) {
+        if (c < C) {  // residual of chunk c (needs x of chunks c-1 .. c+1)
+            e = cudaStreamWaitEvent(s, hin[std::min(c + 1, C - 1)], 0);
+            int64_t s0, s1;
+            slices(c, s0, s1);
+            if (e == cudaSuccess)
+                e = launch_residual_tma(h->window && h->res_win.wmax ? &h->res_win : nullptr, OUT_RG, h->n, s0, s1,
+                                        h->L, h->U, h->d, bd, xd, R, G0, false, s);
+            ++h->launches;
+        }
+        if (c >= 1 && e == cudaSuccess) {  // the k sweeps of chunk c-1, the last with x += g
+            int64_t s0, s1;
+            slices(c - 1, s0, s1);
+            for (int j = 1; j <= k && e == cudaSuccess; ++j) {
+                SweepArgs sa{};
+                sa.n = h->n;
+                sa.nslices = h->nslices;
+                sa.T = &h->L;
+                sa.TG = &h->LG;
+                sa.unit = false;
+                sa.epi = j == k ? EPI_XADD : EPI_STORE;
+                sa.dT = h->d;
+                sa.rhs = R;
+                sa.gin = gbuf[j - 1];
+                sa.gout = j < k ? gbuf[j] : nullptr;
+                sa.x = xd;
+                sa.flag = h->flag;
+                sa.sweep_id = sid0 + j - 1;
+                sa.pdl = false;
+                sa.win = h->window && h->L.win.wmax ? &h->L.win : nullptr;
+                e = launch_sweep_tma(sa, s0, s1, s);
+                ++h->launches;
+            }
+            if (e == cudaSuccess) e = cudaEventRecord(fin[c - 1], s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(h->hs_out, fin[c - 1], 0);
+            int64_t r0, r1;
+            rows(c - 1, r0, r1);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(x_out_host + r0, xd + r0, (size_t)(r1 - r0) * sizeof(double),
+                                    cudaMemcpyDeviceToHost, h->hs_out);
+        }
+        if (e != cudaSuccess) return cuda_fail(h, e, "nsm_smooth_host (chunked passes)");
+    }
+    e = cudaEventRecord(ev1, h->hs_out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev1, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "nsm_smooth_host (device to host)");
+    *done = true;
+    return NSM_OK;
+}
+
 nsm_status nsm_smooth_host(nsm_handle *h, nsm_kind kind, const double *b_host, const double *x_in_host,
                            double *x_out_host, int nu, int k_l, int k_u, int x_is_zero, void *stream) {
     if (!h) return NSM_ERR_ARG;
@@ -1528,6 +1644,11 @@ nsm_status nsm_smooth_host(nsm_handle *h, nsm_kind kind, const double *b_host, c
         }
     }
     cudaStream_t s = S(stream);
+    if (kind == NSM_PGS && nu == 1 && !x_is_zero && x_in_host != x_out_host && h->chunked_host) {
+        bool done = false;
+        const nsm_status cst = smooth_host_chunked(h, b_host, x_in_host, x_out_host, k_l, s, &done);
+        if (cst != NSM_OK || done) return cst;
+    }
     const size_t nb = (size_t)h->n * sizeof(double);
     cudaError_t e = cudaSuccess;
     if (nb) {

@@ -85,3 +85,28 @@ def test_smooth_host_nu_zero():
         out3 = np.full(A.nrows, 7.0)
         S.smooth_host(b, x0, nu=0, out=out3)
         assert np.array_equal(out3, x0)
+
+
+@pytest.mark.parametrize("mat", ["var27_64", "lap_96", "cd_rcm_40"])
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_smooth_host_chunked_matches_device(mat, k):
+    """nsm_smooth_host in row chunks (copies overlapped with the passes,
+    NSM_OPT_HOST_CHUNKS, the default) is bit-identical to the device call and
+    to the unchunked host call; pinned host vectors."""
+    A = {"var27_64": lambda: inputs.var27(64), "lap_96": lambda: inputs.laplace(96, 96, 96),
+         "cd_rcm_40": lambda: inputs.convdiff(40)}[mat]()
+    b = torch.from_numpy(inputs.uniform(0, A.nrows)).pin_memory()
+    x0 = torch.from_numpy(inputs.uniform(1, A.nrows)).pin_memory()
+    with _smoother(A) as S:
+        xd = x0.cuda()
+        S.smooth(b.cuda(), xd, "pgs", nu=1, k_l=k)
+        want = xd.cpu().numpy()
+        out = torch.empty_like(x0).pin_memory()
+        S.smooth_host(b, x0, "pgs", nu=1, k_l=k, out=out)
+        assert np.array_equal(out.numpy(), want), f"{mat} k={k} chunked"
+        S.set_host_chunks(False)
+        out2 = torch.empty_like(x0).pin_memory()
+        S.smooth_host(b, x0, "pgs", nu=1, k_l=k, out=out2)
+        assert np.array_equal(out2.numpy(), want)
+        assert np.array_equal(x0.numpy(), inputs.uniform(1, A.nrows))   # x_in untouched
+        S.check()
