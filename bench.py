@@ -239,11 +239,12 @@ def flush_l2(buf):
 def workload_config(cfg: str, A, kind: str, k_l: int, k_u: int, nranks: int) -> dict:
     """The `config` object of the JSON line: the workload only, identical for
     the nsm arm and the reference arm (implementation details go elsewhere)."""
+    N = WORKLOADS[cfg][0]
     desc = WORKLOADS[cfg][4]
-    return {"workload": desc, "name": cfg, "n_per_gpu": int(A.nrows), "nnz_per_gpu": int(A.nnz), "kind": kind,
+    return {"workload": desc, "name": cfg, "grid_per_gpu": f"{N}^3", "n_per_gpu": int(A.nrows), "kind": kind,
             "k_l": k_l, "k_u": k_u, "nu": 1, "partition": "z-slab rows, HYBRID" if nranks > 1 else "none",
-            "l2": "flushed before every timed step (256 MB read through L2); the matrix alone is "
-                  f"{(12 * A.nnz) / 1e9:.1f} GB, far larger than the 126 MB L2"}
+            "l2": "flushed before every timed step (256 MB read through L2); the matrix is several GB, far "
+                  "larger than the 126 MB L2"}
 
 
 def cpu_oracle(A, kind: str, k_l: int, k_u: int, b, x0, ab: int, seconds: float, all_cores: bool,
@@ -290,10 +291,11 @@ def run_reference(args, rank, nranks):
     cpu = cpu_oracle(A, kind, k_l, k_u, b, x0, ab, 0.0, True, min_apps=args.steps)
     one = cpu_oracle(A, kind, k_l, k_u, b, x0, ab, 0.0, False, min_apps=1) if not args.no_cpu else None
     v, ms = cpu["value"], cpu["ms_per_apply"]
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": nranks,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.config, A, kind, k_l, k_u, 1),
+            "config": workload_config(args.config, A, kind, k_l, k_u, nranks),   # the nsm arm's object
+            "detail": {"nnz": int(A.nnz), "note": "the oracle runs the single-GPU workload on rank 0"},
             "cpu_baseline": {**cpu, "single_core": one},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -458,7 +460,8 @@ def run_nsm(args, rank, nranks, local_rank):
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args.config, A, kind, k_l, k_u, nranks),
-            "detail": {"kernels": ("plain register-blocked, one kernel per pass" if args.plain else
+            "detail": {"nnz_this_rank": int(A.nnz),
+                       "kernels": ("plain register-blocked, one kernel per pass" if args.plain else
                                    ("phase-skewed fused passes (k_skew, cp.async.bulk pipelined, persistent)" if fused
                                     else "cp.async.bulk pipelined (persistent), one kernel per pass")),
                        "bytes": ("algorithmic bytes of the path that ran (DESIGN.md §6): "

@@ -25,9 +25,9 @@ def test_reference_arm_json_line():
     # default workload = C3 (the largest single-GPU config); the config object
     # carries the workload only, the same keys as the nsm arm's
     assert line["config"]["name"] == "C3" and "27-point" in line["config"]["workload"]
-    assert set(line["config"]) == {"workload", "name", "n_per_gpu", "nnz_per_gpu", "kind", "k_l", "k_u", "nu",
+    assert set(line["config"]) == {"workload", "name", "grid_per_gpu", "n_per_gpu", "kind", "k_l", "k_u", "nu",
                                    "partition", "l2"}
-    assert line["config"]["n_per_gpu"] == 256 ** 3 and line["config"]["nnz_per_gpu"] == 449455096
+    assert line["config"]["n_per_gpu"] == 256 ** 3 and line["detail"]["nnz"] == 449455096
 
 
 def test_byte_models():
