@@ -635,7 +635,9 @@ __global__ void __launch_bounds__(kThreadsW, 2) k_fused_pgs_planes(const __grid_
                 }
                 __syncwarp();
             } else {
+#ifndef NSM_FW_NOWAIT   // timing experiment only: readiness skipped (results wrong)
                 if (sidx >= 2) wait_phase(sidx - 2, cur.w);   // phase j reads phase j - 1 of step w - 1
+#endif
                 t_need += ptx::globaltimer_ns() - tB;
                 stage_unit_w(p, sm, st, cur, K, lane, pol_first, pol_keep);
             }
