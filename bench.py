@@ -311,6 +311,8 @@ def run_nsm(args, rank, nranks, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if args.lib_variant:
+        nsm.load(variant=args.lib_variant)
     A, offsets, kind, k_l, k_u, desc = build_workload(args.config, rank, nranks)
     F = nsm.ilu0(A, row_begin=A.row_begin) if kind == "ilu" else None
     S = nsm.Smoother(A, F, device=local_rank, rank=rank, nranks=nranks, row_offsets=offsets)
@@ -497,6 +499,7 @@ def main():
     ap.add_argument("--plain", action="store_true", help="plain register-blocked kernels instead of the bulk-copy pipelined ones")
     ap.add_argument("--pdl", default="auto", choices=["auto", "on", "off"],
                     help="programmatic dependent launch (auto: the library's size-based default)")
+    ap.add_argument("--lib-variant", default="", help="A/B experiments: load libnsm_<variant>.so (build.py --variant)")
     ap.add_argument("--window", default="on", choices=["on", "off"],
                     help="shared-memory gather windows in the pipelined kernels (offset-aligned parts)")
     ap.add_argument("--fused", default="default", choices=["default", "auto", "on", "off", "onepass"],
