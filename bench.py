@@ -56,10 +56,7 @@ def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k
     def mb(count, part):  # bytes of `count` stored entries of a part
         return 8 * count + (count + 31) // 32 * 4 if layout.get(part) else 12 * count
 
-    # U with a transpose map (symmetric A, nsm_layout 'Ut'): the residual reads U's
-    # values from L (counted with L), staging 16 B of map + 4 B of positions per 32 entries
-    u_res = (nnz_u + 31) // 32 * 20 if layout.get("Ut") else mb(nnz_u, "U")
-    res = mb(nnz_l, "L") + u_res + 12 * (nnz_off - nnz_l - nnz_u) + 32 * n + 8 * n_ghost
+    res = mb(nnz_l, "L") + mb(nnz_u, "U") + 12 * (nnz_off - nnz_l - nnz_u) + 32 * n + 8 * n_ghost
     out = {}
     if kind == "pgs":
         # with sweeps following, the residual pass also writes g0 = r / d
@@ -209,14 +206,13 @@ def aligned_parts(A) -> dict:
     """Which strict triangles of A the library stores offset-aligned (the
     builder's criterion: the per-slice unions of column offsets widen the
     SELL-32 slices by at most 15 % with at most 3 % pads; nsm_layout reports
-    it for a handle), and 'Ut': whether U gets a transpose map (A bitwise
-    symmetric and the residual's gather window exists) —
+    it for a handle) —
     for the reference arm, which has no handle, to count the same bytes."""
     n = A.nrows
     rows = np.repeat(np.arange(n, dtype=np.int64) + A.row_begin, np.diff(A.rowptr))
     col = A.col.astype(np.int64)
     local = (col >= A.row_begin) & (col < A.row_begin + n)
-    out, pairs = {}, {}
+    out = {}
     for part, m in (("L", (col < rows) & local), ("U", (col > rows) & local)):
         r = rows[m] - A.row_begin
         off = col[m] - rows[m]
@@ -226,65 +222,11 @@ def aligned_parts(A) -> dict:
         c = np.zeros(ns * 32, dtype=np.int64)
         c[:n] = cnt
         compact = int(c.reshape(ns, 32).max(1).sum())
-        o0 = int(off.min()) if off.size else 0
-        u = np.unique(sl * (1 << 32) + (off - o0)) if off.size else np.zeros(0, np.int64)
-        uni = len(u)
+        uni = len(np.unique(sl * (1 << 32) + (off - off.min() if off.size else off))) if off.size else 0
         pads = uni * 32 - int(m.sum())
         out[part] = compact > 0 and uni * 100 <= compact * 115 and pads * 100 <= uni * 32 * 3
-        pairs[part] = (u >> 32, (u & ((1 << 32) - 1)) + o0)       # (slice, offset) of every stored slot
     out["Ls"], out["Us"] = out["L"], out["U"]   # ILU(0) factors share A's pattern
-    out["Ut"] = bool(out["L"] and out["U"] and symmetric_local(A) and residual_window(n, pairs))
     return out
-
-
-def symmetric_local(A) -> bool:
-    """A(i, j) == A(j, i) bit for bit over the row block's local columns: the
-    generator's guarantee where it gives one (inputs.CSR.symmetric), else
-    checked (small matrices)."""
-    if A.symmetric is not None:
-        return bool(A.symmetric)
-    if A.nnz > 20_000_000:
-        return False
-    import scipy.sparse as sp
-    r0, n = A.row_begin, A.nrows
-    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(A.rowptr))
-    loc = (A.col >= r0) & (A.col < r0 + n)
-    bits = A.val.view(np.int64)[loc]
-    M = sp.csr_matrix((bits, (rows[loc], A.col[loc] - r0)), shape=(n, n))
-    M.sort_indices()
-    T = M.T.tocsr()
-    T.sort_indices()
-    return (np.array_equal(M.indptr, T.indptr) and np.array_equal(M.indices, T.indices)
-            and np.array_equal(M.data, T.data))
-
-
-def residual_window(n: int, pairs: dict, wcap: int = 8192) -> bool:
-    """Mirror of builder.cpp build_window for the residual's (L, U) pair: per
-    256-row tile the gathered column ranges [32 s + o, + 32] (even-aligned)
-    merged with gaps of up to 32, at most wcap doubles and 32 segments per
-    tile, and all windows together at most half the staged entries."""
-    s = np.concatenate([pairs["L"][0], pairs["U"][0]])
-    o = np.concatenate([pairs["L"][1], pairs["U"][1]])
-    if s.size == 0:
-        return False
-    lo = 32 * s + o
-    lo, hi = lo & ~1, (lo + 33) & ~1
-    tile = s // 8
-    order = np.lexsort((lo, tile))
-    lo, hi, tile = lo[order], hi[order], tile[order]
-    big = np.int64(1) << 40
-    cmax = np.maximum.accumulate(tile * big + (hi + (1 << 39))) - tile * big - (1 << 39)
-    prev = np.concatenate([[np.iinfo(np.int64).min // 2], cmax[:-1]])
-    new = np.ones(lo.size, bool)
-    new[1:] = (tile[1:] != tile[:-1]) | (lo[1:] > prev[1:] + 32)
-    starts = np.flatnonzero(new)
-    seg_len = np.maximum.reduceat(hi, starts) - lo[starts]
-    seg_tile = tile[starts]
-    per_tile = np.bincount(seg_tile, weights=seg_len)
-    nseg = np.bincount(seg_tile)
-    if per_tile.max() > wcap or nseg.max() > 32:
-        return False
-    return bool(seg_len.sum() * 2 <= 32 * s.size)
 
 
 def flush_l2(buf):
@@ -386,14 +328,10 @@ def run_nsm(args, rank, nranks, local_rank):
         S.set_pdl(args.pdl == "on")
     if args.window == "off":
         S.set_window(False)
-    if args.sym == "off":
-        S.set_symmetric(False)
     if nranks > 1:
         S.connect(dist)
     nl, nu_, noff = split_counts(A)
     layout = S.layout()
-    if args.sym == "off" or args.window == "off" or args.plain:
-        layout["Ut"] = False     # the residual streams U
     model = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost, layout)   # one kernel per pass
     fmodel = floor_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost)       # fused passes / floor
     b = torch.from_numpy(inputs.uniform(inputs.SEED_B, A.nrows, idx0=A.row_begin)).to(dev)
@@ -562,8 +500,6 @@ def main():
     ap.add_argument("--pdl", default="auto", choices=["auto", "on", "off"],
                     help="programmatic dependent launch (auto: the library's size-based default)")
     ap.add_argument("--lib-variant", default="", help="A/B experiments: load libnsm_<variant>.so (build.py --variant)")
-    ap.add_argument("--sym", default="on", choices=["on", "off"],
-                    help="symmetric A: the residual reads U = L^T from L (off: stream U; A/B)")
     ap.add_argument("--window", default="on", choices=["on", "off"],
                     help="shared-memory gather windows in the pipelined kernels (offset-aligned parts)")
     ap.add_argument("--fused", default="default", choices=["default", "auto", "on", "off", "onepass"],

@@ -334,8 +334,7 @@ nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *hal
  * set when A's L / A's U / the factor's L_s / U_s uses the offset-aligned
  * SELL layout (stencil-like rows: one int32 column offset per slice entry
  * position; the pipelined kernels then read 8 instead of 12 bytes per entry).
- * Chosen automatically at setup when it widens the slices by <= 15 %.
- * Bit 16: U has a transpose map (A bitwise symmetric; NSM_OPT_SYMMETRIC). */
+ * Chosen automatically at setup when it widens the slices by <= 15 %. */
 nsm_status nsm_layout(const nsm_handle *h, int *offset_aligned);
 
 /* Fused-pass synchronisation statistics since setup: work items whose
@@ -409,13 +408,7 @@ typedef enum {
     NSM_OPT_HOST_CHUNKS = 8 /* 1 (default): nsm_smooth_host runs a single-rank forward pGS application
                              * (nu = 1, k <= 3, x_in != x_out) in row chunks longer than A's bandwidth, so
                              * the host-to-device copies, the passes and the device-to-host copy overlap
-                             * (separate copy streams); 0: copy in, smooth, copy out.  Same results. */,
-    NSM_OPT_SYMMETRIC = 9   /* 1 (default): when A is symmetric bit for bit (A(i,j) == A(j,i) for every stored
-                             * entry, same pattern; checked on the device at set-up for offset-aligned L and
-                             * U with a gather window), the residual r = b - (L + D + U) x reads
-                             * U's values from L (U = L^T) instead of streaming U: about half the residual's
-                             * matrix bytes.  0: stream U.  Same results (the same products in the same
-                             * order); nsm_layout reports whether the transpose map exists. */
+                             * (separate copy streams); 0: copy in, smooth, copy out.  Same results. */
 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 

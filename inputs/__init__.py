@@ -72,10 +72,6 @@ class CSR:
     col: np.ndarray
     val: np.ndarray
     row_begin: int = 0
-    # A(i, j) == A(j, i) bit for bit over the whole matrix, when the generator
-    # guarantees it by construction (None: unknown).  Metadata for bench.py's
-    # byte count only (tests/test_inputs_symmetry.py pins it on small grids).
-    symmetric: bool | None = None
 
     @property
     def nnz(self) -> int:
@@ -114,13 +110,13 @@ def uniform_int(seed: int, n: int, bits: int = 20, idx0: int = 0) -> np.ndarray:
 
 
 # ----------------------------------------------------------------- matrices --
-def _fill(nnz_fn, fill_fn, nrows, ncols, row_begin, symmetric=None) -> CSR:
+def _fill(nnz_fn, fill_fn, nrows, ncols, row_begin, *args) -> CSR:
     nnz = nnz_fn()
     rp = np.empty(nrows + 1, dtype=np.int64)
     ci = np.empty(nnz, dtype=np.int64)
     va = np.empty(nnz, dtype=np.float64)
     fill_fn(rp, ci, va)
-    return CSR(nrows, ncols, rp, ci, va, row_begin, symmetric)
+    return CSR(nrows, ncols, rp, ci, va, row_begin)
 
 
 def laplace(nx: int, ny: int, nz: int = 1, r0: int = 0, r1: int | None = None) -> CSR:
@@ -132,7 +128,7 @@ def laplace(nx: int, ny: int, nz: int = 1, r0: int = 0, r1: int | None = None) -
     L = _L()
     return _fill(lambda: L.gen_lap_nnz(nx, ny, nz, dim, r0, r1),
                  lambda rp, ci, va: L.gen_lap_fill(nx, ny, nz, dim, r0, r1, _p(rp), _p(ci), _p(va)),
-                 r1 - r0, n, r0, True)
+                 r1 - r0, n, r0)
 
 
 def kappa_field(nx: int, ny: int, nz: int, seed: int = SEED_FIELD, contrast: float = 1e4) -> np.ndarray:
@@ -150,7 +146,7 @@ def var27(N: int, seed: int = SEED_FIELD, contrast: float = 1e4, r0: int = 0, r1
     L = _L()
     return _fill(lambda: L.gen_var27_nnz(N, N, N, r0, r1),
                  lambda rp, ci, va: L.gen_var27_fill(N, N, N, _p(kap), r0, r1, _p(rp), _p(ci), _p(va)),
-                 r1 - r0, n, r0, True)
+                 r1 - r0, n, r0)
 
 
 def var27_grid(nx: int, ny: int, nz: int, r0: int = 0, r1: int | None = None, seed: int = SEED_FIELD,
@@ -163,7 +159,7 @@ def var27_grid(nx: int, ny: int, nz: int, r0: int = 0, r1: int | None = None, se
     L = _L()
     return _fill(lambda: L.gen_var27_nnz(nx, ny, nz, r0, r1),
                  lambda rp, ci, va: L.gen_var27_fill(nx, ny, nz, _p(kap), r0, r1, _p(rp), _p(ci), _p(va)),
-                 r1 - r0, n, r0, True)
+                 r1 - r0, n, r0)
 
 
 def var27_slab(N: int, nranks: int, rank: int) -> CSR:

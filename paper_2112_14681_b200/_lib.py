@@ -567,10 +567,6 @@ class Smoother:
         """NSM_OPT_HOST_CHUNKS: nsm_smooth_host overlaps copies and passes in row chunks."""
         self._call(load().nsm_set_option(self._h, 8, int(bool(enable))))
 
-    def set_symmetric(self, enable: bool):
-        """NSM_OPT_SYMMETRIC: the residual reads U = L^T from L when A is bitwise symmetric."""
-        self._call(load().nsm_set_option(self._h, 9, int(bool(enable))))
-
     def set_pdl(self, enable: bool):
         """Programmatic dependent launch between consecutive pipelined kernels."""
         self._call(load().nsm_set_option(self._h, 3, int(bool(enable))))
@@ -588,11 +584,10 @@ class Smoother:
                 "fused": (float(ms[2]), int(cnt[2]))}
 
     def layout(self):
-        """{'L', 'U', 'Ls', 'Us'}: which strict parts use the offset-aligned layout;
-        'Ut': U has a transpose map (A bitwise symmetric: the residual reads U = L^T from L)."""
+        """{'L', 'U', 'Ls', 'Us'}: which strict parts use the offset-aligned layout."""
         v = ctypes.c_int(0)
         self._call(load().nsm_layout(self._h, ctypes.byref(v)))
-        return {k: bool(v.value & b) for k, b in (("L", 1), ("U", 2), ("Ls", 4), ("Us", 8), ("Ut", 16))}
+        return {k: bool(v.value & b) for k, b in (("L", 1), ("U", 2), ("Ls", 4), ("Us", 8))}
 
     def fused_stats(self):
         """(waits that had to spin, total spin ns) of the fused passes since setup."""

@@ -53,7 +53,6 @@ struct nsm_handle {
     int64_t plane_tiles = 0;   // NSM_OPT_PLANE_ROWS / 256 when the plane-wavefront check passed
     bool window = true;        // NSM_OPT_WINDOW: windowed pipelined kernels where a window exists
     bool chunked_host = true;  // NSM_OPT_HOST_CHUNKS: nsm_smooth_host overlaps copies and passes
-    bool sym = true;           // NSM_OPT_SYMMETRIC: residual reads U = L^T from L where U.tmap exists
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
     int nslices = 0;
     // A = L + D + U (+ ghost couplings LG / UG)
@@ -168,7 +167,6 @@ void free_sell(Sell &s) {
     cudaFree(s.col);
     cudaFree(s.val);
     cudaFree(s.off);
-    cudaFree(s.tmap);
     free_window(s.win);
     s = Sell();
 }
@@ -192,13 +190,6 @@ bool make_window(DevAlloc &a, int64_t n, const std::vector<const SellHost *> &pa
     w->wmax = wh.wmax;
     w->maxseg = wh.maxseg;
     return true;
-}
-
-// U's transpose map of a symmetric A (transpose.cu), for the windowed
-// residual: absent (no error) when A is not bitwise symmetric.
-bool make_tmap(nsm_handle *h) {
-    bool built = false;
-    return build_tmap(h->n, h->L, &h->U, &h->device_bytes, &built) == cudaSuccess;
 }
 
 void free_handle(nsm_handle *h) {
@@ -431,8 +422,7 @@ nsm_status residual_into(nsm_handle *h, const double *b, const double *x, double
         if (use_pipelined(h, sl, with_ghost, 2, std::max(h->L.maxw, h->U.maxw)))
             return launch_residual_tma((h->window && h->res_win.wmax && sl.begin >= 0 && sl.begin % kTileSlices == 0)
                                            ? &h->res_win : nullptr,
-                                       mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s,
-                                       h->sym);
+                                       mode, h->n, sl.begin, sl.end, h->L, h->U, h->d, b, x, out, out2, h->pdl, s);
         return launch_residual(mode, h->n, sl.count, sl.list, h->LG, h->L, h->U, h->UG, with_ghost, h->d, b, x, ghost,
                                out, out2, h->pdl, s);
     }, 0);
@@ -682,7 +672,6 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
              make_window(a, h->n, {&sa.U}, &h->U.win);
         if (ok && F) ok = make_window(a, h->n, {&sf.L}, &h->Ls.win) && make_window(a, h->n, {&sf.U}, &h->Us.win);
     }
-    if (ok && h->res_win.wmax) ok = make_tmap(h);  // symmetric A: U's transpose map (transpose.cu)
     for (int i = 0; ok && i < 4; ++i) ok = a.get(&h->w[i], std::max<int64_t>(h->n, 1));
     ok = ok && a.get(&h->flag, 1) && a.get(&h->ghost_null, 1) && a.get(&h->d_dist_err, 1) &&
          cudaMemset(h->d_dist_err, 0, sizeof(unsigned int)) == cudaSuccess;
@@ -801,7 +790,6 @@ nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F
     ok = ok && make_window(a, h->n, {&sa.Lh, &sa.Uh}, &h->res_win) && make_window(a, h->n, {&sa.Lh}, &h->L.win) &&
          make_window(a, h->n, {&sa.Uh}, &h->U.win);
     if (ok && F) ok = make_window(a, h->n, {&sf.Lh}, &h->Ls.win) && make_window(a, h->n, {&sf.Uh}, &h->Us.win);
-    if (ok && h->res_win.wmax) ok = make_tmap(h);
     for (int i = 0; ok && i < 4; ++i) ok = a.get(&h->w[i], std::max<int64_t>(h->n, 1));
     ok = ok && a.get(&h->flag, 1) && a.get(&h->ghost_null, 1) && a.get(&h->d_dist_err, 1) &&
          cudaMemset(h->d_dist_err, 0, sizeof(unsigned int)) == cudaSuccess;
@@ -994,7 +982,6 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
         case NSM_OPT_PDL: h->pdl = value != 0; return NSM_OK;
         case NSM_OPT_WINDOW: h->window = value != 0; return NSM_OK;
         case NSM_OPT_HOST_CHUNKS: h->chunked_host = value != 0; return NSM_OK;
-        case NSM_OPT_SYMMETRIC: h->sym = value != 0; return NSM_OK;
         case NSM_OPT_PLANE_ROWS:
             if (value < 0 || value % 256) return NSM_ERR_ARG;
             h->plane_tiles = 0;
@@ -1108,8 +1095,7 @@ nsm_status nsm_set_ruiz(nsm_handle *h, const double *s_r, const double *s_c) {
 
 nsm_status nsm_layout(const nsm_handle *h, int *offset_aligned) {
     if (!h || !offset_aligned) return NSM_ERR_ARG;
-    *offset_aligned = (h->L.off ? 1 : 0) | (h->U.off ? 2 : 0) | (h->Ls.off ? 4 : 0) | (h->Us.off ? 8 : 0) |
-                      (h->U.tmap ? 16 : 0);
+    *offset_aligned = (h->L.off ? 1 : 0) | (h->U.off ? 2 : 0) | (h->Ls.off ? 4 : 0) | (h->Us.off ? 8 : 0);
     return NSM_OK;
 }
 
@@ -1578,7 +1564,7 @@ static nsm_status smooth_host_chunked(nsm_handle *h, const double *b_host, const
             slices(c, s0, s1);
             if (e == cudaSuccess)
                 e = launch_residual_tma(h->window && h->res_win.wmax ? &h->res_win : nullptr, OUT_RG, h->n, s0, s1,
-                                        h->L, h->U, h->d, bd, xd, R, G0, false, s, h->sym);
+                                        h->L, h->U, h->d, bd, xd, R, G0, false, s);
             ++h->launches;
         }
         if (c >= 1 && e == cudaSuccess) {  // the k sweeps of chunk c-1, the last with x += g

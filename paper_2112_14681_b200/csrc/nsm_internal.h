@@ -75,14 +75,6 @@ struct Sell {
     int64_t nnz = 0;          // real entries
     int32_t maxw = 0;         // widest slice
     Window win;               // gather window of sweeps over this part alone (offset-aligned only)
-    // Transpose map (U of a symmetric A only; transpose.cu): for slot j of
-    // slice s (offset o > 0), tmap[s * tmap_w + j] locates the 32 values
-    // A(i + o, i) of the slice's rows i in L's value array, so a kernel can
-    // read U = L^T from L instead of streaming U (tmap_addr below); dense per
-    // slice (tmap_w = maxw) so a kernel finds a slice's entries without ptr.
-    // nullptr: no map (A not bitwise symmetric, compact layout, L too large).
-    int2 *tmap = nullptr;
-    int32_t tmap_w = 0;
     bool empty() const { return padded == 0; }
 };
 
@@ -102,35 +94,9 @@ struct SellView {
     const int32_t *col;
     const double *val;
     const int32_t *off;
-    const int2 *tmap;
-    int32_t tmap_w;
 };
 
-inline SellView view(const Sell &s) { return SellView{s.ptr, s.col, s.val, s.off, s.tmap, s.tmap_w}; }
-
-// Decoding of one transpose-map entry {a, b} for lane l: the mirrored rows
-// 32 s + o + l fall into L's slices sa = (32 s + o) / 32 and sa + 1, with
-// sh = (32 s + o) % 32.  a = index of lane 0's value in slice sa's slot for
-// offset -o (= that slot's start + sh; start a multiple of 32), or
-// INT32_MIN | sh when slice sa has no such slot; b = slice sa + 1's slot
-// start + sh - 32, or INT32_MIN.  Lanes l < 32 - sh read L.val[a + l], the
-// others L.val[b + l]; an index below -32 means "no entry": value 0.
-#ifdef __CUDACC__
-__device__ __forceinline__ int32_t tmap_base(int32_t a, int32_t b, int lane) {
-    return lane + (a & 31) < 32 ? a : b;
-}
-__device__ __forceinline__ int64_t tmap_addr(int32_t a, int32_t b, int lane) {
-    const int32_t base = tmap_base(a, b, lane);
-    return base >= -32 ? (int64_t)base + lane : -1;
-}
-#endif
-
-// U's transpose map (transpose.cu): built when L and U are offset-aligned,
-// U's slices are at most 16 wide, L has fewer than 2^31 stored entries, and every stored value of U (pads
-// included) equals, bit for bit, the value the map reads from L
-// (A(i, j) = A(j, i) with the same pattern).  *built = false (and
-// U.tmap = nullptr) otherwise.  Device bytes are added to *bytes.
-cudaError_t build_tmap(int64_t n, const Sell &L, Sell *U, int64_t *bytes, bool *built);
+inline SellView view(const Sell &s) { return SellView{s.ptr, s.col, s.val, s.off}; }
 
 // Gather-window plan of offset-aligned parts (builder.cpp): false if a
 // tile's window would exceed wcap doubles or 32 segments.
@@ -227,10 +193,9 @@ cudaError_t launch_halo_wait(const unsigned long long *flags, const int *peers, 
 // ---- bulk-copy pipelined kernels (stream.cu), contiguous slice ranges --------
 bool tma_ok(int np, int maxw);
 // win: gather window of (L, U) for the full slice range (or nullptr).
-// sym: read U's values from L through U.tmap where the map exists (windowed kernels).
 cudaError_t launch_residual_tma(const Window *win, int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
                                 const Sell &U, const double *d, const double *b, const double *x, double *out,
-                                double *out2, bool pdl, cudaStream_t st, bool sym = false);
+                                double *out2, bool pdl, cudaStream_t st);
 cudaError_t launch_sweep_tma(const SweepArgs &a, int64_t s_begin, int64_t s_end, cudaStream_t st);
 
 // ---- phase-skewed fused passes (fused.cu) ---------------------------------------

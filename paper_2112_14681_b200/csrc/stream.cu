@@ -85,27 +85,26 @@ struct Layout {
     __host__ __device__ static int64_t part_bytes(int64_t cap, int eb) {
         return eb == 12 ? cap * 12 : cap * 8 + ofs_bytes(cap) + kHdrBytes;
     }
-    __device__ __forceinline__ char *base(char *s, int st, int p) const {
-        return s + 128 + ((int64_t)st * np + p) * part_bytes(cap, eb);
-    }
     __device__ __forceinline__ int32_t *hdr(char *s, int st, int p) const {  // eb 8 only
-        return (int32_t *)(base(s, st, p) + cap * 8 + ofs_bytes(cap));
+        return (int32_t *)(s + 128 + ((int64_t)st * np + p) * part_bytes(cap, eb) + cap * 8 + ofs_bytes(cap));
     }
     __device__ __forceinline__ uint64_t *full(char *s) const { return (uint64_t *)s; }
     __device__ __forceinline__ uint64_t *empty(char *s) const { return (uint64_t *)s + nst; }
-    __device__ __forceinline__ double *val(char *s, int st, int p) const { return (double *)base(s, st, p); }
+    __device__ __forceinline__ double *val(char *s, int st, int p) const {
+        return (double *)(s + 128 + ((int64_t)st * np + p) * part_bytes(cap, eb));
+    }
     __device__ __forceinline__ int32_t *col(char *s, int st, int p) const {   // eb 12: columns; eb 8: offsets
-        return (int32_t *)(base(s, st, p) + cap * 8);
+        return (int32_t *)(s + 128 + ((int64_t)st * np + p) * part_bytes(cap, eb) + cap * 8);
     }
     __device__ __forceinline__ double *win(char *s, int st) const {
         return (double *)(s + 128 + (int64_t)nst * np * part_bytes(cap, eb)) + (int64_t)st * wcap;
     }
 };
 
-__device__ __forceinline__ void init_barriers(const Layout &Ly, char *sm, int full_arrivals = 1) {
+__device__ __forceinline__ void init_barriers(const Layout &Ly, char *sm) {
     if (threadIdx.x == 0) {
         for (int st = 0; st < Ly.nst; ++st) {
-            mbar_init(Ly.full(sm) + st, full_arrivals);
+            mbar_init(Ly.full(sm) + st, 1);
             mbar_init(Ly.empty(sm) + st, kTS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -131,22 +130,7 @@ struct TileRefs {
     // windowed kernels: this tile's gather-window segments, lane k holds segment k
     int32_t nseg, sg_len, sg_base;
     int64_t sg_lo;
-    int2 tm[kTS / 2];  // symmetric residual: the tile's transpose-map entries lane + 32 g (at most 4 x 32 used)
 };
-
-// Symmetric residual: the transpose-map entries of a tile (dense per slice,
-// nq = slices x tmap_w <= 128 of them), one per lane and group of 32.
-template <int NP>
-__device__ __forceinline__ void tile_tmap(const SellView (&P)[NP], int64_t s_begin, int64_t s_end, int64_t t,
-                                          int lane, TileRefs<NP> &r) {
-    const int tw = P[1].tmap_w;
-    const int64_t s0 = s_begin + t * kTS;
-    const int nq = (int)(min(s0 + kTS, s_end) - s0) * tw;
-    const int2 *tm = P[1].tmap + s0 * tw;
-#pragma unroll
-    for (int g = 0; g < kTS / 2; ++g)
-        r.tm[g] = lane + 32 * g < nq ? __ldg(tm + lane + 32 * g) : make_int2(INT32_MIN, INT32_MIN);
-}
 
 // Entry-position arrays staged into the "offsets" slot: the column offsets,
 // or (windowed kernels) the gather-window positions.
@@ -228,16 +212,7 @@ __device__ __forceinline__ void producer_compact(const Layout &Ly, char *sm, con
 // and writes the rest itself (zeros outside [0, n), an odd last element).
 // `vec` is written by the previous kernel, so with programmatic dependent
 // launch the producer waits for it before the first window copy.
-//
-// SYMU (symmetric residual): part 1's (U's) values are not bulk-copied; the
-// producer lanes fill U's value area with U = L^T read from L's values
-// through U's transpose map (transpose.cu): 8-byte asynchronous copies
-// (LDGSTS) of the mirrored entries — mostly L2 hits, L's values of the next
-// rows being streamed by the CTAs working ahead — whose completion each lane
-// reports to the stage's full barrier (cp.async.mbarrier.arrive.noinc; the
-// barrier expects 1 + 32 arrivals).  Layout [slice][j][lane], slice stride
-// tmap_w x 32, so consumers read them exactly like staged U values.
-template <int NP, bool WIN = false, bool SYMU = false>
+template <int NP, bool WIN = false>
 __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellView (&P)[NP], int64_t s_begin,
                                          int64_t s_end, int64_t ntiles, int lane, const WinView &W = WinView{},
                                          const double *vec = nullptr, int64_t n = 0) {
@@ -247,20 +222,13 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
     uint32_t ph = 0;  // (it / nst) & 1
     TileRefs<NP> cur, nxt;
     if (WIN) pdl_wait();
-    if ((int64_t)blockIdx.x < ntiles) {
-        tile_refs<NP>(Ly, P, s_begin, s_end, blockIdx.x, lane, cur, W, WIN);
-        if constexpr (SYMU) tile_tmap<NP>(P, s_begin, s_end, blockIdx.x, lane, cur);
-    }
+    if ((int64_t)blockIdx.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, blockIdx.x, lane, cur, W, WIN);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        if (t + gridDim.x < ntiles) {  // prefetch
-            tile_refs<NP>(Ly, P, s_begin, s_end, t + gridDim.x, lane, nxt, W, WIN);
-            if constexpr (SYMU) tile_tmap<NP>(P, s_begin, s_end, t + gridDim.x, lane, nxt);
-        }
+        if (t + gridDim.x < ntiles) tile_refs<NP>(Ly, P, s_begin, s_end, t + gridDim.x, lane, nxt, W, WIN);  // prefetch
         if (it >= Ly.nst) mbar_wait(Ly.empty(sm) + st, ph ^ 1);
         uint32_t bytes = 0;
 #pragma unroll
-        for (int p = 0; p < NP; ++p)
-            bytes += (uint32_t)((SYMU && p == 1) ? 0 : (cur.e[p] - cur.b[p]) * Ly.eb);
+        for (int p = 0; p < NP; ++p) bytes += (uint32_t)((cur.e[p] - cur.b[p]) * Ly.eb);
         int64_t wa = 0;         // this lane's window segment: bulk part [wa, wa + wbytes / 8)
         uint32_t wbytes = 0;
         if (WIN && lane < cur.nseg) {
@@ -309,7 +277,7 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
                 const int64_t b = cur.b[p], e = cur.e[p];
-                if (e > b && !(SYMU && p == 1)) {
+                if (e > b) {
                     bulk_g2s(Ly.val(sm, st, p), P[p].val + b, (uint32_t)((e - b) * 8), Ly.full(sm) + st, pol);
                     if (Ly.eb == 12)
                         bulk_g2s(Ly.col(sm, st, p), P[p].col + b, (uint32_t)((e - b) * 4), Ly.full(sm) + st, pol);
@@ -321,28 +289,6 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
             if (wbytes)
                 bulk_g2s(Ly.win(sm, st) + cur.sg_base + (wa - cur.sg_lo), vec + wa, wbytes, Ly.full(sm) + st, pol_win);
         }
-        if constexpr (SYMU) {
-            const int64_t s0 = s_begin + t * kTS;
-            const int nq = (int)(min(s0 + kTS, s_end) - s0) * P[1].tmap_w;  // map entries of the tile (<= 128)
-            double *mir = Ly.val(sm, st, 1);
-#pragma unroll
-            for (int g = 0; g < kTS / 2; ++g) {
-                if (32 * g >= nq) break;
-                const int lim = min(32, nq - 32 * g);
-#pragma unroll
-                for (int l = 0; l < 32; ++l) {  // unrolled: the shuffles and copies of all entries overlap
-                    if (l >= lim) break;
-                    const int32_t a = __shfl_sync(0xffffffffu, cur.tm[g].x, l);
-                    const int32_t b = __shfl_sync(0xffffffffu, cur.tm[g].y, l);
-                    const int32_t base = tmap_base(a, b, lane);
-                    const bool ok = base >= -32;
-                    ptx::cp_async8_zfill(mir + (int64_t)(32 * g + l) * kSlice + lane, ok ? P[0].val + base + lane : P[0].val,
-                                         ok ? 8u : 0u);
-                }
-            }
-            ptx::cp_async_mbar_arrive_noinc(Ly.full(sm) + st);
-        }
-
         __syncwarp();
         cur = nxt;
         if (++st == Ly.nst) { st = 0; ph ^= 1; }
@@ -460,7 +406,7 @@ struct WinChunk {
     }
 };
 
-template <int OUT, int CH, bool OFS, bool WIN, bool SYM = false>
+template <int OUT, int CH, bool OFS, bool WIN>
 __device__ __forceinline__ void residual_tma_body(int64_t n, int64_t s_begin, int64_t s_end, SellView L, SellView U,
                                                   const double *__restrict__ d, const double *__restrict__ b,
                                                   const double *__restrict__ x, double *__restrict__ out,
@@ -468,14 +414,13 @@ __device__ __forceinline__ void residual_tma_body(int64_t n, int64_t s_begin, in
     extern __shared__ __align__(128) char sm[];
     constexpr bool ofs = OFS;
     static_assert(!WIN || OFS, "windowed kernels need the offset-aligned layout");
-    static_assert(!SYM || WIN, "the symmetric residual is a windowed kernel");
     const Layout Ly{nst, 2, cap, ofs ? 8 : 12, WIN ? (int64_t)W.wcap : 0};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
-    init_barriers(Ly, sm, SYM ? 1 + 32 : 1);  // SYM: + the producer lanes' cp.async arrivals
+    init_barriers(Ly, sm);
     if (warp == kTS) {
         const SellView P[2] = {L, U};
-        if constexpr (OFS) producer<2, WIN, SYM>(Ly, sm, P, s_begin, s_end, ntiles, lane, W, x, n);
+        if constexpr (OFS) producer<2, WIN>(Ly, sm, P, s_begin, s_end, ntiles, lane, W, x, n);
         else if (lane == 0) producer_compact<2>(Ly, sm, P, s_begin, s_end, ntiles);
         return;
     }
@@ -513,27 +458,7 @@ __device__ __forceinline__ void residual_tma_body(int64_t n, int64_t s_begin, in
             ou.at(Ly.col(sm, st, 1), uo);
         }
         double acc = 0.0;
-        if constexpr (SYM) {  // U's values: the producer's mirror copies, [slice][j][lane] in U's value area
-            if (has) {
-                const double *ws = Ly.win(sm, st);
-                const double *mir = Ly.val(sm, st, 1) + ((int64_t)warp * U.tmap_w * kSlice - uo);
-                if constexpr (CH <= 8) {
-                    WinChunk<CH> cl, cu;
-                    cl.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), ws, lo, lw, lane, row);
-                    cu.load(mir, Ly.col(sm, st, 1), ws, uo, uw, lane, row);
-                    acc = cl.add(acc);
-                    acc = __dadd_rn(acc, __dmul_rn(di, xi));
-                    acc = cu.add(acc);
-                } else {
-                    WinChunk<CH> c;
-                    c.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), ws, lo, lw, lane, row);
-                    acc = c.add(acc);
-                    acc = __dadd_rn(acc, __dmul_rn(di, xi));
-                    c.load(mir, Ly.col(sm, st, 1), ws, uo, uw, lane, row);
-                    acc = c.add(acc);
-                }
-            }
-        } else if constexpr (WIN) {
+        if constexpr (WIN) {
             if (has) {
                 const double *ws = Ly.win(sm, st);
                 if constexpr (CH <= 8) {
@@ -623,15 +548,6 @@ __global__ void __launch_bounds__(kThreadsT, CH <= 8 ? 3 : 2)
                      const double *__restrict__ b, const double *__restrict__ x, double *__restrict__ out,
                      double *__restrict__ out2, int nst, int64_t cap, WinView W) {
     residual_tma_body<OUT, CH, true, true>(n, s_begin, s_end, L, U, d, b, x, out, out2, nst, cap, W);
-}
-
-// Symmetric windowed variant: U's values from L through U's transpose map.
-template <int OUT, int CH>
-__global__ void __launch_bounds__(kThreadsT, CH <= 8 ? 3 : 2)
-    k_residual_tma_ws(int64_t n, int64_t s_begin, int64_t s_end, SellView L, SellView U, const double *__restrict__ d,
-                      const double *__restrict__ b, const double *__restrict__ x, double *__restrict__ out,
-                      double *__restrict__ out2, int nst, int64_t cap, WinView W) {
-    residual_tma_body<OUT, CH, true, true, true>(n, s_begin, s_end, L, U, d, b, x, out, out2, nst, cap, W);
 }
 
 __device__ __forceinline__ const double *gathered(const GatherPlainT &g) { return g.g; }
@@ -823,11 +739,11 @@ WinView win_view(const Window *w) {
     return WinView{w->tseg, w->glo, w->len, w->sbase, {w->wpos[0], w->wpos[1]}, (w->wmax + 31) / 32 * 32};
 }
 
-template <int OUT, int CH, bool OFS, bool WIN, bool SYM = false>
+template <int OUT, int CH, bool OFS, bool WIN>
 cudaError_t residual_tma_ofs(const Window *w, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
                              const double *d, const double *b, const double *x, double *out, double *out2,
                              bool pdl, cudaStream_t st) {
-    auto k = SYM ? k_residual_tma_ws<OUT, CH> : (WIN ? k_residual_tma_w<OUT, CH> : k_residual_tma<OUT, CH, OFS>);
+    auto k = WIN ? k_residual_tma_w<OUT, CH> : k_residual_tma<OUT, CH, OFS>;
     const WinView W = win_view(WIN ? w : nullptr);
     const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw), OFS ? 8 : 12, (int64_t)W.wcap * 8);
     if (!g.nst) return cudaErrorInvalidConfiguration;
@@ -839,12 +755,9 @@ cudaError_t residual_tma_ofs(const Window *w, int64_t n, int64_t s_begin, int64_
 template <int OUT, int CH>
 cudaError_t residual_tma_ch(const Window *w, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L, const Sell &U,
                             const double *d, const double *b, const double *x, double *out, double *out2,
-                            bool pdl, cudaStream_t st, bool sym) {
+                            bool pdl, cudaStream_t st) {
     // offset-aligned layout (both triangles): stage values only, columns = row + offset;
-    // with a gather window over the whole range: gathers from shared memory;
-    // a symmetric A (U's transpose map): U's values read from L
-    if (L.off && U.off && w && s_begin % kTS == 0 && sym && U.tmap)
-        return residual_tma_ofs<OUT, CH, true, true, true>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
+    // with a gather window over the whole range: gathers from shared memory
     if (L.off && U.off && w && s_begin % kTS == 0)
         return residual_tma_ofs<OUT, CH, true, true>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st);
     if (L.off && U.off)
@@ -906,13 +819,13 @@ bool tma_ok(int np, int maxw) {
 
 cudaError_t launch_residual_tma(const Window *w, int out_mode, int64_t n, int64_t s_begin, int64_t s_end, const Sell &L,
                                 const Sell &U, const double *d, const double *b, const double *x, double *out,
-                                double *out2, bool pdl, cudaStream_t st, bool sym) {
+                                double *out2, bool pdl, cudaStream_t st) {
     if (s_end <= s_begin) return cudaSuccess;
     const int ch = chunk_for_t(std::max(L.maxw, U.maxw));
-#define NSM_RT(OUT)                                                                                       \
-    (ch == 4 ? residual_tma_ch<OUT, 4>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st, sym)           \
-             : ch == 8 ? residual_tma_ch<OUT, 8>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st, sym) \
-                       : residual_tma_ch<OUT, 16>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st, sym))
+#define NSM_RT(OUT)                                                                                  \
+    (ch == 4 ? residual_tma_ch<OUT, 4>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st)           \
+             : ch == 8 ? residual_tma_ch<OUT, 8>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st) \
+                       : residual_tma_ch<OUT, 16>(w, n, s_begin, s_end, L, U, d, b, x, out, out2, pdl, st))
     return out_mode == OUT_AX ? NSM_RT(OUT_AX) : (out_mode == OUT_RG ? NSM_RT(OUT_RG) : NSM_RT(OUT_R));
 #undef NSM_RT
 }
@@ -947,9 +860,6 @@ void touch_tma_win() {
     touch_t(k_residual_tma_w<OUT_R, CH>);
     touch_t(k_residual_tma_w<OUT_AX, CH>);
     touch_t(k_residual_tma_w<OUT_RG, CH>);
-    touch_t(k_residual_tma_ws<OUT_R, CH>);
-    touch_t(k_residual_tma_ws<OUT_AX, CH>);
-    touch_t(k_residual_tma_ws<OUT_RG, CH>);
     touch_t(k_sweep_tma_w<true, EPI_STORE2, CH>);
     touch_t(k_sweep_tma_w<false, EPI_STORE2, CH>);
     touch_t(k_sweep_tma_w<true, EPI_STORE, CH>);

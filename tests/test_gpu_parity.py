@@ -73,7 +73,7 @@ SMALL = {
 }
 
 
-KERNELS = ("fused", "fusedw1", "onepass", "onepassw1", "pipelined", "nosym", "nowindow", "plain")
+KERNELS = ("fused", "fusedw1", "onepass", "onepassw1", "pipelined", "nowindow", "plain")
 
 
 def set_kernels(S, mode):
@@ -82,13 +82,11 @@ def set_kernels(S, mode):
     item waits for its predecessor, rings wrap after a few tiles: stresses the
     synchronisation); pipelined: one cp.async.bulk pipelined kernel per pass,
     gathering from shared-memory windows where the layout allows (the
-    default; on a symmetric A the residual reads U = L^T from L); nosym: the
-    same streaming U; nowindow: the same gathering through L1/L2; plain:
+    default); nowindow: the same gathering through L1/L2; plain:
     register-blocked; onepass(w1): the one-pass windowed pGS (NSM_OPT_FUSED = 3)
     where the matrix allows it, else as fused (w1: skew margin 1)."""
     S.set_pipeline(mode != "plain")
     S.set_window(mode != "nowindow")
-    S.set_symmetric(mode != "nosym")
     S.set_fused(1 if mode.startswith("fused") else (3 if mode.startswith("onepass") else 0))
     S.set_fused_window(1 if mode.endswith("w1") else 0)
 
@@ -270,7 +268,7 @@ def test_layout_choice_matches_host_mirror(case):
     import bench
     name, A, F, S = case
     lay, want = S.layout(), bench.aligned_parts(A)
-    assert lay["L"] == want["L"] and lay["U"] == want["U"] and lay["Ut"] == want["Ut"], (name, lay, want)
+    assert lay["L"] == want["L"] and lay["U"] == want["U"], (name, lay, want)
 
 
 @pytest.mark.parametrize("name", ["var27_aligned_40", "var27_ragged"])
