@@ -328,6 +328,8 @@ def run_nsm(args, rank, nranks, local_rank):
         S.set_pdl(args.pdl == "on")
     if args.window == "off":
         S.set_window(False)
+    if args.coupled != "on":
+        S.set_coupled(0 if args.coupled == "off" else int(args.coupled))
     if nranks > 1:
         S.connect(dist)
     nl, nu_, noff = split_counts(A)
@@ -505,6 +507,9 @@ def main():
     ap.add_argument("--fused", default="default", choices=["default", "auto", "on", "off", "onepass"],
                     help="phase-skewed fused passes (default: the library's default, per-pass kernels; "
                          "auto: fused on large problems)")
+    ap.add_argument("--coupled", default="on",
+                    help="forward pGS as concurrent warp groups of one kernel (NSM_OPT_COUPLED): on (the "
+                         "library default), off (one kernel per pass), or a throttle distance in tiles")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: every rank on cuda:0 (halo over same-device IPC), gloo plumbing")
     args = ap.parse_args()

@@ -408,7 +408,13 @@ typedef enum {
     NSM_OPT_HOST_CHUNKS = 8 /* 1 (default): nsm_smooth_host runs a single-rank forward pGS application
                              * (nu = 1, k <= 3, x_in != x_out) in row chunks longer than A's bandwidth, so
                              * the host-to-device copies, the passes and the device-to-host copy overlap
-                             * (separate copy streams); 0: copy in, smooth, copy out.  Same results. */
+                             * (separate copy streams); 0: copy in, smooth, copy out.  Same results. */,
+    NSM_OPT_COUPLED = 9 /* 1 (default): a single-rank forward pGS application with k = 1 or 2 on an
+                         * offset-aligned matrix with gather windows (27-point stencils) runs its residual
+                         * and sweeps as concurrent warp groups of ONE cooperative kernel (coupled.cu,
+                         * DESIGN.md §6): the sweeps re-read L from L2 while the residual streams A from
+                         * HBM.  Bit-identical to the per-pass kernels.  0: one kernel per pass; > 1: on,
+                         * with this throttle distance in 256-row tiles (experiments). */
 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 

@@ -567,6 +567,12 @@ class Smoother:
         """NSM_OPT_HOST_CHUNKS: nsm_smooth_host overlaps copies and passes in row chunks."""
         self._call(load().nsm_set_option(self._h, 8, int(bool(enable))))
 
+    def set_coupled(self, mode):
+        """NSM_OPT_COUPLED: forward pGS (k = 1, 2) on windowed stencil matrices as
+        concurrent warp groups of one kernel (True/1, the default), the per-pass
+        kernels (False/0), or on with a throttle distance of `mode` tiles (> 1)."""
+        self._call(load().nsm_set_option(self._h, 9, int(mode)))
+
     def set_pdl(self, enable: bool):
         """Programmatic dependent launch between consecutive pipelined kernels."""
         self._call(load().nsm_set_option(self._h, 3, int(bool(enable))))

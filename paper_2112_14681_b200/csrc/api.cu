@@ -51,6 +51,11 @@ struct nsm_handle {
     int4 *fw_tseg[2] = {nullptr, nullptr};
     int fw_pst = 0;
     int64_t plane_tiles = 0;   // NSM_OPT_PLANE_ROWS / 256 when the plane-wavefront check passed
+    // coupled passes (coupled.cu): progress counters and launch state, single rank
+    int coupled = 0;           // NSM_OPT_COUPLED: 0 off (default), 1 on, > 1: on with this throttle lag (tiles)
+    unsigned long long *cp_prog = nullptr;
+    unsigned int *cp_sync = nullptr;
+    int64_t bw_upper = 0, bw_lower = 0;   // bandwidths of A in rows
     bool window = true;        // NSM_OPT_WINDOW: windowed pipelined kernels where a window exists
     bool chunked_host = true;  // NSM_OPT_HOST_CHUNKS: nsm_smooth_host overlaps copies and passes
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
@@ -133,6 +138,16 @@ struct DevAlloc {
         return true;
     }
 };
+
+// progress counters and launch state of the coupled passes (coupled.cu):
+// [3][kCpProgStride] per-CTA counters, zero once; sync[0] = epoch 1
+constexpr int64_t kCpProgStride = 1024;
+bool coupled_alloc(DevAlloc &a, nsm_handle *h) {
+    const unsigned int init[4] = {1u, 0u, 0u, 0u};
+    return a.get(&h->cp_prog, 3 * kCpProgStride) && a.get(&h->cp_sync, 4) &&
+           cudaMemset(h->cp_prog, 0, 3 * kCpProgStride * sizeof(unsigned long long)) == cudaSuccess &&
+           cudaMemcpy(h->cp_sync, init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
+}
 
 template <class T>
 bool upload(T *dst, const T *src, int64_t count) {
@@ -227,6 +242,8 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->fw_ring_g);
     cudaFree(h->fw_prog);
     cudaFree(h->fw_sync);
+    cudaFree(h->cp_prog);
+    cudaFree(h->cp_sync);
     for (int q = 0; q < 2; ++q) {
         cudaFree(h->fw_tpos[q]);
         cudaFree(h->fw_nseg[q]);
@@ -643,6 +660,7 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     preload_halo_kernels();
     preload_fused_kernels();
     preload_fused_w_kernels();
+    preload_coupled_kernels();
     nsm_handle *h = new nsm_handle();
     h->uid = next_handle_uid();
     h->device = device;
@@ -688,7 +706,10 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         h->DUA = tiles(sa.bw_upper);
         h->DLs = F ? tiles(sf.bw_lower) : 0;
         h->DUs = F ? tiles(sf.bw_upper) : 0;
+        h->bw_lower = sa.bw_lower;
+        h->bw_upper = sa.bw_upper;
         h->fused_possible = true;
+        ok = coupled_alloc(a, h);
     }
     if (ok && nranks > 1) {
         h->row_offsets.assign(dist->row_offsets, dist->row_offsets + nranks + 1);
@@ -755,6 +776,7 @@ nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F
     preload_halo_kernels();
     preload_fused_kernels();
     preload_fused_w_kernels();
+    preload_coupled_kernels();
     nsm_handle *h = new nsm_handle();
     h->uid = next_handle_uid();
     h->device = device;
@@ -804,7 +826,10 @@ nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F
         h->DUA = tiles(sa.bw_upper);
         h->DLs = F ? tiles(sf.bw_lower) : 0;
         h->DUs = F ? tiles(sf.bw_upper) : 0;
+        h->bw_lower = sa.bw_lower;
+        h->bw_upper = sa.bw_upper;
         h->fused_possible = true;
+        ok = coupled_alloc(a, h);
     }
     if (!ok) {
         cudaGetLastError();
@@ -1003,6 +1028,10 @@ nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value) {
                 h->ev_kind.assign(4096, 0);
             }
             h->ev_used = 0;
+            return NSM_OK;
+        case NSM_OPT_COUPLED:
+            if (value < 0 || value > INT_MAX) return NSM_ERR_ARG;
+            h->coupled = (int)value;
             return NSM_OK;
         case NSM_OPT_HALO_TIMEOUT_MS:
             if (value <= 0) return NSM_ERR_ARG;
@@ -1307,6 +1336,45 @@ static nsm_status fused_w_run(nsm_handle *h, const double *b, double *x, int k, 
     return NSM_OK;
 }
 
+// Forward pGS application (k = 1, 2) as the coupled passes (coupled.cu): one
+// rank, offset-aligned L and U with gather windows; *ran = false otherwise.
+static nsm_status coupled_run(nsm_handle *h, const double *b, double *x, int k, cudaStream_t s, bool *ran) {
+    *ran = false;
+    if (!h->coupled || !h->cp_prog || distributed(h) || !h->pipeline || !h->window || k < 1 || k > 2 || h->n == 0 ||
+        !h->L.off || !h->U.off || !h->res_win.wmax || !h->L.win.wmax)
+        return NSM_OK;
+    CoupledLaunch L{};
+    L.shape = coupled_shape(std::max(h->L.maxw, h->U.maxw), h->L.maxw, h->res_win.wmax, h->L.win.wmax, k, h->n);
+    if (!L.shape.ok) return NSM_OK;
+    L.n = h->n;
+    L.Lp = &h->L;
+    L.Up = &h->U;
+    L.wr = &h->res_win;
+    L.wl = &h->L.win;
+    L.d = h->d;
+    L.b = b;
+    L.x = x;
+    L.r = h->w[0];
+    L.g0 = h->w[3];
+    L.g1 = h->w[1];
+    L.prog = h->cp_prog;
+    L.pstride = kCpProgStride;
+    L.sync = h->cp_sync;
+    L.flag = h->flag;
+    L.sweep_id0 = h->sweep_counter + 1;
+    L.err = h->d_dist_err;
+    L.timeout_ns = h->timeout_ns;
+    L.DA = (h->bw_upper + kTileSlices * kSlice - 1) / (kTileSlices * kSlice) + 1;
+    L.lag = h->coupled > 1 ? h->coupled : 0;
+    ProfScope prof(h, 2, s);
+    const cudaError_t e = launch_coupled(L, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "coupled pGS launch");
+    h->sweep_counter += k;
+    ++h->launches;
+    *ran = true;
+    return NSM_OK;
+}
+
 static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, double *x, int k_l, int k_u, bool fresh,
                              cudaStream_t s) {
     double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
@@ -1352,6 +1420,10 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
             }
             const int DT = fwd ? h->DLA : h->DUA;
             st = skew_run(h, L, false, DT, DT, s, &ran);
+            if (st != NSM_OK || ran) return st;
+        }
+        if (fwd && !fresh) {  // rows a2-a4 as concurrent warp groups (coupled.cu)
+            st = coupled_run(h, b, x, k_l, s, &ran);
             if (st != NSM_OK || ran) return st;
         }
         // the residual pass also writes g^(0) = r / d (eq:jr-initial-guess)

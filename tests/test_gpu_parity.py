@@ -73,7 +73,7 @@ SMALL = {
 }
 
 
-KERNELS = ("fused", "fusedw1", "onepass", "onepassw1", "pipelined", "nowindow", "plain")
+KERNELS = ("fused", "fusedw1", "onepass", "onepassw1", "coupled", "coupledlag", "pipelined", "nowindow", "plain")
 
 
 def set_kernels(S, mode):
@@ -84,7 +84,12 @@ def set_kernels(S, mode):
     gathering from shared-memory windows where the layout allows (the
     default); nowindow: the same gathering through L1/L2; plain:
     register-blocked; onepass(w1): the one-pass windowed pGS (NSM_OPT_FUSED = 3)
-    where the matrix allows it, else as fused (w1: skew margin 1)."""
+    where the matrix allows it, else as fused (w1: skew margin 1); coupled: the
+    default — forward pGS (k = 1, 2) on windowed matrices as concurrent warp
+    groups of one kernel (NSM_OPT_COUPLED), the rest pipelined; coupledlag: the
+    same at the tightest throttle distance (group 0 waits for the last sweep
+    group at the dependency distance: stresses the synchronisation)."""
+    S.set_coupled(1 if mode == "coupled" else (2 if mode == "coupledlag" else 0))
     S.set_pipeline(mode != "plain")
     S.set_window(mode != "nowindow")
     S.set_fused(1 if mode.startswith("fused") else (3 if mode.startswith("onepass") else 0))
@@ -318,3 +323,35 @@ def test_onepass_plane_wavefront(grid, xz, k):
         S.check()
         with pytest.raises(nsm.NsmError):
             S.set_plane_rows(nx * ny * 2 if (nx * ny) % 256 == 0 and nz % 2 == 1 else nx * ny // 2 * 3)
+
+
+@pytest.mark.parametrize("name", ["var27_aligned_40", "var27_ragged", "var27_48tiles"])
+@pytest.mark.parametrize("lag", [1, 2])
+@pytest.mark.parametrize("xz", [False, True])
+@pytest.mark.parametrize("k", [1, 2])
+def test_coupled_pgs(name, lag, xz, k):
+    """The coupled passes (coupled.cu, NSM_OPT_COUPLED) really run on 27-point
+    matrices (one 'fused' pass per non-fresh application) and are bit-identical
+    to the oracle for k = 1, 2, nu = 2 (the first application from x = 0 runs
+    per pass, the second coupled), at the automatic and the tightest throttle
+    distance; several tiles per CTA, a ragged last tile, and fewer tiles than
+    SMs (var27_48tiles)."""
+    A = (SMALL[name]() if name in SMALL else
+         inputs.var27_grid(64, 16, 12) if name == "var27_48tiles" else inputs.var27_grid(130, 20, 6))
+    b = inputs.uniform(0, A.nrows)
+    x0 = np.zeros(A.nrows) if xz else inputs.uniform(1, A.nrows)
+    want = oracle.pgs_apply(A, b, x0, k, nu=2, x_is_zero=xz)
+    with nsm.Smoother(A) as S:
+        S.set_coupled(lag)
+        S.set_profile(True)
+        S.profile()
+        x = start(x0, xz)
+        S.smooth(dev(b), x, "pgs", nu=2, k_l=k, x_is_zero=xz)
+        agree(host(x), want, f"{name} coupled k={k} xz={xz} lag={lag}")
+        assert S.profile()["fused"][1] == (1 if xz else 2), "the coupled kernel did not run"
+        S.check()
+        for rep in range(3):   # repeated launches: the epoch advances, results stay identical
+            x = start(x0, xz)
+            S.smooth(dev(b), x, "pgs", nu=2, k_l=k, x_is_zero=xz)
+            agree(host(x), want, f"{name} coupled rep {rep}")
+        S.check()
