@@ -45,12 +45,14 @@ WORKLOADS = {
 
 # ------------------------------------------------------------------ helpers --
 def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k_l: int, k_u: int,
-                      n_ghost: int = 0, layout: dict | None = None) -> dict:
+                      n_ghost: int = 0, layout: dict | None = None, coupled: bool = False) -> dict:
     """Bytes each kernel of one application must move (DESIGN.md §6 byte
     model): every stored matrix entry once (8 B value + 4 B int32 column; an
     offset-aligned part, nsm_layout, reads 8 B per entry plus one 4 B offset
     per 32 entries), every n-vector the kernel reads or writes once; gathered
-    neighbour values are counted once (they hit L1/L2 after first touch)."""
+    neighbour values are counted once (they hit L1/L2 after first touch).
+    coupled: the k pGS sweeps run as ONE kernel (coupled.cu) that streams L
+    once; each sweep's vectors are still counted."""
     layout = layout or {}
 
     def mb(count, part):  # bytes of `count` stored entries of a part
@@ -68,6 +70,8 @@ def algorithmic_bytes(kind: str, n: int, nnz_off: int, nnz_l: int, nnz_u: int, k
             sw.append(b)
         if k_l == 0:
             sw.append(32 * n)                             # x += r/d
+        if coupled and k_l >= 2:                          # one kernel, L streamed once
+            sw = [sum(sw) - (k_l - 1) * mb(nnz_l, "L")]
         out["sweeps"] = sw
     else:
         out["residual"] = res
@@ -328,8 +332,8 @@ def run_nsm(args, rank, nranks, local_rank):
         S.set_pdl(args.pdl == "on")
     if args.window == "off":
         S.set_window(False)
-    if args.coupled != "on":
-        S.set_coupled(0 if args.coupled == "off" else int(args.coupled))
+    if args.coupled != "default":
+        S.set_coupled({"on": 1, "off": 0}.get(args.coupled) if args.coupled in ("on", "off") else int(args.coupled))
     if nranks > 1:
         S.connect(dist)
     nl, nu_, noff = split_counts(A)
@@ -388,6 +392,12 @@ def run_nsm(args, rank, nranks, local_rank):
     prof = S.profile()
     S.set_profile(False)
     fused = prof["fused"][1] > 0
+    # the coupled sweeps (one sweep kernel per application instead of k)
+    coupled = kind == "pgs" and k_l >= 2 and not fused and prof["sweep"][1] == args.steps
+    if coupled and args.coupled == "default":
+        raise RuntimeError("the library's default path now couples the sweeps: the reference arm's byte "
+                           "count (one kernel per pass) must follow")
+    model = algorithmic_bytes(kind, A.nrows, noff, nl, nu_, k_l, k_u, S.n_ghost, layout, coupled)
     # algorithmic bytes of the path that ran (per-pass kernels or fused passes)
     ab = fmodel["total"] if fused else model["total"]
     value = ab * nranks * args.steps / (t_ms * 1e-3) / 1e9
@@ -467,9 +477,13 @@ def run_nsm(args, rank, nranks, local_rank):
             "detail": {"nnz_this_rank": int(A.nnz),
                        "kernels": ("plain register-blocked, one kernel per pass" if args.plain else
                                    ("phase-skewed fused passes (k_skew, cp.async.bulk pipelined, persistent)" if fused
-                                    else "cp.async.bulk pipelined (persistent), one kernel per pass")),
+                                    else ("cp.async.bulk pipelined (persistent): the residual kernel, then the k "
+                                          "sweeps as concurrent CTA groups of one cooperative kernel "
+                                          "(k_sweeps_coupled)" if coupled
+                                          else "cp.async.bulk pipelined (persistent), one kernel per pass"))),
                        "bytes": ("algorithmic bytes of the path that ran (DESIGN.md §6): "
-                                 + ("fused passes = the floor" if fused else "one kernel per pass")),
+                                 + ("fused passes = the floor" if fused else
+                                    ("the coupled sweeps stream L once" if coupled else "one kernel per pass"))),
                        "bytes_per_step_per_gpu": ab, "floor_bytes_per_step_per_gpu": fmodel["total"],
                        "offset_aligned_parts": [k for k, v in layout.items() if v],
                        "floor_gbs": round(floor_gbs, 2),
@@ -507,9 +521,9 @@ def main():
     ap.add_argument("--fused", default="default", choices=["default", "auto", "on", "off", "onepass"],
                     help="phase-skewed fused passes (default: the library's default, per-pass kernels; "
                          "auto: fused on large problems)")
-    ap.add_argument("--coupled", default="on",
-                    help="forward pGS as concurrent warp groups of one kernel (NSM_OPT_COUPLED): on (the "
-                         "library default), off (one kernel per pass), or a throttle distance in tiles")
+    ap.add_argument("--coupled", default="default",
+                    help="the pGS sweeps as concurrent CTA groups of one kernel (NSM_OPT_COUPLED, experimental): "
+                         "default (the library's: off), on, off, or on with a throttle distance in tiles")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: every rank on cuda:0 (halo over same-device IPC), gloo plumbing")
     args = ap.parse_args()

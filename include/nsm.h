@@ -409,12 +409,14 @@ typedef enum {
                              * (nu = 1, k <= 3, x_in != x_out) in row chunks longer than A's bandwidth, so
                              * the host-to-device copies, the passes and the device-to-host copy overlap
                              * (separate copy streams); 0: copy in, smooth, copy out.  Same results. */,
-    NSM_OPT_COUPLED = 9 /* 1 (default): a single-rank forward pGS application with k = 1 or 2 on an
-                         * offset-aligned matrix with gather windows (27-point stencils) runs its residual
-                         * and sweeps as concurrent warp groups of ONE cooperative kernel (coupled.cu,
-                         * DESIGN.md §6): the sweeps re-read L from L2 while the residual streams A from
-                         * HBM.  Bit-identical to the per-pass kernels.  0: one kernel per pass; > 1: on,
-                         * with this throttle distance in 256-row tiles (experiments). */
+    NSM_OPT_COUPLED = 9 /* 1: a single-rank forward pGS application with k = 2 or 3 on an offset-aligned L
+                         * with a gather window (27-point stencils) runs the residual pass, then its k sweeps
+                         * as concurrent CTA groups of ONE cooperative kernel (coupled.cu): the
+                         * later sweeps re-read L from L2, so L is streamed from HBM once instead of k times.
+                         * Bit-identical to the per-pass kernels.  Experimental: reads the predicted bytes
+                         * (C3: 2.3 GB for both sweeps instead of 4.6) but is latency-bound and slower than the
+                         * per-pass sweeps.  0 (default): one kernel per pass; > 1: on, with this throttle
+                         * distance in 256-row tiles (a test knob: 2 makes group 0 wait at almost every tile). */
 } nsm_option;
 nsm_status nsm_set_option(nsm_handle *h, nsm_option opt, int64_t value);
 
@@ -533,6 +535,15 @@ nsm_status nsm_diag_copy(const nsm_handle *h, int which, double *out);
  * free stage, [3] ns in readiness checks, [4] ns per unit in total, [5]
  * acquire fences.  Diagnostics; out has 6 entries. */
 nsm_status nsm_fused_counters(const nsm_handle *h, int64_t *out);
+
+/* nsm_coupled_counters: cumulative SM-cycle counters of the coupled sweeps
+ * kernel (coupled.cu), collected while NSM_OPT_PROFILE is on: for sweep group
+ * g = 0..2, out[4g + 0] producer cycles in dependency waits, out[4g + 1]
+ * producer cycles waiting for a free stage, out[4g + 2] producer cycles in
+ * total (summed over CTAs), out[4g + 3] consumer cycles waiting for staged
+ * data (warp 0 of the group, summed over CTAs).  `out` has 16 entries;
+ * synchronises the device. */
+nsm_status nsm_coupled_counters(const nsm_handle *h, int64_t *out);
 
 /* Frees all device memory of the handle (synchronises its device).  NULL ok. */
 void nsm_destroy(nsm_handle *h);

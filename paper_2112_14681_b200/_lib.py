@@ -28,7 +28,7 @@ SYMBOLS = sorted(["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual
                   "nsm_comm_connect_ipc", "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout",
                   "nsm_comm_stats", "nsm_comm_last_error", "nsm_comm_destroy", "nsm_set_comm", "nsm_ruiz_dep",
                   "nsm_dep", "nsm_setup_device", "nsm_part_info", "nsm_part_copy", "nsm_diag_copy",
-                  "nsm_fused_counters"])
+                  "nsm_fused_counters", "nsm_coupled_counters"])
 
 
 class NsmError(RuntimeError):
@@ -130,6 +130,7 @@ def load(variant: str = ""):
     L.nsm_part_copy.argtypes = [vp, ci, vp, vp, vp, vp]
     L.nsm_diag_copy.argtypes = [vp, ci, vp]
     L.nsm_fused_counters.argtypes = [vp, vp]
+    L.nsm_coupled_counters.argtypes = [vp, vp]
     for name in ["nsm_setup", "nsm_ilu0", "nsm_ilu0_fixed_point", "nsm_residual", "nsm_spmv", "nsm_lsolve", "nsm_usolve", "nsm_smooth",
                  "nsm_smooth_host", "nsm_check", "nsm_info", "nsm_stats", "nsm_halo_plan", "nsm_halo_set_send", "nsm_halo_mailbox",
                  "nsm_halo_connect_ipc", "nsm_halo_connect", "nsm_halo_commit", "nsm_set_option",
@@ -138,7 +139,7 @@ def load(variant: str = ""):
                  "nsm_comm_create", "nsm_comm_mailbox", "nsm_comm_connect", "nsm_comm_connect_ipc",
                  "nsm_comm_allreduce", "nsm_comm_check", "nsm_comm_set_timeout", "nsm_comm_stats", "nsm_set_comm",
                  "nsm_ruiz_dep", "nsm_dep", "nsm_setup_device", "nsm_part_info", "nsm_part_copy", "nsm_diag_copy",
-                 "nsm_fused_counters"]:
+                 "nsm_fused_counters", "nsm_coupled_counters"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -568,9 +569,10 @@ class Smoother:
         self._call(load().nsm_set_option(self._h, 8, int(bool(enable))))
 
     def set_coupled(self, mode):
-        """NSM_OPT_COUPLED: forward pGS (k = 1, 2) on windowed stencil matrices as
-        concurrent warp groups of one kernel (True/1, the default), the per-pass
-        kernels (False/0), or on with a throttle distance of `mode` tiles (> 1)."""
+        """NSM_OPT_COUPLED: the k = 2, 3 sweeps of a forward pGS application on
+        windowed stencil matrices as concurrent CTA groups of one kernel (True/1,
+        experimental), the per-pass kernels (False/0, the default), or on with a
+        throttle distance of `mode` tiles (> 1)."""
         self._call(load().nsm_set_option(self._h, 9, int(mode)))
 
     def set_pdl(self, enable: bool):
@@ -605,6 +607,14 @@ class Smoother:
         """nsm_fused_counters: polls, poll ns, stage-wait ns, readiness ns, unit ns, fences."""
         out = np.zeros(6, dtype=np.int64)
         self._call(load().nsm_fused_counters(self._h, out.ctypes.data))
+        return out
+
+    def coupled_counters(self) -> np.ndarray:
+        """nsm_coupled_counters: per sweep group g, [4g..4g+3] = producer cycles in
+        dependency waits, producer cycles waiting for a stage, producer cycles in
+        total, consumer (warp 0) cycles waiting for staged data (NSM_OPT_PROFILE on)."""
+        out = np.zeros(16, dtype=np.int64)
+        self._call(load().nsm_coupled_counters(self._h, out.ctypes.data))
         return out
 
     def set_halo_timeout(self, ms: int):

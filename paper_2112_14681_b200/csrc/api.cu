@@ -53,9 +53,8 @@ struct nsm_handle {
     int64_t plane_tiles = 0;   // NSM_OPT_PLANE_ROWS / 256 when the plane-wavefront check passed
     // coupled passes (coupled.cu): progress counters and launch state, single rank
     int coupled = 0;           // NSM_OPT_COUPLED: 0 off (default), 1 on, > 1: on with this throttle lag (tiles)
-    unsigned long long *cp_prog = nullptr;
+    unsigned long long *cp_prog = nullptr, *cp_stats = nullptr;
     unsigned int *cp_sync = nullptr;
-    int64_t bw_upper = 0, bw_lower = 0;   // bandwidths of A in rows
     bool window = true;        // NSM_OPT_WINDOW: windowed pipelined kernels where a window exists
     bool chunked_host = true;  // NSM_OPT_HOST_CHUNKS: nsm_smooth_host overlaps copies and passes
     int64_t n = 0, row_begin = 0, n_ghost = 0, nnz_off = 0, device_bytes = 0;
@@ -144,7 +143,8 @@ struct DevAlloc {
 constexpr int64_t kCpProgStride = 1024;
 bool coupled_alloc(DevAlloc &a, nsm_handle *h) {
     const unsigned int init[4] = {1u, 0u, 0u, 0u};
-    return a.get(&h->cp_prog, 3 * kCpProgStride) && a.get(&h->cp_sync, 4) &&
+    return a.get(&h->cp_prog, 3 * kCpProgStride) && a.get(&h->cp_sync, 4) && a.get(&h->cp_stats, 16) &&
+           cudaMemset(h->cp_stats, 0, 16 * sizeof(unsigned long long)) == cudaSuccess &&
            cudaMemset(h->cp_prog, 0, 3 * kCpProgStride * sizeof(unsigned long long)) == cudaSuccess &&
            cudaMemcpy(h->cp_sync, init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess;
 }
@@ -243,6 +243,7 @@ void free_handle(nsm_handle *h) {
     cudaFree(h->fw_prog);
     cudaFree(h->fw_sync);
     cudaFree(h->cp_prog);
+    cudaFree(h->cp_stats);
     cudaFree(h->cp_sync);
     for (int q = 0; q < 2; ++q) {
         cudaFree(h->fw_tpos[q]);
@@ -706,8 +707,6 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         h->DUA = tiles(sa.bw_upper);
         h->DLs = F ? tiles(sf.bw_lower) : 0;
         h->DUs = F ? tiles(sf.bw_upper) : 0;
-        h->bw_lower = sa.bw_lower;
-        h->bw_upper = sa.bw_upper;
         h->fused_possible = true;
         ok = coupled_alloc(a, h);
     }
@@ -826,8 +825,6 @@ nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F
         h->DUA = tiles(sa.bw_upper);
         h->DLs = F ? tiles(sf.bw_lower) : 0;
         h->DUs = F ? tiles(sf.bw_upper) : 0;
-        h->bw_lower = sa.bw_lower;
-        h->bw_upper = sa.bw_upper;
         h->fused_possible = true;
         ok = coupled_alloc(a, h);
     }
@@ -1162,6 +1159,17 @@ nsm_status nsm_fused_counters(const nsm_handle *h, int64_t *out) {
     return NSM_OK;
 }
 
+nsm_status nsm_coupled_counters(const nsm_handle *h, int64_t *out) {
+    if (!h || !out) return NSM_ERR_ARG;
+    for (int i = 0; i < 16; ++i) out[i] = 0;
+    if (!h->cp_stats) return NSM_OK;
+    DeviceScope dev(h->device);
+    unsigned long long v[16] = {};
+    if (cudaMemcpy(v, h->cp_stats, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return NSM_ERR_CUDA;
+    for (int i = 0; i < 16; ++i) out[i] = (int64_t)v[i];
+    return NSM_OK;
+}
+
 nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *halo_exchanges) {
     if (!h) return NSM_ERR_ARG;
     if (kernel_launches) *kernel_launches = h->launches;
@@ -1336,27 +1344,29 @@ static nsm_status fused_w_run(nsm_handle *h, const double *b, double *x, int k, 
     return NSM_OK;
 }
 
-// Forward pGS application (k = 1, 2) as the coupled passes (coupled.cu): one
-// rank, offset-aligned L and U with gather windows; *ran = false otherwise.
+// Forward pGS application with k = 2, 3: the residual pass (r, g(0)), then
+// the k sweeps as concurrent warp groups of one kernel (coupled.cu): one
+// rank, offset-aligned L with a gather window; *ran = false otherwise.
 static nsm_status coupled_run(nsm_handle *h, const double *b, double *x, int k, cudaStream_t s, bool *ran) {
     *ran = false;
-    if (!h->coupled || !h->cp_prog || distributed(h) || !h->pipeline || !h->window || k < 1 || k > 2 || h->n == 0 ||
-        !h->L.off || !h->U.off || !h->res_win.wmax || !h->L.win.wmax)
+    if (!h->coupled || !h->cp_prog || distributed(h) || !h->pipeline || !h->window || k < 2 || k > 3 || h->n == 0 ||
+        !h->L.off || !h->L.win.wmax)
         return NSM_OK;
     CoupledLaunch L{};
-    L.shape = coupled_shape(std::max(h->L.maxw, h->U.maxw), h->L.maxw, h->res_win.wmax, h->L.win.wmax, k, h->n);
+    L.shape = coupled_shape(h->L.maxw, h->L.win.wmax, k, h->n);
     if (!L.shape.ok) return NSM_OK;
+    double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
+    nsm_status st = residual_into(h, b, x, R, OUT_RG, s, W2);
+    if (st != NSM_OK) return st;
     L.n = h->n;
     L.Lp = &h->L;
-    L.Up = &h->U;
-    L.wr = &h->res_win;
     L.wl = &h->L.win;
     L.d = h->d;
-    L.b = b;
+    L.r = R;
     L.x = x;
-    L.r = h->w[0];
-    L.g0 = h->w[3];
-    L.g1 = h->w[1];
+    L.g[0] = W2;
+    L.g[1] = W0;
+    L.g[2] = W1;
     L.prog = h->cp_prog;
     L.pstride = kCpProgStride;
     L.sync = h->cp_sync;
@@ -1364,11 +1374,11 @@ static nsm_status coupled_run(nsm_handle *h, const double *b, double *x, int k, 
     L.sweep_id0 = h->sweep_counter + 1;
     L.err = h->d_dist_err;
     L.timeout_ns = h->timeout_ns;
-    L.DA = (h->bw_upper + kTileSlices * kSlice - 1) / (kTileSlices * kSlice) + 1;
     L.lag = h->coupled > 1 ? h->coupled : 0;
-    ProfScope prof(h, 2, s);
+    L.stats = h->profile ? h->cp_stats : nullptr;
+    ProfScope prof(h, 1, s);
     const cudaError_t e = launch_coupled(L, s);
-    if (e != cudaSuccess) return cuda_fail(h, e, "coupled pGS launch");
+    if (e != cudaSuccess) return cuda_fail(h, e, "coupled sweeps launch");
     h->sweep_counter += k;
     ++h->launches;
     *ran = true;
@@ -1422,7 +1432,7 @@ static nsm_status apply_once(nsm_handle *h, nsm_kind kind, const double *b, doub
             st = skew_run(h, L, false, DT, DT, s, &ran);
             if (st != NSM_OK || ran) return st;
         }
-        if (fwd && !fresh) {  // rows a2-a4 as concurrent warp groups (coupled.cu)
+        if (fwd && !fresh) {  // rows a2-a4: residual, then the sweeps as concurrent warp groups (coupled.cu)
             st = coupled_run(h, b, x, k_l, s, &ran);
             if (st != NSM_OK || ran) return st;
         }

@@ -1,45 +1,50 @@
-// coupled.cu — one forward pGS application (residual, k Jacobi sweeps, x
-// update; the pGS application of P:L743-785 with g(0) = D^{-1} r,
-// eq:jr-initial-guess) as CONCURRENT WARP GROUPS of one persistent kernel,
-// so the matrix rows the sweeps re-read come from L2 instead of HBM
-// (DESIGN.md §6 "Coupled passes").
+// coupled.cu — the k Jacobi sweeps of a forward pGS application (and its x
+// update, eq:jacobi, the last sweep fused with x += g(k)) as
+// CONCURRENT CTA GROUPS of one persistent cooperative kernel, so L is
+// streamed from HBM once per application instead of once per sweep
+// (DESIGN.md §6 "Coupled sweeps").
 //
-// The per-pass schedule (stream.cu) reads L three times from HBM for k = 2:
-// once in the residual, once per sweep.  Here every CTA (one per SM) holds
-// k + 1 warp groups, each an instance of the per-pass pipeline — a producer
-// warp staging tiles by bulk copy (values, window positions, slice header,
-// gather window) and consumer warps with one row per thread:
+// The per-pass schedule (stream.cu) launches the residual, then one kernel
+// per sweep, each streaming L from HBM.  Here the residual pass stays as it
+// is (k_residual_tma_w, writing r and g(0) = r / d, eq:jr-initial-guess), and
+// ONE kernel runs all k sweeps: its CTAs are dealt to k groups (CTA b serves
+// sweep b mod k, so every SM holds one CTA of each), each CTA an instance of
+// the per-pass sweep pipeline — a producer warp staging tiles by bulk copy
+// (L's values, window positions, slice header, the gather window of the
+// previous iterate, and the tile's r rows; tile references loaded three
+// tiles ahead) and 8 consumer warps with one row per thread:
 //
-//   group 0      8 consumer warps   r = b - A x, g(0) = r / d         tile t
-//   group j      4 consumer warps   g(j) = (r - L g(j-1)) / d         tile t - lag_j
-//   (j = 1..k)   (two slices each)  the last one x += g(k)
+//   group j (j = 0..k-1):  g(j+1) = (r - L g(j)) / d       tiles c, c + Gg, ...
+//                          the last one: x += (r - L g(k-1)) / d
 //
-// All groups walk the same tiles (t = CTA, CTA + G, ...), so tile t's L values
-// are streamed from HBM by group 0 and re-read shortly after by groups 1..k
-// of the same CTA while they are still in L2 (group 0 copies L with the
-// evict_normal policy, U and the last sweep's L with evict_first).
+// Group 0 streams tile t's L values from HBM (evict_normal); the later
+// groups re-read them from L2 shortly after (the last one with evict_first).
 //
-// Dependencies (256-row tiles; "phase q done through t" = every CTA's group q
-// has completed all of its tiles <= t, read from per-CTA progress counters
-// like fused_w.cu's frontiers):
-//   group j >= 1, tile t:  phase j-1 done through t       (its gather window
-//                          of g(j-1) covers rows below and inside tile t; r of
-//                          tile t follows by causality)
-//   group k, tile t:       phase 0 done through t + DA     (x of tile t: every
-//                          residual window reading it has been consumed)
-//   group 0, tile t:       phase k done through t - lag    (throttle: keeps the
-//                          L rows group 0 streamed L2-resident until re-read)
-// Each condition refers to tiles strictly earlier in the chain (lag > DA), so
-// the lowest unfinished tile can always proceed; a cooperative launch makes
-// all CTAs resident, so the kernel is deadlock-free.  A wait longer than the
-// handle's timeout sets the error word (nsm_check: NSM_ERR_DIST) instead of
-// hanging.
+// Dependencies (256-row tiles; "group q done through t" = every CTA of group
+// q has completed all of its tiles <= t, from per-CTA progress counters):
+//   group j >= 1, tile t:  group j-1 done through t   (its gather window of
+//                          g(j) covers rows below and inside tile t)
+//   group 0, tile t:       group k-1 done through t - lag   (throttle: keeps
+//                          the L rows group 0 streamed L2-resident until the
+//                          last group re-reads them)
+// r, g(0) and the old x come from the residual kernel, complete at launch; x
+// of tile t is read and written only by the last group's tile t.  Each
+// condition refers to strictly earlier tiles of the chain (lag >= 1), so the
+// lowest unfinished tile can always proceed; the cooperative launch makes all
+// CTAs resident: deadlock-free.  A wait longer than the handle's timeout sets
+// the error word (nsm_check: NSM_ERR_DIST) instead of hanging.
 //
-// Arithmetic: the consumers run the per-pass kernels' code on the same staged
+// Publication is off the critical path: consumers release a stage as soon as
+// they have read it, write their rows, then count the tile in a shared
+// per-tile-slot counter (release, CTA scope); a publisher warp acquires the
+// counts and advances the CTA's gpu-scope progress counter (red.release).
+// A warp counts tile m + kSlots only after every warp has released the stage
+// of tile m + kSlots - nst, i.e. after every warp has counted tile m, so a
+// slot's count reaches (m / kSlots + 1) * 8 exactly when tile m is complete.
+//
+// Arithmetic: the consumers run the per-pass sweep code on the same staged
 // operands — the same products and stored-order additions, the same division
 // — so results are bit-identical to the per-pass path and to the oracle.
-// The r rows a sweep needs are bulk-copied into its stage by the producer
-// (after the dependency wait), never read through L1.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -57,267 +62,228 @@ namespace nsm {
 
 namespace {
 
-constexpr int kRW = kTS;      // residual consumer warps: one slice each
-constexpr int kSW = 4;        // consumer warps per sweep group: slices w and w + 4
-constexpr int kMaxK = 2;
-constexpr int kPubBytes = 256;  // per-group, per-stage publication counters
+constexpr int kCW = kTS;        // consumer warps: one slice each
+constexpr int kMaxG = 3;        // sweeps (groups) per launch
+constexpr int kSlots = 4;       // tile-count slots (> stages)
+constexpr int kCtlBytes = 128;  // publication counters
+constexpr int kThreadsC = (kCW + 2) * 32;   // + producer + publisher
 constexpr int64_t kSmemMaxC = 227 * 1024;
-template <int K>
-constexpr int threads_c() { return (kRW + K * kSW + K + 1) * 32; }
 
 struct CoupledParams {
     int64_t n, nslices, ntiles;
-    SellView L, U;
-    WinView WR, WL;              // residual window (L and U), sweep window (L)
-    const double *d, *b;
-    double *x, *r;
-    double *g[kMaxK];            // g[j] = g(j), j = 0 .. k-1
-    unsigned long long *prog;    // [k + 1][pstride] per-CTA progress (epoch << 32 | tiles done)
+    SellView L;
+    WinView WL;                  // gather window of L (per 256-row tile)
+    const double *d, *r;
+    double *x;
+    double *g[kMaxG];            // g[j] = g(j): gathered by group j (g[0] from the residual kernel)
+    unsigned long long *prog;    // [k][pstride] per-CTA progress (epoch << 32 | tiles done)
     int64_t pstride;
     unsigned int *sync;          // [0] epoch, [1] CTAs finished
     unsigned long long *flag;
     int64_t sweep_id0;
     unsigned int *err;
     unsigned long long timeout_ns;
-    int64_t DA, lag;
-    int nst_r, nst_s;
-    int64_t cap_r, cap_s, goff_s;   // goff_s: bytes from group 1's base to group 2's
+    int64_t lag;
+    int nst;
+    int64_t cap;                 // entries per stage
+    unsigned long long *stats;   // nullable: [group][4] cycle counters (nsm_coupled_counters)
 };
 
-__device__ __forceinline__ unsigned int *pubc(char *sm, int g, int st) { return (unsigned int *)sm + g * 8 + st; }
-
-// frontier of one phase: all tiles < F are complete (acquire reads of the
-// per-CTA progress counters, refreshed only when a wait needs more)
-__device__ __forceinline__ void need(const CoupledParams &p, int64_t &F, bool &dirty, int q, int64_t t,
-                                     unsigned int epoch, int lane) {
-    t = min(t, p.ntiles - 1);
-    if (t < F) return;
-    const int64_t G = gridDim.x;
-    const unsigned long long *pr = p.prog + (int64_t)q * p.pstride;
-    const uint64_t t0 = ptx::globaltimer_ns();
-    while (true) {
+// The frontier of the awaited group (all its tiles < F complete) is kept
+// current without stalling: the per-CTA counters are read (relaxed, all in
+// flight together) at the end of one tile's staging and reduced at the start
+// of the next; an acquire fence is paid only when the producer starts relying
+// on a frontier it has not fenced yet (about once per round of tiles), and it
+// spins only when the prefetched view is not enough.
+constexpr int kPV = 8;   // counters per lane (groups of <= 256 CTAs)
+template <int NG>
+struct CoupledHook {
+    const CoupledParams *p;
+    int g;
+    int64_t c, Gg;         // this CTA's index in its group, CTAs per group
+    unsigned int epoch;
+    double *rslot0;        // r rows of stage 0 (256 doubles per stage)
+    int64_t Fs, Ff;        // frontier of the awaited group: seen (relaxed reads), fenced
+    bool pending;
+    unsigned long long rv[kPV];
+    uint64_t pol_keep, pol_first;
+    long long c_last, c_wait, c_empty, c_fence;   // statistics (lane 0): cycles in dependency spins / stage waits / fences
+    __device__ __forceinline__ int64_t first() const { return c; }
+    __device__ __forceinline__ int64_t stride() const { return Gg; }
+    __device__ __forceinline__ int64_t rows(int64_t t) const { return min((int64_t)kTS * kSlice, p->n - t * kTS * kSlice); }
+    __device__ __forceinline__ int waited() const { return g == 0 ? NG - 1 : g - 1; }
+    __device__ __forceinline__ void issue(int lane) {
+        const unsigned long long *pr = p->prog + (int64_t)waited() * p->pstride;
+#pragma unroll
+        for (int r = 0; r < kPV; ++r) {
+            const int64_t q = lane + 32 * r;
+            rv[r] = q < Gg ? ptx::ld_relaxed_gpu_u64(pr + q) : 0ull;
+        }
+        pending = true;
+    }
+    __device__ __forceinline__ void reduce(int lane) {
         int64_t f = INT64_MAX;
-        for (int64_t c = lane; c < G; c += 32) {
-            const unsigned long long v = ptx::ld_acquire_gpu_u64(pr + c);
-            const int64_t cnt = (unsigned int)(v >> 32) == epoch ? (int64_t)(v & 0xffffffffull) : 0;
-            f = min(f, c + cnt * G);
+#pragma unroll
+        for (int r = 0; r < kPV; ++r) {
+            const int64_t q = lane + 32 * r;
+            if (q < Gg) {
+                const int64_t cnt = (unsigned int)(rv[r] >> 32) == epoch ? (int64_t)(rv[r] & 0xffffffffull) : 0;
+                f = min(f, q + cnt * Gg);
+            }
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) f = min(f, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)f, o));
-        F = max(F, f);
-        if (t < F) break;
-        if (ptx::globaltimer_ns() - t0 > p.timeout_ns) {
-            if (lane == 0) atomicOr(p.err, 2u);
-            F = INT64_MAX;
-            break;
-        }
-        __nanosleep(128);
+        Fs = max(Fs, f);
+        pending = false;
     }
-    dirty = true;
-}
-
-// Producer hooks (stream_dev.cuh): dependency waits before a tile is staged,
-// then a proxy fence (the bulk copies read vectors other SMs wrote through
-// the generic proxy); sweeps also stage the tile's r rows.
-template <int K>
-struct CoupledHook {
-    const CoupledParams *p;
-    int g;                 // 0: residual, j >= 1: sweep j
-    unsigned int epoch;
-    double *rslot0;        // sweeps: r rows of stage 0 (256 doubles per stage)
-    int64_t Fa, Fb;        // frontiers: Fa of the phase this group waits on (k for group 0, g - 1 for
-                           // group g), Fb of phase 0 (group k)
-    bool dirty;
-    uint64_t pol_keep, pol_first;
-    __device__ __forceinline__ int64_t first() const { return blockIdx.x; }
-    __device__ __forceinline__ int64_t stride() const { return gridDim.x; }
-    __device__ __forceinline__ int64_t rows(int64_t t) const { return min((int64_t)kTS * kSlice, p->n - t * kTS * kSlice); }
     __device__ __forceinline__ void before(int64_t t, int st, int lane) {
-        if (g == 0) {
-            if (t - p->lag >= 0) need(*p, Fa, dirty, K, t - p->lag, epoch, lane);
-        } else {
-            need(*p, Fa, dirty, g - 1, t, epoch, lane);
-            if (g == K) need(*p, Fb, dirty, 0, t + p->DA, epoch, lane);
-        }
-        if (dirty) {
+        if (c_last) c_empty += clock64() - c_last;
+        const int64_t need = min(g == 0 ? t - p->lag : t, p->ntiles - 1);   // all tiles <= need complete
+        if (pending) reduce(lane);
+        if (need >= Ff) {
+            if (need >= Fs) {
+                const long long c0 = clock64();
+                const uint64_t t0 = ptx::globaltimer_ns();
+                while (true) {
+                    issue(lane);
+                    reduce(lane);
+                    if (need < Fs) break;
+                    if (ptx::globaltimer_ns() - t0 > p->timeout_ns) {
+                        if (lane == 0) atomicOr(p->err, 2u);
+                        Fs = INT64_MAX;
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+                c_wait += clock64() - c0;
+            }
+            const long long c1 = clock64();
+            ptx::fence_acq_rel_gpu();   // acquire: the counters read above were published with release
+            Ff = Fs;
             __syncwarp();
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            dirty = false;
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and the window copies follow it
+            c_fence += clock64() - c1;
         }
-        if (g > 0 && lane == 0) {
+        if (lane == 0) {
             const int64_t m = rows(t);
-            if (m & 1) rslot0[st * kTS * kSlice + m - 1] = __ldcg(p->r + t * kTS * kSlice + m - 1);  // odd n: last row
+            if (m & 1) rslot0[st * kTS * kSlice + m - 1] = p->r[t * kTS * kSlice + m - 1];  // odd n: last row
         }
+        if (Fs < p->ntiles) issue(lane);   // the view for the next tile, in flight while this one is staged
     }
-    __device__ __forceinline__ uint32_t extra_bytes(int64_t t) const {
-        return g > 0 ? (uint32_t)((rows(t) & ~(int64_t)1) * 8) : 0u;
-    }
-    __device__ __forceinline__ void extra_copy(int64_t t, int st, uint64_t *bar) const {
+    __device__ __forceinline__ uint32_t extra_bytes(int64_t t) const { return (uint32_t)((rows(t) & ~(int64_t)1) * 8); }
+    __device__ __forceinline__ void extra_copy(int64_t t, int st, uint64_t *bar) {
         const uint32_t bytes = extra_bytes(t);
         if (bytes) ptx::bulk_g2s(rslot0 + st * kTS * kSlice, p->r + t * kTS * kSlice, bytes, bar, pol_keep);
+        c_last = clock64();
     }
-    __device__ __forceinline__ uint64_t val_policy(int part, uint64_t) const {
-        if (g == 0) return part == 0 ? pol_keep : pol_first;  // L is re-read by the sweeps, U is not
-        return g == K ? pol_first : pol_keep;
-    }
+    __device__ __forceinline__ uint64_t val_policy(int, uint64_t) const { return g == NG - 1 ? pol_first : pol_keep; }
 };
 
-// publish "this CTA's group g has completed its tiles 0..m" once every
-// consumer warp of the group has counted tile m (CTA-scope acq_rel count,
-// then a gpu-scope release); the stage is released after the count, so no
-// warp counts the stage's next tile before every warp has counted this one
-__device__ __forceinline__ void publish_and_release(const CoupledParams &p, char *sm, int g, int st, int nwarps,
-                                                    uint64_t *empty, int64_t m, unsigned int epoch, int lane) {
-    __syncwarp();
-    if (lane == 0) {
-        const unsigned int prev = ptx::atom_add_acqrel_cta_shared(pubc(sm, g, st), 1u);
-        if ((prev + 1) % (unsigned)nwarps == 0)
-            ptx::red_max_release_gpu_u64(p.prog + (int64_t)g * p.pstride + blockIdx.x,
-                                         ((unsigned long long)epoch << 32) | (unsigned long long)(m + 1));
-        ptx::mbar_arrive(empty);
-    }
-}
-
-template <int CH, int K>
-__global__ void __launch_bounds__(threads_c<K>(), 1) k_pgs_coupled(const __grid_constant__ CoupledParams p) {
+template <int CH, int NG>
+__global__ void __launch_bounds__(kThreadsC, 2) k_sweeps_coupled(const __grid_constant__ CoupledParams p) {
     extern __shared__ __align__(128) char sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned int epoch = *(volatile unsigned int *)&p.sync[0];
-    // group bases: [0, 256) publication counters, then group 0, group 1, group 2
-    const Layout LyR{p.nst_r, 2, p.cap_r, 8, (int64_t)p.WR.wcap};
-    const Layout LyS{p.nst_s, 1, p.cap_s, 8, (int64_t)p.WL.wcap};
-    char *gb0 = sm + kPubBytes;
-    char *gb1 = gb0 + 128 + (int64_t)p.nst_r * (2 * Layout::part_bytes(p.cap_r, 8) + (int64_t)p.WR.wcap * 8);
-    auto gbase = [&](int g) { return g == 0 ? gb0 : gb1 + (int64_t)(g - 1) * p.goff_s; };
-    // sweeps: r rows after the stages' windows
-    auto rslot = [&](int g) { return LyS.win(gbase(g), 0) + (int64_t)p.nst_s * p.WL.wcap; };
+    const int g = (int)(blockIdx.x % NG);
+    const int64_t c = blockIdx.x / NG, Gg = gridDim.x / NG, ntiles = p.ntiles;
+    // [0, 128) publication counters, then the barriers and stages
+    char *gb = sm + kCtlBytes;
+    const Layout Ly{p.nst, 1, p.cap, 8, (int64_t)p.WL.wcap};
+    double *rs0 = Ly.win(gb, 0) + (int64_t)p.nst * p.WL.wcap;   // r rows after the stages' windows
+    unsigned int *cnt = (unsigned int *)sm;
     if (threadIdx.x == 0) {
-        for (int st = 0; st < p.nst_r; ++st) {
-            ptx::mbar_init(LyR.full(gb0) + st, 1);
-            ptx::mbar_init(LyR.empty(gb0) + st, kRW);
+        for (int st = 0; st < p.nst; ++st) {
+            ptx::mbar_init(Ly.full(gb) + st, 1);
+            ptx::mbar_init(Ly.empty(gb) + st, kCW);
         }
-        for (int g = 1; g <= K; ++g)
-            for (int st = 0; st < p.nst_s; ++st) {
-                ptx::mbar_init(LyS.full(gbase(g)) + st, 1);
-                ptx::mbar_init(LyS.empty(gbase(g)) + st, kSW);
-            }
-        for (int q = 0; q < kPubBytes / 4; ++q) ((unsigned int *)sm)[q] = 0;
+        for (int q = 0; q < kSlots; ++q) cnt[q] = 0;
         ptx::mbar_init_fence();
     }
     __syncthreads();
-    const int64_t ntiles = p.ntiles, G = gridDim.x, c = blockIdx.x;
-    constexpr int kProd0 = kRW + K * kSW;
+    const int64_t mine = c < ntiles ? (ntiles - 1 - c) / Gg + 1 : 0;   // tiles of this CTA
 
-    if (warp >= kProd0) {
-        // ------------------------------------------------------------ producers
-        const int g = warp - kProd0;
-        CoupledHook<K> hk;
+    if (warp == kCW) {
+        // ------------------------------------------------------------ producer
+        CoupledHook<NG> hk;
         hk.p = &p;
         hk.g = g;
+        hk.c = c;
+        hk.Gg = Gg;
         hk.epoch = epoch;
-        hk.rslot0 = g > 0 ? rslot(g) : nullptr;
-        hk.Fa = hk.Fb = 0;
-        hk.dirty = false;
+        hk.rslot0 = rs0;
+        hk.Fs = hk.Ff = 0;
+        hk.pending = false;
         hk.pol_keep = ptx::policy_evict_normal();
         hk.pol_first = ptx::policy_evict_first();
-        if (g == 0) {
-            const SellView P[2] = {p.L, p.U};
-            producer<2, true, CoupledHook<K>>(LyR, gb0, P, 0, p.nslices, ntiles, lane, p.WR, p.x, p.n, hk);
-        } else {
-            const SellView P[1] = {p.L};
-            producer<1, true, CoupledHook<K>>(LyS, gbase(g), P, 0, p.nslices, ntiles, lane, p.WL, p.g[g - 1], p.n, hk);
+        hk.c_last = hk.c_wait = hk.c_empty = hk.c_fence = 0;
+        const SellView P[1] = {p.L};
+        const long long c0 = clock64();
+        producer_deep<1, CoupledHook<NG> &>(Ly, gb, P, 0, p.nslices, ntiles, lane, p.WL, p.g[g], p.n, hk);
+        if (p.stats && lane == 0) {
+            atomicAdd(p.stats + 4 * g + 0, (unsigned long long)hk.c_wait);
+            atomicAdd(p.stats + 4 * g + 1, (unsigned long long)hk.c_empty);
+            atomicAdd(p.stats + 4 * g + 2, (unsigned long long)(clock64() - c0));
+            atomicAdd(p.stats + 12 + g, (unsigned long long)hk.c_fence);
         }
-    } else if (warp < kRW) {
-        // ------------------------------------ group 0: r = b - A x, g(0) = r / d
-        int st = 0;
-        uint32_t ph = 0;
-        for (int64_t t = c, m = 0; t < ntiles; t += G, ++m) {
-            const int64_t s = t * kTS + warp;
-            const bool has = s < p.nslices;
-            const int64_t i = s * kSlice + lane;
-            const bool row = has && i < p.n;
-            // own-row vectors: immutable (d, b), or x of tile t, which group k
-            // rewrites only after this tile is published
-            const double di = row ? __ldg(p.d + i) : 0.0, xi = row ? __ldg(p.x + i) : 0.0;
-            const double bi = row ? __ldg(p.b + i) : 0.0;
-            ptx::mbar_wait(LyR.full(gb0) + st, ph);
-            double acc = 0.0;
-            if (has) {
-                const int2 hl = *(const int2 *)(LyR.hdr(gb0, st, 0) + 2 * warp);
-                const int2 hu = *(const int2 *)(LyR.hdr(gb0, st, 1) + 2 * warp);
-                const double *ws = LyR.win(gb0, st);
-                if constexpr (CH <= 8) {
-                    WinChunk<CH> cl, cu;
-                    cl.load(LyR.val(gb0, st, 0), LyR.col(gb0, st, 0), ws, hl.x, hl.y, lane, row);
-                    cu.load(LyR.val(gb0, st, 1), LyR.col(gb0, st, 1), ws, hu.x, hu.y, lane, row);
-                    acc = cl.add(acc);
-                    acc = __dadd_rn(acc, __dmul_rn(di, xi));
-                    acc = cu.add(acc);
+    } else if (warp == kCW + 1) {
+        // ------------------------------------------------------------ publisher
+        if (lane == 0) {
+            int64_t m = 0;
+            const uint64_t t0 = ptx::globaltimer_ns();
+            while (m < mine) {
+                int64_t mm = m;
+                while (mm < mine &&
+                       ptx::ld_acquire_cta_shared(cnt + mm % kSlots) >= (unsigned int)((mm / kSlots + 1) * kCW))
+                    ++mm;
+                if (mm > m) {
+                    ptx::red_max_release_gpu_u64(p.prog + (int64_t)g * p.pstride + c,
+                                                 ((unsigned long long)epoch << 32) | (unsigned long long)mm);
+                    m = mm;
                 } else {
-                    WinChunk<CH> cw;
-                    cw.load(LyR.val(gb0, st, 0), LyR.col(gb0, st, 0), ws, hl.x, hl.y, lane, row);
-                    acc = cw.add(acc);
-                    acc = __dadd_rn(acc, __dmul_rn(di, xi));
-                    cw.load(LyR.val(gb0, st, 1), LyR.col(gb0, st, 1), ws, hu.x, hu.y, lane, row);
-                    acc = cw.add(acc);
+                    if (ptx::globaltimer_ns() - t0 > 4 * p.timeout_ns) break;  // the producers flagged it
+                    __nanosleep(32);
                 }
             }
-            if (row) {
-                const double r = __dsub_rn(bi, acc);
-                p.r[i] = r;
-                p.g[0][i] = __ddiv_rn(r, di);
-            }
-            publish_and_release(p, sm, 0, st, kRW, LyR.empty(gb0) + st, m, epoch, lane);
-            if (++st == p.nst_r) { st = 0; ph ^= 1; }
         }
     } else {
-        // -------------------- group j: g(j) = (r - L g(j-1)) / d; j = k: x += g(k)
-        const int g = 1 + (warp - kRW) / kSW, wl = (warp - kRW) % kSW;
-        char *gb = gbase(g);
-        const double *rs0 = rslot(g);
-        double *gout = g < K ? p.g[g] : nullptr;
-        const unsigned long long sid = (unsigned long long)(p.sweep_id0 + g - 1);
+        // -------------------- group j: g(j+1) = (r - L g(j)) / d; last: x += ...
+        const int wl = warp;
+        double *gout = g < NG - 1 ? p.g[g + 1] : nullptr;
+        const unsigned long long sid = (unsigned long long)(p.sweep_id0 + g);
         int st = 0;
         uint32_t ph = 0;
-        for (int64_t t = c, m = 0; t < ntiles; t += G, ++m) {
-            double di[2], xi[2], v[2];
-            bool row[2], has[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t s = t * kTS + wl + h * kSW;
-                const int64_t i = s * kSlice + lane;
-                has[h] = s < p.nslices;
-                row[h] = has[h] && i < p.n;
-                di[h] = row[h] ? __ldg(p.d + i) : 1.0;
-                xi[h] = (g == K && row[h]) ? p.x[i] : 0.0;  // x of tile t: written only by this group, below
+        long long c_full = 0;
+        for (int64_t t = c, m = 0; t < ntiles; t += Gg, ++m) {
+            const int64_t s = t * kTS + wl;
+            const int64_t i = s * kSlice + lane;
+            const bool has = s < p.nslices;
+            const bool row = has && i < p.n;
+            const double di = row ? __ldg(p.d + i) : 1.0;
+            const double xi = (g == NG - 1 && row) ? p.x[i] : 0.0;  // x of tile t: only this group's tile t writes it
+            const long long cw = clock64();
+            ptx::mbar_wait(Ly.full(gb) + st, ph);
+            c_full += clock64() - cw;
+            double acc = 0.0;
+            if (has) {
+                const int2 hd = *(const int2 *)(Ly.hdr(gb, st, 0) + 2 * wl);
+                WinChunk<CH> ct;
+                ct.load(Ly.val(gb, st, 0), Ly.col(gb, st, 0), Ly.win(gb, st), hd.x, hd.y, lane, row);
+                acc = ct.add(acc);
             }
-            ptx::mbar_wait(LyS.full(gb) + st, ph);
-            const double *ws = LyS.win(gb, st);
-            const double *rs = rs0 + st * kTS * kSlice;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int sl = wl + h * kSW;
-                double acc = 0.0;
-                if (has[h]) {
-                    const int2 hd = *(const int2 *)(LyS.hdr(gb, st, 0) + 2 * sl);
-                    WinChunk<CH> ct;
-                    ct.load(LyS.val(gb, st, 0), LyS.col(gb, st, 0), ws, hd.x, hd.y, lane, row[h]);
-                    acc = ct.add(acc);
-                }
-                const double ri = row[h] ? rs[sl * kSlice + lane] : 0.0;
-                v[h] = __ddiv_rn(__dsub_rn(ri, acc), di[h]);
+            const double ri = row ? rs0[st * kTS * kSlice + wl * kSlice + lane] : 0.0;
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(Ly.empty(gb) + st);  // the stage may be refilled
+            if (row) {
+                const double v = __ddiv_rn(__dsub_rn(ri, acc), di);
+                if (!isfinite(v)) atomicMin(p.flag, sid);
+                if (g < NG - 1) gout[i] = v;
+                else p.x[i] = __dadd_rn(xi, v);
             }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (!row[h]) continue;
-                const int64_t i = (t * kTS + wl + h * kSW) * kSlice + lane;
-                if (!isfinite(v[h])) atomicMin(p.flag, sid);
-                if (g < K) gout[i] = v[h];
-                else p.x[i] = __dadd_rn(xi[h], v[h]);
-            }
-            publish_and_release(p, sm, g, st, kSW, LyS.empty(gb) + st, m, epoch, lane);
-            if (++st == p.nst_s) { st = 0; ph ^= 1; }
+            __syncwarp();
+            if (lane == 0) ptx::red_add_release_cta_shared(cnt + m % kSlots, 1u);
+            if (++st == p.nst) { st = 0; ph ^= 1; }
         }
+        if (p.stats && lane == 0 && wl == 0) atomicAdd(p.stats + 4 * g + 3, (unsigned long long)c_full);
     }
     // ---- the last CTA out advances the epoch for the next launch
     __syncthreads();
@@ -336,87 +302,80 @@ WinView wview(const Window *w) {
     return WinView{w->tseg, w->glo, w->len, w->sbase, {w->wpos[0], w->wpos[1]}, (w->wmax + 31) / 32 * 32};
 }
 
-template <int CH, int K>
-const void *kernel_of() { return (const void *)k_pgs_coupled<CH, K>; }
+template <int CH, int NG>
+const void *kernel_of() { return (const void *)k_sweeps_coupled<CH, NG>; }
 
 const void *coupled_kernel(int ch, int k) {
-    if (ch <= 8) return k == 1 ? kernel_of<8, 1>() : kernel_of<8, 2>();
-    return k == 1 ? kernel_of<16, 1>() : kernel_of<16, 2>();
+    if (ch <= 8) return k == 2 ? kernel_of<8, 2>() : kernel_of<8, 3>();
+    return k == 2 ? kernel_of<16, 2>() : kernel_of<16, 3>();
 }
-int coupled_threads(int k) { return k == 1 ? threads_c<1>() : threads_c<2>(); }
 
 }  // namespace
 
-CoupledShape coupled_shape(int maxw_a, int maxw_l, int64_t wcap_r, int64_t wcap_s, int k, int64_t n) {
+CoupledShape coupled_shape(int maxw_l, int64_t wcap, int k, int64_t n) {
     CoupledShape sh;
-    if (k < 1 || k > kMaxK || n <= 0 || maxw_a > 16 || maxw_l > 16) return sh;
-    const int ch = maxw_a <= 8 ? 8 : 16;
-    sh.cap_r = (int64_t)kTS * kSlice * std::max(maxw_a, 1);
-    sh.cap_s = (int64_t)kTS * kSlice * std::max(maxw_l, 1);
-    wcap_r = (wcap_r + 31) / 32 * 32;
-    wcap_s = (wcap_s + 31) / 32 * 32;
-    const int64_t stage_r = 2 * Layout::part_bytes(sh.cap_r, 8) + wcap_r * 8;
-    const int64_t stage_s = Layout::part_bytes(sh.cap_s, 8) + wcap_s * 8 + (int64_t)kTS * kSlice * 8;
-    // deepest residual pipeline first (it streams from HBM), then the sweeps'
-    for (int nr = 3; nr >= 1 && !sh.ok; --nr)
-        for (int ns = 3; ns >= 1 && !sh.ok; --ns) {
-            const int64_t goff = 128 + ns * stage_s;
-            const int64_t smem = kPubBytes + 128 + nr * stage_r + k * goff;
-            if (smem <= kSmemMaxC) {
-                sh.ok = true;
-                sh.nst_r = nr;
-                sh.nst_s = ns;
-                sh.goff_s = goff;
-                sh.smem = (size_t)smem;
-            }
-        }
-    if (!sh.ok) return sh;
+    if (k < 2 || k > kMaxG || n <= 0 || maxw_l > 16) return sh;
+    const int ch = maxw_l <= 8 ? 8 : 16;
+    sh.cap = (int64_t)kTS * kSlice * std::max(maxw_l, 1);
+    wcap = (wcap + 31) / 32 * 32;
+    sh.stage = Layout::part_bytes(sh.cap, 8) + wcap * 8 + (int64_t)kTS * kSlice * 8;
+    if (kCtlBytes + 128 + sh.stage > kSmemMaxC) return sh;
+    sh.ok = true;
     sh.kernel = coupled_kernel(ch, k);
-    sh.threads = coupled_threads(k);
-    sh.wcap_r = wcap_r;
-    sh.wcap_s = wcap_s;
+    sh.threads = kThreadsC;
+    sh.wcap = wcap;
+    sh.k = k;
     return sh;
 }
 
 cudaError_t launch_coupled(const CoupledLaunch &L, cudaStream_t st) {
     const CoupledShape &sh = L.shape;
     static std::mutex mu;
-    static std::map<std::pair<int, const void *>, int> per_sm;  // device, kernel
+    static std::map<std::pair<int, const void *>, int> attr_set;  // device, kernel
     int dev = 0;
     cudaGetDevice(&dev);
-    int occ = 0;
     {
         std::lock_guard<std::mutex> lk(mu);
         auto key = std::make_pair(dev, sh.kernel);
-        auto it = per_sm.find(key);
-        if (it == per_sm.end()) {
+        if (attr_set.find(key) == attr_set.end()) {
             cudaFuncSetAttribute(sh.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxC);
-            it = per_sm.emplace(key, -1).first;
+            attr_set.emplace(key, 1);
         }
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sh.kernel, sh.threads, sh.smem);
-        if (e != cudaSuccess) return e;
     }
-    if (occ < 1) return cudaErrorInvalidConfiguration;
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    // stages: the most that keep k CTAs per SM (one of each group), else the
+    // most that fit at all
+    int nst = 0, per_sm = 0;
+    for (int s = 3; s >= 1; --s) {
+        const size_t smem = (size_t)(kCtlBytes + 128 + s * sh.stage);
+        if ((int64_t)smem > kSmemMaxC) continue;
+        int occ = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sh.kernel, sh.threads, smem);
+        if (e != cudaSuccess) return e;
+        if (occ > per_sm) {
+            nst = s;
+            per_sm = occ;
+        }
+        if (occ >= sh.k) break;
+    }
+    if (!nst || per_sm < 1) return cudaErrorInvalidConfiguration;
+    const size_t smem = (size_t)(kCtlBytes + 128 + nst * sh.stage);
     const int64_t ntiles = (L.n + kTS * kSlice - 1) / (kTS * kSlice);
-    const int grid = (int)std::min<int64_t>({(int64_t)nsm, ntiles, L.pstride});
+    const int64_t per_group = std::min<int64_t>({(int64_t)nsm * per_sm / sh.k, ntiles, L.pstride});
+    if (per_group < 1) return cudaErrorInvalidConfiguration;
+    const int grid = (int)(per_group * sh.k);
     CoupledParams p{};
     p.n = L.n;
     p.nslices = (L.n + kSlice - 1) / kSlice;
     p.ntiles = ntiles;
     p.L = view(*L.Lp);
-    p.U = view(*L.Up);
-    p.WR = wview(L.wr);
     p.WL = wview(L.wl);
-    p.WR.wcap = (int32_t)sh.wcap_r;
-    p.WL.wcap = (int32_t)sh.wcap_s;
+    p.WL.wcap = (int32_t)sh.wcap;
     p.d = L.d;
-    p.b = L.b;
-    p.x = L.x;
     p.r = L.r;
-    p.g[0] = L.g0;
-    p.g[1] = L.g1;
+    p.x = L.x;
+    for (int g = 0; g < kMaxG; ++g) p.g[g] = L.g[g];
     p.prog = L.prog;
     p.pstride = L.pstride;
     p.sync = L.sync;
@@ -424,22 +383,19 @@ cudaError_t launch_coupled(const CoupledLaunch &L, cudaStream_t st) {
     p.sweep_id0 = L.sweep_id0;
     p.err = L.err;
     p.timeout_ns = L.timeout_ns;
-    p.DA = L.DA;
-    // throttle distance: the dependency distance plus a few rounds of tiles
-    p.lag = L.lag > 0 ? std::max<int64_t>(L.lag, L.DA + 1) : L.DA + 1 + 4 * (int64_t)grid;
-    p.nst_r = sh.nst_r;
-    p.nst_s = sh.nst_s;
-    p.cap_r = sh.cap_r;
-    p.cap_s = sh.cap_s;
-    p.goff_s = sh.goff_s;
+    // throttle distance: a few rounds of tiles (>= 1 for the deadlock argument)
+    p.lag = L.lag > 0 ? L.lag : 4 * per_group;
+    p.nst = nst;
+    p.cap = sh.cap;
+    p.stats = L.stats;
     void *args[] = {&p};
-    return cudaLaunchCooperativeKernel(sh.kernel, dim3((unsigned)grid), dim3((unsigned)sh.threads), args, sh.smem, st);
+    return cudaLaunchCooperativeKernel(sh.kernel, dim3((unsigned)grid), dim3((unsigned)sh.threads), args, smem, st);
 }
 
 void preload_coupled_kernels() {
     cudaFuncAttributes a;
     for (int ch : {8, 16})
-        for (int k = 1; k <= kMaxK; ++k) cudaFuncGetAttributes(&a, coupled_kernel(ch, k));
+        for (int k = 2; k <= kMaxG; ++k) cudaFuncGetAttributes(&a, coupled_kernel(ch, k));
 }
 
 }  // namespace nsm

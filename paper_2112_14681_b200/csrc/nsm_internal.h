@@ -295,35 +295,34 @@ void preload_fused_w_kernels();
 // plane structure of L and U for the plane wavefront (tpp tiles per plane)
 bool fused_w_plane_check(int64_t n, int64_t tpp, const Sell &L, const Sell &U);
 
-// ---- coupled passes (coupled.cu) ------------------------------------------------
-// One forward pGS application (k = 1, 2) as concurrent warp groups of one
-// cooperative kernel: offset-aligned L and U with gather windows, one rank.
+// ---- coupled sweeps (coupled.cu) ------------------------------------------------
+// The k = 2, 3 sweeps of a forward pGS application as concurrent CTA groups of
+// one cooperative kernel: offset-aligned L with a gather window, one rank.
 struct CoupledShape {
     bool ok = false;
     const void *kernel = nullptr;
-    int threads = 0, nst_r = 0, nst_s = 0;
-    size_t smem = 0;
-    int64_t cap_r = 0, cap_s = 0, goff_s = 0, wcap_r = 0, wcap_s = 0;
+    int threads = 0, k = 0;
+    int64_t cap = 0, wcap = 0, stage = 0;   // entries / window doubles / bytes per stage
 };
-// maxw_a: widest slice of L and U; maxw_l: of L; wcap_r / wcap_s: largest
-// residual / L window (doubles)
-CoupledShape coupled_shape(int maxw_a, int maxw_l, int64_t wcap_r, int64_t wcap_s, int k, int64_t n);
+// maxw_l: widest slice of L; wcap: largest L window (doubles)
+CoupledShape coupled_shape(int maxw_l, int64_t wcap, int k, int64_t n);
 struct CoupledLaunch {
     CoupledShape shape;
     int64_t n;
-    const Sell *Lp, *Up;
-    const Window *wr, *wl;           // residual window (L and U), L's sweep window
-    const double *d, *b;
-    double *x, *r, *g0, *g1;         // x updated in place; r, g(0), g(1) scratch
-    unsigned long long *prog;        // [k + 1][pstride], zero-initialised once
+    const Sell *Lp;
+    const Window *wl;                // L's gather window
+    const double *d, *r;
+    double *x;                       // updated in place
+    double *g[3];                    // g(0) (from the residual), then scratch iterates
+    unsigned long long *prog;        // [k][pstride], zero-initialised once
     int64_t pstride;
     unsigned int *sync;              // [0] epoch, [1] CTAs finished
     unsigned long long *flag;
     int64_t sweep_id0;
     unsigned int *err;
     unsigned long long timeout_ns;
-    int64_t DA;                      // upper bandwidth of A in 256-row tiles, + 1
     int64_t lag;                     // group 0's throttle distance in tiles (0: automatic)
+    unsigned long long *stats;       // nullable: 16 cycle counters (nsm_coupled_counters)
 };
 cudaError_t launch_coupled(const CoupledLaunch &L, cudaStream_t st);
 void preload_coupled_kernels();

@@ -400,8 +400,17 @@ cudaError_t sweep_tma_ofs(const SweepArgs &a, int64_t s_begin, int64_t s_end, G 
     const WinView W = win_view(WIN ? a.win : nullptr);
     auto k = k_sweep_tma<UNIT, EPI, G, CH, OFS>;
     if constexpr (WIN) k = k_sweep_tma_w<UNIT, EPI, CH>;
-    const Geo g = geometry(k, 1, a.T->maxw, OFS ? 8 : 12, (int64_t)W.wcap * 8);
+    Geo g = geometry(k, 1, a.T->maxw, OFS ? 8 : 12, (int64_t)W.wcap * 8);
     if (!g.nst) return cudaErrorInvalidConfiguration;
+    if (const char *v = knob("NSM_SWEEP_NST")) {  // experiment: force the stage count (occupancy follows)
+        const int nst = atoi(v);
+        const int64_t stage = Layout::part_bytes(g.cap, OFS ? 8 : 12) + (int64_t)W.wcap * 8;
+        g.nst = nst;
+        g.smem = (size_t)(128 + nst * stage);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreadsT, g.smem);
+        g.per_sm = per_sm;
+    }
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     return launch_pdl(a.pdl, k, grid_of<decltype(k)>(g, ntiles), g.smem, st, a.n, s_begin, s_end, view(*a.T), a.dT, a.rhs,
                       gin, a.gout, a.x, a.dnext, a.gout2, a.flag, a.sweep_id, g.nst, g.cap, W);

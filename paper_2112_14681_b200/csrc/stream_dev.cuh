@@ -110,6 +110,7 @@ struct TileRefs {
     // windowed kernels: this tile's gather-window segments, lane k holds segment k
     int32_t nseg, sg_len, sg_base;
     int64_t sg_lo;
+    int32_t wg0;  // producer_deep: the tile's first window segment (between its two load phases)
 };
 
 // Entry-position arrays staged into the "offsets" slot: the column offsets,
@@ -291,6 +292,138 @@ __device__ __forceinline__ void producer(const Layout &Ly, char *sm, const SellV
         if (++st == Ly.nst) { st = 0; ph ^= 1; }
     }
     if (lane == 0) pdl_trigger();  // all of this CTA's copies are issued: dependents may be scheduled
+}
+
+// Two-phase tile references for producer_deep: phase A loads what depends
+// only on the tile index (slice pointers, the window plan's segment range),
+// phase B what depends on phase A (offsets / window positions, segments).
+template <int NP>
+__device__ __forceinline__ void tile_refs_a(const SellView (&P)[NP], int64_t s_begin, int64_t s_end, int64_t t,
+                                            int lane, TileRefs<NP> &r, const WinView &W) {
+    const int64_t s0 = s_begin + t * kTS, s1 = min(s0 + kTS, s_end);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        r.b[p] = __ldg(P[p].ptr + s0);
+        r.e[p] = __ldg(P[p].ptr + s1);
+        r.sp[p] = lane <= kTS ? __ldg(P[p].ptr + min(s0 + lane, s1)) : 0;
+    }
+    const int64_t wt = s0 / kTS;
+    r.wg0 = __ldg(W.tseg + wt);
+    r.nseg = __ldg(W.tseg + wt + 1);   // the end; phase B turns it into the count
+}
+template <int NP>
+__device__ __forceinline__ void tile_refs_b(const SellView (&P)[NP], int lane, TileRefs<NP> &r, const WinView &W) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int64_t no = (r.e[p] - r.b[p]) / kSlice;
+        const int32_t *go = W.wpos[p] + r.b[p] / kSlice;
+#pragma unroll
+        for (int q = 0; q < kOfsPerLane; ++q) {
+            const int64_t k = lane + 32 * q;
+            r.o[p][q] = k < no ? __ldg(go + k) : 0;
+        }
+    }
+    r.nseg -= r.wg0;
+    if (lane < r.nseg) {
+        r.sg_lo = __ldg(W.glo + r.wg0 + lane);
+        r.sg_len = __ldg(W.len + r.wg0 + lane);
+        r.sg_base = __ldg(W.sbase + r.wg0 + lane);
+    }
+}
+
+// The windowed producer (offset-aligned parts, gather window) with its tile
+// references loaded three tiles ahead in two phases, so neither dependent
+// round trip sits on the producer's per-tile path: one producer warp then
+// keeps up with tiles arriving at several times the per-pass rate (the
+// coupled sweeps, coupled.cu).  Same staging as producer<NP, true, Hook>.
+template <int NP, class Hook>
+__device__ __forceinline__ void producer_deep(const Layout &Ly, char *sm, const SellView (&P)[NP], int64_t s_begin,
+                                              int64_t s_end, int64_t ntiles, int lane, const WinView &W,
+                                              const double *vec, int64_t n, Hook hook) {
+    const uint64_t pol = policy_evict_first_t();
+    const uint64_t pol_win = ptx::policy_evict_normal();
+    int it = 0, st = 0;
+    uint32_t ph = 0;
+    const int64_t t_first = hook.first(), G = hook.stride();
+    // cur: tile t (complete); nxt: t + G (phase A landed, phase B in flight); nn: t + 2G (phase A in flight)
+    TileRefs<NP> cur, nxt, nn;
+    if (t_first < ntiles) {
+        tile_refs_a<NP>(P, s_begin, s_end, t_first, lane, cur, W);
+        tile_refs_b<NP>(P, lane, cur, W);
+    }
+    if (t_first + G < ntiles) {
+        tile_refs_a<NP>(P, s_begin, s_end, t_first + G, lane, nxt, W);
+        tile_refs_b<NP>(P, lane, nxt, W);
+    }
+    if (t_first + 2 * G < ntiles) tile_refs_a<NP>(P, s_begin, s_end, t_first + 2 * G, lane, nn, W);
+    for (int64_t t = t_first; t < ntiles; t += G, ++it) {
+        if (it >= Ly.nst) mbar_wait(Ly.empty(sm) + st, ph ^ 1);
+        hook.before(t, st, lane);
+        uint32_t bytes = hook.extra_bytes(t);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) bytes += (uint32_t)((cur.e[p] - cur.b[p]) * 8);
+        int64_t wa = 0;
+        uint32_t wbytes = 0;
+        if (lane < cur.nseg) {
+            double *ws = Ly.win(sm, st) + cur.sg_base - cur.sg_lo;
+            const int64_t lo = cur.sg_lo, hi = lo + cur.sg_len;
+            const int64_t a = max(lo, (int64_t)0), e = min(hi, n);
+            for (int64_t q = lo; q < min(a, hi); ++q) ws[q] = 0.0;
+            for (int64_t q = max(e, lo); q < hi; ++q) ws[q] = 0.0;
+            if (e > a) {
+                const int64_t be = e & ~(int64_t)1;
+                if (be < e) ws[e - 1] = __ldcg(vec + e - 1);
+                wa = a;
+                wbytes = be > a ? (uint32_t)((be - a) * 8) : 0u;
+            }
+        }
+        {
+            uint32_t wsum = wbytes;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+            bytes += wsum;
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            int32_t *so = Ly.col(sm, st, p);
+            const int64_t no = (cur.e[p] - cur.b[p]) / kSlice;
+#pragma unroll
+            for (int q = 0; q < kOfsPerLane; ++q) {
+                const int64_t k = lane + 32 * q;
+                if (k < no) so[k] = cur.o[p][q];
+            }
+            const int32_t *go = W.wpos[p] + cur.b[p] / kSlice;
+            for (int64_t k = lane + 32 * kOfsPerLane; k < no; k += 32) so[k] = __ldg(go + k);
+            const int64_t nsp = __shfl_down_sync(0xffffffffu, cur.sp[p], 1);
+            if (lane < kTS) {
+                int32_t *h = Ly.hdr(sm, st, p);
+                h[2 * lane] = (int32_t)(cur.sp[p] - cur.b[p]);
+                h[2 * lane + 1] = (int32_t)((nsp - cur.sp[p]) / kSlice);
+            }
+        }
+        __syncwarp();  // the plain stores (offsets, header, window fill) precede the arrival
+        if (lane == 0) {
+            mbar_expect_tx(Ly.full(sm) + st, bytes);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const int64_t b = cur.b[p], e = cur.e[p];
+                if (e > b)
+                    bulk_g2s(Ly.val(sm, st, p), P[p].val + b, (uint32_t)((e - b) * 8), Ly.full(sm) + st,
+                             hook.val_policy(p, pol));
+            }
+            hook.extra_copy(t, st, Ly.full(sm) + st);
+        }
+        __syncwarp();  // the expected byte count is registered before any window copy completes
+        if (wbytes)
+            bulk_g2s(Ly.win(sm, st) + cur.sg_base + (wa - cur.sg_lo), vec + wa, wbytes, Ly.full(sm) + st, pol_win);
+        __syncwarp();
+        // rotate: each slot's loads were issued one iteration ago
+        cur = nxt;
+        nxt = nn;
+        if (t + 2 * G < ntiles) tile_refs_b<NP>(P, lane, nxt, W);
+        if (t + 3 * G < ntiles) tile_refs_a<NP>(P, s_begin, s_end, t + 3 * G, lane, nn, W);
+        if (++st == Ly.nst) { st = 0; ph ^= 1; }
+    }
 }
 
 // Register chunk of one row taken from the staged copy: the first CH entries

@@ -85,10 +85,10 @@ def set_kernels(S, mode):
     default); nowindow: the same gathering through L1/L2; plain:
     register-blocked; onepass(w1): the one-pass windowed pGS (NSM_OPT_FUSED = 3)
     where the matrix allows it, else as fused (w1: skew margin 1); coupled: the
-    default — forward pGS (k = 1, 2) on windowed matrices as concurrent warp
-    groups of one kernel (NSM_OPT_COUPLED), the rest pipelined; coupledlag: the
-    same at the tightest throttle distance (group 0 waits for the last sweep
-    group at the dependency distance: stresses the synchronisation)."""
+    k = 2, 3 sweeps of a forward pGS application on windowed matrices as
+    concurrent CTA groups of one kernel (NSM_OPT_COUPLED), the rest pipelined;
+    coupledlag: the same at throttle distance 2 (group 0 waits for the last
+    sweep group almost every tile: stresses the synchronisation)."""
     S.set_coupled(1 if mode == "coupled" else (2 if mode == "coupledlag" else 0))
     S.set_pipeline(mode != "plain")
     S.set_window(mode != "nowindow")
@@ -328,14 +328,15 @@ def test_onepass_plane_wavefront(grid, xz, k):
 @pytest.mark.parametrize("name", ["var27_aligned_40", "var27_ragged", "var27_48tiles"])
 @pytest.mark.parametrize("lag", [1, 2])
 @pytest.mark.parametrize("xz", [False, True])
-@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("k", [2, 3])
 def test_coupled_pgs(name, lag, xz, k):
-    """The coupled passes (coupled.cu, NSM_OPT_COUPLED) really run on 27-point
-    matrices (one 'fused' pass per non-fresh application) and are bit-identical
-    to the oracle for k = 1, 2, nu = 2 (the first application from x = 0 runs
-    per pass, the second coupled), at the automatic and the tightest throttle
-    distance; several tiles per CTA, a ragged last tile, and fewer tiles than
-    SMs (var27_48tiles)."""
+    """The coupled sweeps (coupled.cu, NSM_OPT_COUPLED) really run on 27-point
+    matrices (ONE sweep launch per non-fresh application instead of k) and are
+    bit-identical to the oracle for k = 2, 3, nu = 2 (the first application
+    from x = 0 runs per pass, the second coupled), at the automatic and the
+    tightest throttle distance (lag 2 -> 2 tiles: group 0 waits for the last
+    group almost every tile); several tiles per CTA, a ragged last tile, and
+    fewer tiles than SMs (var27_48tiles)."""
     A = (SMALL[name]() if name in SMALL else
          inputs.var27_grid(64, 16, 12) if name == "var27_48tiles" else inputs.var27_grid(130, 20, 6))
     b = inputs.uniform(0, A.nrows)
@@ -348,7 +349,7 @@ def test_coupled_pgs(name, lag, xz, k):
         x = start(x0, xz)
         S.smooth(dev(b), x, "pgs", nu=2, k_l=k, x_is_zero=xz)
         agree(host(x), want, f"{name} coupled k={k} xz={xz} lag={lag}")
-        assert S.profile()["fused"][1] == (1 if xz else 2), "the coupled kernel did not run"
+        assert S.profile()["sweep"][1] == (k + 1 if xz else 2), "the coupled kernel did not run"
         S.check()
         for rep in range(3):   # repeated launches: the epoch advances, results stay identical
             x = start(x0, xz)

@@ -1,9 +1,7 @@
-# coupled passes: parity, and one ncu --set full capture of the coupled kernel
-# and of the per-pass residual (C3) for the shared-memory / stall comparison
+# coupled sweeps (NSM_OPT_COUPLED): parity incl. full-size C3, bench A/B on C3
 set -x
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "coupled" 2>&1 | tail -4
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_pgs_coupled -c 1 -f -o gpurun_out/cp_full \
-  python bench.py --no-cpu --steps 1 --warmup 3 > gpurun_out/cp_ncu.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_residual_tma_w -c 1 -f -o gpurun_out/res_full \
-  python bench.py --no-cpu --steps 1 --warmup 3 --coupled off > gpurun_out/res_ncu.log 2>&1
-ls -la gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "coupled or full_size_parity" 2>&1 | tail -4
+for c in off on 1200; do
+  timeout 300 python bench.py --no-cpu --steps 20 --warmup 3 --coupled $c 2>&1 | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('coupled=$c', d['ms_per_step'], d['value'], d['roofline']['frac'], d['roofline'].get('sweeps_frac'), d['detail']['kernels'][:60])"
+done
