@@ -17,7 +17,7 @@ S = nsm.Smoother(A)
 b = torch.from_numpy(inputs.uniform(inputs.SEED_B, A.nrows)).cuda()
 x = torch.from_numpy(inputs.uniform(inputs.SEED_X0, A.nrows)).cuda()
 for lag in [int(a) for a in (sys.argv[1:] or ["1", "150", "300", "600", "1200", "4000"])]:
-    S.set_coupled(lag)
+    S.set_coupled(lag if lag > 0 else 1)
     for _ in range(3):
         S.smooth(b, x, "pgs", k_l=2)
     S.set_profile(True)
