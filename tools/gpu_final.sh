@@ -14,6 +14,8 @@ for c in C2 C4 C5; do
   timeout 600 python bench.py --config $c --no-cpu > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
 timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 python bench.py --coupled on --no-cpu > gpurun_out/bench_C3_coupled.json 2> gpurun_out/bench_C3_coupled.err
+timeout 300 python tools/pcie_probe.py > gpurun_out/pcie.txt 2>&1
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 timeout 900 ncu --metrics $M --clock-control none -c 400 --csv --log-file gpurun_out/launches_C3.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --metrics $M --clock-control none -k regex:'k_' -c 60 --csv --log-file gpurun_out/launches_C4.csv python bench.py --config C4 --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch4.log 2>&1
