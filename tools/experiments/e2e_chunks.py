@@ -1,0 +1,38 @@
+"""C3 e2e (nsm_smooth_host, pinned host vectors) against the number of row
+chunks (NSM_HOST_CHUNKS_N, libnsm_exp.so) and without chunking; events around
+each call as in bench.py, L2 not flushed."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import numpy as np, torch
+import bench, inputs
+import paper_2112_14681_b200 as nsm
+
+nsm.load(variant="exp")
+A, offsets, kind, k_l, k_u, desc = bench.build_workload("C3", 0, 1)
+S = nsm.Smoother(A)
+bh = torch.from_numpy(inputs.uniform(inputs.SEED_B, A.nrows)).pin_memory()
+xh = torch.from_numpy(inputs.uniform(inputs.SEED_X0, A.nrows)).pin_memory()
+xo = torch.empty_like(xh).pin_memory()
+st = torch.cuda.current_stream()
+for label in ["16/2", "32/2", "16/1", "32/1", "16/2nc", "32/2nc", "off"]:
+    os.environ.pop("NSM_HOST_NOCOMPUTE", None)
+    os.environ.pop("NSM_HOST_ONE_INSTREAM", None)
+    if label == "off":
+        S.set_host_chunks(False)
+    else:
+        chunks, streams = label.rstrip("nc").split("/")
+        os.environ["NSM_HOST_CHUNKS_N"] = chunks
+        if streams == "1":
+            os.environ["NSM_HOST_ONE_INSTREAM"] = "1"
+        if label.endswith("nc"):
+            os.environ["NSM_HOST_NOCOMPUTE"] = "1"
+    S.smooth_host(bh, xh, "pgs", k_l=2, out=xo)
+    ts = []
+    for _ in range(8):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        S.smooth_host(bh, xh, "pgs", k_l=2, out=xo)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(f"chunks/in-streams {label:>7}: {np.median(ts):.3f} ms per step (min {min(ts):.3f})", flush=True)
