@@ -1601,7 +1601,10 @@ static nsm_status smooth_host_chunked(nsm_handle *h, const double *b_host, const
     // (the copy pattern alone takes 5.7 ms; one 256 MB + 128 MB copy pair 5.1)
     int64_t nchunks = 32;
     if (const char *v = knob("NSM_HOST_CHUNKS_N")) nchunks = std::max(3, atoi(v));   // experiments
-    const int64_t ct = std::max<int64_t>(std::max(h->DLA, h->DUA) + 1, (nt + nchunks - 1) / nchunks);  // tiles per chunk
+    // tiles per chunk: longer than A's bandwidth (DLA / DUA, in 256-row
+    // tiles), so chunk c's residual reads x only from chunks c - 1 .. c + 1
+    // and never a row a finished sweep already updated
+    const int64_t ct = std::max<int64_t>(std::max(h->DLA, h->DUA) + 1, (nt + nchunks - 1) / nchunks);
     const int64_t C = (nt + ct - 1) / ct;
     if (C < 3 || C > 64) return NSM_OK;
     if (!h->hs_in) {

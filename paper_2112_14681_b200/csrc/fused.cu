@@ -79,7 +79,7 @@ namespace {
 constexpr int kWarpsC = 8;                  // consumer warps
 constexpr int kRPT = 1;                     // rows per consumer thread (2 measured slower: spills)
 constexpr int kTSF = kWarpsC * kRPT;        // slices per tile
-constexpr int kRowsF = kTSF * kSlice;       // 512 rows per tile
+constexpr int kRowsF = kTSF * kSlice;       // 256 rows per tile
 constexpr int kWarpP = kWarpsC, kWarpS = kWarpsC + 1;
 constexpr int kThreadsF = (kWarpsC + 2) * 32;  // + producer warp + sync warp
 constexpr int kMaxStages = 8;

@@ -87,14 +87,27 @@ def test_smooth_host_nu_zero():
         assert np.array_equal(out3, x0)
 
 
-@pytest.mark.parametrize("mat", ["var27_64", "lap_96", "cd_rcm_40"])
+def _wide_band(n=100_000, w=20_000, seed=3):
+    """A matrix whose bandwidth (20,000 rows) exceeds n / 32: the chunk length
+    follows the bandwidth, not the chunk count (a CPU model of the chunk
+    schedule with chunks shorter than the bandwidth gives a wrong x)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(seed)
+    offs = [-w, -1, 1, w]
+    diags = [rng.uniform(-1, 1, n - abs(o)) for o in offs]
+    M = sp.diags(diags, offs, shape=(n, n), format="csr")
+    M = M + sp.diags(np.abs(M).sum(1).A1 + 1.0)
+    return inputs.CSR.from_scipy(M.tocsr())
+
+
+@pytest.mark.parametrize("mat", ["var27_64", "lap_96", "cd_rcm_40", "wide_band"])
 @pytest.mark.parametrize("k", [1, 2, 3])
 def test_smooth_host_chunked_matches_device(mat, k):
     """nsm_smooth_host in row chunks (copies overlapped with the passes,
     NSM_OPT_HOST_CHUNKS, the default) is bit-identical to the device call and
     to the unchunked host call; pinned host vectors."""
     A = {"var27_64": lambda: inputs.var27(64), "lap_96": lambda: inputs.laplace(96, 96, 96),
-         "cd_rcm_40": lambda: inputs.convdiff(40)}[mat]()
+         "cd_rcm_40": lambda: inputs.convdiff(40), "wide_band": _wide_band}[mat]()
     b = torch.from_numpy(inputs.uniform(0, A.nrows)).pin_memory()
     x0 = torch.from_numpy(inputs.uniform(1, A.nrows)).pin_memory()
     with _smoother(A) as S:
@@ -102,7 +115,9 @@ def test_smooth_host_chunked_matches_device(mat, k):
         S.smooth(b.cuda(), xd, "pgs", nu=1, k_l=k)
         want = xd.cpu().numpy()
         out = torch.empty_like(x0).pin_memory()
+        l0 = S.stats()[0]
         S.smooth_host(b, x0, "pgs", nu=1, k_l=k, out=out)
+        assert S.stats()[0] - l0 > 2 * (k + 1), "the chunked path did not run"   # (k + 1) launches per chunk
         assert np.array_equal(out.numpy(), want), f"{mat} k={k} chunked"
         S.set_host_chunks(False)
         out2 = torch.empty_like(x0).pin_memory()
