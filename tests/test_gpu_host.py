@@ -119,6 +119,11 @@ def test_smooth_host_chunked_matches_device(mat, k):
         S.smooth_host(b, x0, "pgs", nu=1, k_l=k, out=out)
         assert S.stats()[0] - l0 > 2 * (k + 1), "the chunked path did not run"   # (k + 1) launches per chunk
         assert np.array_equal(out.numpy(), want), f"{mat} k={k} chunked"
+        # a pageable result buffer: the chunked path copies x back instead of
+        # writing it over PCIe from the last sweep
+        outp = np.full(A.nrows, 7.0)
+        S.smooth_host(b, x0, "pgs", nu=1, k_l=k, out=outp)
+        assert np.array_equal(outp, want), f"{mat} k={k} chunked, pageable out"
         S.set_host_chunks(False)
         out2 = torch.empty_like(x0).pin_memory()
         S.smooth_host(b, x0, "pgs", nu=1, k_l=k, out=out2)

@@ -14,18 +14,14 @@ bh = torch.from_numpy(inputs.uniform(inputs.SEED_B, A.nrows)).pin_memory()
 xh = torch.from_numpy(inputs.uniform(inputs.SEED_X0, A.nrows)).pin_memory()
 xo = torch.empty_like(xh).pin_memory()
 st = torch.cuda.current_stream()
-for label in ["16/2", "32/2", "16/1", "32/1", "16/2nc", "32/2nc", "off"]:
-    os.environ.pop("NSM_HOST_NOCOMPUTE", None)
-    os.environ.pop("NSM_HOST_ONE_INSTREAM", None)
+for label in ["32", "32copyout", "16", "16copyout", "off"]:
+    os.environ.pop("NSM_HOST_NO_MAPPED_OUT", None)
     if label == "off":
         S.set_host_chunks(False)
     else:
-        chunks, streams = label.rstrip("nc").split("/")
-        os.environ["NSM_HOST_CHUNKS_N"] = chunks
-        if streams == "1":
-            os.environ["NSM_HOST_ONE_INSTREAM"] = "1"
-        if label.endswith("nc"):
-            os.environ["NSM_HOST_NOCOMPUTE"] = "1"
+        os.environ["NSM_HOST_CHUNKS_N"] = label.replace("copyout", "")
+        if label.endswith("copyout"):
+            os.environ["NSM_HOST_NO_MAPPED_OUT"] = "1"
     S.smooth_host(bh, xh, "pgs", k_l=2, out=xo)
     ts = []
     for _ in range(8):
@@ -35,4 +31,4 @@ for label in ["16/2", "32/2", "16/1", "32/1", "16/2nc", "32/2nc", "off"]:
         e1.record(st)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    print(f"chunks/in-streams {label:>7}: {np.median(ts):.3f} ms per step (min {min(ts):.3f})", flush=True)
+    print(f"chunks {label:>9}: {np.median(ts):.3f} ms per step (min {min(ts):.3f})", flush=True)
