@@ -22,3 +22,4 @@ timeout 900 ncu --metrics $M --clock-control none -k regex:'k_' -c 60 --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_residual' -s 6 -c 1 -o gpurun_out/prof_residual_C3 python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep' -s 10 -c 1 -o gpurun_out/prof_sweep_C3 python bench.py --steps 2 --warmup 3 --no-cpu >> gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_residual' -s 6 -c 1 -o gpurun_out/prof_residual_C4 python bench.py --config C4 --steps 2 --warmup 3 --no-cpu >> gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweeps_coupled' -c 1 -o gpurun_out/prof_coupled_C3 python bench.py --steps 2 --warmup 3 --no-cpu --coupled on >> gpurun_out/ncu_full.log 2>&1

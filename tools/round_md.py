@@ -50,6 +50,14 @@ def main(name, title, intro):
               open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     for c in ["C3", "C4"]:
         shutil.copy(os.path.join(G, f"launches_{c}.csv"), os.path.join(ROOT, "profiles", f"{name}_launches_{c}.csv"))
+    coupled_md = ""
+    cp = os.path.join(G, "prof_coupled_C3.ncu-rep")
+    cl = os.path.join(G, "bench_C3_coupled.json")
+    if os.path.exists(cp) and os.path.exists(cl):
+        dc = json.loads(open(cl).readline())
+        coupled_md = (f"## Coupled sweeps (opt-in, `--coupled on`): C3 {dc['ms_per_step']} ms per application, "
+                      f"sweeps kernel at {dc['roofline'].get('sweeps_frac')} of peak on its algorithmic bytes\n\n"
+                      + sh("full", cp) + "\n")
     rows = []
     for c, d in b.items():
         r = d["roofline"]
@@ -102,11 +110,12 @@ Full bench line (C3, the default workload):
 ## ncu --set full, C4 residual kernel
 
 {fulls['residual_C4']}
-DRAM traffic per launch (ncu, cold): C3 residual {(traffic['residual_C3'] or 0) / 1e6:.1f} MB vs the algorithmic
+{coupled_md}DRAM traffic per launch (ncu, cold): C3 residual {(traffic['residual_C3'] or 0) / 1e6:.1f} MB vs the algorithmic
 {b['C3']['roofline']['bytes_per_launch'] / 1e6:.1f} MB; C4 residual {(traffic['residual_C4'] or 0) / 1e6:.1f} MB vs
 {b['C4']['roofline']['bytes_per_launch'] / 1e6:.1f} MB.
 """
     open(os.path.join(ROOT, "profiles", f"{name}.md"), "w").write(md)
+    return md
     print(f"profiles/{name}.md written; traffic {traffic}")
 
 
