@@ -1597,9 +1597,12 @@ static nsm_status smooth_host_chunked(nsm_handle *h, const double *b_host, const
         wide_rows(mwr, h->nslices) || !tma_ok(1, h->L.maxw) || wide_rows(h->L.maxw, h->nslices))
         return NSM_OK;
     const int64_t nt = (h->n + 255) / 256;
-    // 32 chunks: C3 e2e 6.0 ms per step against 6.3 with 16 and 6.8 with 64
-    // (the copy pattern alone takes 5.7 ms; one 256 MB + 128 MB copy pair 5.1)
-    int64_t nchunks = 32;
+    // chunk count, measured (tools/experiments/e2e_chunks.py, ms per step for
+    // 8 / 12 / 16 / 24 / 32 / 48 chunks): C3 (27-point rows) 6.38 / 6.27 /
+    // 6.30 / 5.93 / 5.95 / 6.27, C5 (7-point) 6.30 / 6.24 / 6.30 / 6.55 /
+    // 6.90 / 6.78 — so 32 for wide rows, 12 for narrow ones (the copy pattern
+    // alone takes 5.7 ms; one 256 MB + 128 MB copy pair 5.1)
+    int64_t nchunks = h->nnz_off >= 16 * h->n ? 32 : 12;
     if (const char *v = knob("NSM_HOST_CHUNKS_N")) nchunks = std::max(3, atoi(v));   // experiments
     // tiles per chunk: longer than A's bandwidth (DLA / DUA, in 256-row
     // tiles), so chunk c's residual reads x only from chunks c - 1 .. c + 1

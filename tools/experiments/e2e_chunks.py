@@ -8,20 +8,18 @@ import bench, inputs
 import paper_2112_14681_b200 as nsm
 
 nsm.load(variant="exp")
-A, offsets, kind, k_l, k_u, desc = bench.build_workload("C3", 0, 1)
+CFG = sys.argv[1] if len(sys.argv) > 1 else "C3"
+A, offsets, kind, k_l, k_u, desc = bench.build_workload(CFG, 0, 1)
 S = nsm.Smoother(A)
 bh = torch.from_numpy(inputs.uniform(inputs.SEED_B, A.nrows)).pin_memory()
 xh = torch.from_numpy(inputs.uniform(inputs.SEED_X0, A.nrows)).pin_memory()
 xo = torch.empty_like(xh).pin_memory()
 st = torch.cuda.current_stream()
-for label in ["32", "32copyout", "16", "16copyout", "off"]:
-    os.environ.pop("NSM_HOST_NO_MAPPED_OUT", None)
+for label in (sys.argv[2:] or ["16", "24", "32", "off"]):
     if label == "off":
         S.set_host_chunks(False)
     else:
-        os.environ["NSM_HOST_CHUNKS_N"] = label.replace("copyout", "")
-        if label.endswith("copyout"):
-            os.environ["NSM_HOST_NO_MAPPED_OUT"] = "1"
+        os.environ["NSM_HOST_CHUNKS_N"] = label
     S.smooth_host(bh, xh, "pgs", k_l=2, out=xo)
     ts = []
     for _ in range(8):
@@ -31,4 +29,4 @@ for label in ["32", "32copyout", "16", "16copyout", "off"]:
         e1.record(st)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    print(f"chunks {label:>9}: {np.median(ts):.3f} ms per step (min {min(ts):.3f})", flush=True)
+    print(f"{CFG} chunks {label:>5}: {np.median(ts):.3f} ms per step (min {min(ts):.3f})", flush=True)
