@@ -383,8 +383,11 @@ cudaError_t launch_coupled(const CoupledLaunch &L, cudaStream_t st) {
     p.sweep_id0 = L.sweep_id0;
     p.err = L.err;
     p.timeout_ns = L.timeout_ns;
-    // throttle distance: a few rounds of tiles (>= 1 for the deadlock argument)
-    p.lag = L.lag > 0 ? L.lag : 4 * per_group;
+    // throttle distance (>= 1 for the deadlock argument): 32 rounds of tiles —
+    // measured on C3, sweeps kernel 1.54 ms at 4 rounds, 1.25 at 8, 1.18 at 27
+    // with the DRAM traffic unchanged (2.31 GB: the later sweeps stay close
+    // behind on their own)
+    p.lag = L.lag > 0 ? L.lag : 32 * per_group;
     p.nst = nst;
     p.cap = sh.cap;
     p.stats = L.stats;
