@@ -362,7 +362,9 @@ cudaError_t launch_coupled(const CoupledLaunch &L, cudaStream_t st) {
     if (!nst || per_sm < 1) return cudaErrorInvalidConfiguration;
     const size_t smem = (size_t)(kCtlBytes + 128 + nst * sh.stage);
     const int64_t ntiles = (L.n + kTS * kSlice - 1) / (kTS * kSlice);
-    const int64_t per_group = std::min<int64_t>({(int64_t)nsm * per_sm / sh.k, ntiles, L.pstride});
+    // CTAs per group: one round per SM slot, at most what a producer lane set
+    // reads per frontier refresh (32 lanes x kPV counters)
+    const int64_t per_group = std::min<int64_t>({(int64_t)nsm * per_sm / sh.k, ntiles, L.pstride, (int64_t)32 * kPV});
     if (per_group < 1) return cudaErrorInvalidConfiguration;
     const int grid = (int)(per_group * sh.k);
     CoupledParams p{};
