@@ -47,3 +47,12 @@ def test_byte_models():
     assert pp["residual"] == 12 * noff + 40 * n                      # OUT_RG: r and g0 written
     assert pp["sweeps"] == [12 * nl + 32 * n, 12 * nl + 40 * n]      # last sweep: x read + write
     assert bench.floor_bytes("pgs", n, noff, nl, nu, 2, 0)["total"] == 12 * noff + 32 * n
+    # the coupled sweeps (one kernel, L streamed once): the per-pass sweeps'
+    # vectors, L's entries once; k = 1 has nothing to couple
+    cp = bench.algorithmic_bytes("pgs", n, noff, nl, nu, 2, 0, coupled=True)
+    assert cp["residual"] == pp["residual"]
+    assert cp["sweeps"] == [12 * nl + 32 * n + 8 * n + 32 * n]      # L once; r, d, g0 | r, d, g1, x rd+wr; g1 written
+    k3 = bench.algorithmic_bytes("pgs", n, noff, nl, nu, 3, 0, coupled=True)
+    assert k3["sweeps"] == [sum(bench.algorithmic_bytes("pgs", n, noff, nl, nu, 3, 0)["sweeps"]) - 2 * 12 * nl]
+    assert bench.algorithmic_bytes("pgs", n, noff, nl, nu, 1, 0, coupled=True) == \
+        bench.algorithmic_bytes("pgs", n, noff, nl, nu, 1, 0)
