@@ -231,7 +231,9 @@ __device__ __forceinline__ void sweep_tma_body(int64_t n, int64_t s_begin, int64
             ot.at(Ly.col(sm, st, 0), to);
         }
         double acc = 0.0;
-        if constexpr (WIN) {
+        if constexpr (WIN && CH == 7) {   // chunks of 7 (fewer registers: four CTAs per SM)
+            if (has) acc = win_sum_chunked<7>(Ly.val(sm, st, 0), Ly.col(sm, st, 0), Ly.win(sm, st), to, tw, lane, row, acc);
+        } else if constexpr (WIN) {
             if (has) {
                 WinChunk<CH> ct;
                 ct.load(Ly.val(sm, st, 0), Ly.col(sm, st, 0), Ly.win(sm, st), to, tw, lane, row);
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(kThreadsT) k_sweep_tma(int64_t n, int64_t s_be
 }
 
 template <bool UNIT, int EPI, int CH>
-__global__ void __launch_bounds__(kThreadsT, 3)
+__global__ void __launch_bounds__(kThreadsT, CH == 7 ? 4 : 3)
     k_sweep_tma_w(int64_t n, int64_t s_begin, int64_t s_end, SellView T, const double *__restrict__ dT,
                   const double *__restrict__ rhs, GatherPlainT gin, double *__restrict__ gout, double *__restrict__ x,
                   const double *__restrict__ dnext, double *__restrict__ gout2, unsigned long long *flag,
@@ -422,6 +424,14 @@ cudaError_t sweep_tma_launch(const SweepArgs &a, int64_t s_begin, int64_t s_end,
     // gather window of the plain iterate over the whole range: gathers from
     // shared memory
     if constexpr (std::is_same<G, GatherPlainT>::value) {
+        // windowed sweeps over rows wider than 8 entries: the window sum in
+        // chunks of 7 fits 56 registers, so four CTAs share an SM instead of
+        // three at CH = 16 (C3 sweeps 0.95 -> 0.98 of peak, 1.384 -> 1.360 ms
+        // per application; tools/experiments/README.md)
+        if constexpr (CH == 16) {
+            if (a.T->off && a.win && s_begin % kTS == 0)
+                return sweep_tma_ofs<UNIT, EPI, G, 7, true, true>(a, s_begin, s_end, gin, st);
+        }
         if (a.T->off && a.win && s_begin % kTS == 0)
             return sweep_tma_ofs<UNIT, EPI, G, CH, true, true>(a, s_begin, s_end, gin, st);
     }
@@ -540,6 +550,14 @@ void touch_tma_ch() {
 }  // namespace
 
 void preload_tma_kernels() {
+    touch_t(k_sweep_tma_w<true, EPI_STORE2, 7>);   // the chunk-7 windowed sweeps
+    touch_t(k_sweep_tma_w<false, EPI_STORE2, 7>);
+    touch_t(k_sweep_tma_w<true, EPI_STORE, 7>);
+    touch_t(k_sweep_tma_w<true, EPI_XADD, 7>);
+    touch_t(k_sweep_tma_w<true, EPI_XADD_SCALE, 7>);
+    touch_t(k_sweep_tma_w<false, EPI_STORE, 7>);
+    touch_t(k_sweep_tma_w<false, EPI_XADD, 7>);
+    touch_t(k_sweep_tma_w<false, EPI_XADD_SCALE, 7>);
     touch_t(k_residual_tma_w<OUT_R, 14>);
     touch_t(k_residual_tma_w<OUT_AX, 14>);
     touch_t(k_residual_tma_w<OUT_RG, 14>);

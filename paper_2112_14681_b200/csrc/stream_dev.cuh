@@ -536,6 +536,27 @@ struct WinChunk {
     }
 };
 
+// The same sum in chunks of CH entries (each chunk's products in flight
+// together, added in stored order): fewer registers than one wide chunk.
+template <int CH>
+__device__ __forceinline__ double win_sum_chunked(const double *sv_, const int32_t *stage_pos, const double *win,
+                                                  int64_t off, int w, int lane, bool row, double acc) {
+    const double *sv = sv_ + off + lane;
+    const int32_t *wp = stage_pos + off / kSlice;
+    const double *ws = win + lane;
+    if (!row) return acc;
+    for (int j0 = 0; j0 < w; j0 += CH) {
+        double v[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j0 + j < w) v[j] = __dmul_rn(sv[(j0 + j) * kSlice], ws[wp[j0 + j]]);
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j0 + j < w) acc = __dadd_rn(acc, v[j]);
+    }
+    return acc;
+}
+
 }  // namespace
 
 }  // namespace nsm
