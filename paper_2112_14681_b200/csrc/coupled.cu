@@ -168,7 +168,10 @@ struct CoupledHook {
             const int64_t m = rows(t);
             if (m & 1) rslot0[st * kTS * kSlice + m - 1] = p->r[t * kTS * kSlice + m - 1];  // odd n: last row
         }
-        if (Fs < p->ntiles) issue(lane);   // the view for the next tile, in flight while this one is staged
+        // refresh the view (in flight while this tile is staged) only when the
+        // need is within two rounds of what has been seen: the loads and the
+        // reduction stay off most tiles' path
+        if (!pending && Fs < p->ntiles && need + 2 * Gg >= Fs) issue(lane);
     }
     __device__ __forceinline__ uint32_t extra_bytes(int64_t t) const { return (uint32_t)((rows(t) & ~(int64_t)1) * 8); }
     __device__ __forceinline__ void extra_copy(int64_t t, int st, uint64_t *bar) {
