@@ -66,6 +66,9 @@ constexpr int kCW = kTS;        // consumer warps: one slice each
 constexpr int kMaxG = 3;        // sweeps (groups) per launch
 constexpr int kSlots = 4;       // tile-count slots (> stages)
 constexpr int kCtlBytes = 128;  // publication counters
+#ifndef NSM_CP_STATS
+#define NSM_CP_STATS 1   // cycle counters (nsm_coupled_counters)
+#endif
 constexpr int kThreadsC = (kCW + 2) * 32;   // + producer + publisher
 constexpr int64_t kSmemMaxC = 227 * 1024;
 
@@ -76,7 +79,7 @@ struct CoupledParams {
     const double *d, *r;
     double *x;
     double *g[kMaxG];            // g[j] = g(j): gathered by group j (g[0] from the residual kernel)
-    unsigned long long *prog;    // [k][pstride] per-CTA progress (epoch << 32 | tiles done)
+    unsigned int *prog;          // [k][pstride] per-CTA progress: tag_of(epoch) | tiles done
     int64_t pstride;
     unsigned int *sync;          // [0] epoch, [1] CTAs finished
     unsigned long long *flag;
@@ -96,6 +99,9 @@ struct CoupledParams {
 // on a frontier it has not fenced yet (about once per round of tiles), and it
 // spins only when the prefetched view is not enough.
 constexpr int kPV = 8;   // counters per lane (groups of <= 256 CTAs)
+// progress words: the launch epoch's low 11 bits above a 21-bit tile count; the
+// last CTA out clears the words before the tag wraps (red.max stays monotone)
+__device__ __forceinline__ unsigned int tag_of(unsigned int epoch) { return (epoch & 0x7ffu) << 21; }
 template <int NG>
 struct CoupledHook {
     const CoupledParams *p;
@@ -105,19 +111,21 @@ struct CoupledHook {
     double *rslot0;        // r rows of stage 0 (256 doubles per stage)
     int64_t Fs, Ff;        // frontier of the awaited group: seen (relaxed reads), fenced
     bool pending;
-    unsigned long long rv[kPV];
+    unsigned int rv[kPV];
     uint64_t pol_keep, pol_first;
+#if NSM_CP_STATS
     long long c_last, c_wait, c_empty, c_fence;   // statistics (lane 0): cycles in dependency spins / stage waits / fences
+#endif
     __device__ __forceinline__ int64_t first() const { return c; }
     __device__ __forceinline__ int64_t stride() const { return Gg; }
     __device__ __forceinline__ int64_t rows(int64_t t) const { return min((int64_t)kTS * kSlice, p->n - t * kTS * kSlice); }
     __device__ __forceinline__ int waited() const { return g == 0 ? NG - 1 : g - 1; }
     __device__ __forceinline__ void issue(int lane) {
-        const unsigned long long *pr = p->prog + (int64_t)waited() * p->pstride;
+        const unsigned int *pr = p->prog + (int64_t)waited() * p->pstride;
 #pragma unroll
         for (int r = 0; r < kPV; ++r) {
             const int64_t q = lane + 32 * r;
-            rv[r] = q < Gg ? ptx::ld_relaxed_gpu_u64(pr + q) : 0ull;
+            rv[r] = q < Gg ? ptx::ld_relaxed_gpu_u32(pr + q) : 0u;
         }
         pending = true;
     }
@@ -127,7 +135,7 @@ struct CoupledHook {
         for (int r = 0; r < kPV; ++r) {
             const int64_t q = lane + 32 * r;
             if (q < Gg) {
-                const int64_t cnt = (unsigned int)(rv[r] >> 32) == epoch ? (int64_t)(rv[r] & 0xffffffffull) : 0;
+                const int64_t cnt = (rv[r] & 0xffe00000u) == tag_of(epoch) ? (int64_t)(rv[r] & 0x1fffffu) : 0;
                 f = min(f, q + cnt * Gg);
             }
         }
@@ -137,12 +145,16 @@ struct CoupledHook {
         pending = false;
     }
     __device__ __forceinline__ void before(int64_t t, int st, int lane) {
+#if NSM_CP_STATS
         if (c_last) c_empty += clock64() - c_last;
+#endif
         const int64_t need = min(g == 0 ? t - p->lag : t, p->ntiles - 1);   // all tiles <= need complete
         if (pending) reduce(lane);
         if (need >= Ff) {
             if (need >= Fs) {
+#if NSM_CP_STATS
                 const long long c0 = clock64();
+#endif
                 const uint64_t t0 = ptx::globaltimer_ns();
                 while (true) {
                     issue(lane);
@@ -155,14 +167,20 @@ struct CoupledHook {
                     }
                     __nanosleep(64);
                 }
+#if NSM_CP_STATS
                 c_wait += clock64() - c0;
+#endif
             }
+#if NSM_CP_STATS
             const long long c1 = clock64();
+#endif
             ptx::fence_acq_rel_gpu();   // acquire: the counters read above were published with release
             Ff = Fs;
             __syncwarp();
             asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and the window copies follow it
+#if NSM_CP_STATS
             c_fence += clock64() - c1;
+#endif
         }
         if (lane == 0) {
             const int64_t m = rows(t);
@@ -177,7 +195,9 @@ struct CoupledHook {
     __device__ __forceinline__ void extra_copy(int64_t t, int st, uint64_t *bar) {
         const uint32_t bytes = extra_bytes(t);
         if (bytes) ptx::bulk_g2s(rslot0 + st * kTS * kSlice, p->r + t * kTS * kSlice, bytes, bar, pol_keep);
+#if NSM_CP_STATS
         c_last = clock64();
+#endif
     }
     __device__ __forceinline__ uint64_t val_policy(int, uint64_t) const { return g == NG - 1 ? pol_first : pol_keep; }
 };
@@ -218,16 +238,22 @@ __global__ void __launch_bounds__(kThreadsC, 2) k_sweeps_coupled(const __grid_co
         hk.pending = false;
         hk.pol_keep = ptx::policy_evict_normal();
         hk.pol_first = ptx::policy_evict_first();
+#if NSM_CP_STATS
         hk.c_last = hk.c_wait = hk.c_empty = hk.c_fence = 0;
+#endif
         const SellView P[1] = {p.L};
+#if NSM_CP_STATS
         const long long c0 = clock64();
+#endif
         producer_deep<1, CoupledHook<NG> &>(Ly, gb, P, 0, p.nslices, ntiles, lane, p.WL, p.g[g], p.n, hk);
+#if NSM_CP_STATS
         if (p.stats && lane == 0) {
             atomicAdd(p.stats + 4 * g + 0, (unsigned long long)hk.c_wait);
             atomicAdd(p.stats + 4 * g + 1, (unsigned long long)hk.c_empty);
             atomicAdd(p.stats + 4 * g + 2, (unsigned long long)(clock64() - c0));
             atomicAdd(p.stats + 12 + g, (unsigned long long)hk.c_fence);
         }
+#endif
     } else if (warp == kCW + 1) {
         // ------------------------------------------------------------ publisher
         if (lane == 0) {
@@ -239,8 +265,7 @@ __global__ void __launch_bounds__(kThreadsC, 2) k_sweeps_coupled(const __grid_co
                        ptx::ld_acquire_cta_shared(cnt + mm % kSlots) >= (unsigned int)((mm / kSlots + 1) * kCW))
                     ++mm;
                 if (mm > m) {
-                    ptx::red_max_release_gpu_u64(p.prog + (int64_t)g * p.pstride + c,
-                                                 ((unsigned long long)epoch << 32) | (unsigned long long)mm);
+                    ptx::red_max_release_gpu_u32(p.prog + (int64_t)g * p.pstride + c, tag_of(epoch) | (unsigned int)mm);
                     m = mm;
                 } else {
                     if (ptx::globaltimer_ns() - t0 > 4 * p.timeout_ns) break;  // the producers flagged it
@@ -255,7 +280,9 @@ __global__ void __launch_bounds__(kThreadsC, 2) k_sweeps_coupled(const __grid_co
         const unsigned long long sid = (unsigned long long)(p.sweep_id0 + g);
         int st = 0;
         uint32_t ph = 0;
+#if NSM_CP_STATS
         long long c_full = 0;
+#endif
         for (int64_t t = c, m = 0; t < ntiles; t += Gg, ++m) {
             const int64_t s = t * kTS + wl;
             const int64_t i = s * kSlice + lane;
@@ -263,9 +290,13 @@ __global__ void __launch_bounds__(kThreadsC, 2) k_sweeps_coupled(const __grid_co
             const bool row = has && i < p.n;
             const double di = row ? __ldg(p.d + i) : 1.0;
             const double xi = (g == NG - 1 && row) ? p.x[i] : 0.0;  // x of tile t: only this group's tile t writes it
+#if NSM_CP_STATS
             const long long cw = clock64();
+#endif
             ptx::mbar_wait(Ly.full(gb) + st, ph);
+#if NSM_CP_STATS
             c_full += clock64() - cw;
+#endif
             double acc = 0.0;
             if (has) {
                 const int2 hd = *(const int2 *)(Ly.hdr(gb, st, 0) + 2 * wl);
@@ -286,7 +317,9 @@ __global__ void __launch_bounds__(kThreadsC, 2) k_sweeps_coupled(const __grid_co
             if (lane == 0) ptx::red_add_release_cta_shared(cnt + m % kSlots, 1u);
             if (++st == p.nst) { st = 0; ph ^= 1; }
         }
+#if NSM_CP_STATS
         if (p.stats && lane == 0 && wl == 0) atomicAdd(p.stats + 4 * g + 3, (unsigned long long)c_full);
+#endif
     }
     // ---- the last CTA out advances the epoch for the next launch
     __syncthreads();
@@ -294,8 +327,11 @@ __global__ void __launch_bounds__(kThreadsC, 2) k_sweeps_coupled(const __grid_co
         __threadfence();
         const unsigned int prev = atomicAdd(&p.sync[1], 1u);
         if (prev == gridDim.x - 1) {
+            const unsigned int next = epoch + 1 == 0 ? 1 : epoch + 1;
+            if (tag_of(next) == 0)   // the tag wraps: clear the words so red.max starts from 0 again
+                for (int64_t q = 0; q < (int64_t)NG * p.pstride; ++q) p.prog[q] = 0u;
             p.sync[1] = 0;
-            p.sync[0] = epoch + 1 == 0 ? 1 : epoch + 1;
+            p.sync[0] = next;
             __threadfence();
         }
     }
@@ -381,7 +417,7 @@ cudaError_t launch_coupled(const CoupledLaunch &L, cudaStream_t st) {
     p.r = L.r;
     p.x = L.x;
     for (int g = 0; g < kMaxG; ++g) p.g[g] = L.g[g];
-    p.prog = L.prog;
+    p.prog = (unsigned int *)L.prog;
     p.pstride = L.pstride;
     p.sync = L.sync;
     p.flag = L.flag;

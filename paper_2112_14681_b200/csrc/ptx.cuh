@@ -118,6 +118,9 @@ __device__ __forceinline__ unsigned int atom_add_acqrel_cta_shared(unsigned int 
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
     return old;
 }
+__device__ __forceinline__ void red_max_release_gpu_u32(unsigned int *p, unsigned int v) {
+    asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_max_release_gpu_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.release.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
