@@ -377,8 +377,17 @@ cudaError_t residual_tma_ofs(const Window *w, int64_t n, int64_t s_begin, int64_
                              bool pdl, cudaStream_t st) {
     auto k = WIN ? k_residual_tma_w<OUT, CH> : k_residual_tma<OUT, CH, OFS>;
     const WinView W = win_view(WIN ? w : nullptr);
-    const Geo g = geometry(k, 2, std::max(L.maxw, U.maxw), OFS ? 8 : 12, (int64_t)W.wcap * 8);
+    Geo g = geometry(k, 2, std::max(L.maxw, U.maxw), OFS ? 8 : 12, (int64_t)W.wcap * 8);
     if (!g.nst) return cudaErrorInvalidConfiguration;
+    if (const char *v = knob("NSM_RES_NST")) {  // experiment: force the stage count (occupancy follows)
+        const int nst = atoi(v);
+        const int64_t stage = 2 * Layout::part_bytes(g.cap, OFS ? 8 : 12) + (int64_t)W.wcap * 8;
+        g.nst = nst;
+        g.smem = (size_t)(128 + nst * stage);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreadsT, g.smem);
+        g.per_sm = per_sm;
+    }
     const int64_t ntiles = (s_end - s_begin + kTS - 1) / kTS;
     return launch_pdl(pdl, k, grid_of<decltype(k)>(g, ntiles), g.smem, st, n, s_begin, s_end, view(L), view(U), d, b, x,
                       out, out2, g.nst, g.cap, W);
