@@ -708,7 +708,11 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
         h->DLs = F ? tiles(sf.bw_lower) : 0;
         h->DUs = F ? tiles(sf.bw_upper) : 0;
         h->fused_possible = true;
-        ok = coupled_alloc(a, h);
+        // PDL also pays for the windowed (27-point) kernels at any size: C3,
+        // 3 reps, 1.3517 vs 1.3559 ms per application (tools/experiments/pdl_c3.sh;
+        // 7-point and compact 16.7 M-row passes lose 1-3 %)
+        if (h->res_win.wmax) h->pdl = true;
+        ok = ok && coupled_alloc(a, h);
     }
     if (ok && nranks > 1) {
         h->row_offsets.assign(dist->row_offsets, dist->row_offsets + nranks + 1);
@@ -826,7 +830,11 @@ nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F
         h->DLs = F ? tiles(sf.bw_lower) : 0;
         h->DUs = F ? tiles(sf.bw_upper) : 0;
         h->fused_possible = true;
-        ok = coupled_alloc(a, h);
+        // PDL also pays for the windowed (27-point) kernels at any size: C3,
+        // 3 reps, 1.3517 vs 1.3559 ms per application (tools/experiments/pdl_c3.sh;
+        // 7-point and compact 16.7 M-row passes lose 1-3 %)
+        if (h->res_win.wmax) h->pdl = true;
+        ok = ok && coupled_alloc(a, h);
     }
     if (!ok) {
         cudaGetLastError();
