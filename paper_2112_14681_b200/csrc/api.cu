@@ -662,7 +662,6 @@ nsm_status nsm_setup(nsm_handle **out, const nsm_csr *A, const nsm_csr *F, const
     preload_fused_kernels();
     preload_fused_w_kernels();
     preload_coupled_kernels();
-    preload_pair_kernels();
     nsm_handle *h = new nsm_handle();
     h->uid = next_handle_uid();
     h->device = device;
@@ -781,7 +780,6 @@ nsm_status nsm_setup_device(nsm_handle **out, const nsm_csr *A, const nsm_csr *F
     preload_fused_kernels();
     preload_fused_w_kernels();
     preload_coupled_kernels();
-    preload_pair_kernels();
     nsm_handle *h = new nsm_handle();
     h->uid = next_handle_uid();
     h->device = device;
@@ -1362,38 +1360,10 @@ static nsm_status coupled_run(nsm_handle *h, const double *b, double *x, int k, 
     if (!h->coupled || !h->cp_prog || distributed(h) || !h->pipeline || !h->window || k < 2 || k > 3 || h->n == 0 ||
         !h->L.off || !h->L.win.wmax)
         return NSM_OK;
-    double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
-    if (k == 2 && knob("NSM_CP_PAIR") && pair_possible(h->L.maxw, h->L.win.wmax, h->L.win.maxseg)) {
-        // the paired sweeps (pair.cu): one CTA runs both sweeps of its tiles
-        nsm_status st = residual_into(h, b, x, R, OUT_RG, s, W2);
-        if (st != NSM_OK) return st;
-        PairLaunch P{};
-        P.n = h->n;
-        P.Lp = &h->L;
-        P.wl = &h->L.win;
-        P.d = h->d;
-        P.r = R;
-        P.g0 = W2;
-        P.g1 = W0;
-        P.x = x;
-        P.prog = (unsigned int *)h->cp_prog;
-        P.pstride = kCpProgStride;
-        P.sync = h->cp_sync;
-        P.flag = h->flag;
-        P.sweep_id0 = h->sweep_counter + 1;
-        P.err = h->d_dist_err;
-        P.timeout_ns = h->timeout_ns;
-        ProfScope prof(h, 1, s);
-        const cudaError_t e = launch_pair(P, s);
-        if (e != cudaSuccess) return cuda_fail(h, e, "paired sweeps launch");
-        h->sweep_counter += k;
-        ++h->launches;
-        *ran = true;
-        return NSM_OK;
-    }
     CoupledLaunch L{};
     L.shape = coupled_shape(h->L.maxw, h->L.win.wmax, k, h->n);
     if (!L.shape.ok) return NSM_OK;
+    double *R = h->w[0], *W0 = h->w[1], *W1 = h->w[2], *W2 = h->w[3];
     nsm_status st = residual_into(h, b, x, R, OUT_RG, s, W2);
     if (st != NSM_OK) return st;
     L.n = h->n;

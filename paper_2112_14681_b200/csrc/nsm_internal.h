@@ -327,27 +327,6 @@ struct CoupledLaunch {
 cudaError_t launch_coupled(const CoupledLaunch &L, cudaStream_t st);
 void preload_coupled_kernels();
 
-// ---- paired sweeps (pair.cu) -----------------------------------------------------
-// The two sweeps of a forward pGS application with k = 2 in one cooperative
-// kernel, every CTA running both on its own tiles with L kept in shared memory.
-bool pair_possible(int maxw_l, int64_t wmax, int maxseg);
-struct PairLaunch {
-    int64_t n;
-    const Sell *Lp;
-    const Window *wl;
-    const double *d, *r, *g0;
-    double *g1, *x;
-    unsigned int *prog;              // >= grid words, zero-initialised once
-    int64_t pstride;
-    unsigned int *sync;              // [0] epoch, [1] CTAs finished
-    unsigned long long *flag;
-    int64_t sweep_id0;
-    unsigned int *err;
-    unsigned long long timeout_ns;
-};
-cudaError_t launch_pair(const PairLaunch &L, cudaStream_t st);
-void preload_pair_kernels();
-
 // Force-load every kernel of the library (see kernels.cu "eager loading").
 void preload_plain_kernels();
 void preload_tma_kernels();
