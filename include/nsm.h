@@ -386,10 +386,13 @@ const char *nsm_last_error(const nsm_handle *h);
  *                           items (0 = automatic, about the items in flight);
  *                           a small value forces frequent waits and ring
  *                           reuse (a test knob; slower).
- *   NSM_OPT_PDL             1 (default) = launch the pipelined kernels with
+ *   NSM_OPT_PDL             1 = launch the pipelined kernels with
  *                           programmatic dependent launch (a kernel's matrix
  *                           prefetch overlaps the previous kernel's drain);
- *                           0 = plain stream order. */
+ *                           0 = plain stream order.  Default: 1 up to 8 M
+ *                           rows per rank and for single-rank matrices with
+ *                           gather windows, 0 otherwise (measured per
+ *                           configuration). */
 typedef enum {
     NSM_OPT_PIPELINE = 0, NSM_OPT_HALO_TIMEOUT_MS = 1, NSM_OPT_FUSED = 2, NSM_OPT_PDL = 3,
     NSM_OPT_PROFILE = 4 /* 1: record a CUDA event pair around every residual / sweep / fused pass
