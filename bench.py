@@ -485,7 +485,7 @@ def run_nsm(args, rank, nranks, local_rank):
                                  + ("fused passes = the floor" if fused else
                                     ("the coupled sweeps stream L once" if coupled else "one kernel per pass"))),
                        "bytes_per_step_per_gpu": ab, "floor_bytes_per_step_per_gpu": fmodel["total"],
-                       "offset_aligned_parts": [k for k, v in layout.items() if v],
+                       "offset_aligned_parts": [k for k, v in layout.items() if v and k in ("L", "U", "Ls", "Us")],
                        "floor_gbs": round(floor_gbs, 2),
                        "frac_of_hbm_peak": round(value / nranks / peak, 4)},
             "ms_per_apply": round(ms_step, 4),

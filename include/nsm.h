@@ -334,7 +334,10 @@ nsm_status nsm_stats(const nsm_handle *h, int64_t *kernel_launches, int64_t *hal
  * set when A's L / A's U / the factor's L_s / U_s uses the offset-aligned
  * SELL layout (stencil-like rows: one int32 column offset per slice entry
  * position; the pipelined kernels then read 8 instead of 12 bytes per entry).
- * Chosen automatically at setup when it widens the slices by <= 15 %. */
+ * Chosen automatically at setup when it widens the slices by <= 15 %.
+ * Bits 16 / 32 / 64: the residual (L and U) / L / U have a shared-memory
+ * gather window (built where it is at most half the staged
+ * entries), i.e. the windowed kernels run. */
 nsm_status nsm_layout(const nsm_handle *h, int *offset_aligned);
 
 /* Fused-pass synchronisation statistics since setup: work items whose

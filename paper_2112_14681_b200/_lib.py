@@ -597,6 +597,12 @@ class Smoother:
         self._call(load().nsm_layout(self._h, ctypes.byref(v)))
         return {k: bool(v.value & b) for k, b in (("L", 1), ("U", 2), ("Ls", 4), ("Us", 8))}
 
+    def windows(self):
+        """{'residual', 'L', 'U'}: which gather windows exist (the windowed kernels run)."""
+        v = ctypes.c_int(0)
+        self._call(load().nsm_layout(self._h, ctypes.byref(v)))
+        return {k: bool(v.value & b) for k, b in (("residual", 16), ("L", 32), ("U", 64))}
+
     def fused_stats(self):
         """(waits that had to spin, total spin ns) of the fused passes since setup."""
         w, t = ctypes.c_int64(0), ctypes.c_int64(0)

@@ -1129,7 +1129,8 @@ nsm_status nsm_set_ruiz(nsm_handle *h, const double *s_r, const double *s_c) {
 
 nsm_status nsm_layout(const nsm_handle *h, int *offset_aligned) {
     if (!h || !offset_aligned) return NSM_ERR_ARG;
-    *offset_aligned = (h->L.off ? 1 : 0) | (h->U.off ? 2 : 0) | (h->Ls.off ? 4 : 0) | (h->Us.off ? 8 : 0);
+    *offset_aligned = (h->L.off ? 1 : 0) | (h->U.off ? 2 : 0) | (h->Ls.off ? 4 : 0) | (h->Us.off ? 8 : 0) |
+                      (h->res_win.wmax ? 16 : 0) | (h->L.win.wmax ? 32 : 0) | (h->U.win.wmax ? 64 : 0);
     return NSM_OK;
 }
 

@@ -356,3 +356,48 @@ def test_coupled_pgs(name, lag, xz, k):
             S.smooth(dev(b), x, "pgs", nu=2, k_l=k, x_is_zero=xz)
             agree(host(x), want, f"{name} coupled rep {rep}")
         S.check()
+
+
+def _stencil(nx, ny, nz, offsets, seed=11):
+    """Variable-coefficient stencil on an nx x ny x nz grid (x fastest),
+    diagonally dominant, rows ordered lexicographically."""
+    rng = np.random.default_rng(seed)
+    n = nx * ny * nz
+    idx = np.arange(n)
+    x, y, z = idx % nx, (idx // nx) % ny, idx // (nx * ny)
+    rows, cols = [], []
+    for dx, dy, dz in offsets:
+        ok = (x + dx >= 0) & (x + dx < nx) & (y + dy >= 0) & (y + dy < ny) & (z + dz >= 0) & (z + dz < nz)
+        rows.append(idx[ok])
+        cols.append(idx[ok] + dx + dy * nx + dz * nx * ny)
+    r, c = np.concatenate(rows), np.concatenate(cols)
+    M = sp.csr_matrix((rng.uniform(-1, 1, len(r)), (r, c)), shape=(n, n))
+    M.setdiag(0.0)
+    M.eliminate_zeros()
+    M = M + sp.diags(np.abs(M).sum(1).A1 + 1.0)
+    return inputs.CSR.from_scipy(M.tocsr())
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_windowed_register_chunks(wide):
+    """The windowed kernels' register-chunk variants: 27-point rows (13 entries
+    per triangle: the 14-entry residual chunk, three CTAs per SM, and the sweeps'
+    7-entry chunks) and 27-point + (+-2, 0, 0) rows (15 per triangle: the 16-entry
+    residual chunk, and three 7-entry sweep chunks, the last partial); bitwise
+    against the oracle, with the windows verifiably in use."""
+    offs = [(dx, dy, dz) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+    if wide:
+        offs += [(2, 0, 0), (-2, 0, 0)]
+    A = _stencil(64, 24, 10, offs)
+    b, x0 = inputs.uniform(0, A.nrows), inputs.uniform(1, A.nrows)
+    with nsm.Smoother(A) as S:
+        assert S.windows() == {"residual": True, "L": True, "U": True}, S.windows()
+        agree(host(S.residual(dev(b), dev(x0))), oracle.residual(A, b, x0), f"wide={wide} residual")
+        for k in (1, 2, 3):
+            x = dev(x0)
+            S.smooth(dev(b), x, "pgs", nu=2, k_l=k)
+            agree(host(x), oracle.pgs_apply(A, b, x0, k, nu=2), f"wide={wide} pgs k={k}")
+        r = inputs.uniform(3, A.nrows)
+        for k in (1, 3):
+            agree(host(S.lsolve(dev(r), k)), oracle.tri_jacobi(A, r, k, lower=True), f"wide={wide} lsolve k={k}")
+        S.check()
