@@ -236,7 +236,7 @@ bool build_window(int64_t n, const std::vector<const SellHost *> &parts, int32_t
     for (const SellHost *p : parts) entries += p->ptr[ns];
     for (int64_t t = 0; t < nt; ++t)
         for (const Seg &g : segs[t]) wtot += g.hi - g.lo;
-    if (wtot * 2 > entries) return false;
+    if (wtot * 2 > entries && !knob("NSM_WINDOW_ALWAYS")) return false;   // (experiments: windows for any ratio)
     out->tseg.assign(nt + 1, 0);
     for (int64_t t = 0; t < nt; ++t) out->tseg[t + 1] = out->tseg[t] + (int32_t)segs[t].size();
     const int64_t nseg = out->tseg[nt];
